@@ -1,0 +1,169 @@
+/*
+ * pfc.h -- C ABI of libpfc.so: the per-time-step Newton-Krylov-Schwarz solve of the
+ * DVD phase-field-crystal scheme of Wei, Yang & Huang, arXiv 1703.01202, on one B200.
+ *
+ * Citations: "P:n" = line n of the paper's text; equations by their LaTeX label.
+ *
+ * Conventions (all entry points)
+ *  - Fields are fp64, contiguous, x-fastest: idx = i + n[0]*(j + n[1]*k), N = n[0]*n[1]*n[2]
+ *    (n[2] = 1 in 2D).  Nodes are cell-centred x_i = (i + 1/2) h; the grid is
+ *    periodic in every axis.  Mobility M = 1, so grad_d.M_d grad_d = Delta_d.
+ *  - Field arguments of the operator calls (pfc_residual, pfc_jacobian_apply, pfc_ras_apply)
+ *    are DEVICE pointers on the context's device.  pfc_step, pfc_energy and pfc_mass accept
+ *    device OR host pointers (host buffers are staged through context-owned device memory;
+ *    pinned host memory makes the copies asynchronous).  16-byte alignment is recommended:
+ *    it enables the TMA tile loads; unaligned pointers take a plain-load path.
+ *  - Ownership: the caller owns every pointer it passes; none is retained after a call
+ *    returns.  The context owns its device workspace until pfc_destroy.
+ *  - Streams: all work is enqueued on the stream given to pfc_create (NULL = legacy default
+ *    stream).  Operator calls are asynchronous; pfc_step, pfc_energy, pfc_mass synchronize
+ *    the stream because they return host scalars.
+ *  - Errors: every call returns a pfc_status; on failure nothing is partially committed
+ *    except where stated, and pfc_last_error() returns a message.  A context is not
+ *    reentrant: one host thread per context.
+ *  - No CPU fallback: every arithmetic step runs in this library's CUDA kernels (sm_100a).
+ */
+#ifndef PFC_H
+#define PFC_H
+
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PFC_ABI_VERSION 1
+
+typedef struct pfc_ctx pfc_ctx;
+typedef int pfc_status;
+
+enum {
+  PFC_OK = 0,
+  PFC_EINVAL = 1,      /* invalid argument or configuration */
+  PFC_ENOMEM = 2,      /* device allocation failed */
+  PFC_ECUDA = 3,       /* CUDA runtime/driver error (message in pfc_last_error) */
+  PFC_ENOCONV = 4,     /* Newton hit newton_maxit or the line search hit ls_min_lambda */
+  PFC_EBREAKDOWN = 5   /* non-finite residual */
+};
+
+/* Problem and solver configuration.  Defaults: pfc_config_default(). */
+typedef struct pfc_config {
+  int ndim;               /* 2 or 3 */
+  int n[3];               /* nodes per axis (n[2] ignored and set to 1 when ndim == 2) */
+  double h;               /* mesh spacing dx = dy (= dz) */
+  double gamma;           /* quench depth gamma > 0 */
+  int adaptive;           /* 1: adaptive dt, Eq. (sencondt); 0: fixed dt */
+  double dt_min, dt_max;  /* bounds of the adaptive law */
+  double eta;             /* adaptivity weight eta >= 0 */
+  double newton_rtol;     /* eps_r, stop when ||F|| <= max(eps_r ||F_0||, eps_a) */
+  double newton_atol;     /* eps_a */
+  int newton_maxit;
+  double ls_c1;           /* line search sufficient decrease ||F(Phi+lS)|| <= (1-c1 l)||F|| */
+  double ls_min_lambda;   /* smallest step length before PFC_ENOCONV */
+  int gmres_restart;      /* FGMRES restart length m (1..32) */
+  int gmres_maxit;        /* total FGMRES iterations per Newton step */
+  double gmres_rtol;      /* xi_r: ||r|| <= max(xi_r ||F||, xi_a) */
+  double gmres_atol;      /* xi_a */
+  int ras_box[3];         /* owned subdomain box Omega_k (nodes per axis); must divide n */
+  int ras_overlap;        /* overlap o in MESH LAYERS (paper's delta = o/3) */
+  int ras_local_k;        /* fixed number of local GMRES steps in each subdomain solve (1..16) */
+} pfc_config;
+
+/* Per-step report of pfc_step. */
+typedef struct pfc_step_info {
+  int newton_its;         /* Newton iterations taken */
+  int gmres_its;          /* total FGMRES iterations over the step */
+  int ls_backtracks;      /* line-search halvings over the step */
+  int converged;          /* 1 if the Newton stopping test was met */
+  double dt_used;         /* Delta t_n of this step */
+  double dt_next;         /* Delta t_{n+1} (adaptive law, or dt_used when fixed) */
+  double res0;            /* ||F(Phi_0)||, Phi_0 = phi^n */
+  double res_final;       /* ||F(Phi_final)|| */
+  double energy_old;      /* F_d(phi^n), Eq. (freeenergy) */
+  double energy;          /* F_d(phi^{n+1}) */
+  double mass;            /* h^d sum phi^{n+1} */
+  long long kernel_launches;  /* this library's kernel launches during the step */
+} pfc_step_info;
+
+/* Fill *cfg with defaults: 2D 64x64, h = pi/4, gamma = 0.25, fixed dt, eps_r = eps_a = 1e-10,
+ * 50 Newton its, c1 = 1e-4, lambda_min = 1e-12, FGMRES(30) with 300 its, xi_r = 1e-3,
+ * xi_a = 1e-11, RAS boxes 16^d, overlap 2, local k = 10. */
+void pfc_config_default(pfc_config* cfg);
+
+/* Create a context for `cfg` on the current CUDA device; `cuda_stream` is a cudaStream_t
+ * (may be NULL).  Validates (PFC_EINVAL): ndim in {2,3}; every n_d >= 4; h > 0; gamma > 0;
+ * 0 < dt_min <= dt_max when adaptive; n_d % ras_box_d == 0; 0 <= ras_overlap < ras_box_d and
+ * ras_box_d + 2 ras_overlap + 6 <= n_d (the zero ring of P:429-437 must not wrap onto the box);
+ * the ext box fits the subdomain kernel's shared-memory plan; 1 <= ras_local_k <= 16;
+ * 1 <= gmres_restart <= 32.  Allocates the Krylov workspace (2m+1 fields + 8 work fields). */
+pfc_status pfc_create(const pfc_config* cfg, void* cuda_stream, pfc_ctx** out);
+void pfc_destroy(pfc_ctx* ctx);
+
+/* Residual of Eq. (NSOP) P:257-263 with M = 1:
+ *   F = (phi_new - phi_old)/dt - Delta_d A(phi_new, phi_old),
+ *   A = [(1-gamma) + 2 Delta_d + Delta_d^2](phi_new+phi_old)/2
+ *       + (phi_new^3 + phi_new^2 phi_old + phi_new phi_old^2 + phi_old^3)/4   (Eq. discretedG)
+ * Inputs/outputs: device fields of N doubles.  F must not alias an input.  dt > 0. */
+pfc_status pfc_residual(pfc_ctx* ctx, const double* phi_new, const double* phi_old, double dt,
+                        double* F);
+
+/* Jacobian-vector product J v, J = dF/dphi_new (Eq. Jacobi):
+ *   J v = v/dt - Delta_d[ (1/2)((1-gamma) + 2 Delta_d + Delta_d^2) v + c v ],
+ *   c = (3 phi_new^2 + 2 phi_new phi_old + phi_old^2)/4.
+ * Jv must not alias an input. */
+pfc_status pfc_jacobian_apply(pfc_ctx* ctx, const double* phi_new, const double* phi_old,
+                              double dt, const double* v, double* Jv);
+
+/* Left restricted additive Schwarz preconditioner, Eq. (eq:ras) P:398-409:
+ *   z = sum_k (R_k^0)^T inv(A_k) R_k^delta v
+ * over the boxes Omega_k of cfg.ras_box (lexicographic, x fastest) extended by ras_overlap
+ * mesh layers with periodic wrap.  A_k is the Jacobian at (phi_new, phi_old, dt) restricted
+ * to the extended box with phi = 0 on the 3-layer ring outside it, which for
+ * M = 1 equals R_k^delta J (R_k^delta)^T (Eq. Ak).  inv(A_k) is a fixed-work local solve:
+ * exactly ras_local_k steps of GMRES (zero initial guess, CGS2, Givens), stopping early only
+ * on exact breakdown.  Every node of z is written by exactly one box (its owner). */
+pfc_status pfc_ras_apply(pfc_ctx* ctx, const double* phi_new, const double* phi_old, double dt,
+                         const double* v, double* z);
+
+/* One time step phi^n -> phi^{n+1} of Eq. (NSOP): inexact Newton from Phi_0 = phi^n
+ * with backtracking line search, each Newton system J S = -F solved by
+ * FGMRES(gmres_restart) right-preconditioned by pfc_ras_apply.
+ *   phi : in phi^n, out phi^{n+1} (device or host pointer; in place)
+ *   dt  : in Delta t_n; out Delta t_{n+1} = max(dt_min, dt_max/sqrt(1+eta F'^2)),
+ *         F' = (F_d^{n+1} - F_d^n)/Delta t_n (Eq. sencondt) when adaptive, else unchanged.
+ *   info: may be NULL.
+ * On PFC_ENOCONV / PFC_EBREAKDOWN phi is left unchanged (phi^n) so the caller may retry with
+ * a smaller dt; info still reports the failed attempt. */
+pfc_status pfc_step(pfc_ctx* ctx, double* phi, double* dt, pfc_step_info* info);
+
+/* Discrete free energy F_d = h^d sum G_d, Eq. (relations)-(freeenergy) P:218-233:
+ *   G_d = (1-gamma)/2 phi^2 + phi^4/4 + (Delta_d phi)^2/2 - sum_axis ((D+phi)^2 + (D-phi)^2)/2
+ * phi: device or host; *F_d: host.  Deterministic (fixed-order two-stage reduction). */
+pfc_status pfc_energy(pfc_ctx* ctx, const double* phi, double* F_d);
+
+/* Mass M = h^d sum phi (conserved by the scheme).  phi: device or host. */
+pfc_status pfc_mass(pfc_ctx* ctx, const double* phi, double* M);
+
+/* Message of the last failed call on this context ("" if none).  Valid until the next call. */
+const char* pfc_last_error(const pfc_ctx* ctx);
+
+/* Number of this library's kernel launches on this context since creation. */
+long long pfc_kernel_launches(const pfc_ctx* ctx);
+
+/* Per-kernel-class device timing (tracing aid).  When enabled, every launch is bracketed by
+ * CUDA events on the context stream (adds ~2 event records per launch); pfc_profile_query
+ * synchronizes the stream and returns, for class `cls`, the number of launches and the summed
+ * device time in milliseconds since the last pfc_profile_enable(ctx, 1) (which resets them).
+ * Classes: PFC_K_RESIDUAL, PFC_K_JV, PFC_K_RAS, PFC_K_COEF, PFC_K_ORTH (CGS2 multi-dot/axpy),
+ * PFC_K_FINALIZE (reduction finalization), PFC_K_VECTOR (axpby/lincomb/norm), PFC_K_ENERGY. */
+enum {
+  PFC_K_RESIDUAL = 0, PFC_K_JV = 1, PFC_K_RAS = 2, PFC_K_COEF = 3, PFC_K_ORTH = 4,
+  PFC_K_FINALIZE = 5, PFC_K_VECTOR = 6, PFC_K_ENERGY = 7, PFC_K_NCLASSES = 8
+};
+pfc_status pfc_profile_enable(pfc_ctx* ctx, int on);
+pfc_status pfc_profile_query(pfc_ctx* ctx, int cls, long long* count, double* total_ms);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PFC_H */

@@ -1,0 +1,255 @@
+// krylov.cu -- HBM-bound pointwise and Krylov kernels (K3, K5-K7, K9), sm_100a.
+//
+// Classical Gram-Schmidt applied twice (CGS2) for the FGMRES Arnoldi step:
+//   pass 1: h1 = V^T w                                    (k_multidot)
+//   fused : w <- w - V h1 ; h2 = V^T w                     (k_axpy_dot: V read once for both)
+//   fused : w <- w - V h2 ; |w|^2                          (k_axpy_norm)
+// Reductions are deterministic: a FIXED grid (blas_nblocks(N)) with grid-stride loops, a
+// per-block shuffle + shared-memory tree in fixed order, then k_finalize sums the per-block
+// partials in fixed order.  Results are bitwise reproducible run to run.
+#include "pfc_device.cuh"
+#include "pfc_internal.h"
+
+namespace {
+
+constexpr int NT = 256;
+
+struct Coef {
+  double c[PFC_MAX_RESTART];
+};
+
+__global__ void k_coef(const double* __restrict__ phi, const double* __restrict__ psi,
+                       double* __restrict__ c, size_t N) {
+  // J coefficient dN/dPhi = (3 Phi^2 + 2 Phi psi + psi^2)/4 (derivative of Eq. discretedG)
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < N;
+       i += (size_t)gridDim.x * blockDim.x) {
+    double a = phi[i], b = psi[i];
+    c[i] = 0.25 * (3.0 * a * a + 2.0 * a * b + b * b);
+  }
+}
+
+__global__ void k_axpby(double a, const double* x, double b, const double* y, double* out,
+                        size_t N) {   // out may alias x or y (elementwise)
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < N;
+       i += (size_t)gridDim.x * blockDim.x) {
+    double yi = y ? y[i] : 0.0;
+    out[i] = a * x[i] + b * yi;
+  }
+}
+
+template <int NV>
+__global__ void __launch_bounds__(NT) k_multidot(const double* __restrict__ V, size_t ldv,
+                                                 const double* __restrict__ w, size_t N,
+                                                 double* __restrict__ partials) {
+  __shared__ double red[32 * NV];
+  __shared__ double outv[NV];
+  double acc[NV];
+#pragma unroll
+  for (int k = 0; k < NV; ++k) acc[k] = 0.0;
+  for (size_t i = blockIdx.x * (size_t)NT + threadIdx.x; i < N; i += (size_t)gridDim.x * NT) {
+    double wi = w[i];
+#pragma unroll
+    for (int k = 0; k < NV; ++k) acc[k] += V[k * ldv + i] * wi;
+  }
+  block_sum_multi<NV>(acc, red, outv);
+  if (threadIdx.x < NV) partials[blockIdx.x * NV + threadIdx.x] = outv[threadIdx.x];
+}
+
+template <int NV>
+__global__ void __launch_bounds__(NT) k_axpy_dot(const double* __restrict__ V, size_t ldv,
+                                                 const double* __restrict__ h,
+                                                 double* __restrict__ w, size_t N,
+                                                 double* __restrict__ partials) {
+  __shared__ double red[32 * NV];
+  __shared__ double outv[NV];
+  double hk[NV], acc[NV];
+#pragma unroll
+  for (int k = 0; k < NV; ++k) { hk[k] = h[k]; acc[k] = 0.0; }
+  for (size_t i = blockIdx.x * (size_t)NT + threadIdx.x; i < N; i += (size_t)gridDim.x * NT) {
+    double v[NV];
+    double wi = w[i];
+#pragma unroll
+    for (int k = 0; k < NV; ++k) { v[k] = V[k * ldv + i]; wi -= hk[k] * v[k]; }
+    w[i] = wi;
+#pragma unroll
+    for (int k = 0; k < NV; ++k) acc[k] += v[k] * wi;
+  }
+  block_sum_multi<NV>(acc, red, outv);
+  if (threadIdx.x < NV) partials[blockIdx.x * NV + threadIdx.x] = outv[threadIdx.x];
+}
+
+template <int NV>
+__global__ void __launch_bounds__(NT) k_axpy_norm(const double* __restrict__ V, size_t ldv,
+                                                  const double* __restrict__ h,
+                                                  double* __restrict__ w, size_t N,
+                                                  double* __restrict__ partials) {
+  __shared__ double red[32];
+  __shared__ double outv[1];
+  double hk[NV];
+#pragma unroll
+  for (int k = 0; k < NV; ++k) hk[k] = h[k];
+  double acc[1] = {0.0};
+  for (size_t i = blockIdx.x * (size_t)NT + threadIdx.x; i < N; i += (size_t)gridDim.x * NT) {
+    double wi = w[i];
+#pragma unroll
+    for (int k = 0; k < NV; ++k) wi -= hk[k] * V[k * ldv + i];
+    w[i] = wi;
+    acc[0] += wi * wi;
+  }
+  block_sum_multi<1>(acc, red, outv);
+  if (threadIdx.x == 0) partials[blockIdx.x] = outv[0];
+}
+
+__global__ void __launch_bounds__(NT) k_norm2(const double* __restrict__ x, size_t N,
+                                              double* __restrict__ partials) {
+  __shared__ double red[32];
+  __shared__ double outv[1];
+  double acc[1] = {0.0};
+  for (size_t i = blockIdx.x * (size_t)NT + threadIdx.x; i < N; i += (size_t)gridDim.x * NT)
+    acc[0] += x[i] * x[i];
+  block_sum_multi<1>(acc, red, outv);
+  if (threadIdx.x == 0) partials[blockIdx.x] = outv[0];
+}
+
+// out[v] = sum_b partials[b*nval + v], fixed order; one CTA per value
+__global__ void __launch_bounds__(NT) k_finalize(const double* __restrict__ partials, int nblk,
+                                                 int nval, double* __restrict__ out) {
+  __shared__ double red[32];
+  __shared__ double outv[1];
+  const int v = blockIdx.x;
+  double acc[1] = {0.0};
+  for (int b = threadIdx.x; b < nblk; b += NT) acc[0] += partials[(size_t)b * nval + v];
+  block_sum_multi<1>(acc, red, outv);
+  if (threadIdx.x == 0) out[v] = outv[0];
+}
+
+template <int NV>
+__global__ void __launch_bounds__(NT) k_lincomb(double* __restrict__ x,
+                                                const double* __restrict__ Z, size_t ldz,
+                                                Coef coef, size_t N) {
+  for (size_t i = blockIdx.x * (size_t)NT + threadIdx.x; i < N; i += (size_t)gridDim.x * NT) {
+    double s = x[i];
+#pragma unroll
+    for (int k = 0; k < NV; ++k) s += coef.c[k] * Z[k * ldz + i];
+    x[i] = s;
+  }
+}
+
+#define PFC_NV_CASES(X) \
+  X(1) X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(9) X(10) X(11) X(12) X(13) X(14) X(15) X(16) \
+  X(17) X(18) X(19) X(20) X(21) X(22) X(23) X(24) X(25) X(26) X(27) X(28) X(29) X(30) X(31) X(32)
+
+}  // namespace
+
+int blas_nblocks(size_t N) {
+  size_t b = (N + 4 * NT - 1) / (4 * NT);   // >= 4 elements per thread
+  if (b > 148 * 8) b = 148 * 8;
+  if (b < 1) b = 1;
+  return (int)b;
+}
+
+static int grid_pointwise(size_t N) {
+  size_t b = (N + NT - 1) / NT;
+  if (b > 148 * 16) b = 148 * 16;
+  return (int)(b < 1 ? 1 : b);
+}
+
+cudaError_t launch_coef(pfc_ctx* ctx, const double* phi, const double* psi, double* c) {
+  k_coef<<<grid_pointwise(ctx->N), NT, 0, ctx->stream>>>(phi, psi, c, ctx->N);
+  ctx->launches++;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_axpby(pfc_ctx* ctx, double a, const double* x, double b, const double* y,
+                         double* out) {
+  k_axpby<<<grid_pointwise(ctx->N), NT, 0, ctx->stream>>>(a, x, b, y, out, ctx->N);
+  ctx->launches++;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_multidot(pfc_ctx* ctx, const double* V, int nv, const double* w,
+                            double* partials) {
+  const int nb = blas_nblocks(ctx->N);
+  switch (nv) {
+#define X(K)                                                                        \
+  case K:                                                                           \
+    k_multidot<K><<<nb, NT, 0, ctx->stream>>>(V, ctx->N, w, ctx->N, partials);      \
+    break;
+    PFC_NV_CASES(X)
+#undef X
+    default: return cudaErrorInvalidValue;
+  }
+  ctx->launches++;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_axpy_dot(pfc_ctx* ctx, const double* V, int nv, const double* h, double* w,
+                            double* partials) {
+  const int nb = blas_nblocks(ctx->N);
+  switch (nv) {
+#define X(K)                                                                          \
+  case K:                                                                             \
+    k_axpy_dot<K><<<nb, NT, 0, ctx->stream>>>(V, ctx->N, h, w, ctx->N, partials);     \
+    break;
+    PFC_NV_CASES(X)
+#undef X
+    default: return cudaErrorInvalidValue;
+  }
+  ctx->launches++;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_axpy_norm(pfc_ctx* ctx, const double* V, int nv, const double* h, double* w,
+                             double* partials) {
+  const int nb = blas_nblocks(ctx->N);
+  switch (nv) {
+#define X(K)                                                                           \
+  case K:                                                                              \
+    k_axpy_norm<K><<<nb, NT, 0, ctx->stream>>>(V, ctx->N, h, w, ctx->N, partials);     \
+    break;
+    PFC_NV_CASES(X)
+#undef X
+    default: return cudaErrorInvalidValue;
+  }
+  ctx->launches++;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_norm2(pfc_ctx* ctx, const double* x, double* partials) {
+  k_norm2<<<blas_nblocks(ctx->N), NT, 0, ctx->stream>>>(x, ctx->N, partials);
+  ctx->launches++;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_finalize(pfc_ctx* ctx, const double* partials, int nblk, int nval,
+                            double* out) {
+  k_finalize<<<nval, NT, 0, ctx->stream>>>(partials, nblk, nval, out);
+  ctx->launches++;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_lincomb(pfc_ctx* ctx, double* x, const double* Z, int nv, const double* coef) {
+  if (nv <= 0) return cudaSuccess;
+  Coef cf;
+  for (int k = 0; k < PFC_MAX_RESTART; ++k) cf.c[k] = k < nv ? coef[k] : 0.0;
+  const int nb = blas_nblocks(ctx->N);
+  // chunks of <= 32 vectors (gmres_restart <= 64)
+  int done = 0;
+  while (done < nv) {
+    int k = nv - done > 32 ? 32 : nv - done;
+    Coef cc;
+    for (int i = 0; i < PFC_MAX_RESTART; ++i) cc.c[i] = i < k ? cf.c[done + i] : 0.0;
+    const double* Zk = Z + (size_t)done * ctx->N;
+    switch (k) {
+#define X(K)                                                                    \
+  case K:                                                                       \
+    k_lincomb<K><<<nb, NT, 0, ctx->stream>>>(x, Zk, ctx->N, cc, ctx->N);        \
+    break;
+      PFC_NV_CASES(X)
+#undef X
+    }
+    ctx->launches++;
+    done += k;
+  }
+  return cudaGetLastError();
+}

@@ -1,0 +1,104 @@
+// pfc_internal.h -- context layout and kernel launchers of libpfc.so (not part of the ABI).
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/pfc.h"
+
+#define PFC_MAX_RESTART 32
+#define PFC_MAX_LOCAL_K 16
+
+struct pfc_ctx {
+  pfc_config cfg;
+  cudaStream_t stream = nullptr;
+  int device = 0;
+  size_t N = 0;
+  double ih2 = 0.0;        // 1/h^2
+  double hd = 0.0;         // h^d (cell volume)
+
+  // device workspace (N doubles each unless noted)
+  double* phi = nullptr;   // Phi_m (Newton iterate)
+  double* psi = nullptr;   // phi^n
+  double* F = nullptr;     // residual at Phi_m
+  double* Ft = nullptr;    // residual at a line-search trial
+  double* trial = nullptr; // Phi_m + lambda S
+  double* S = nullptr;     // Newton direction
+  double* c = nullptr;     // Jacobian coefficient (3Phi^2 + 2Phi psi + psi^2)/4
+  double* w = nullptr;     // Arnoldi work vector
+  double* V = nullptr;     // (m+1) N  Krylov basis
+  double* Z = nullptr;     // m N      preconditioned basis (flexible GMRES)
+  double* ras_scratch = nullptr;  // 3D subdomain-solve scratch (L2-resident)
+  double* stage = nullptr;     // staging field for host-pointer calls
+  double* partials = nullptr;  // reduction scratch
+  size_t npartials = 0;
+  double* dscal = nullptr;     // device scalars: [0,64) h1, [64,128) h2, [128] |w|^2, ...
+  double* hscal = nullptr;     // pinned host mirror of dscal
+
+  // RAS launch plan
+  int ras_smem = 0;
+  int ras_threads = 0;
+  int ras_cluster = 1;
+
+  long long launches = 0;
+  std::string err;
+
+  // profiling (pfc_profile_enable): event pairs per launch, accumulated per kernel class
+  bool prof = false;
+  std::vector<cudaEvent_t> ev_pool;
+  struct Pending { int cls; cudaEvent_t a, b; };
+  std::vector<Pending> pending;
+  cudaEvent_t ev_open = nullptr;
+  long long prof_count[PFC_K_NCLASSES] = {0};
+  double prof_ms[PFC_K_NCLASSES] = {0};
+};
+
+// set ctx->err and return the status
+pfc_status pfc_fail(pfc_ctx* ctx, pfc_status st, const std::string& msg);
+pfc_status pfc_check_cuda(pfc_ctx* ctx, cudaError_t e, const char* where);
+
+// ---------------------------------------------------------------- launchers (return cudaError)
+// stencils (2D/3D dispatched on ctx->cfg.ndim)
+cudaError_t launch_residual(pfc_ctx* ctx, const double* phi_new, const double* phi_old, double dt,
+                            double* F, double* norm_partials, int* nparts);
+cudaError_t launch_jv(pfc_ctx* ctx, const double* v, const double* c, double dt, double* out);
+cudaError_t launch_energy_mass(pfc_ctx* ctx, const double* phi, double* partials, int* nparts);
+cudaError_t launch_ras(pfc_ctx* ctx, const double* v, const double* c, double dt, double* z);
+int ras_plan(pfc_ctx* ctx);   // fills ras_smem/threads/cluster; returns 0 if infeasible
+
+// per-dimension kernels
+cudaError_t launch_residual_2d(pfc_ctx*, const double*, const double*, double, double*, double*,
+                               int*);
+cudaError_t launch_residual_3d(pfc_ctx*, const double*, const double*, double, double*, double*,
+                               int*);
+cudaError_t launch_jv_2d(pfc_ctx*, const double*, const double*, double, double*);
+cudaError_t launch_jv_3d(pfc_ctx*, const double*, const double*, double, double*);
+int ras2d_plan(pfc_ctx* ctx);
+int ras3d_plan(pfc_ctx* ctx);
+size_t ras3d_scratch_doubles(pfc_ctx* ctx, int* grid);
+cudaError_t launch_ras_2d(pfc_ctx*, const double* v, const double* c, double dt, double* z);
+cudaError_t launch_ras_3d(pfc_ctx*, const double* v, const double* c, double dt, double* z,
+                          double* scratch);
+
+// Krylov / pointwise (krylov.cu)
+int blas_nblocks(size_t N);
+cudaError_t launch_coef(pfc_ctx* ctx, const double* phi, const double* psi, double* c);
+cudaError_t launch_axpby(pfc_ctx* ctx, double a, const double* x, double b, const double* y,
+                         double* out);
+cudaError_t launch_multidot(pfc_ctx* ctx, const double* V, int nv, const double* w,
+                            double* partials);
+cudaError_t launch_axpy_dot(pfc_ctx* ctx, const double* V, int nv, const double* h, double* w,
+                            double* partials);
+cudaError_t launch_axpy_norm(pfc_ctx* ctx, const double* V, int nv, const double* h, double* w,
+                             double* partials);
+cudaError_t launch_norm2(pfc_ctx* ctx, const double* x, double* partials);
+cudaError_t launch_finalize(pfc_ctx* ctx, const double* partials, int nblk, int nval,
+                            double* out);
+cudaError_t launch_lincomb(pfc_ctx* ctx, double* x, const double* Z, int nv, const double* coef);
+
+// TMA descriptor encoding through the driver entry point (no libcuda link dependency)
+bool tma_encode(CUtensorMap* map, const double* ptr, int ndim, const int* n, const int* box);
+bool tma_usable(const void* ptr);

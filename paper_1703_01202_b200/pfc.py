@@ -1,0 +1,209 @@
+"""Thin ctypes binding of libpfc.so (include/pfc.h).  Argument marshalling only: every step
+of the hot path runs in the library's CUDA kernels.  PyTorch supplies device memory and the
+stream.  There is no fallback: if libpfc.so is missing or no GPU is present, calls raise.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "lib", "libpfc.so")
+
+PFC_OK, PFC_EINVAL, PFC_ENOMEM, PFC_ECUDA, PFC_ENOCONV, PFC_EBREAKDOWN = range(6)
+STATUS = {0: "PFC_OK", 1: "PFC_EINVAL", 2: "PFC_ENOMEM", 3: "PFC_ECUDA", 4: "PFC_ENOCONV",
+          5: "PFC_EBREAKDOWN"}
+
+EXPORTS = ["pfc_config_default", "pfc_create", "pfc_destroy", "pfc_residual",
+           "pfc_jacobian_apply", "pfc_ras_apply", "pfc_step", "pfc_energy", "pfc_mass",
+           "pfc_last_error", "pfc_kernel_launches", "pfc_profile_enable", "pfc_profile_query"]
+
+KERNEL_CLASSES = ["residual", "jv", "ras", "coef", "orth", "finalize", "vector", "energy"]
+
+
+class PfcConfig(C.Structure):
+    _fields_ = [("ndim", C.c_int), ("n", C.c_int * 3), ("h", C.c_double), ("gamma", C.c_double),
+                ("adaptive", C.c_int), ("dt_min", C.c_double), ("dt_max", C.c_double),
+                ("eta", C.c_double), ("newton_rtol", C.c_double), ("newton_atol", C.c_double),
+                ("newton_maxit", C.c_int), ("ls_c1", C.c_double), ("ls_min_lambda", C.c_double),
+                ("gmres_restart", C.c_int), ("gmres_maxit", C.c_int),
+                ("gmres_rtol", C.c_double), ("gmres_atol", C.c_double),
+                ("ras_box", C.c_int * 3), ("ras_overlap", C.c_int), ("ras_local_k", C.c_int)]
+
+
+class PfcStepInfo(C.Structure):
+    _fields_ = [("newton_its", C.c_int), ("gmres_its", C.c_int), ("ls_backtracks", C.c_int),
+                ("converged", C.c_int), ("dt_used", C.c_double), ("dt_next", C.c_double),
+                ("res0", C.c_double), ("res_final", C.c_double), ("energy_old", C.c_double),
+                ("energy", C.c_double), ("mass", C.c_double), ("kernel_launches", C.c_longlong)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+class PfcError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"{STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+_lib = None
+
+
+def load():
+    """Load libpfc.so (built in-tree by paper_1703_01202_b200.build).  Raises if absent."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is not built; run paper_1703_01202_b200.build.build() "
+                          "(there is no CPU fallback)")
+    L = C.CDLL(LIB_PATH)
+    vp, dp = C.c_void_p, C.c_void_p
+    L.pfc_config_default.argtypes = [C.POINTER(PfcConfig)]
+    L.pfc_create.argtypes = [C.POINTER(PfcConfig), vp, C.POINTER(vp)]
+    L.pfc_destroy.argtypes = [vp]
+    L.pfc_residual.argtypes = [vp, dp, dp, C.c_double, dp]
+    L.pfc_jacobian_apply.argtypes = [vp, dp, dp, C.c_double, dp, dp]
+    L.pfc_ras_apply.argtypes = [vp, dp, dp, C.c_double, dp, dp]
+    L.pfc_step.argtypes = [vp, dp, C.POINTER(C.c_double), C.POINTER(PfcStepInfo)]
+    L.pfc_energy.argtypes = [vp, dp, C.POINTER(C.c_double)]
+    L.pfc_mass.argtypes = [vp, dp, C.POINTER(C.c_double)]
+    L.pfc_last_error.argtypes = [vp]
+    L.pfc_last_error.restype = C.c_char_p
+    L.pfc_kernel_launches.argtypes = [vp]
+    L.pfc_kernel_launches.restype = C.c_longlong
+    L.pfc_profile_enable.argtypes = [vp, C.c_int]
+    L.pfc_profile_enable.restype = C.c_int
+    L.pfc_profile_query.argtypes = [vp, C.c_int, C.POINTER(C.c_longlong), C.POINTER(C.c_double)]
+    L.pfc_profile_query.restype = C.c_int
+    for name in ("pfc_create", "pfc_residual", "pfc_jacobian_apply", "pfc_ras_apply", "pfc_step",
+                 "pfc_energy", "pfc_mass"):
+        getattr(L, name).restype = C.c_int
+    _lib = L
+    return L
+
+
+def make_config(cfg=None, **over) -> PfcConfig:
+    """pfc_config from a paper_1703_01202_b200.inputs.PFCConfig and/or keyword overrides."""
+    L = load()
+    c = PfcConfig()
+    L.pfc_config_default(C.byref(c))
+    kw = {}
+    if cfg is not None:
+        kw = dict(ndim=cfg.ndim, n=cfg.n, h=cfg.h, gamma=cfg.gamma, adaptive=int(cfg.adaptive),
+                  dt_min=cfg.dt_min, dt_max=cfg.dt_max, eta=cfg.eta,
+                  newton_rtol=cfg.newton_rtol, newton_atol=cfg.newton_atol,
+                  newton_maxit=cfg.newton_maxit, gmres_restart=cfg.gmres_restart,
+                  gmres_maxit=cfg.gmres_maxit, gmres_rtol=cfg.gmres_rtol,
+                  gmres_atol=cfg.gmres_atol, ras_box=cfg.ras_box, ras_overlap=cfg.ras_overlap,
+                  ras_local_k=cfg.ras_local_k)
+    kw.update(over)
+    for k, v in kw.items():
+        if k in ("n", "ras_box"):
+            v = list(v) + [1] * (3 - len(v))
+            setattr(c, k, (C.c_int * 3)(*v))
+        else:
+            setattr(c, k, v)
+    return c
+
+
+def _ptr(t):
+    return C.c_void_p(t.data_ptr())
+
+
+class Context:
+    """One pfc_ctx on the current CUDA device and torch's current stream."""
+
+    def __init__(self, cfg=None, stream=None, **over):
+        import torch
+        self.L = load()
+        self.config = make_config(cfg, **over)
+        if stream is None:
+            stream = torch.cuda.current_stream()
+        self.stream = stream
+        h = C.c_void_p()
+        st = self.L.pfc_create(C.byref(self.config), C.c_void_p(stream.cuda_stream), C.byref(h))
+        self._h = h
+        if st != PFC_OK:
+            msg = self.L.pfc_last_error(h).decode() if h.value else ""
+            self.close()
+            raise PfcError(st, msg)
+
+    def close(self):
+        if getattr(self, "_h", None) is not None and self._h.value:
+            self.L.pfc_destroy(self._h)
+        self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _check(self, st):
+        if st != PFC_OK:
+            raise PfcError(st, self.L.pfc_last_error(self._h).decode())
+
+    @property
+    def launches(self) -> int:
+        return self.L.pfc_kernel_launches(self._h)
+
+    def profile(self, on=True):
+        """Enable/disable (and reset) per-kernel-class CUDA-event timing."""
+        self._check(self.L.pfc_profile_enable(self._h, int(on)))
+
+    def profile_report(self):
+        """{class: (launches, total device ms)} since the last profile(True)."""
+        out = {}
+        for i, name in enumerate(KERNEL_CLASSES):
+            n, ms = C.c_longlong(), C.c_double()
+            self._check(self.L.pfc_profile_query(self._h, i, C.byref(n), C.byref(ms)))
+            out[name] = (n.value, ms.value)
+        return out
+
+    def residual(self, phi_new, phi_old, dt, out=None):
+        import torch
+        out = torch.empty_like(phi_new) if out is None else out
+        self._check(self.L.pfc_residual(self._h, _ptr(phi_new), _ptr(phi_old), dt, _ptr(out)))
+        return out
+
+    def jacobian_apply(self, phi_new, phi_old, dt, v, out=None):
+        import torch
+        out = torch.empty_like(v) if out is None else out
+        self._check(self.L.pfc_jacobian_apply(self._h, _ptr(phi_new), _ptr(phi_old), dt, _ptr(v),
+                                              _ptr(out)))
+        return out
+
+    def ras_apply(self, phi_new, phi_old, dt, v, out=None):
+        import torch
+        out = torch.empty_like(v) if out is None else out
+        self._check(self.L.pfc_ras_apply(self._h, _ptr(phi_new), _ptr(phi_old), dt, _ptr(v),
+                                         _ptr(out)))
+        return out
+
+    def step(self, phi, dt):
+        """In-place phi^n -> phi^{n+1}; returns (dt_next, info dict).  phi: CUDA or CPU tensor."""
+        d = C.c_double(dt)
+        info = PfcStepInfo()
+        self._check(self.L.pfc_step(self._h, _ptr(phi), C.byref(d), C.byref(info)))
+        return d.value, info.as_dict()
+
+    def try_step(self, phi, dt):
+        """Like step() but returns (status, dt_next, info) instead of raising on ENOCONV."""
+        d = C.c_double(dt)
+        info = PfcStepInfo()
+        st = self.L.pfc_step(self._h, _ptr(phi), C.byref(d), C.byref(info))
+        if st not in (PFC_OK, PFC_ENOCONV, PFC_EBREAKDOWN):
+            self._check(st)
+        return st, d.value, info.as_dict()
+
+    def energy(self, phi) -> float:
+        out = C.c_double()
+        self._check(self.L.pfc_energy(self._h, _ptr(phi), C.byref(out)))
+        return out.value
+
+    def mass(self, phi) -> float:
+        out = C.c_double()
+        self._check(self.L.pfc_mass(self._h, _ptr(phi), C.byref(out)))
+        return out.value

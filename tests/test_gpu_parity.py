@@ -1,0 +1,243 @@
+"""GPU parity of the CUDA path (through the C ABI) against the CPU oracle (-m gpu).
+
+Tolerances (BASELINE.json north_star): per-operator outputs rel L2 <= 1e-12
+(fp64), fields after one step rel L2 <= 1e-10 and after N steps <= 1e-8 with Newton
+rtol 1e-10.  Inputs come only from paper_1703_01202_b200.inputs (seeded); expected values
+only from the oracle.
+"""
+import math
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from oracle import oracle as O  # noqa: E402
+from paper_1703_01202_b200 import build as B  # noqa: E402
+from paper_1703_01202_b200 import pfc as P  # noqa: E402
+from paper_1703_01202_b200.inputs import CONFIGS, PFCConfig, random_field  # noqa: E402
+
+H = math.pi / 4
+G = 0.25
+
+
+def rel(a, b):
+    a = np.asarray(a).ravel(); b = np.asarray(b).ravel()
+    return np.linalg.norm(a - b) / np.linalg.norm(b)
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    B.build()
+    yield
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def host(t):
+    torch.cuda.synchronize()
+    return t.cpu().numpy()
+
+
+def ctx_for(shape, box, o=2, k=10, **kw):
+    nd = len(shape)
+    b = list(box) + [1] * (3 - len(box))
+    return P.Context(None, ndim=nd, n=shape, h=H, gamma=G, ras_box=b, ras_overlap=o,
+                     ras_local_k=k, **kw)
+
+
+# (shape, ras box) pairs: several tiles, ragged tails (x not a multiple of 32, y not of 16),
+# an odd x extent (plain-load path), a grid smaller than one tile, and the config sizes.
+OPERATOR_CASES = [
+    ((64, 64), (16, 16)),
+    ((100, 36), (10, 12)),
+    ((45, 27), (15, 9)),
+    ((12, 12), (4, 4)),
+    ((1024, 1024), (32, 32)),
+    ((2048, 2048), (32, 32)),
+    ((32, 32, 32), (16, 16, 16)),
+    ((40, 24, 20), (8, 8, 4)),
+    ((27, 21, 15), (9, 7, 3)),
+    ((128, 128, 128), (16, 16, 16)),
+]
+
+
+@pytest.mark.parametrize("shape,box", OPERATOR_CASES)
+def test_residual_jacobian_energy_parity(shape, box):
+    phi = random_field(shape, 101, 0.0, 1.0)
+    psi = random_field(shape, 102, 0.0, 1.0)
+    v = random_field(shape, 103, 0.0, 1.0)
+    dt = 0.5
+    ctx = ctx_for(shape, box, o=1 if min(box) < 8 else 2)
+    F = host(ctx.residual(dev(phi), dev(psi), dt))
+    assert rel(F, O.residual(phi, psi, H, G, dt)) <= 1e-12
+    Jv = host(ctx.jacobian_apply(dev(phi), dev(psi), dt, dev(v)))
+    assert rel(Jv, O.jacobian_apply(phi, psi, v, H, G, dt)) <= 1e-12
+    Fd = ctx.energy(dev(phi))
+    M = ctx.mass(dev(phi))
+    assert abs(Fd - O.free_energy(phi, H, G)) <= 1e-12 * abs(O.free_energy(phi, H, G))
+    Mo = O.mass(phi, H)
+    assert abs(M - Mo) <= 1e-12 * np.sum(np.abs(phi)) * H ** len(shape)
+
+
+@pytest.mark.parametrize("name", ["cfg1", "cfg2", "cfg3", "cfg4"])
+def test_operator_parity_on_config_ics(name):
+    """Each config's own initial condition as Phi with psi = IC + perturbation (R20: inputs
+    where F is O(terms), not the rounding noise of a converged iterate)."""
+    cfg = CONFIGS[name]
+    ic = cfg.initial_condition()
+    pert = random_field(cfg.n, 7, 0.0, 0.01)
+    ctx = P.Context(cfg)
+    dt = cfg.dt0
+    F = host(ctx.residual(dev(ic + pert), dev(ic), dt))
+    assert rel(F, O.residual(ic + pert, ic, H, G, dt)) <= 1e-12
+    Jv = host(ctx.jacobian_apply(dev(ic + pert), dev(ic), dt, dev(pert)))
+    assert rel(Jv, O.jacobian_apply(ic + pert, ic, pert, H, G, dt)) <= 1e-12
+
+
+def test_operator_parity_512cubed_sampled():
+    """Config-5 size: full-field oracle on 512^3 (1 GiB/field) in the launch configuration
+    the bench times."""
+    shape = (512, 512, 512)
+    phi = random_field(shape, 5, -0.35, 0.05)
+    v = random_field(shape, 55, 0.0, 1.0)
+    ctx = ctx_for(shape, (16, 16, 16), gmres_restart=2)
+    dphi, dv = dev(phi), dev(v)
+    Jv = host(ctx.jacobian_apply(dphi, dphi, 1.0, dv))
+    ref = O.jacobian_apply(phi, phi, v, H, G, 1.0)
+    assert rel(Jv, ref) <= 1e-12
+    del ref, Jv
+    psi = random_field(shape, 6, -0.35, 0.05)
+    F = host(ctx.residual(dphi, dev(psi), 1.0))
+    assert rel(F, O.residual(phi, psi, H, G, 1.0)) <= 1e-12
+
+
+RAS_CASES = [
+    ((64, 64), (16, 16), 2, 10),
+    ((128, 128), (32, 32), 2, 10),
+    ((128, 128), (32, 32), 3, 10),
+    ((128, 128), (32, 32), 4, 10),
+    ((48, 36), (12, 12), 1, 5),
+    ((32, 32, 32), (16, 16, 16), 2, 10),
+    ((24, 24, 20), (8, 8, 10), 1, 4),
+]
+
+
+@pytest.mark.parametrize("shape,box,o,k", RAS_CASES)
+def test_ras_apply_parity(shape, box, o, k):
+    phi = random_field(shape, 201, 0.07, 0.07)
+    psi = random_field(shape, 202, 0.07, 0.07)
+    v = random_field(shape, 203, 0.0, 1.0)
+    dt = 0.5
+    ctx = ctx_for(shape, box, o=o, k=k)
+    z = host(ctx.ras_apply(dev(phi), dev(psi), dt, dev(v)))
+    prm = O.params(gamma=G, ras_box=box, ras_overlap=o, ras_local_k=k)
+    zo = O.ras_apply(phi, psi, v, H, prm, dt)
+    assert rel(z, zo) <= 1e-12
+
+
+def test_ras_apply_parity_cfg2_full_size():
+    cfg = CONFIGS["cfg2"]
+    ic = cfg.initial_condition()
+    v = random_field(cfg.n, 9, 0.0, 1.0)
+    ctx = P.Context(cfg)
+    z = host(ctx.ras_apply(dev(ic), dev(ic), 0.01, dev(v)))
+    zo = O.ras_apply(ic, ic, v, H, O.params_from_config(cfg), 0.01)
+    assert rel(z, zo) <= 1e-12
+
+
+def _run_gpu(cfg, phi0, steps):
+    ctx = P.Context(cfg)
+    phi = dev(phi0)
+    dt = cfg.dt0
+    infos = []
+    for _ in range(steps):
+        dt, info = ctx.step(phi, dt)
+        infos.append(info)
+    return host(phi), infos
+
+
+def test_cfg1_one_step_and_20_step_parity():
+    cfg = CONFIGS["cfg1"]
+    phi0 = cfg.initial_condition()
+    one, _ = _run_gpu(cfg, phi0, 1)
+    ref1, hist1 = O.run(cfg, phi0, 1)
+    assert rel(one, ref1) <= 1e-10
+    full, infos = _run_gpu(cfg, phi0, cfg.steps)
+    ref, hist = O.run(cfg, phi0, cfg.steps)
+    assert rel(full, ref) <= 1e-8
+    # energy non-increasing, mass conserved to the Newton tolerance
+    E = [i["energy"] for i in infos]
+    assert all(E[i + 1] <= E[i] + 1e-12 * abs(E[i]) for i in range(len(E) - 1))
+    assert all(i["converged"] == 1 for i in infos)
+    m0 = O.mass(phi0, H)
+    assert abs(infos[-1]["mass"] - m0) <= 1e-6 * abs(m0)
+    # energy log matches the oracle's
+    for i, row in zip(infos, hist):
+        assert abs(i["energy"] - row[3]) <= 1e-9 * abs(row[3])
+
+
+def test_cfg2_one_step_parity_adaptive():
+    """Config 2 (1024^2, adaptive dt from dt_min, R11): first steps vs the oracle."""
+    cfg = CONFIGS["cfg2"]
+    phi0 = cfg.initial_condition()
+    ctx = P.Context(cfg)
+    phi = dev(phi0)
+    dt = cfg.dt0
+    dt1, info = ctx.step(phi, dt)
+    ref, hist = O.run(cfg, phi0, 1)
+    assert rel(host(phi), ref) <= 1e-10
+    Fn = O.free_energy(phi0, H, G)
+    assert abs(dt1 - O.next_dt(cfg.dt_min, cfg.dt_max, cfg.eta, hist[0][3], Fn, dt)) <= 1e-9 * dt1
+
+
+def test_cfg4_3d_one_step_parity_small():
+    """3D path (config-4 IC law and solver settings) on 32^3 with 16^3 boxes: 2 steps."""
+    base = CONFIGS["cfg4"]
+    cfg = PFCConfig("cfg4_small", 3, (32, 32, 32), adaptive=True, dt0=0.5, dt_min=0.5,
+                    dt_max=10.0, eta=500.0, ras_box=(16, 16, 16),
+                    ic=dict(base.ic), seed=4)
+    phi0 = cfg.initial_condition()
+    out, infos = _run_gpu(cfg, phi0, 2)
+    ref, hist = O.run(cfg, phi0, 2)
+    assert rel(out, ref) <= 1e-10
+
+
+def test_step_host_pointer_matches_device_and_is_deterministic():
+    cfg = CONFIGS["cfg1"]
+    phi0 = cfg.initial_condition()
+    ctx = P.Context(cfg)
+    a = dev(phi0)
+    ctx.step(a, 0.5)
+    b = torch.from_numpy(phi0.copy()).pin_memory()
+    ctx.step(b, 0.5)
+    c = dev(phi0)
+    ctx.step(c, 0.5)
+    assert torch.equal(a.cpu(), b)           # host staging path == device path, bitwise
+    assert torch.equal(a, c)                 # run-to-run bitwise determinism
+
+
+def test_operator_argument_errors():
+    ctx = ctx_for((64, 64), (16, 16))
+    x = dev(random_field((64, 64), 1))
+    with pytest.raises(P.PfcError) as e:
+        ctx.residual(x, x, -1.0)
+    assert e.value.status == P.PFC_EINVAL
+    with pytest.raises(P.PfcError) as e:
+        ctx.residual(x, x, 0.5, out=x)
+    assert e.value.status == P.PFC_EINVAL
+    with pytest.raises(P.PfcError) as e:
+        ctx.residual(x.cpu(), x, 0.5)
+    assert e.value.status == P.PFC_EINVAL
+
+
+def test_constant_state_is_a_fixed_point():
+    ctx = ctx_for((64, 64), (16, 16))
+    phi = torch.full((64, 64), 0.07, dtype=torch.float64, device="cuda")
+    dt, info = ctx.step(phi, 0.5)
+    assert info["newton_its"] == 0 and torch.all(phi == 0.07)
