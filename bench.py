@@ -1,0 +1,343 @@
+#!/usr/bin/env python
+"""Benchmark of the DVD-PFC Newton-Krylov-Schwarz time step on B200.
+
+Metric (BASELINE.json): "PFC time steps/sec and Jacobian-apply HBM GB/s (fp64, 1 B200)".
+  value  = whole-job time steps per second on config 2 (1024^2, adaptive dt from dt_min,
+           RAS 32^2 boxes, overlap 2): W untimed steps from the seeded IC, then K timed steps,
+           device pointers, CUDA events on the library's stream, barrier + sync both sides.
+  e2e    = the same steps through the C ABI with a pinned HOST buffer (H2D of phi^n and D2H of
+           phi^{n+1} inside every timed step).
+  roofline = the dominant kernel class of the step (library-side CUDA-event profile pass).
+  jacobian_apply = isolated J v on 512^3 (config-5 size, 3 GiB algorithmic per apply > L2).
+  cpu_baseline = the oracle on this host, bounded sample (rank 0, N=1 only).
+  --impl reference: the oracle arm (rank 0 only) on the same config/metric/unit.
+Multi-GPU (torchrun): independent replicas, one per GPU (the north star allows no multi-GPU
+data path); torch.distributed is used only for the barrier and the max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "PFC time steps/sec and Jacobian-apply HBM GB/s (fp64, 1 B200)"
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d.get("hbm_gbs", 6650.0), "measured"
+    return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clock/throttle samples every 200 ms during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        self.p = None
+
+    def __enter__(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "200"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except OSError:
+            self.p = None
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *a):
+        if self.p:
+            self.p.terminate()
+            self.p.wait()
+
+    def summary(self):
+        self.f.flush()
+        rows = []
+        for line in open(self.f.name):
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) == 6 and parts[0].replace(".", "").isdigit():
+                rows.append(parts)
+        os.unlink(self.f.name)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        sm = [float(r[0]) for r in rows]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[2 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": float(rows[0][1]),
+                "reasons": reasons, "samples": len(rows)}
+
+
+def run_steps(ctx, phi, dt, k):
+    infos = []
+    for _ in range(k):
+        dt, info = ctx.step(phi, dt)
+        infos.append(info)
+    return dt, infos
+
+
+def bench_cuda(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_1703_01202_b200 import build as B
+    from paper_1703_01202_b200 import pfc as P
+    from paper_1703_01202_b200.inputs import CONFIGS
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    if ws > 1:
+        dist.init_process_group("nccl")
+    if rank == 0:
+        B.build()
+    if ws > 1:
+        dist.barrier()
+    cfg = CONFIGS[args.config]
+    W, K = args.warmup, args.steps
+    phi0 = cfg.initial_condition()
+    ctx = P.Context(cfg)
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        if ws > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x):
+        if ws == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # ---- device-resident timed run
+    phi = torch.from_numpy(phi0.copy()).cuda()
+    dt, _ = run_steps(ctx, phi, cfg.dt0, W)
+    dt_first_timed = dt
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    l0 = ctx.launches
+    with ClockSampler(local) as clk:
+        e0.record(stream)
+        dt_end, infos = run_steps(ctx, phi, dt, K)
+        e1.record(stream)
+        barrier()
+    launches = ctx.launches - l0
+    ms = max_over_ranks(e0.elapsed_time(e1))
+    clocks = clk.summary()
+    value = ws * K / (ms / 1e3)
+
+    # ---- end to end through the C ABI with a pinned host buffer (same trajectory)
+    ph = torch.from_numpy(phi0.copy()).pin_memory()
+    dt, _ = run_steps(ctx, ph, cfg.dt0, W)
+    barrier()
+    e0.record(stream)
+    run_steps(ctx, ph, dt, K)
+    e1.record(stream)
+    barrier()
+    ms_e2e = max_over_ranks(e0.elapsed_time(e1))
+    e2e = {"value": ws * K / (ms_e2e / 1e3), "unit": "steps/s",
+           "h2d_bytes_per_step": cfg.N * 8, "d2h_bytes_per_step": cfg.N * 8}
+
+    # ---- per-kernel-class profile of the same K steps (separate pass; events per launch)
+    phi = torch.from_numpy(phi0.copy()).cuda()
+    dt, _ = run_steps(ctx, phi, cfg.dt0, W)
+    ctx.profile(True)
+    run_steps(ctx, phi, dt, K)
+    prof = ctx.profile_report()
+    ctx.profile(False)
+    hbm_peak, peak_kind = load_peaks()
+    total_ms = sum(v["ms"] for v in prof.values())
+    dom = max(prof, key=lambda k: prof[k]["ms"])
+    classes = {}
+    for k, v in prof.items():
+        if v["launches"]:
+            classes[k] = {"launches": v["launches"], "ms": round(v["ms"], 4),
+                          "share": round(v["ms"] / total_ms, 4),
+                          "algo_GBps": round(v["bytes"] / (v["ms"] * 1e-3) / 1e9, 1),
+                          "algo_GFLOPs": round(v["flops"] / (v["ms"] * 1e-3) / 1e9, 1)}
+
+    def roofline_for(name, v):
+        if name == "ras":
+            # FP64-ALU bound local solve: peak = 148 SMs x 64 FP64 FMA/clk x 2 flop x clock
+            clk_mhz = clocks.get("sm_mhz") or 1965.0
+            peak = 148 * 64 * 2 * clk_mhz * 1e6 / 1e12
+            ach = v["flops"] / (v["ms"] * 1e-3) / 1e12
+            return {"kernel": "ras_apply", "bound": "alu", "achieved": round(ach, 3),
+                    "peak": round(peak, 2), "unit": "TFLOP/s", "frac": round(ach / peak, 4),
+                    "peak_kind": "derived: 148 SM x 64 DFMA/clk x 2 x median SM clock",
+                    "traffic": None}
+        ach = v["bytes"] / (v["ms"] * 1e-3) / 1e9
+        return {"kernel": name, "bound": "hbm", "achieved": round(ach, 1), "peak": hbm_peak,
+                "unit": "GB/s", "frac": round(ach / hbm_peak, 4), "peak_kind": peak_kind,
+                "traffic": None}
+
+    roofline = roofline_for(dom, prof[dom])
+    roofline["share_of_step"] = round(prof[dom]["ms"] / total_ms, 4)
+
+    # ---- isolated Jacobian apply at the config-5 size (inputs >> L2)
+    jv = None
+    if args.jv_size > 0:
+        n = args.jv_size
+        del ctx
+        torch.cuda.empty_cache()
+        cj = P.Context(None, ndim=3, n=(n, n, n), h=cfg.h, gamma=cfg.gamma, ras_box=(16, 16, 16),
+                       ras_overlap=2, gmres_restart=1)
+        g = torch.Generator(device="cuda").manual_seed(5)
+        a = (-0.35 + 0.05 * (2 * torch.rand((n, n, n), dtype=torch.float64, device="cuda",
+                                             generator=g) - 1))
+        v = torch.rand((n, n, n), dtype=torch.float64, device="cuda", generator=g)
+        out = torch.empty_like(v)
+        for _ in range(3):
+            cj.jacobian_apply(a, a, 1.0, v, out)
+        cj.profile(True)
+        reps = 10
+        for _ in range(reps):
+            cj.jacobian_apply(a, a, 1.0, v, out)
+            cj.residual(a, v, 1.0, out)
+        pr = cj.profile_report()
+        cj.profile(False)
+        jv_gbs = pr["jv"]["bytes"] / (pr["jv"]["ms"] * 1e-3) / 1e9
+        rs_gbs = pr["residual"]["bytes"] / (pr["residual"]["ms"] * 1e-3) / 1e9
+        jv = {"grid": [n, n, n], "GBps": round(jv_gbs, 1), "frac": round(jv_gbs / hbm_peak, 4),
+              "ms_per_apply": round(pr["jv"]["ms"] / reps, 4),
+              "residual_GBps": round(rs_gbs, 1), "residual_frac": round(rs_gbs / hbm_peak, 4),
+              "algo_bytes_per_apply": 24 * n ** 3, "peak": hbm_peak, "peak_kind": peak_kind,
+              "l2": "fields 1 GiB each >> 126 MB L2"}
+        del cj, a, v, out
+
+    newton = sum(i["newton_its"] for i in infos)
+    gmres = sum(i["gmres_its"] for i in infos)
+    line = {
+        "metric": METRIC, "value": round(value, 3), "unit": "steps/s", "n_gpus": ws, "steps": K,
+        "warmup": W, "ms_per_step": round(ms / K, 4), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded SplitMix64 IC per BASELINE config)",
+        "config": {"workload": cfg.name, "grid": list(cfg.n), "h": "pi/4", "gamma": cfg.gamma,
+                   "dt": (f"adaptive [{cfg.dt_min},{cfg.dt_max}] eta={cfg.eta}, timed steps "
+                          f"{W}..{W + K - 1} from dt_min" if cfg.adaptive else f"fixed {cfg.dt0}"),
+                   "dt_first_timed": dt_first_timed, "dt_last": dt_end,
+                   "solver": (f"Newton rtol {cfg.newton_rtol} / FGMRES({cfg.gmres_restart}) rtol "
+                              f"{cfg.gmres_rtol} / left-RAS {cfg.ras_box[:cfg.ndim]} overlap "
+                              f"{cfg.ras_overlap} local GMRES k={cfg.ras_local_k}"),
+                   "parallelism": f"{ws} independent replica(s)",
+                   "l2": "step working set (61-field Krylov basis, 0.5 GB) > 126 MB L2; no flush"},
+        "newton_its": newton, "gmres_its": gmres,
+        "clocks": clocks, "e2e": e2e, "gpu_launches": launches,
+        "roofline": roofline, "kernel_classes": classes, "jacobian_apply": jv,
+    }
+    if ws == 1 and rank == 0 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(cfg, phi0, W, args.cpu_steps)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.destroy_process_group()
+
+
+def cpu_baseline(cfg, phi0, W, nsteps):
+    """The oracle as it stands (single-threaded C) on this host: W untimed steps of the same
+    trajectory, then `nsteps` timed steps (the first timed steps of the GPU run)."""
+    from oracle import oracle as O
+    prm = O.params_from_config(cfg)
+    phi = phi0.copy()
+    dt = cfg.dt0
+    for _ in range(W):
+        new, ok, info, Fn, Fn1 = O.step(phi, cfg.h, prm, dt)
+        dt = O.next_dt(cfg.dt_min, cfg.dt_max, cfg.eta, Fn1, Fn, dt) if cfg.adaptive else dt
+        phi = new
+    t0 = time.perf_counter()
+    for _ in range(nsteps):
+        new, ok, info, Fn, Fn1 = O.step(phi, cfg.h, prm, dt)
+        dt = O.next_dt(cfg.dt_min, cfg.dt_max, cfg.eta, Fn1, Fn, dt) if cfg.adaptive else dt
+        phi = new
+    t = time.perf_counter() - t0
+    return {"value": round(nsteps / t, 5), "unit": "steps/s", "cores": 1, "kind": "oracle",
+            "sample": f"{cfg.name}: oracle steps {W}..{W + nsteps - 1} of the same trajectory "
+                      f"(single-threaded C, -O2), {t:.1f} s; host {os.cpu_count()} cores"}
+
+
+def bench_reference(args):
+    """Oracle arm: rank 0 runs the CPU oracle on the same config/metric/unit."""
+    ws, rank, local = dist_env()
+    if rank != 0:
+        return
+    from oracle import oracle as O
+    from paper_1703_01202_b200.inputs import CONFIGS
+    O.build()
+    cfg = CONFIGS[args.config]
+    W, K = args.warmup, args.steps
+    phi = cfg.initial_condition()
+    prm = O.params_from_config(cfg)
+    dt = cfg.dt0
+
+    def one(phi, dt):
+        new, ok, info, Fn, Fn1 = O.step(phi, cfg.h, prm, dt)
+        return new, (O.next_dt(cfg.dt_min, cfg.dt_max, cfg.eta, Fn1, Fn, dt) if cfg.adaptive
+                     else dt)
+
+    for _ in range(W):
+        phi, dt = one(phi, dt)
+    t0 = time.perf_counter()
+    for _ in range(K):
+        phi, dt = one(phi, dt)
+    t = time.perf_counter() - t0
+    value = K / t
+    sample = (f"{cfg.name}: oracle steps {W}..{W + K - 1} of the seeded trajectory "
+              f"(single-threaded C -O2)")
+    line = {"impl": "reference", "metric": METRIC, "value": round(value, 5), "unit": "steps/s",
+            "n_gpus": ws, "steps": K, "warmup": W, "ms_per_step": round(1e3 * t / K, 2),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded SplitMix64 IC per BASELINE config)",
+            "config": {"workload": cfg.name, "grid": list(cfg.n)},
+            "cpu_baseline": {"value": round(value, 5), "unit": "steps/s", "cores": 1,
+                             "kind": "oracle", "sample": sample},
+            "e2e": {"value": round(value, 5), "unit": "steps/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="cuda", choices=["cuda", "reference"])
+    ap.add_argument("--config", default="cfg2")
+    ap.add_argument("--jv-size", type=int, default=512)
+    ap.add_argument("--cpu-steps", type=int, default=2)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        print("note: --warmup < 3 is below the timing contract", file=sys.stderr)
+    if args.impl == "reference":
+        bench_reference(args)
+    else:
+        bench_cuda(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -66,7 +66,7 @@ typedef struct pfc_config {
   double gmres_atol;      /* xi_a */
   int ras_box[3];         /* owned subdomain box Omega_k (nodes per axis); must divide n */
   int ras_overlap;        /* overlap o in MESH LAYERS (paper's delta = o/3) */
-  int ras_local_k;        /* fixed number of local GMRES steps in each subdomain solve (1..16) */
+  int ras_local_k;        /* fixed number of local GMRES steps in each subdomain solve (1..15) */
 } pfc_config;
 
 /* Per-step report of pfc_step. */
@@ -94,7 +94,7 @@ void pfc_config_default(pfc_config* cfg);
  * (may be NULL).  Validates (PFC_EINVAL): ndim in {2,3}; every n_d >= 4; h > 0; gamma > 0;
  * 0 < dt_min <= dt_max when adaptive; n_d % ras_box_d == 0; 0 <= ras_overlap < ras_box_d and
  * ras_box_d + 2 ras_overlap + 6 <= n_d (the zero ring of P:429-437 must not wrap onto the box);
- * the ext box fits the subdomain kernel's shared-memory plan; 1 <= ras_local_k <= 16;
+ * the ext box fits the subdomain kernel's shared-memory plan; 1 <= ras_local_k <= 15;
  * 1 <= gmres_restart <= 32.  Allocates the Krylov workspace (2m+1 fields + 8 work fields). */
 pfc_status pfc_create(const pfc_config* cfg, void* cuda_stream, pfc_ctx** out);
 void pfc_destroy(pfc_ctx* ctx);
@@ -152,8 +152,10 @@ long long pfc_kernel_launches(const pfc_ctx* ctx);
 
 /* Per-kernel-class device timing (tracing aid).  When enabled, every launch is bracketed by
  * CUDA events on the context stream (adds ~2 event records per launch); pfc_profile_query
- * synchronizes the stream and returns, for class `cls`, the number of launches and the summed
- * device time in milliseconds since the last pfc_profile_enable(ctx, 1) (which resets them).
+ * synchronizes the stream and returns, for class `cls`, the number of launches, the summed
+ * device time in milliseconds, and the summed ALGORITHMIC bytes and flops of those launches
+ * (DESIGN.md §6 gives the per-node counts) since the last pfc_profile_enable(ctx, 1) (which
+ * resets them).  Any output pointer may be NULL.
  * Classes: PFC_K_RESIDUAL, PFC_K_JV, PFC_K_RAS, PFC_K_COEF, PFC_K_ORTH (CGS2 multi-dot/axpy),
  * PFC_K_FINALIZE (reduction finalization), PFC_K_VECTOR (axpby/lincomb/norm), PFC_K_ENERGY. */
 enum {
@@ -161,7 +163,8 @@ enum {
   PFC_K_FINALIZE = 5, PFC_K_VECTOR = 6, PFC_K_ENERGY = 7, PFC_K_NCLASSES = 8
 };
 pfc_status pfc_profile_enable(pfc_ctx* ctx, int on);
-pfc_status pfc_profile_query(pfc_ctx* ctx, int cls, long long* count, double* total_ms);
+pfc_status pfc_profile_query(pfc_ctx* ctx, int cls, long long* count, double* total_ms,
+                             double* bytes, double* flops);
 
 #ifdef __cplusplus
 }

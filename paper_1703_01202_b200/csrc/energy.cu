@@ -61,6 +61,7 @@ cudaError_t launch_energy_mass(pfc_ctx* ctx, const double* phi, double* partials
     k_energy_mass<3><<<nb, NT, 0, ctx->stream>>>(phi, n[0], n[1], n[2], ctx->cfg.gamma, ih,
                                                  partials);
   ctx->launches++;
+  pfc_account(ctx, PFC_K_ENERGY, 8.0 * ctx->N, 25.0 * ctx->N);
   *nparts = nb;
   return cudaGetLastError();
 }

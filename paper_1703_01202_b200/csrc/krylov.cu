@@ -157,6 +157,7 @@ static int grid_pointwise(size_t N) {
 cudaError_t launch_coef(pfc_ctx* ctx, const double* phi, const double* psi, double* c) {
   k_coef<<<grid_pointwise(ctx->N), NT, 0, ctx->stream>>>(phi, psi, c, ctx->N);
   ctx->launches++;
+  pfc_account(ctx, PFC_K_COEF, 24.0 * ctx->N, 5.0 * ctx->N);
   return cudaGetLastError();
 }
 
@@ -164,6 +165,7 @@ cudaError_t launch_axpby(pfc_ctx* ctx, double a, const double* x, double b, cons
                          double* out) {
   k_axpby<<<grid_pointwise(ctx->N), NT, 0, ctx->stream>>>(a, x, b, y, out, ctx->N);
   ctx->launches++;
+  pfc_account(ctx, PFC_K_VECTOR, (y ? 24.0 : 16.0) * ctx->N, (y ? 3.0 : 1.0) * ctx->N);
   return cudaGetLastError();
 }
 
@@ -180,6 +182,7 @@ cudaError_t launch_multidot(pfc_ctx* ctx, const double* V, int nv, const double*
     default: return cudaErrorInvalidValue;
   }
   ctx->launches++;
+  pfc_account(ctx, PFC_K_ORTH, 8.0 * (nv + 1) * ctx->N, 2.0 * nv * ctx->N);
   return cudaGetLastError();
 }
 
@@ -196,6 +199,7 @@ cudaError_t launch_axpy_dot(pfc_ctx* ctx, const double* V, int nv, const double*
     default: return cudaErrorInvalidValue;
   }
   ctx->launches++;
+  pfc_account(ctx, PFC_K_ORTH, 8.0 * (nv + 2) * ctx->N, 4.0 * nv * ctx->N);
   return cudaGetLastError();
 }
 
@@ -212,12 +216,14 @@ cudaError_t launch_axpy_norm(pfc_ctx* ctx, const double* V, int nv, const double
     default: return cudaErrorInvalidValue;
   }
   ctx->launches++;
+  pfc_account(ctx, PFC_K_ORTH, 8.0 * (nv + 2) * ctx->N, (2.0 * nv + 2.0) * ctx->N);
   return cudaGetLastError();
 }
 
 cudaError_t launch_norm2(pfc_ctx* ctx, const double* x, double* partials) {
   k_norm2<<<blas_nblocks(ctx->N), NT, 0, ctx->stream>>>(x, ctx->N, partials);
   ctx->launches++;
+  pfc_account(ctx, PFC_K_VECTOR, 8.0 * ctx->N, 2.0 * ctx->N);
   return cudaGetLastError();
 }
 
@@ -225,6 +231,7 @@ cudaError_t launch_finalize(pfc_ctx* ctx, const double* partials, int nblk, int 
                             double* out) {
   k_finalize<<<nval, NT, 0, ctx->stream>>>(partials, nblk, nval, out);
   ctx->launches++;
+  pfc_account(ctx, PFC_K_FINALIZE, 8.0 * nblk * nval, 1.0 * nblk * nval);
   return cudaGetLastError();
 }
 
@@ -249,6 +256,7 @@ cudaError_t launch_lincomb(pfc_ctx* ctx, double* x, const double* Z, int nv, con
 #undef X
     }
     ctx->launches++;
+    pfc_account(ctx, PFC_K_VECTOR, 8.0 * (k + 2) * ctx->N, 2.0 * k * ctx->N);
     done += k;
   }
   return cudaGetLastError();

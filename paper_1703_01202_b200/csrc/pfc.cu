@@ -370,7 +370,7 @@ static pfc_status validate(const pfc_config& c, std::string* why) {
   if (!(c.gamma > 0)) return bad("gamma must be > 0");
   if (c.adaptive && !(c.dt_min > 0 && c.dt_min <= c.dt_max)) return bad("need 0 < dt_min <= dt_max");
   if (c.adaptive && !(c.eta >= 0)) return bad("eta must be >= 0");
-  if (c.ras_local_k < 1 || c.ras_local_k > PFC_MAX_LOCAL_K) return bad("ras_local_k in [1,16]");
+  if (c.ras_local_k < 1 || c.ras_local_k > PFC_MAX_LOCAL_K) return bad("ras_local_k in [1,15]");
   if (c.gmres_restart < 1 || c.gmres_restart > PFC_MAX_RESTART) return bad("gmres_restart in [1,32]");
   if (c.gmres_maxit < 1 || c.newton_maxit < 0) return bad("iteration limits must be positive");
   if (!(c.newton_rtol >= 0 && c.newton_atol >= 0 && c.gmres_rtol >= 0 && c.gmres_atol >= 0))
@@ -462,15 +462,20 @@ pfc_status pfc_profile_enable(pfc_ctx* ctx, int on) {
   for (int i = 0; i < PFC_K_NCLASSES; ++i) {
     ctx->prof_count[i] = 0;
     ctx->prof_ms[i] = 0.0;
+    ctx->prof_bytes[i] = 0.0;
+    ctx->prof_flops[i] = 0.0;
   }
   return PFC_OK;
 }
 
-pfc_status pfc_profile_query(pfc_ctx* ctx, int cls, long long* count, double* total_ms) {
+pfc_status pfc_profile_query(pfc_ctx* ctx, int cls, long long* count, double* total_ms,
+                             double* bytes, double* flops) {
   if (!ctx || cls < 0 || cls >= PFC_K_NCLASSES) return PFC_EINVAL;
   prof_drain(ctx);
   if (count) *count = ctx->prof_count[cls];
   if (total_ms) *total_ms = ctx->prof_ms[cls];
+  if (bytes) *bytes = ctx->prof_bytes[cls];
+  if (flops) *flops = ctx->prof_flops[cls];
   return PFC_OK;
 }
 

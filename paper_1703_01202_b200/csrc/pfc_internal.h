@@ -10,7 +10,7 @@
 #include "../../include/pfc.h"
 
 #define PFC_MAX_RESTART 32
-#define PFC_MAX_LOCAL_K 16
+#define PFC_MAX_LOCAL_K 15
 
 struct pfc_ctx {
   pfc_config cfg;
@@ -54,7 +54,17 @@ struct pfc_ctx {
   cudaEvent_t ev_open = nullptr;
   long long prof_count[PFC_K_NCLASSES] = {0};
   double prof_ms[PFC_K_NCLASSES] = {0};
+  double prof_bytes[PFC_K_NCLASSES] = {0};   // algorithmic bytes of the launched kernels
+  double prof_flops[PFC_K_NCLASSES] = {0};   // algorithmic flops
 };
+
+// algorithmic bytes/flops of a launch (counted only while profiling)
+inline void pfc_account(pfc_ctx* ctx, int cls, double bytes, double flops) {
+  if (ctx->prof) {
+    ctx->prof_bytes[cls] += bytes;
+    ctx->prof_flops[cls] += flops;
+  }
+}
 
 // set ctx->err and return the status
 pfc_status pfc_fail(pfc_ctx* ctx, pfc_status st, const std::string& msg);

@@ -4,24 +4,35 @@
 //
 // One CTA per subdomain box Omega_k (b_x x b_y owned nodes).  The CTA gathers v and the
 // Jacobian coefficient c on the extended box Omega_k^delta (E = b + 2o nodes per axis,
-// periodic wrap = restriction R_k^delta), then runs exactly k steps of GMRES on
-// A_k y = R_k^delta v entirely in shared memory (reading R9: fixed-work local solve, zero
-// initial guess, CGS2, Givens, early exit only on exact breakdown), and writes only the owned
-// nodes (R_k^0)^T -- disjoint writes, no atomics.
+// periodic wrap = restriction R_k^delta), then runs exactly K steps of GMRES on
+// A_k y = R_k^delta v entirely on chip (reading R9: fixed-work local solve, zero initial guess,
+// CGS2, Givens, early exit only on exact breakdown), and writes only the owned nodes
+// (R_k^0)^T -- disjoint writes, no atomics.
 //
 // A_k is the local Jacobian with phi = 0 on the 3-layer ring around the extended box
-// (modified subdomain BC): the Krylov vector is copied into the interior of a
-// zero-padded (E+6)^2 array whose ring is never written, and the local J v is the same
-// three-stage composed stencil as K2 (halo 2 -> 1 -> 0 on the padded grid):
+// (modified subdomain BC): the Krylov vector lives in the interior of a zero-padded
+// (E+6)^2 shared-memory plane whose ring is never written, and the local J v is the composed
+// stencil of K2 in three stages (halo 2 -> 1 -> 0):
 //   L1 = Delta v,  B = ((1-gamma)/2 + c) v + L1 + Delta L1 / 2,  w = v/dt - Delta B.
-// Shared memory: basis V (k+1 vectors of E^2), c, w, three padded planes, Hessenberg.
+//
+// Latency design (one box per SM at E = 36..40: the K basis vectors take 104-128 KB):
+//  * the Arnoldi vector w of the thread's own nodes stays in registers;
+//  * each CGS2 pass is ONE block reduction: warp reduce-scatter (16 values in 16 shuffles
+//    instead of 80), one barrier, lane-parallel cross-warp sums, shuffle broadcast;
+//  * pass 2 also reduces |w'|^2 and the new norm is |w''|^2 = |w'|^2 - |h2|^2 (exact for an
+//    orthonormal basis; pass 2 only removes rounding-size components), with an explicit extra
+//    reduction when |h2|^2 > 1e-8 |w'|^2;
+//  * normalisation writes V_{j+1} and the padded plane in one pass; Givens runs on one thread
+//    concurrently with it.  Five barriers per Arnoldi step.
 #include "pfc_device.cuh"
 #include "pfc_internal.h"
 
 namespace {
 
 constexpr int NT = 512;
-constexpr int KMAX = PFC_MAX_LOCAL_K;
+constexpr int NW = NT / 32;
+constexpr int MAXN = 1600;                 // largest ext box (E = 40)
+constexpr int SLOTS = (MAXN + NT - 1) / NT;
 
 struct RasArgs {
   const double* v;
@@ -29,11 +40,70 @@ struct RasArgs {
   double* z;
   int nx, ny;
   int bx, by, o;
-  int k;
   double idt, gamma, ih2;
 };
 
+constexpr int pow2_at_least(int x) { return x <= 1 ? 1 : 2 * pow2_at_least((x + 1) / 2); }
+
+// One reduce-scatter step: lanes exchange the half they do not keep across lane offset
+// `off`; both halves are shuffled and the kept sum selected afterwards (a select of operands,
+// a[upper ? i : i + half], would be lowered to a local-memory index).
+template <int NVP, int HALF>
+__device__ __forceinline__ void rs_step(double (&a)[NVP], int lane, int off) {
+  const bool upper = (lane & off) != 0;
+#pragma unroll
+  for (int i = 0; i < HALF; ++i) {
+    const double lo = a[i], hi = a[i + HALF];
+    const double rlo = __shfl_xor_sync(0xffffffffu, lo, off);
+    const double rhi = __shfl_xor_sync(0xffffffffu, hi, off);
+    a[i] = upper ? hi + rhi : lo + rlo;
+  }
+  if constexpr (HALF > 1) rs_step<NVP, HALF / 2>(a, lane, off >> 1);
+}
+
+// Warp reduce-scatter of NVP (power of two, <= 32) values: afterwards lane l holds the warp
+// sum of value (l >> (5 - log2 NVP)).  Fixed shuffle tree, deterministic.
+template <int NVP>
+__device__ __forceinline__ double warp_reduce_scatter(double (&a)[NVP]) {
+  const int lane = threadIdx.x & 31;
+  int off = 16;
+  if constexpr (NVP > 1) {
+    rs_step<NVP, NVP / 2>(a, lane, 16);
+    off = 16 / (NVP / 2) / 2;
+  }
+  double s = a[0];
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1)
+    if (o <= off) s += __shfl_xor_sync(0xffffffffu, s, o);
+  return s;
+}
+
+// Block sum of nv (runtime, <= NVP) values held by every thread in acc[]: the sums are left in
+// this warp's private copy hw[0..nv) (valid after return for every lane of the warp).  One
+// barrier; `red` alternates between two buffers so consecutive reductions never race.
+// Value NVP-1 is also reduced when `with_last` (the norm slot).
+template <int NVP>
+__device__ __forceinline__ void block_allreduce(double (&acc)[NVP], int nv, double* red,
+                                                double* hw, bool with_last = false) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  constexpr int SH = 5 - (NVP == 1 ? 0 : NVP == 2 ? 1 : NVP == 4 ? 2 : NVP == 8 ? 3 : NVP == 16 ? 4 : 5);
+  double s = warp_reduce_scatter<NVP>(acc);
+  const int vi = lane >> SH;
+  if ((lane & ((1 << SH) - 1)) == 0 && (vi < nv || (with_last && vi == NVP - 1)))
+    red[wid * NVP + vi] = s;
+  __syncthreads();
+  if (lane < nv || (with_last && lane == NVP - 1)) {
+    double t = 0.0;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) t += red[w * NVP + lane];
+    hw[lane] = t;
+  }
+  __syncwarp();
+}
+
+template <int K>
 __global__ void __launch_bounds__(NT, 1) ras2d_kernel(RasArgs p) {
+  constexpr int NVP = pow2_at_least(K + 2);   // values 0..K-1 plus the norm slot NVP-1
   extern __shared__ unsigned char smem_raw[];
   double* sm = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) &
                                          ~uintptr_t(127));
@@ -41,67 +111,77 @@ __global__ void __launch_bounds__(NT, 1) ras2d_kernel(RasArgs p) {
   const int n = Ex * Ey;
   const int Px = Ex + 6, Py = Ey + 6;
   const int np = Px * Py;
-  const int k = p.k;
-  double* V = sm;                        // (k+1) n
-  double* cl = V + (size_t)(k + 1) * n;  // n
-  double* w = cl + n;                    // n
-  double* pv = w + n;                    // np (zero ring)
+  double* V = sm;                        // K n
+  double* cl = V + (size_t)K * n;        // n
+  double* pv = cl + n;                   // np (zero ring)
   double* pl = pv + np;                  // np
   double* pb = pl + np;                  // np
-  double* H = pb + np;                   // (k+1) k, column-major H[i + (k+1) j]
-  double* gv = H + (k + 1) * k;          // k+1
-  double* cs = gv + (k + 1);             // k
-  double* sn = cs + k;                   // k
-  double* yv = sn + k;                   // k
-  double* hs = yv + k;                   // 2 (KMAX+1) : h1 | h2
-  double* red = hs + 2 * (KMAX + 1);     // 32 (KMAX+1)
-  double* scal = red + 32 * (KMAX + 1);  // 4: beta, hn, jm flag
+  double* red = pb + np;                 // 2 x NW x NVP
+  double* hwall = red + 2 * NW * NVP;    // NW x 3 NVP: per-warp copies of h1 | h2 | misc
+  __shared__ double H[(K + 1) * K];
+  __shared__ double gv[K + 1], cs[K], sn[K], yv[K];
 
   const int tid = threadIdx.x;
+  double* h1 = hwall + (tid >> 5) * 3 * NVP;
+  double* h2 = h1 + NVP;
+  double* hx = h2 + NVP;
   const int nbx = p.nx / p.bx;
   const int ibx = blockIdx.x % nbx, iby = blockIdx.x / nbx;
   const int gx0 = ibx * p.bx - p.o, gy0 = iby * p.by - p.o;
   const double ih2 = p.ih2, idt = p.idt, alpha = 0.5 * (1.0 - p.gamma);
 
-  // R_k^delta: gather v and c on the extended box (periodic wrap)
-  double acc[KMAX + 1];
-  acc[0] = 0.0;
-  for (int l = tid; l < n; l += NT) {
-    int li = l % Ex, lj = l / Ex;
-    size_t g = (size_t)wrapi(gx0 + li, p.nx) + (size_t)p.nx * wrapi(gy0 + lj, p.ny);
-    double vv = p.v[g];
-    V[l] = vv;
-    cl[l] = p.c[g];
-    acc[0] += vv * vv;
+  // own box nodes: l = tid + s*NT; padded index of node l
+  int pidx[SLOTS];
+  bool own[SLOTS];
+#pragma unroll
+  for (int s = 0; s < SLOTS; ++s) {
+    int l = tid + s * NT;
+    own[s] = l < n;
+    pidx[s] = own[s] ? ((l / Ex) + 3) * Px + (l % Ex) + 3 : 0;
   }
-  for (int q = tid; q < 3 * np; q += NT) pv[q] = 0.0;   // pv, pl, pb contiguous
-  for (int q = tid; q < (k + 1) * k; q += NT) H[q] = 0.0;
-  for (int q = tid; q < k + 1; q += NT) gv[q] = 0.0;
-  {
-    double a1[1] = {acc[0]};
-    block_sum_multi<1>(a1, red, scal);
-  }
-  const double beta = sqrt(scal[0]);
-  if (beta == 0.0) {
-    for (int l = tid; l < p.bx * p.by; l += NT) {
-      int li = l % p.bx, lj = l / p.bx;
-      p.z[(size_t)(ibx * p.bx + li) + (size_t)p.nx * (iby * p.by + lj)] = 0.0;
+
+  // zero the padded planes (ring stays zero), gather R_k^delta v and c with periodic wrap
+  for (int q = tid; q < 3 * np; q += NT) pv[q] = 0.0;
+  double w[SLOTS];
+  double acc[NVP];
+#pragma unroll
+  for (int i = 0; i < NVP; ++i) acc[i] = 0.0;
+#pragma unroll
+  for (int s = 0; s < SLOTS; ++s) {
+    w[s] = 0.0;
+    if (own[s]) {
+      int l = tid + s * NT;
+      size_t g = (size_t)wrapi(gx0 + l % Ex, p.nx) + (size_t)p.nx * wrapi(gy0 + l / Ex, p.ny);
+      w[s] = p.v[g];
+      cl[l] = p.c[g];
+      acc[0] += w[s] * w[s];
     }
+  }
+  int rb = 0;
+  block_allreduce<NVP>(acc, 1, red + rb * NW * NVP, hx);
+  rb ^= 1;
+  const double beta = sqrt(hx[0]);
+  if (beta == 0.0) {
+    for (int l = tid; l < p.bx * p.by; l += NT)
+      p.z[(size_t)(ibx * p.bx + l % p.bx) + (size_t)p.nx * (iby * p.by + l / p.bx)] = 0.0;
     return;
   }
-  const double ib = 1.0 / beta;
-  for (int l = tid; l < n; l += NT) V[l] *= ib;
+  {
+    const double ib = 1.0 / beta;
+#pragma unroll
+    for (int s = 0; s < SLOTS; ++s)
+      if (own[s]) {
+        double v0 = w[s] * ib;
+        V[tid + s * NT] = v0;
+        pv[pidx[s]] = v0;
+      }
+  }
   if (tid == 0) gv[0] = beta;
 
   int jm = 0;
-  for (int j = 0; j < k; ++j) {
-    const double* Vj = V + (size_t)j * n;
-    // A_k V_j: interior of the zero-padded array
-    for (int l = tid; l < n; l += NT) {
-      int li = l % Ex, lj = l / Ex;
-      pv[(lj + 3) * Px + li + 3] = Vj[l];
-    }
-    __syncthreads();
+#pragma unroll 1
+  for (int j = 0; j < K; ++j) {
+    __syncthreads();                                   // pv holds V_j
     {   // L1 = Delta v on padded [1, P-1)
       const int wx = Px - 2, cnt = wx * (Py - 2);
       for (int q = tid; q < cnt; q += NT) {
@@ -110,7 +190,7 @@ __global__ void __launch_bounds__(NT, 1) ras2d_kernel(RasArgs p) {
       }
     }
     __syncthreads();
-    {   // B on padded [2, P-2)
+    {   // B on padded [2, P-2); c v = 0 outside the extended box
       const int wx = Px - 4, cnt = wx * (Py - 4);
       for (int q = tid; q < cnt; q += NT) {
         int pi = 2 + q % wx, pj = 2 + q / wx;
@@ -123,50 +203,76 @@ __global__ void __launch_bounds__(NT, 1) ras2d_kernel(RasArgs p) {
       }
     }
     __syncthreads();
-    // w = v/dt - Delta B on the box, and CGS2 pass-1 dots
+    // w = v/dt - Delta B on own nodes (registers); CGS2 pass 1: h1 = V^T w
 #pragma unroll
-    for (int i = 0; i <= KMAX; ++i) acc[i] = 0.0;
-    for (int l = tid; l < n; l += NT) {
-      int li = l % Ex, lj = l / Ex;
-      int f = (lj + 3) * Px + li + 3;
-      double lapb = ih2 * ((pb[f - 1] + pb[f + 1]) + (pb[f - Px] + pb[f + Px]) - 4.0 * pb[f]);
-      double ww = pv[f] * idt - lapb;
-      w[l] = ww;
+    for (int i = 0; i < NVP; ++i) acc[i] = 0.0;
 #pragma unroll
-      for (int i = 0; i <= KMAX; ++i)
-        if (i <= j) acc[i] += V[(size_t)i * n + l] * ww;
+    for (int s = 0; s < SLOTS; ++s) {
+      if (own[s]) {
+        const int f = pidx[s], l = tid + s * NT;
+        double lapb = ih2 * ((pb[f - 1] + pb[f + 1]) + (pb[f - Px] + pb[f + Px]) - 4.0 * pb[f]);
+        double ww = pv[f] * idt - lapb;
+        w[s] = ww;
+#pragma unroll
+        for (int i = 0; i < K; ++i)
+          if (i <= j) acc[i] += V[(size_t)i * n + l] * ww;
+      }
     }
-    block_sum_multi<KMAX + 1>(acc, red, hs, j + 1);
-    // w -= V h1 ; pass-2 dots
+    block_allreduce<NVP>(acc, j + 1, red + rb * NW * NVP, h1);
+    rb ^= 1;
+    // w' = w - V h1 ; pass 2: h2 = V^T w', and |w'|^2 (slot K of the reduction)
 #pragma unroll
-    for (int i = 0; i <= KMAX; ++i) acc[i] = 0.0;
-    for (int l = tid; l < n; l += NT) {
-      double ww = w[l];
+    for (int i = 0; i < NVP; ++i) acc[i] = 0.0;
 #pragma unroll
-      for (int i = 0; i <= KMAX; ++i)
-        if (i <= j) ww -= hs[i] * V[(size_t)i * n + l];
+    for (int s = 0; s < SLOTS; ++s) {
+      if (own[s]) {
+        const int l = tid + s * NT;
+        double vv[K];
+        double ww = w[s];
 #pragma unroll
-      for (int i = 0; i <= KMAX; ++i)
-        if (i <= j) acc[i] += V[(size_t)i * n + l] * ww;
-      w[l] = ww;
+        for (int i = 0; i < K; ++i) {
+          vv[i] = (i <= j) ? V[(size_t)i * n + l] : 0.0;
+          ww -= h1[i] * vv[i];
+        }
+#pragma unroll
+        for (int i = 0; i < K; ++i) acc[i] += vv[i] * ww;
+        acc[NVP - 1] += ww * ww;
+        w[s] = ww;
+      }
     }
-    block_sum_multi<KMAX + 1>(acc, red, hs + (KMAX + 1), j + 1);
-    // w -= V h2 ; |w|^2
-    double a1[1] = {0.0};
-    for (int l = tid; l < n; l += NT) {
-      double ww = w[l];
+    block_allreduce<NVP>(acc, j + 1, red + rb * NW * NVP, h2, true);
+    rb ^= 1;
+    const double wn2 = h2[NVP - 1];
+    double h2n = 0.0;
+    for (int i = 0; i <= j; ++i) h2n += h2[i] * h2[i];
 #pragma unroll
-      for (int i = 0; i <= KMAX; ++i)
-        if (i <= j) ww -= hs[KMAX + 1 + i] * V[(size_t)i * n + l];
-      w[l] = ww;
-      a1[0] += ww * ww;
+    for (int s = 0; s < SLOTS; ++s) {
+      if (own[s]) {
+        const int l = tid + s * NT;
+        double ww = w[s];
+#pragma unroll
+        for (int i = 0; i < K; ++i)
+          if (i <= j) ww -= h2[i] * V[(size_t)i * n + l];
+        w[s] = ww;
+      }
     }
-    block_sum_multi<1>(a1, red, scal + 1);
-    // Hessenberg column j, Givens (one thread)
-    if (tid == 0) {
-      const int ld = k + 1;
-      const double hn = sqrt(scal[1]);
-      for (int i = 0; i <= j; ++i) H[i + ld * j] = hs[i] + hs[KMAX + 1 + i];
+    double hn2;
+    if (h2n <= 1e-8 * wn2) {
+      hn2 = wn2 - h2n;                                  // |w''|^2 = |w'|^2 - |h2|^2
+    } else {                                            // rare: explicit |w''|^2
+#pragma unroll
+      for (int i = 0; i < NVP; ++i) acc[i] = 0.0;
+#pragma unroll
+      for (int s = 0; s < SLOTS; ++s)
+        if (own[s]) acc[0] += w[s] * w[s];
+      block_allreduce<NVP>(acc, 1, red + rb * NW * NVP, hx);
+      rb ^= 1;
+      hn2 = hx[0];
+    }
+    const double hn = sqrt(hn2 > 0.0 ? hn2 : 0.0);
+    if (tid == 0) {   // Hessenberg column j and Givens rotation
+      const int ld = K + 1;
+      for (int i = 0; i <= j; ++i) H[i + ld * j] = h1[i] + h2[i];
       H[j + 1 + ld * j] = hn;
       for (int i = 0; i < j; ++i) {
         double a = H[i + ld * j], b = H[i + 1 + ld * j];
@@ -182,19 +288,23 @@ __global__ void __launch_bounds__(NT, 1) ras2d_kernel(RasArgs p) {
       H[j + 1 + ld * j] = 0.0;
       gv[j + 1] = -ss * gv[j];
       gv[j] = cc * gv[j];
-      scal[2] = (hn <= 1e-14 * beta) ? 1.0 : 0.0;
-      scal[3] = hn;
     }
-    __syncthreads();
     jm = j + 1;
-    if (scal[2] != 0.0) break;           // exact breakdown (uniform)
-    const double ihn = 1.0 / scal[3];
-    double* Vn = V + (size_t)(j + 1) * n;
-    for (int l = tid; l < n; l += NT) Vn[l] = w[l] * ihn;
-    // (the next iteration's first __syncthreads orders these writes)
+    if (hn <= 1e-14 * beta) break;                     // exact breakdown (uniform)
+    if (j + 1 < K) {
+      const double ihn = 1.0 / hn;
+#pragma unroll
+      for (int s = 0; s < SLOTS; ++s)
+        if (own[s]) {
+          double vn = w[s] * ihn;
+          V[(size_t)(j + 1) * n + tid + s * NT] = vn;
+          pv[pidx[s]] = vn;
+        }
+    }
   }
+  __syncthreads();
   if (tid == 0) {   // back substitution R y = g
-    const int ld = k + 1;
+    const int ld = K + 1;
     for (int i = jm - 1; i >= 0; --i) {
       double s = gv[i];
       for (int l = i + 1; l < jm; ++l) s -= H[i + ld * l] * yv[l];
@@ -214,17 +324,28 @@ __global__ void __launch_bounds__(NT, 1) ras2d_kernel(RasArgs p) {
 
 size_t ras2d_smem_bytes(int bx, int by, int o, int k) {
   const size_t Ex = bx + 2 * o, Ey = by + 2 * o, n = Ex * Ey, np = (Ex + 6) * (Ey + 6);
-  size_t d = (size_t)(k + 1) * n + 2 * n + 3 * np + (size_t)(k + 1) * k + (k + 1) + 3 * k +
-             2 * (KMAX + 1) + 32 * (KMAX + 1) + 4;
+  size_t d = (size_t)k * n + n + 3 * np + 2 * NW * 16 + NW * 3 * 16;
   return d * sizeof(double) + 128;
+}
+
+typedef void (*ras2d_fn)(RasArgs);
+ras2d_fn pick(int k) {
+  switch (k) {
+#define X(K) case K: return ras2d_kernel<K>;
+    X(1) X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(9) X(10) X(11) X(12) X(13) X(14) X(15)
+#undef X
+  }
+  return nullptr;
 }
 
 }  // namespace
 
 int ras2d_plan(pfc_ctx* ctx) {
   const pfc_config& c = ctx->cfg;
+  const int Ex = c.ras_box[0] + 2 * c.ras_overlap, Ey = c.ras_box[1] + 2 * c.ras_overlap;
+  if (Ex * Ey > MAXN) return 0;
   size_t sm = ras2d_smem_bytes(c.ras_box[0], c.ras_box[1], c.ras_overlap, c.ras_local_k);
-  if (sm > 227 * 1024) return 0;
+  if (sm > 200 * 1024) return 0;
   ctx->ras_smem = (int)sm;
   ctx->ras_threads = NT;
   ctx->ras_cluster = 1;
@@ -233,17 +354,27 @@ int ras2d_plan(pfc_ctx* ctx) {
 
 cudaError_t launch_ras_2d(pfc_ctx* ctx, const double* v, const double* c, double dt, double* z) {
   const pfc_config& cf = ctx->cfg;
-  static int attr_bytes = 0;
-  if (ctx->ras_smem > attr_bytes) {
-    cudaError_t e = cudaFuncSetAttribute(ras2d_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  ras2d_fn fn = pick(cf.ras_local_k);
+  if (!fn) return cudaErrorInvalidValue;
+  static int attr_bytes[PFC_MAX_LOCAL_K + 1] = {0};
+  if (ctx->ras_smem > attr_bytes[cf.ras_local_k]) {
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          ctx->ras_smem);
     if (e != cudaSuccess) return e;
-    attr_bytes = ctx->ras_smem;
+    attr_bytes[cf.ras_local_k] = ctx->ras_smem;
   }
   RasArgs p{v, c, z, cf.n[0], cf.n[1], cf.ras_box[0], cf.ras_box[1], cf.ras_overlap,
-            cf.ras_local_k, 1.0 / dt, cf.gamma, ctx->ih2};
+            1.0 / dt, cf.gamma, ctx->ih2};
   const int nb = (cf.n[0] / cf.ras_box[0]) * (cf.n[1] / cf.ras_box[1]);
-  ras2d_kernel<<<nb, NT, ctx->ras_smem, ctx->stream>>>(p);
+  fn<<<nb, NT, ctx->ras_smem, ctx->stream>>>(p);
   ctx->launches++;
+  {  // algorithmic: v, c gathered on the extended boxes, z written on owned nodes; flops of
+     // k local J v (25/pt) + CGS2 vector work 4k(k+1) + 3k + 3 per ext node + V y
+    const double k = cf.ras_local_k;
+    const double next = (double)nb * (cf.ras_box[0] + 2 * cf.ras_overlap) *
+                        (cf.ras_box[1] + 2 * cf.ras_overlap);
+    pfc_account(ctx, PFC_K_RAS, 8.0 * (2.0 * next + ctx->N),
+                next * (25.0 * k + 4.0 * k * (k + 1) + 3.0 * k + 3.0) + 2.0 * k * ctx->N);
+  }
   return cudaGetLastError();
 }

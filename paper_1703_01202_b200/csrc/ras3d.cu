@@ -242,5 +242,14 @@ cudaError_t launch_ras_3d(pfc_ctx* ctx, const double* v, const double* c, double
              1.0 / dt, cf.gamma, ctx->ih2};
   ras3d_kernel<<<grid, NT, 0, ctx->stream>>>(p);
   ctx->launches++;
+  {
+    const double k = cf.ras_local_k;
+    const double nb = (double)(cf.n[0] / cf.ras_box[0]) * (cf.n[1] / cf.ras_box[1]) *
+                      (cf.n[2] / cf.ras_box[2]);
+    const double next = nb * (cf.ras_box[0] + 2 * cf.ras_overlap) *
+                        (cf.ras_box[1] + 2 * cf.ras_overlap) * (cf.ras_box[2] + 2 * cf.ras_overlap);
+    pfc_account(ctx, PFC_K_RAS, 8.0 * (2.0 * next + ctx->N),
+                next * (31.0 * k + 4.0 * k * (k + 1) + 3.0 * k + 3.0) + 2.0 * k * ctx->N);
+  }
   return cudaGetLastError();
 }

@@ -172,6 +172,9 @@ cudaError_t launch2d(pfc_ctx* ctx, const double* a, const double* b, double dt, 
   if (nparts) *nparts = grid.x * grid.y;
   stencil2d_kernel<OP><<<grid, NT, SMEM_BYTES, ctx->stream>>>(ma, mb, p);
   ctx->launches++;
+  // algorithmic: 2 fields in, 1 out; flops of the composed operator per node (2D)
+  pfc_account(ctx, OP == OP_RESID ? PFC_K_RESIDUAL : PFC_K_JV, 24.0 * ctx->N,
+              (OP == OP_RESID ? 36.0 : 25.0) * ctx->N);
   return cudaGetLastError();
 }
 

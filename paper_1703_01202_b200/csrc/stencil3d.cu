@@ -1,18 +1,18 @@
 // stencil3d.cu -- fused 3D DVD residual (K1) and Jacobian-vector product (K2), sm_100a.
 //
 // Same operators as stencil2d.cu (Eq. NSOP, Eq. discretedG, Eq. Jacobi
-// P:351-356), 7-point Delta_d composed three times: a radius-3, 63-point stencil.
+// P:351-356), the 7-point Delta_d composed three times: a radius-3, 63-point stencil.
 //
-// 2.5D z-march.  A CTA owns a TX x TY column of outputs and a chunk of ZC z-planes.  It streams
-// the input planes z0-3 .. z0+ZC+2 through a ring of RING plane buffers per field, filled by
-// TMA (cp.async.bulk.tensor.3d, one (TX+8) x (TY+6) x 1 box per field and plane, PREFETCH
-// planes ahead, one mbarrier per ring slot).  Every thread owns fixed xy positions of the
-// plane window ("slots") for all stages; at plane t it computes
+// 2.5D z-march.  A CTA (1024 threads, one per SM) owns a TX x TY column of outputs and a chunk
+// of ZC z-planes.  Input planes z0-3 .. z0+ZC+2 stream through an 8-slot ring per field filled
+// by TMA (cp.async.bulk.tensor.3d, one (TX+8) x (TY+6) x 1 box per field and plane, 4 planes in
+// flight, one mbarrier per slot).  Every thread owns ONE fixed position of the 40 x 22 plane
+// window for all stages and keeps its z-neighbours in registers; at streamed plane t it computes
 //     u(t) [halo 3]  ->  L1(t-1) [halo 2]  ->  A(t-2) [halo 1]  ->  F(t-3) [halo 0]
-// where the xy-neighbours come from one shared-memory plane per stage (double-buffered) and
-// the z-neighbours from per-thread register queues of the thread's own slots.  Periodic x/y
-// wrap: TMA zero-fills out-of-range cells and edge tiles reload exactly those own-slot cells
-// with wrapped loads; z wraps by plane index.  Optional fused ||F||^2 partial per CTA.
+// taking xy-neighbours from one shared-memory plane per stage (double-buffered).  Two
+// barriers per plane.  Periodic x/y wrap: TMA zero-fills out-of-range cells and edge tiles
+// reload exactly those cells with wrapped loads; z wraps incrementally.  Optional fused
+// ||F||^2 partial per CTA.
 #include "pfc_device.cuh"
 #include "pfc_internal.h"
 
@@ -23,10 +23,9 @@ constexpr int HX = 4, HY = 3;
 constexpr int WX = TX + 2 * HX;   // 40
 constexpr int WY = TY + 2 * HY;   // 22
 constexpr int WN = WX * WY;       // 880
-constexpr int NT = 512;
-constexpr int NS = (WN + NT - 1) / NT;  // slots per thread (2)
-constexpr int RING = 6;
-constexpr int PREFETCH = 3;
+constexpr int NT = 1024;
+constexpr int RING = 8;           // power of two
+constexpr int PREFETCH = 4;
 
 enum { OP_RESID = 0, OP_JV = 1 };
 
@@ -41,11 +40,6 @@ struct S3Args {
   int use_tma;
 };
 
-__device__ __forceinline__ bool in_region(int q, int r) {
-  int qx = q % WX, qy = q / WX;
-  return qx >= HX - r && qx < HX + TX + r && qy >= HY - r && qy < HY + TY + r;
-}
-
 __device__ __forceinline__ double lap_xy(const double* f, int q) {
   return (f[q - 1] + f[q + 1]) + (f[q - WX] + f[q + WX]) - 4.0 * f[q];
 }
@@ -59,9 +53,9 @@ __global__ void __launch_bounds__(NT, 1) stencil3d_kernel(const __grid_constant_
                                            ~uintptr_t(127));
   double* ringA = base;                    // RING planes
   double* ringB = ringA + RING * WN;       // RING planes
-  double* Ub = ringB + RING * WN;          // 2 planes (resid only)
-  double* L1b = Ub + 2 * WN;               // 2 planes
+  double* L1b = ringB + RING * WN;         // 2 planes
   double* AAb = L1b + 2 * WN;              // 2 planes
+  double* Ub = AAb + 2 * WN;               // 2 planes (resid only)
   __shared__ uint64_t bars[RING];
   __shared__ double red[64];
 
@@ -77,165 +71,130 @@ __global__ void __launch_bounds__(NT, 1) stencil3d_kernel(const __grid_constant_
   const bool edge = gx0 < 0 || gy0 < 0 || gx0 + WX > nx || gy0 + WY > ny;
   const double ih2 = p.ih2;
 
-  // slot geometry
-  int qs[NS];
-  bool r3[NS], r2[NS], r1[NS], r0[NS], valid[NS];
-  size_t gofs[NS];  // in-plane global offset (wrapped) of the slot
-#pragma unroll
-  for (int s = 0; s < NS; ++s) {
-    int q = tid + s * NT;
-    valid[s] = q < WN;
-    qs[s] = valid[s] ? q : 0;
-    r3[s] = valid[s] && in_region(q, 3) && (OP == OP_RESID);
-    r2[s] = valid[s] && in_region(q, 2);
-    r1[s] = valid[s] && in_region(q, 1);
-    r0[s] = valid[s] && in_region(q, 0);
-    int gx = gx0 + qs[s] % WX, gy = gy0 + qs[s] / WX;
-    gofs[s] = (size_t)wrapi(gx, nx) + (size_t)nx * wrapi(gy, ny);
-    if (r0[s] && (gx >= nx || gy >= ny)) r0[s] = false;   // ragged tile: no output
-  }
-
-  auto issue = [&](int t) {   // TMA of streamed plane t into ring slot t % RING
-    int zp = wrapi(z0 - 3 + t, nz);
-    int slot = t % RING;
-    mbar_expect_tx(&bars[slot], 2u * WN * sizeof(double));
-    tma_load_3d(ringA + slot * WN, &ma, &bars[slot], gx0, gy0, zp);
-    tma_load_3d(ringB + slot * WN, &mb, &bars[slot], gx0, gy0, zp);
+  // this thread's window position and its stage memberships
+  const int q = tid < WN ? tid : 0;
+  const bool valid = tid < WN;
+  const int qx = q % WX, qy = q / WX;
+  auto inr = [&](int r) {
+    return valid && qx >= HX - r && qx < HX + TX + r && qy >= HY - r && qy < HY + TY + r;
   };
+  const bool r3 = inr(3) && OP == OP_RESID, r2 = inr(2), r1 = inr(1);
+  const int gx = gx0 + qx, gy = gy0 + qy;
+  const bool r0 = inr(0) && gx < nx && gy < ny;                 // ragged tiles: no output
+  const bool reload = valid && (!p.use_tma || (edge && (gx < 0 || gx >= nx || gy < 0 || gy >= ny)));
+  const size_t gofs = (size_t)wrapi(gx, nx) + (size_t)nx * wrapi(gy, ny);
 
+  const int zfirst = wrapi(z0 - 3, nz);
   if (p.use_tma) {
     if (tid == 0) {
       for (int i = 0; i < RING; ++i) mbar_init(&bars[i], 1);
       fence_mbar_init();
     }
     __syncthreads();
-    if (tid == 0)
-      for (int t = 0; t < PREFETCH && t < T; ++t) issue(t);
-  }
-
-  // register z-queues: index 0 = oldest
-  double qU[NS][3], qL[NS][3], qA[NS][3], qa[NS][4], qb[NS][4];
-#pragma unroll
-  for (int s = 0; s < NS; ++s)
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      if (i < 3) qU[s][i] = qL[s][i] = qA[s][i] = 0.0;
-      qa[s][i] = qb[s][i] = 0.0;
+    if (tid == 0) {
+      int zi = zfirst;
+      for (int t = 0; t < PREFETCH && t < T; ++t) {
+        const int slot = t & (RING - 1);
+        mbar_expect_tx(&bars[slot], 2u * WN * sizeof(double));
+        tma_load_3d(ringA + slot * WN, &ma, &bars[slot], gx0, gy0, zi);
+        tma_load_3d(ringB + slot * WN, &mb, &bars[slot], gx0, gy0, zi);
+        zi = (zi + 1 == nz) ? 0 : zi + 1;
+      }
     }
-  double nrm = 0.0;
+  }
+  int zpre = wrapi(z0 - 3 + PREFETCH, nz);   // plane of the next TMA issue
+  int zcur = zfirst;                          // plane t
 
+  // register z-queues of this thread's position: [0] oldest
+  double a0 = 0, a1 = 0, a2 = 0, a3 = 0;      // input A (Phi | v) planes t-3..t
+  double b0 = 0, b1 = 0, b2 = 0, b3 = 0;      // input B (psi | c) planes t-3..t
+  double u0 = 0, u1 = 0, u2 = 0;              // u planes t-2..t (resid)
+  double l0 = 0, l1 = 0, l2 = 0;              // L1 planes t-3..t-1
+  double A0 = 0, A1 = 0, A2 = 0;              // A planes t-4..t-2
+  double nrm = 0.0;
+  double* outp = p.out + gofs + plane * (size_t)z0;
+
+#pragma unroll 2
   for (int t = 0; t < T; ++t) {
-    const int slot = t % RING;
+    const int slot = t & (RING - 1);
     double* pa = ringA + slot * WN;
     double* pb = ringB + slot * WN;
-    const int zp = wrapi(z0 - 3 + t, nz);
     if (p.use_tma) {
-      if (tid == 0 && t + PREFETCH < T) issue(t + PREFETCH);
+      if (tid == 0 && t + PREFETCH < T) {
+        const int ps = (t + PREFETCH) & (RING - 1);
+        mbar_expect_tx(&bars[ps], 2u * WN * sizeof(double));
+        tma_load_3d(ringA + ps * WN, &ma, &bars[ps], gx0, gy0, zpre);
+        tma_load_3d(ringB + ps * WN, &mb, &bars[ps], gx0, gy0, zpre);
+      }
+      zpre = (zpre + 1 == nz) ? 0 : zpre + 1;
       mbar_wait(&bars[slot], (t / RING) & 1);
     }
-    // own-slot inputs of plane t (wrapped reload of out-of-range cells on edge tiles)
-#pragma unroll
-    for (int s = 0; s < NS; ++s) {
-#pragma unroll
-      for (int i = 0; i < 3; ++i) { qa[s][i] = qa[s][i + 1]; qb[s][i] = qb[s][i + 1]; }
-      double va = 0.0, vb = 0.0;
-      if (valid[s]) {
-        if (!p.use_tma || edge) {
-          int gx = gx0 + qs[s] % WX, gy = gy0 + qs[s] / WX;
-          bool oob = !p.use_tma || gx < 0 || gx >= nx || gy < 0 || gy >= ny;
-          if (oob) {
-            size_t g = gofs[s] + plane * zp;
-            va = p.a[g];
-            vb = p.b[g];
-            pa[qs[s]] = va;
-            pb[qs[s]] = vb;
-          } else {
-            va = pa[qs[s]];
-            vb = pb[qs[s]];
-          }
-        } else {
-          va = pa[qs[s]];
-          vb = pb[qs[s]];
-        }
+    // own inputs of plane t
+    double va = 0.0, vb = 0.0;
+    if (valid) {
+      if (reload) {
+        const size_t g = gofs + plane * zcur;
+        va = p.a[g];
+        vb = p.b[g];
+        pa[q] = va;
+        pb[q] = vb;
+        if (p.use_tma) fence_proxy_async();   // generic write before a later TMA overwrite
+      } else {
+        va = pa[q];
+        vb = pb[q];
       }
-      qa[s][3] = va;
-      qb[s][3] = vb;
     }
-    // generic-proxy patch writes must be ordered before later TMA writes to the same slot
-    if (p.use_tma && edge) fence_proxy_async();
-    double* Lin;   // plane buffer whose xy-Laplacian feeds L1(t-1)
+    zcur = (zcur + 1 == nz) ? 0 : zcur + 1;
+    a0 = a1; a1 = a2; a2 = a3; a3 = va;
+    b0 = b1; b1 = b2; b2 = b3; b3 = vb;
+    const double* Lin;                         // plane whose xy-Laplacian feeds L1(t-1)
     if (OP == OP_RESID) {
-      // u(t) on halo 3
-      double* Ucur = Ub + (t & 1) * WN;
-#pragma unroll
-      for (int s = 0; s < NS; ++s) {
-        qU[s][0] = qU[s][1]; qU[s][1] = qU[s][2];
-        double u = 0.5 * (qa[s][3] + qb[s][3]);
-        qU[s][2] = u;
-        if (r3[s]) Ucur[qs[s]] = u;
-      }
+      u0 = u1; u1 = u2; u2 = 0.5 * (va + vb);
+      if (r3) Ub[(t & 1) * WN + q] = u2;
       Lin = Ub + ((t - 1) & 1) * WN;
     } else {
-      // v planes t-2, t-1, t live in qa[.][1..3]; xy-neighbours of plane t-1 in the ring
-#pragma unroll
-      for (int s = 0; s < NS; ++s) { qU[s][0] = qa[s][1]; qU[s][1] = qa[s][2]; qU[s][2] = qa[s][3]; }
-      Lin = ringA + ((t + RING - 1) % RING) * WN;
+      u0 = a1; u1 = a2; u2 = a3;              // v planes t-2, t-1, t
+      Lin = ringA + ((t - 1) & (RING - 1)) * WN;
     }
-    __syncthreads();
-    // L1(t-1) on halo 2
+    // L1(t-1) on halo 2: xy-neighbours of plane t-1 were completed before the previous
+    // iteration's barriers
     if (t >= 2) {
-      double* Lcur = L1b + ((t - 1) & 1) * WN;
-#pragma unroll
-      for (int s = 0; s < NS; ++s) {
-        qL[s][0] = qL[s][1]; qL[s][1] = qL[s][2];
-        double l = 0.0;
-        if (r2[s]) {
-          l = ih2 * (lap_xy(Lin, qs[s]) + (qU[s][0] + qU[s][2] - 2.0 * qU[s][1]) +
-                     0.0);
-          Lcur[qs[s]] = l;
-        }
-        qL[s][2] = l;
+      l0 = l1; l1 = l2;
+      double l = 0.0;
+      if (r2) {
+        l = ih2 * (lap_xy(Lin, q) + (u0 + u2 - 2.0 * u1));
+        L1b[((t - 1) & 1) * WN + q] = l;
       }
+      l2 = l;
     }
     __syncthreads();
     // A(t-2) | bracket(t-2) on halo 1
     if (t >= 4) {
-      const double* Lp = L1b + ((t - 2) & 1) * WN;
-      double* Acur = AAb + ((t - 2) & 1) * WN;
-#pragma unroll
-      for (int s = 0; s < NS; ++s) {
-        qA[s][0] = qA[s][1]; qA[s][1] = qA[s][2];
-        double aval = 0.0;
-        if (r1[s]) {
-          double lapL = ih2 * (lap_xy(Lp, qs[s]) + (qL[s][0] + qL[s][2] - 2.0 * qL[s][1]));
-          double a = qa[s][1], b = qb[s][1];   // plane t-2
-          if (OP == OP_RESID) {
-            double N = 0.25 * (a * a * a + a * a * b + a * b * b + b * b * b);
-            aval = (1.0 - p.gamma) * qU[s][0] + 2.0 * qL[s][1] + lapL + N;
-          } else {
-            aval = (0.5 * (1.0 - p.gamma) + b) * a + qL[s][1] + 0.5 * lapL;
-          }
-          Acur[qs[s]] = aval;
+      A0 = A1; A1 = A2;
+      double av = 0.0;
+      if (r1) {
+        const double lapL = ih2 * (lap_xy(L1b + ((t - 2) & 1) * WN, q) + (l0 + l2 - 2.0 * l1));
+        const double a = a1, b = b1;           // plane t-2
+        if (OP == OP_RESID) {
+          const double N = 0.25 * (a * a * a + a * a * b + a * b * b + b * b * b);
+          av = (1.0 - p.gamma) * u0 + 2.0 * l1 + lapL + N;
+        } else {
+          av = (0.5 * (1.0 - p.gamma) + b) * a + l1 + 0.5 * lapL;
         }
-        qA[s][2] = aval;
+        AAb[((t - 2) & 1) * WN + q] = av;
       }
+      A2 = av;
     }
     __syncthreads();
     // F(t-3) on halo 0
-    if (t >= 6) {
-      const double* Ap = AAb + ((t - 3) & 1) * WN;
-      const int zo = z0 + (t - 6);   // output plane
-#pragma unroll
-      for (int s = 0; s < NS; ++s) {
-        if (r0[s]) {
-          double lapA = ih2 * (lap_xy(Ap, qs[s]) + (qA[s][0] + qA[s][2] - 2.0 * qA[s][1]));
-          double o;
-          if (OP == OP_RESID) o = (qa[s][0] - qb[s][0]) * p.idt - lapA;
-          else o = qa[s][0] * p.idt - lapA;
-          p.out[gofs[s] + plane * zo] = o;
-          nrm += o * o;
-        }
-      }
+    if (t >= 6 && r0) {
+      const double lapA = ih2 * (lap_xy(AAb + ((t - 3) & 1) * WN, q) + (A0 + A2 - 2.0 * A1));
+      double o;
+      if (OP == OP_RESID) o = (a0 - b0) * p.idt - lapA;
+      else o = a0 * p.idt - lapA;
+      *outp = o;
+      outp += plane;
+      nrm += o * o;
     }
   }
   if (p.partials) {
@@ -275,6 +234,8 @@ cudaError_t launch3d(pfc_ctx* ctx, const double* a, const double* b, double dt, 
   if (nparts) *nparts = grid.x * grid.y;
   stencil3d_kernel<OP><<<grid, NT, SMEM_BYTES, ctx->stream>>>(ma, mb, p);
   ctx->launches++;
+  pfc_account(ctx, OP == OP_RESID ? PFC_K_RESIDUAL : PFC_K_JV, 24.0 * ctx->N,
+              (OP == OP_RESID ? 42.0 : 31.0) * ctx->N);
   return cudaGetLastError();
 }
 

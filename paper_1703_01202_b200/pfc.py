@@ -75,7 +75,8 @@ def load():
     L.pfc_kernel_launches.restype = C.c_longlong
     L.pfc_profile_enable.argtypes = [vp, C.c_int]
     L.pfc_profile_enable.restype = C.c_int
-    L.pfc_profile_query.argtypes = [vp, C.c_int, C.POINTER(C.c_longlong), C.POINTER(C.c_double)]
+    L.pfc_profile_query.argtypes = [vp, C.c_int, C.POINTER(C.c_longlong), C.POINTER(C.c_double),
+                                    C.POINTER(C.c_double), C.POINTER(C.c_double)]
     L.pfc_profile_query.restype = C.c_int
     for name in ("pfc_create", "pfc_residual", "pfc_jacobian_apply", "pfc_ras_apply", "pfc_step",
                  "pfc_energy", "pfc_mass"):
@@ -154,12 +155,14 @@ class Context:
         self._check(self.L.pfc_profile_enable(self._h, int(on)))
 
     def profile_report(self):
-        """{class: (launches, total device ms)} since the last profile(True)."""
+        """{class: dict(launches, ms, bytes, flops)} since the last profile(True); bytes and
+        flops are the algorithmic counts of DESIGN.md §6."""
         out = {}
         for i, name in enumerate(KERNEL_CLASSES):
-            n, ms = C.c_longlong(), C.c_double()
-            self._check(self.L.pfc_profile_query(self._h, i, C.byref(n), C.byref(ms)))
-            out[name] = (n.value, ms.value)
+            n, ms, b, f = C.c_longlong(), C.c_double(), C.c_double(), C.c_double()
+            self._check(self.L.pfc_profile_query(self._h, i, C.byref(n), C.byref(ms), C.byref(b),
+                                                 C.byref(f)))
+            out[name] = dict(launches=n.value, ms=ms.value, bytes=b.value, flops=f.value)
         return out
 
     def residual(self, phi_new, phi_old, dt, out=None):
