@@ -104,9 +104,10 @@ __device__ __forceinline__ void block_allreduce(double (&acc)[NVP], int nv, doub
 template <int K>
 __global__ void __launch_bounds__(NT, 1) ras2d_kernel(RasArgs p) {
   constexpr int NVP = pow2_at_least(K + 2);   // values 0..K-1 plus the norm slot NVP-1
-  extern __shared__ unsigned char smem_raw[];
-  double* sm = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) &
-                                         ~uintptr_t(127));
+  // declared as a shared array (not re-derived through an integer) so that every access
+  // compiles to LDS/STS with 32-bit shared addressing; 128-B aligned for TMA destinations
+  extern __shared__ __align__(128) double smem_dyn[];
+  double* sm = smem_dyn;
   const int Ex = p.bx + 2 * p.o, Ey = p.by + 2 * p.o;
   const int n = Ex * Ey;
   const int Px = Ex + 6, Py = Ey + 6;

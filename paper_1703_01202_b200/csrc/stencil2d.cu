@@ -46,9 +46,10 @@ template <int OP>
 __global__ void __launch_bounds__(NT) stencil2d_kernel(const __grid_constant__ CUtensorMap ma,
                                                        const __grid_constant__ CUtensorMap mb,
                                                        S2Args p) {
-  extern __shared__ unsigned char smem_raw[];
-  double* base = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) &
-                                           ~uintptr_t(127));
+  // declared as a shared array (not re-derived through an integer) so that every access
+  // compiles to LDS/STS with 32-bit shared addressing; 128-B aligned for TMA destinations
+  extern __shared__ __align__(128) double smem_dyn[];
+  double* base = smem_dyn;
   double* A0 = base;            // Phi | v
   double* B0 = A0 + WN;         // psi | c
   double* U = B0 + WN;          // u (resid only)
