@@ -168,19 +168,21 @@ __global__ void __launch_bounds__(NT, 1) stencil3d_kernel(const __grid_constant_
   uint32_t phase = 0;
 
   const blk Z{{0, 0}, {0, 0}};
-  // register queues ([0] oldest): a = v | Phi-psi (t-3..t), c = c | N (t-2..t), u (t-2..t),
-  // l = L1 (t-3..t-1), A (t-4..t-2)
-  blk a0 = Z, a1 = Z, a2 = Z, a3 = Z, c0 = Z, c1 = Z, c2 = Z, u0 = Z, u1 = Z, u2 = Z;
+  // register queues, all of length 3 so that the 3x-unrolled loop rotates them by renaming.
+  // At the start of iteration t:  a = v | Phi-psi at t-3, t-2, t-1;  c = c | N at t-3, t-2, t-1;
+  // u at t-3, t-2, t-1 (resid);  l = L1 at t-4, t-3, t-2;  A at t-5, t-4, t-3.
+  blk a0 = Z, a1 = Z, a2 = Z, c0 = Z, c1 = Z, c2 = Z, u0 = Z, u1 = Z, u2 = Z;
   blk l0 = Z, l1 = Z, l2 = Z, A0 = Z, A1 = Z, A2 = Z;
   double nrm = 0.0;
   const size_t zoff0 = plane * (size_t)z0;
+  const int Tp = (T + 2) / 3 * 3;          // padded to the unroll factor; extra planes are inert
 
-#pragma unroll 1
-  for (int t = 0; t < T; ++t) {
+#pragma unroll 3
+  for (int t = 0; t < Tp; ++t) {
     double* pa = ringA + slot * WN;
     double* pb = ringB + slot * WN;
     if (p.use_tma) {
-      if (tid == 0 && t + PREFETCH < T) {
+      if (tid == 0 && t + PREFETCH < Tp) {
         mbar_expect_tx(&bars[pslot], 2u * WN * sizeof(double));
         tma_load_3d(ringA + pslot * WN, &ma, &bars[pslot], gx0, gy0, zpre);
         tma_load_3d(ringB + pslot * WN, &mb, &bars[pslot], gx0, gy0, zpre);
@@ -217,53 +219,58 @@ __global__ void __launch_bounds__(NT, 1) stencil3d_kernel(const __grid_constant_
     const blk x2 = outside_sum(L1b + ((t - 2) & 1) * WN, nb);
     const blk x3 = outside_sum(AAb + ((t - 3) & 1) * WN, nb);
     // ---- compute (garbage of the warm-up iterations never reaches a stored output)
+    blk anew, cnew, ufresh;          // plane-t values entering the queues
     if (OP == OP_RESID) {
-      a0 = a1; a1 = a2; a2 = a3;
-      a3 = {{va.r0.x - vb.r0.x, va.r0.y - vb.r0.y}, {va.r1.x - vb.r1.x, va.r1.y - vb.r1.y}};
-      c0 = c1; c1 = c2;
-      c2 = {{cubic(va.r0.x, vb.r0.x), cubic(va.r0.y, vb.r0.y)},
-            {cubic(va.r1.x, vb.r1.x), cubic(va.r1.y, vb.r1.y)}};
-      u0 = u1; u1 = u2;
-      u2 = {{0.5 * (va.r0.x + vb.r0.x), 0.5 * (va.r0.y + vb.r0.y)},
-            {0.5 * (va.r1.x + vb.r1.x), 0.5 * (va.r1.y + vb.r1.y)}};
+      anew = {{va.r0.x - vb.r0.x, va.r0.y - vb.r0.y}, {va.r1.x - vb.r1.x, va.r1.y - vb.r1.y}};
+      cnew = {{cubic(va.r0.x, vb.r0.x), cubic(va.r0.y, vb.r0.y)},
+              {cubic(va.r1.x, vb.r1.x), cubic(va.r1.y, vb.r1.y)}};
+      ufresh = {{0.5 * (va.r0.x + vb.r0.x), 0.5 * (va.r0.y + vb.r0.y)},
+                {0.5 * (va.r1.x + vb.r1.x), 0.5 * (va.r1.y + vb.r1.y)}};
     } else {
-      a0 = a1; a1 = a2; a2 = a3; a3 = va;     // v
-      c0 = c1; c1 = c2; c2 = vb;              // c
-      u0 = a1; u1 = a2; u2 = a3;
+      anew = va;                      // v
+      cnew = vb;                      // c
+      ufresh = va;
     }
+    const blk& um = (OP == OP_RESID) ? u1 : a1;   // u | v at t-2
+    const blk& uc = (OP == OP_RESID) ? u2 : a2;   // u | v at t-1
     // L1(t-1) on halo 2
-    l0 = l1; l1 = l2;
-    l2 = lap3(x1, u0, u1, u2, ih2);
+    const blk lnew = lap3(x1, um, uc, ufresh, ih2);
     // A(t-2) | bracket(t-2) on halo 1
-    A0 = A1; A1 = A2;
+    blk Anew;
     {
-      const blk lapL = lap3(x2, l0, l1, l2, ih2);
+      const blk lapL = lap3(x2, l1, l2, lnew, ih2);
       if (OP == OP_RESID) {
         const double gm = 1.0 - p.gamma;
-        A2.r0.x = gm * u0.r0.x + 2.0 * l1.r0.x + lapL.r0.x + c0.r0.x;
-        A2.r0.y = gm * u0.r0.y + 2.0 * l1.r0.y + lapL.r0.y + c0.r0.y;
-        A2.r1.x = gm * u0.r1.x + 2.0 * l1.r1.x + lapL.r1.x + c0.r1.x;
-        A2.r1.y = gm * u0.r1.y + 2.0 * l1.r1.y + lapL.r1.y + c0.r1.y;
+        Anew.r0.x = gm * u1.r0.x + 2.0 * l2.r0.x + lapL.r0.x + c1.r0.x;
+        Anew.r0.y = gm * u1.r0.y + 2.0 * l2.r0.y + lapL.r0.y + c1.r0.y;
+        Anew.r1.x = gm * u1.r1.x + 2.0 * l2.r1.x + lapL.r1.x + c1.r1.x;
+        Anew.r1.y = gm * u1.r1.y + 2.0 * l2.r1.y + lapL.r1.y + c1.r1.y;
       } else {
         const double al = 0.5 * (1.0 - p.gamma);
-        A2.r0.x = (al + c0.r0.x) * a1.r0.x + l1.r0.x + 0.5 * lapL.r0.x;
-        A2.r0.y = (al + c0.r0.y) * a1.r0.y + l1.r0.y + 0.5 * lapL.r0.y;
-        A2.r1.x = (al + c0.r1.x) * a1.r1.x + l1.r1.x + 0.5 * lapL.r1.x;
-        A2.r1.y = (al + c0.r1.y) * a1.r1.y + l1.r1.y + 0.5 * lapL.r1.y;
+        Anew.r0.x = (al + c1.r0.x) * a1.r0.x + l2.r0.x + 0.5 * lapL.r0.x;
+        Anew.r0.y = (al + c1.r0.y) * a1.r0.y + l2.r0.y + 0.5 * lapL.r0.y;
+        Anew.r1.x = (al + c1.r1.x) * a1.r1.x + l2.r1.x + 0.5 * lapL.r1.x;
+        Anew.r1.y = (al + c1.r1.y) * a1.r1.y + l2.r1.y + 0.5 * lapL.r1.y;
       }
     }
     // F(t-3) on halo 0: (Phi-psi)/dt | v/dt  minus  Delta A
-    const blk lapA = lap3(x3, A0, A1, A2, ih2);
+    const blk lapA = lap3(x3, A1, A2, Anew, ih2);
     const d2 oa = {a0.r0.x * p.idt - lapA.r0.x, a0.r0.y * p.idt - lapA.r0.y};
     const d2 obv = {a0.r1.x * p.idt - lapA.r1.x, a0.r1.y * p.idt - lapA.r1.y};
+    // ---- queue rotation (renames under the 3x unroll)
+    a0 = a1; a1 = a2; a2 = anew;
+    c0 = c1; c1 = c2; c2 = cnew;
+    if (OP == OP_RESID) { u0 = u1; u1 = u2; u2 = ufresh; }
+    l0 = l1; l1 = l2; l2 = lnew;
+    A0 = A1; A1 = A2; A2 = Anew;
     // ---- stores
     double* Lw = L1b + ((t - 1) & 1) * WN;
     double* Aw = AAb + ((t - 2) & 1) * WN;
-    if (w2a) st2(Lw + qa, l2.r0);
-    if (w2b) st2(Lw + qb, l2.r1);
-    if (w1a) st2(Aw + qa, A2.r0);
-    if (w1b) st2(Aw + qb, A2.r1);
-    if (t >= 6) {
+    if (w2a) st2(Lw + qa, lnew.r0);
+    if (w2b) st2(Lw + qb, lnew.r1);
+    if (w1a) st2(Aw + qa, Anew.r0);
+    if (w1b) st2(Aw + qb, Anew.r1);
+    if (t >= 6 && t - 6 < zc) {
       const size_t zo = zoff0 + plane * (size_t)(t - 6);
       if (vec_a) {
         st2(p.out + g0 + zo, oa);
