@@ -91,12 +91,28 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(rows)}
 
 
-def run_steps(ctx, phi, dt, k):
+def run_steps(ctx, phi, dt, k, dt_min=None):
+    """k accepted steps; a step whose Newton solve fails (PFC_ENOCONV) is retried with dt/2,
+    never below dt_min (SPEC S:492 policy); phi is unchanged by a failed attempt."""
+    from paper_1703_01202_b200 import pfc as P
     infos = []
     for _ in range(k):
-        dt, info = ctx.step(phi, dt)
+        st, dt_next, info = ctx.try_step(phi, dt)
+        while st != P.PFC_OK and dt_min is not None and dt > dt_min * (1 + 1e-12):
+            dt = max(0.5 * dt, dt_min)
+            st, dt_next, info = ctx.try_step(phi, dt)
+        if st != P.PFC_OK:
+            raise RuntimeError(f"step failed at dt={dt}: status {st}")
+        dt = dt_next
         infos.append(info)
     return dt, infos
+
+
+def fp64_peak():
+    p = os.path.join(ROOT, "profiles", "fp64_peak_r01.json")
+    if os.path.exists(p):
+        return json.load(open(p))["fp64_dfma_tflops"], "measured (tools/fp64_peak.cu)"
+    return None, None
 
 
 def bench_cuda(args):
@@ -136,14 +152,14 @@ def bench_cuda(args):
 
     # ---- device-resident timed run
     phi = torch.from_numpy(phi0.copy()).cuda()
-    dt, _ = run_steps(ctx, phi, cfg.dt0, W)
+    dt, _ = run_steps(ctx, phi, cfg.dt0, W, cfg.dt_min)
     dt_first_timed = dt
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     barrier()
     l0 = ctx.launches
     with ClockSampler(local) as clk:
         e0.record(stream)
-        dt_end, infos = run_steps(ctx, phi, dt, K)
+        dt_end, infos = run_steps(ctx, phi, dt, K, cfg.dt_min)
         e1.record(stream)
         barrier()
     launches = ctx.launches - l0
@@ -153,10 +169,10 @@ def bench_cuda(args):
 
     # ---- end to end through the C ABI with a pinned host buffer (same trajectory)
     ph = torch.from_numpy(phi0.copy()).pin_memory()
-    dt, _ = run_steps(ctx, ph, cfg.dt0, W)
+    dt, _ = run_steps(ctx, ph, cfg.dt0, W, cfg.dt_min)
     barrier()
     e0.record(stream)
-    run_steps(ctx, ph, dt, K)
+    run_steps(ctx, ph, dt, K, cfg.dt_min)
     e1.record(stream)
     barrier()
     ms_e2e = max_over_ranks(e0.elapsed_time(e1))
@@ -165,9 +181,9 @@ def bench_cuda(args):
 
     # ---- per-kernel-class profile of the same K steps (separate pass; events per launch)
     phi = torch.from_numpy(phi0.copy()).cuda()
-    dt, _ = run_steps(ctx, phi, cfg.dt0, W)
+    dt, _ = run_steps(ctx, phi, cfg.dt0, W, cfg.dt_min)
     ctx.profile(True)
-    run_steps(ctx, phi, dt, K)
+    run_steps(ctx, phi, dt, K, cfg.dt_min)
     prof = ctx.profile_report()
     ctx.profile(False)
     hbm_peak, peak_kind = load_peaks()
@@ -183,14 +199,16 @@ def bench_cuda(args):
 
     def roofline_for(name, v):
         if name == "ras":
-            # FP64-ALU bound local solve: peak = 148 SMs x 64 FP64 FMA/clk x 2 flop x clock
-            clk_mhz = clocks.get("sm_mhz") or 1965.0
-            peak = 148 * 64 * 2 * clk_mhz * 1e6 / 1e12
+            # FP64-ALU bound local solve: measured DFMA peak (tools/fp64_peak.cu), else derived
+            # 148 SMs x 64 FP64 FMA/clk x 2 flop x median SM clock
+            peak, kind = fp64_peak()
+            if peak is None:
+                clk_mhz = clocks.get("sm_mhz") or 1965.0
+                peak, kind = 148 * 64 * 2 * clk_mhz * 1e6 / 1e12, "derived: 148 SM x 64 DFMA/clk x 2 x clock"
             ach = v["flops"] / (v["ms"] * 1e-3) / 1e12
             return {"kernel": "ras_apply", "bound": "alu", "achieved": round(ach, 3),
                     "peak": round(peak, 2), "unit": "TFLOP/s", "frac": round(ach / peak, 4),
-                    "peak_kind": "derived: 148 SM x 64 DFMA/clk x 2 x median SM clock",
-                    "traffic": None}
+                    "peak_kind": kind, "traffic": None}
         ach = v["bytes"] / (v["ms"] * 1e-3) / 1e9
         return {"kernel": name, "bound": "hbm", "achieved": round(ach, 1), "peak": hbm_peak,
                 "unit": "GB/s", "frac": round(ach / hbm_peak, 4), "peak_kind": peak_kind,
@@ -323,7 +341,7 @@ def bench_reference(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=197)   # W + K = 200 = config 2 run length
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="cuda", choices=["cuda", "reference"])
     ap.add_argument("--config", default="cfg2")

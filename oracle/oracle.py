@@ -63,6 +63,7 @@ def lib():
         L.or_num_boxes.argtypes = [G, PR]
         L.or_local_jacobian_apply.argtypes = [G, PR, C.c_double, _P, _P, _P]
         L.or_ras_apply.argtypes = [G, PR, C.c_double, _P, _P, _P, _P]
+        L.or_ras_apply_box.argtypes = [G, PR, C.c_double, _P, _P, _P, C.c_int, _P]
         L.or_fgmres.argtypes = [G, PR, C.c_double, _P, _P, _P, _P, C.c_int, C.POINTER(C.c_int)]
         L.or_newton.argtypes = [G, PR, C.c_double, _P, _P, _P, C.POINTER(NewtonInfo)]
         L.or_next_dt.argtypes = [C.c_double] * 6
@@ -159,6 +160,17 @@ def ras_apply(phi_new, phi_old, v, h, prm, dt):
     a, b, v = _f(phi_new), _f(phi_old), _f(v); out = np.zeros_like(a)
     lib().or_ras_apply(C.byref(_grid(_shape(a), h)), C.byref(prm), dt, _ptr(a), _ptr(b), _ptr(v),
                        _ptr(out))
+    return out
+
+
+def ras_apply_box(phi_new, phi_old, v, h, prm, dt, box):
+    """Owned-node output of one RAS box (numpy shape reversed(ras_box[:nd]))."""
+    a, b, v = _f(phi_new), _f(phi_old), _f(v)
+    nd = a.ndim
+    shp = tuple(reversed([prm.ras_box[d] for d in range(nd)]))
+    out = np.zeros(shp)
+    lib().or_ras_apply_box(C.byref(_grid(_shape(a), h)), C.byref(prm), dt, _ptr(a), _ptr(b),
+                           _ptr(v), int(box), _ptr(out))
     return out
 
 

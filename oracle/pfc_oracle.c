@@ -358,6 +358,43 @@ void or_ras_apply(const or_grid* g, const or_params* p, double dt, const double*
   free(r); free(c); free(y);
 }
 
+/* The contribution of ONE box k to the left-RAS output: its owned nodes of
+ * (R_k^0)^T inv(A_k) R_k^delta v, written to z_owned (b[0] x b[1] (x b[2]), x-fastest).  Same
+ * steps as the box loop of or_ras_apply; used to check sampled boxes at sizes where the full
+ * loop is too slow for a test. */
+void or_ras_apply_box(const or_grid* g, const or_params* p, double dt, const double* pn,
+                      const double* po, const double* v, int box, double* z_owned) {
+  int b[3] = {1, 1, 1}, nb[3] = {1, 1, 1}, E[3] = {1, 1, 1}, o[3] = {0, 0, 0};
+  for (int d = 0; d < g->nd; ++d) {
+    b[d] = p->ras_box[d];
+    nb[d] = g->n[d] / b[d];
+    o[d] = p->ras_overlap;
+    E[d] = b[d] + 2 * o[d];
+  }
+  int bx = box % nb[0], by = (box / nb[0]) % nb[1], bz = box / (nb[0] * nb[1]);
+  size_t n = (size_t)E[0] * E[1] * E[2];
+  double* r = alloc0(n);
+  double* c = alloc0(n);
+  double* y = alloc0(n);
+  int x0 = bx * b[0] - o[0], y0 = by * b[1] - o[1], z0 = bz * b[2] - o[2];
+  for (int k = 0; k < E[2]; ++k)
+    for (int j = 0; j < E[1]; ++j)
+      for (int i = 0; i < E[0]; ++i) {
+        size_t q = gidx(g, x0 + i, y0 + j, z0 + k);
+        size_t l = (size_t)i + (size_t)E[0] * ((size_t)j + (size_t)E[1] * k);
+        r[l] = v[q];
+        c[l] = (3.0 * pn[q] * pn[q] + 2.0 * pn[q] * po[q] + po[q] * po[q]) / 4.0;
+      }
+  local_gmres(g, p, dt, c, r, y, n);
+  for (int k = 0; k < b[2]; ++k)
+    for (int j = 0; j < b[1]; ++j)
+      for (int i = 0; i < b[0]; ++i) {
+        size_t l = (size_t)(i + o[0]) + (size_t)E[0] * ((size_t)(j + o[1]) + (size_t)E[1] * (k + o[2]));
+        z_owned[(size_t)i + (size_t)b[0] * ((size_t)j + (size_t)b[1] * k)] = y[l];
+      }
+  free(r); free(c); free(y);
+}
+
 /* ------------------------------------------------- Krylov, Newton, dt */
 
 /* Right-preconditioned GMRES, Eq. (hjacobi), in flexible form (FGMRES: the

@@ -54,6 +54,8 @@ void or_local_jacobian_apply(const or_grid* g, const or_params* p, double dt,
                              const double* c_loc, const double* v_loc, double* w_loc);
 void or_ras_apply(const or_grid* g, const or_params* p, double dt, const double* phi_new,
                   const double* phi_old, const double* v, double* z);
+void or_ras_apply_box(const or_grid* g, const or_params* p, double dt, const double* phi_new,
+                      const double* phi_old, const double* v, int box, double* z_owned);
 
 /* Krylov, Newton and time step control */
 int or_fgmres(const or_grid* g, const or_params* p, double dt, const double* phi_new,

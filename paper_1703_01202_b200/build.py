@@ -9,12 +9,13 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIBDIR = os.path.join(HERE, "lib")
-LIB = os.path.join(LIBDIR, "libpfc.so")
+LIB = os.path.join(LIBDIR, os.environ.get("PFC_LIB_NAME", "libpfc.so"))
 SOURCES = ["pfc.cu", "stencil2d.cu", "stencil3d.cu", "krylov.cu", "energy.cu", "ras2d.cu",
            "ras3d.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
          "-Xcompiler", "-fPIC", "-Xptxas", "-v", "--expt-relaxed-constexpr"]
+FLAGS += os.environ.get("PFC_EXTRA_NVCC_FLAGS", "").split()   # diagnostic builds only
 
 
 def _stale() -> bool:
@@ -29,7 +30,7 @@ def _stale() -> bool:
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not _stale():
         return LIB
-    objdir = os.path.join(HERE, "..", "build", "obj")
+    objdir = os.path.join(HERE, "..", "build", "obj" + os.environ.get("PFC_LIB_NAME", ""))
     os.makedirs(objdir, exist_ok=True)
     os.makedirs(LIBDIR, exist_ok=True)
 

@@ -8,7 +8,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "lib", "libpfc.so")
+LIB_PATH = os.environ.get("PFC_LIB_PATH", os.path.join(HERE, "lib", "libpfc.so"))
 
 PFC_OK, PFC_EINVAL, PFC_ENOMEM, PFC_ECUDA, PFC_ENOCONV, PFC_EBREAKDOWN = range(6)
 STATUS = {0: "PFC_OK", 1: "PFC_EINVAL", 2: "PFC_ENOMEM", 3: "PFC_ECUDA", 4: "PFC_ENOCONV",
