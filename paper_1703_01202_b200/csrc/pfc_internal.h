@@ -42,6 +42,7 @@ struct pfc_ctx {
   int ras_smem = 0;
   int ras_threads = 0;
   int ras_cluster = 1;
+  int ras_rows = 0;        // 2D column-strip RAS kernel: node rows per thread (0: other kernel)
 
   long long launches = 0;
   std::string err;

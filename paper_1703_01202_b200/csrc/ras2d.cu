@@ -346,276 +346,345 @@ __global__ void __launch_bounds__(NT, 1) ras2d_kernel(RasArgs p) {
 }
 
 // ---------------------------------------------------------------------------------------
-// Register-basis variant (extended boxes of up to SLOTS*NTT nodes, e.g. 36^2 on 384 threads x 4
-// slots; 12 warps = 3 per SM sub-partition leaves up to 168 registers per thread):
-// every thread keeps the K basis vectors of its own nodes in registers, so CGS2 touches no
-// shared memory at all; shared memory holds only c and the three zero-padded stencil planes.
-// Same arithmetic and order as ras2d_kernel (parity with the oracle).
-#ifdef PFC_RAS_PROFILE
-// diagnostic build only: thread 0 of block 0 records clock64() at phase boundaries and writes
-// the deltas over z[0..] at exit (the output is garbage in this build)
-#define RPROF(i) do { if (blockIdx.x == 0 && threadIdx.x == 0) prof_t[i] += clock64() - prof_last; \
-                      prof_last = clock64(); } while (0)
-#else
-#define RPROF(i) do {} while (0)
-#endif
+// Column-strip variant (the production path for extended boxes up to 42 x 42).
+//
+// Thread (x, s) owns the R nodes (x, sR .. sR+R-1) of the extended box for the whole solve:
+//  * the K basis vectors of its nodes live in registers, so CGS2 touches no shared memory;
+//  * the local J v is ONE pass of the direct 25-point stencil of the linear part
+//      w = v/dt - alpha Delta v - Delta^2 v - Delta^3 v / 2 - Delta(c v),  alpha = (1-gamma)/2
+//    (the class weights of h^2 Delta = L, L^2 and L^3 summed on the host) read
+//    column by column from the zero-padded plane of v (immediate offsets: the plane pitch is a
+//    compile-time 48), plus the 5-point Laplacian of c v from a second padded plane; one barrier
+//    per Arnoldi step for the stencil instead of three;
+//  * step j is dispatched to code specialised for J = j (compile-time CGS2 lengths, register
+//    indices and block-reduction widths), so no predicated K-long loops remain;
+//  * each block reduction is a warp reduce-scatter sized to the number of values (1, 2, 4, 8
+//    or 16), one barrier, and lane-parallel cross-warp sums: fixed order, deterministic.
+// Arithmetic: same algorithm as ras2d_kernel and the oracle (reading R9); the stencil sums the
+// 25 weighted terms instead of composing three 5-point Laplacians (rounding-level difference).
+constexpr int PP = 48;          // padded plane pitch (doubles): Ex + 6 <= 48
+constexpr int PPY = 56;         // padded plane rows: Ey + R + 5 <= 56
+constexpr int NTC = 384;        // threads per CTA at most (1 CTA per SM, <= 168 registers)
+constexpr int NWC = NTC / 32;
 
-template <int K, int SLOTS, int NTT>
-__global__ void __launch_bounds__(NTT, 1) ras2d_reg_kernel(RasArgs p) {
-#ifdef PFC_RAS_PROFILE
-  long long prof_t[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  long long prof_last = clock64();
-#endif
-  constexpr int NVP = pow2_at_least(K + 2);
-  constexpr int NWT = NTT / 32;
+struct RasColArgs {
+  const double* v;
+  const double* c;
+  double* z;
+  int nx, ny, bx, by, o;
+  int Ex, Ey, ns;               // extended box, strips per column
+  double W[6];                  // 25-point class weights: (0,0) (0,1) (0,2) (1,1) (0,3) (1,2)
+  double ih2;
+};
+
+constexpr int wclass(int ax, int ay) {
+  return (ax + ay == 0) ? 0 : (ax + ay == 1) ? 1 : (ax == 1 && ay == 1) ? 3
+         : (ax + ay == 2) ? 2 : (ax + ay == 3 && (ax == 0 || ay == 0)) ? 4 : 5;
+}
+constexpr int iabs(int a) { return a < 0 ? -a : a; }
+
+// Block all-reduce of NV values per thread (NV <= 16): totals in hw[0..NV) of this warp.
+template <int NV>
+__device__ __forceinline__ void col_allreduce(const double (&acc)[NV], double* red, double* hw,
+                                              int nwt) {
+  constexpr int NVP = pow2_at_least(NV);
+  constexpr int SH = 5 - (NVP == 1 ? 0 : NVP == 2 ? 1 : NVP == 4 ? 2 : NVP == 8 ? 3 : 4);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  double a[NVP];
+#pragma unroll
+  for (int i = 0; i < NVP; ++i) a[i] = i < NV ? acc[i] : 0.0;
+  const double s = warp_reduce_scatter<NVP>(a);
+  const int vi = lane >> SH;
+  if ((lane & ((1 << SH) - 1)) == 0 && vi < NV) red[wid * 16 + vi] = s;
+  __syncthreads();
+  if (lane < NV) {   // all partials loaded first, then a fixed pairwise tree (absent warps add 0)
+    double t[NWC];
+#pragma unroll
+    for (int w = 0; w < NWC; ++w) t[w] = w < nwt ? red[w * 16 + lane] : 0.0;
+#pragma unroll
+    for (int st = 1; st < NWC; st *= 2)
+#pragma unroll
+      for (int w = 0; w + st < NWC; w += 2 * st) t[w] += t[w + st];
+    hw[lane] = t[0];
+  }
+  __syncwarp();
+}
+
+// Tail of Arnoldi step J (after w = A_k v_J is in registers): CGS2, norm, next basis vector.
+// Returns true when the solve stops (exact breakdown).
+template <int K, int R, int J>
+__device__ __forceinline__ bool col_step(double (&Vr)[K][R], double (&w)[R], double (&cvv)[R],
+                                         const double (&cr)[R], const bool (&own)[R],
+                                         double* red, int& rb, double* h1, double* h2,
+                                         double* hx, double* H, double* cs, double* sn,
+                                         double* gv, double* pvb, double* pcvb, double beta,
+                                         int nwt) {
+  // pass 1: h1 = V^T w
+  {
+    double acc[J + 1];
+#pragma unroll
+    for (int i = 0; i <= J; ++i) {
+      double t = 0.0;
+#pragma unroll
+      for (int r = 0; r < R; ++r) t = fma(Vr[i][r], w[r], t);
+      acc[i] = t;
+    }
+    col_allreduce<J + 1>(acc, red + rb * NWC * 16, h1, nwt);
+    rb ^= 1;
+  }
+  // w' = w - V h1 ; pass 2: h2 = V^T w', |w'|^2 in slot J+1
+  {
+    double hv[J + 1];
+#pragma unroll
+    for (int i = 0; i <= J; ++i) hv[i] = h1[i];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      double ww = w[r];
+#pragma unroll
+      for (int i = 0; i <= J; ++i) ww = fma(-hv[i], Vr[i][r], ww);
+      w[r] = ww;
+    }
+    double acc[J + 2];
+#pragma unroll
+    for (int i = 0; i <= J; ++i) {
+      double t = 0.0;
+#pragma unroll
+      for (int r = 0; r < R; ++r) t = fma(Vr[i][r], w[r], t);
+      acc[i] = t;
+    }
+    double t = 0.0;
+#pragma unroll
+    for (int r = 0; r < R; ++r) t = fma(w[r], w[r], t);
+    acc[J + 1] = t;
+    col_allreduce<J + 2>(acc, red + rb * NWC * 16, h2, nwt);
+    rb ^= 1;
+  }
+  double hv[J + 1];
+  double h2n = 0.0;
+#pragma unroll
+  for (int i = 0; i <= J; ++i) {
+    hv[i] = h2[i];
+    h2n += hv[i] * hv[i];
+  }
+  const double wn2 = h2[J + 1];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    double ww = w[r];
+#pragma unroll
+    for (int i = 0; i <= J; ++i) ww = fma(-hv[i], Vr[i][r], ww);
+    w[r] = ww;
+  }
+  double hn2;
+  if (h2n <= 1e-8 * wn2) {
+    hn2 = wn2 - h2n;                                  // |w''|^2 = |w'|^2 - |h2|^2
+  } else {                                            // rare: explicit |w''|^2
+    double acc[1] = {0.0};
+#pragma unroll
+    for (int r = 0; r < R; ++r) acc[0] = fma(w[r], w[r], acc[0]);
+    col_allreduce<1>(acc, red + rb * NWC * 16, hx, nwt);
+    rb ^= 1;
+    hn2 = hx[0];
+  }
+  const double hn = sqrt(hn2 > 0.0 ? hn2 : 0.0);
+  if (threadIdx.x == 0) {
+    // Hessenberg column J, reduced at once by the previous Givens rotations and a new one, in
+    // the oracle's incremental order (registers; rotations and the R factor kept in shared)
+    double col[J + 2];
+    double cp[J + 1], sp[J + 1];
+#pragma unroll
+    for (int i = 0; i < J; ++i) { cp[i] = cs[i]; sp[i] = sn[i]; }
+#pragma unroll
+    for (int i = 0; i <= J; ++i) col[i] = h1[i] + h2[i];
+    col[J + 1] = hn;
+#pragma unroll
+    for (int i = 0; i < J; ++i) {
+      const double a = col[i], b = col[i + 1];
+      col[i] = cp[i] * a + sp[i] * b;
+      col[i + 1] = -sp[i] * a + cp[i] * b;
+    }
+    const double a = col[J], b = col[J + 1];
+    const double rr = sqrt(a * a + b * b);
+    double cc = 1.0, ss = 0.0;
+    if (rr != 0.0) { cc = a / rr; ss = b / rr; }
+    cs[J] = cc; sn[J] = ss;
+    col[J] = cc * a + ss * b;
+    const double g = gv[J];
+    gv[J + 1] = -ss * g;
+    gv[J] = cc * g;
+#pragma unroll
+    for (int i = 0; i <= J; ++i) H[i + (K + 1) * J] = col[i];
+  }
+  if (hn <= 1e-14 * beta) return true;               // exact breakdown (uniform)
+  if constexpr (J + 1 < K) {
+    const double ihn = 1.0 / hn;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const double vn = w[r] * ihn;
+      Vr[J + 1][r] = vn;
+      cvv[r] = cr[r] * vn;
+      if (own[r]) {
+        pvb[r * PP] = vn;
+        pcvb[r * PP] = cvv[r];
+      }
+    }
+  }
+  return false;
+}
+
+template <int K, int R, int J>
+__device__ __forceinline__ bool col_dispatch(int j, double (&Vr)[K][R], double (&w)[R],
+                                             double (&cvv)[R], const double (&cr)[R],
+                                             const bool (&own)[R], double* red, int& rb,
+                                             double* h1, double* h2, double* hx, double* H,
+                                             double* cs, double* sn, double* gv, double* pvb,
+                                             double* pcvb, double beta, int nwt) {
+  if constexpr (J < K) {
+    if (j == J)
+      return col_step<K, R, J>(Vr, w, cvv, cr, own, red, rb, h1, h2, hx, H, cs, sn, gv, pvb,
+                               pcvb, beta, nwt);
+    return col_dispatch<K, R, J + 1>(j, Vr, w, cvv, cr, own, red, rb, h1, h2, hx, H, cs, sn, gv,
+                                     pvb, pcvb, beta, nwt);
+  } else {
+    return true;
+  }
+}
+
+template <int K, int R>
+__global__ void __launch_bounds__(NTC, 1) ras2d_col_kernel(const __grid_constant__ RasColArgs p) {
   extern __shared__ __align__(128) double smem_dyn[];
-  const int Ex = p.bx + 2 * p.o, Ey = p.by + 2 * p.o;
-  const int n = Ex * Ey;
-  const int Px = Ex + 6, Py = Ey + 6;
-  const int np = Px * Py;
-  double* cl = smem_dyn;                 // n
-  double* pv = cl + n;                   // np (zero ring)
-  double* pl = pv + np;                  // np
-  double* pb = pl + np;                  // np
-  double* red = pb + np;                 // 2 x NWT x NVP
-  double* hwall = red + 2 * NWT * NVP;   // NWT x 3 NVP
+  double* pv = smem_dyn;                     // PP x PPY padded v (zero ring)
+  double* pcv = pv + PP * PPY;               // PP x PPY padded c v
+  double* red = pcv + PP * PPY;              // 2 x NWC x 16
+  double* hwall = red + 2 * NWC * 16;        // NWC x 3 x 16
   __shared__ double H[(K + 1) * K];
   __shared__ double gv[K + 1], cs[K], sn[K], yv[K];
 
-  const int tid = threadIdx.x;
-  double* h1 = hwall + (tid >> 5) * 3 * NVP;
-  double* h2 = h1 + NVP;
-  double* hx = h2 + NVP;
+  const int tid = threadIdx.x, nwt = blockDim.x >> 5;
+  double* h1 = hwall + (tid >> 5) * 48;
+  double* h2 = h1 + 16;
+  double* hx = h2 + 16;
+  const int Ex = p.Ex, Ey = p.Ey;
   const int nbx = p.nx / p.bx;
   const int ibx = blockIdx.x % nbx, iby = blockIdx.x / nbx;
   const int gx0 = ibx * p.bx - p.o, gy0 = iby * p.by - p.o;
-  const double ih2 = p.ih2, idt = p.idt, alpha = 0.5 * (1.0 - p.gamma);
 
-  int pidx[SLOTS];
-  bool own[SLOTS];
+  const int xs = tid % Ex, ss = tid / Ex;
+  const bool active = ss < p.ns;
+  const int x = active ? xs : 0, y0 = active ? ss * R : 0;   // inactive threads read in-bounds
+  bool own[R];
 #pragma unroll
-  for (int s = 0; s < SLOTS; ++s) {
-    const int l = tid + s * NTT;
-    own[s] = l < n;
-    pidx[s] = own[s] ? ((l / Ex) + 3) * Px + (l % Ex) + 3 : 0;
-  }
-  for (int q = tid; q < 3 * np; q += NTT) pv[q] = 0.0;
-  double Vr[K][SLOTS];                    // basis, own nodes
-  double w[SLOTS];
-  double acc[NVP];
+  for (int r = 0; r < R; ++r) own[r] = active && (y0 + r < Ey);
+  double* pvb = pv + (y0 + 3) * PP + x + 3;
+  double* pcvb = pcv + (y0 + 3) * PP + x + 3;
+
+  for (int q = tid; q < 2 * PP * PPY; q += blockDim.x) pv[q] = 0.0;
+  // gather R_k^delta v and c (periodic wrap)
+  double Vr[K][R];
+  double w[R], cr[R], cvv[R];
+  double acc0[1] = {0.0};
 #pragma unroll
-  for (int i = 0; i < NVP; ++i) acc[i] = 0.0;
-#pragma unroll
-  for (int s = 0; s < SLOTS; ++s) {
-    w[s] = 0.0;
-    if (own[s]) {
-      const int l = tid + s * NTT;
-      const size_t g = (size_t)wrapi(gx0 + l % Ex, p.nx) + (size_t)p.nx * wrapi(gy0 + l / Ex, p.ny);
-      w[s] = p.v[g];
-      cl[l] = p.c[g];
-      acc[0] += w[s] * w[s];
+  for (int r = 0; r < R; ++r) {
+    w[r] = 0.0;
+    cr[r] = 0.0;
+    if (own[r]) {
+      const size_t g = (size_t)wrapi(gx0 + x, p.nx) + (size_t)p.nx * wrapi(gy0 + y0 + r, p.ny);
+      w[r] = p.v[g];
+      cr[r] = p.c[g];
+      acc0[0] = fma(w[r], w[r], acc0[0]);
     }
   }
   int rb = 0;
-  block_allreduce<NVP, NWT>(acc, 1, red + rb * NWT * NVP, hx);
+  col_allreduce<1>(acc0, red + rb * NWC * 16, hx, nwt);   // also orders the zero fill
   rb ^= 1;
   const double beta = sqrt(hx[0]);
   if (beta == 0.0) {
-    for (int l = tid; l < p.bx * p.by; l += NTT)
-      p.z[(size_t)(ibx * p.bx + l % p.bx) + (size_t)p.nx * (iby * p.by + l / p.bx)] = 0.0;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int li = x - p.o, lj = y0 + r - p.o;
+      if (own[r] && li >= 0 && li < p.bx && lj >= 0 && lj < p.by)
+        p.z[(size_t)(ibx * p.bx + li) + (size_t)p.nx * (iby * p.by + lj)] = 0.0;
+    }
     return;
   }
   {
     const double ib = 1.0 / beta;
 #pragma unroll
-    for (int s = 0; s < SLOTS; ++s) {
-      const double v0 = w[s] * ib;
-      Vr[0][s] = v0;
-      if (own[s]) pv[pidx[s]] = v0;
+    for (int r = 0; r < R; ++r) {
+      const double v0 = w[r] * ib;
+      Vr[0][r] = v0;
+      cvv[r] = cr[r] * v0;
+      if (own[r]) {
+        pvb[r * PP] = v0;
+        pcvb[r * PP] = cvv[r];
+      }
     }
   }
   if (tid == 0) gv[0] = beta;
 
-  const int wxL = Px - 2, cntL = wxL * (Py - 2), r0L = tid / wxL, c0L = tid % wxL;
-  const int wxB = Px - 4, cntB = wxB * (Py - 4), r0B = tid / wxB, c0B = tid % wxB;
-  const int drL = NTT / wxL, dcL = NTT % wxL, drB = NTT / wxB, dcB = NTT % wxB;
-
   int jm = 0;
-  RPROF(0);
 #pragma unroll 1
   for (int j = 0; j < K; ++j) {
-    __syncthreads();                                   // pv holds V_j
-    RPROF(1);
-    {   // L1 = Delta v on padded [1, P-1)
-      int r = r0L, c = c0L;
-      for (int q = tid; q < cntL; q += NTT) {
-        const int f = (1 + r) * Px + 1 + c;
-        pl[f] = ih2 * ((pv[f - 1] + pv[f + 1]) + (pv[f - Px] + pv[f + Px]) - 4.0 * pv[f]);
-        r += drL; c += dcL;
-        if (c >= wxL) { c -= wxL; ++r; }
-      }
+    __syncthreads();                                  // planes hold v_j and c v_j
+    // ---- w = A_k v_j: direct 25-point linear part, column by column
+    double out[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) out[r] = 0.0;
+#pragma unroll
+    for (int dx = -3; dx <= 3; ++dx) {
+      const int a = 3 - iabs(dx);
+      double col[R + 6];
+#pragma unroll
+      for (int rr = -a; rr < R + a; ++rr) col[rr + a] = pvb[rr * PP + dx];
+#pragma unroll
+      for (int r = 0; r < R; ++r)
+#pragma unroll
+        for (int dy = -a; dy <= a; ++dy)
+          out[r] = fma(p.W[wclass(iabs(dx), iabs(dy))], col[r + dy + a], out[r]);
     }
-    __syncthreads();
-    {   // B on padded [2, P-2); c v = 0 outside the extended box
-      int r = r0B, c = c0B;
-      for (int q = tid; q < cntB; q += NTT) {
-        const int pi = 2 + c, pj = 2 + r;
-        r += drB; c += dcB;
-        if (c >= wxB) { c -= wxB; ++r; }
-        const int f = pj * Px + pi;
-        const double vv = pv[f];
-        const int li = pi - 3, lj = pj - 3;
-        const double cv = (li >= 0 && li < Ex && lj >= 0 && lj < Ey) ? cl[lj * Ex + li] * vv : 0.0;
-        const double lapl = ih2 * ((pl[f - 1] + pl[f + 1]) + (pl[f - Px] + pl[f + Px]) - 4.0 * pl[f]);
-        pb[f] = alpha * vv + cv + pl[f] + 0.5 * lapl;
-      }
+    // ---- minus Delta(c v): x-neighbours from the plane, y-neighbours from registers
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const double up = (r == 0) ? pcvb[-PP] : cvv[r - 1];
+      const double dn = (r == R - 1) ? pcvb[R * PP] : cvv[r + 1];
+      const double lap = (pcvb[r * PP - 1] + pcvb[r * PP + 1]) + (up + dn) - 4.0 * cvv[r];
+      w[r] = own[r] ? fma(-p.ih2, lap, out[r]) : 0.0;
     }
-    __syncthreads();
-    RPROF(2);
-    // w = v/dt - Delta B (registers); CGS2 pass 1: h1 = V^T w
-#pragma unroll
-    for (int i = 0; i < NVP; ++i) acc[i] = 0.0;
-#pragma unroll
-    for (int s = 0; s < SLOTS; ++s) {
-      if (own[s]) {
-        const int f = pidx[s];
-        const double lapb = ih2 * ((pb[f - 1] + pb[f + 1]) + (pb[f - Px] + pb[f + Px]) - 4.0 * pb[f]);
-        w[s] = pv[f] * idt - lapb;
-      } else {
-        w[s] = 0.0;
-      }
-#pragma unroll
-      for (int i = 0; i < K; ++i) {
-        if (i > j) break;
-        acc[i] += Vr[i][s] * w[s];
-      }
-    }
-    RPROF(3);
-    block_allreduce<NVP, NWT>(acc, j + 1, red + rb * NWT * NVP, h1);
-    rb ^= 1;
-    RPROF(4);
-    // w' = w - V h1 ; pass 2: h2 = V^T w' and |w'|^2 (norm slot NVP-1)
-#pragma unroll
-    for (int i = 0; i < NVP; ++i) acc[i] = 0.0;
-#pragma unroll
-    for (int s = 0; s < SLOTS; ++s) {
-      double ww = w[s];
-#pragma unroll
-      for (int i = 0; i < K; ++i) {
-        if (i > j) break;
-        ww -= h1[i] * Vr[i][s];
-      }
-#pragma unroll
-      for (int i = 0; i < K; ++i) {
-        if (i > j) break;
-        acc[i] += Vr[i][s] * ww;
-      }
-      acc[NVP - 1] += ww * ww;
-      w[s] = ww;
-    }
-    RPROF(5);
-    block_allreduce<NVP, NWT>(acc, j + 1, red + rb * NWT * NVP, h2, true);
-    rb ^= 1;
-    RPROF(6);
-    const double wn2 = h2[NVP - 1];
-    double h2n = 0.0;
-    for (int i = 0; i <= j; ++i) h2n += h2[i] * h2[i];
-#pragma unroll
-    for (int s = 0; s < SLOTS; ++s) {
-      double ww = w[s];
-#pragma unroll
-      for (int i = 0; i < K; ++i) {
-        if (i > j) break;
-        ww -= h2[i] * Vr[i][s];
-      }
-      w[s] = ww;
-    }
-    double hn2;
-    if (h2n <= 1e-8 * wn2) {
-      hn2 = wn2 - h2n;                                  // |w''|^2 = |w'|^2 - |h2|^2
-    } else {                                            // rare: explicit |w''|^2
-#pragma unroll
-      for (int i = 0; i < NVP; ++i) acc[i] = 0.0;
-#pragma unroll
-      for (int s = 0; s < SLOTS; ++s) acc[0] += w[s] * w[s];
-      block_allreduce<NVP, NWT>(acc, 1, red + rb * NWT * NVP, hx);
-      rb ^= 1;
-      hn2 = hx[0];
-    }
-    const double hn = sqrt(hn2 > 0.0 ? hn2 : 0.0);
-    if (tid == 0) {
-      const int ld = K + 1;
-      for (int i = 0; i <= j; ++i) H[i + ld * j] = h1[i] + h2[i];
-      H[j + 1 + ld * j] = hn;
-    }
+    const bool stop = col_dispatch<K, R, 0>(j, Vr, w, cvv, cr, own, red, rb, h1, h2, hx, H, cs,
+                                            sn, gv, pvb, pcvb, beta, nwt);
     jm = j + 1;
-    if (hn <= 1e-14 * beta) break;                     // exact breakdown (uniform)
-    if (j + 1 < K) {
-      const double ihn = 1.0 / hn;
-#pragma unroll
-      for (int s = 0; s < SLOTS; ++s) {
-        const double vn = w[s] * ihn;
-#pragma unroll
-        for (int i = 1; i < K; ++i)
-          if (i == j + 1) Vr[i][s] = vn;               // compile-time register index
-        if (own[s]) pv[pidx[s]] = vn;
-      }
-    }
-    RPROF(7);
+    if (stop) break;
   }
   __syncthreads();
-#ifdef PFC_RAS_PROFILE
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    for (int i = 0; i < 8; ++i) p.z[i] = (double)prof_t[i];
-  }
-  return;
-#endif
-  if (tid == 0) {
+  if (tid == 0) {   // back substitution R yv = g (R already reduced column by column)
     const int ld = K + 1;
-    for (int j = 0; j < jm; ++j) {
-      for (int i = 0; i < j; ++i) {
-        const double a = H[i + ld * j], b = H[i + 1 + ld * j];
-        H[i + ld * j] = cs[i] * a + sn[i] * b;
-        H[i + 1 + ld * j] = -sn[i] * a + cs[i] * b;
-      }
-      const double a = H[j + ld * j], b = H[j + 1 + ld * j];
-      const double r = sqrt(a * a + b * b);
-      double cc = 1.0, ss = 0.0;
-      if (r != 0.0) { cc = a / r; ss = b / r; }
-      cs[j] = cc; sn[j] = ss;
-      H[j + ld * j] = cc * a + ss * b;
-      H[j + 1 + ld * j] = 0.0;
-      gv[j + 1] = -ss * gv[j];
-      gv[j] = cc * gv[j];
-    }
-    for (int i = jm - 1; i >= 0; --i) {
-      double s2 = gv[i];
-      for (int l = i + 1; l < jm; ++l) s2 -= H[i + ld * l] * yv[l];
-      yv[i] = s2 / H[i + ld * i];
+    double y[K];
+#pragma unroll
+    for (int i = K - 1; i >= 0; --i) {
+      if (i >= jm) continue;
+      double sacc = gv[i];
+#pragma unroll
+      for (int l = i + 1; l < K; ++l)
+        if (l < jm) sacc -= H[i + ld * l] * y[l];
+      y[i] = sacc / H[i + ld * i];
+      yv[i] = y[i];
     }
   }
   __syncthreads();
   // (R_k^0)^T: the owner thread of each owned node writes y = V yv
 #pragma unroll
-  for (int s = 0; s < SLOTS; ++s) {
-    if (!own[s]) continue;
-    const int l = tid + s * NTT;
-    const int li = l % Ex - p.o, lj = l / Ex - p.o;
-    if (li < 0 || li >= p.bx || lj < 0 || lj >= p.by) continue;
-    double acc2 = 0.0;
+  for (int r = 0; r < R; ++r) {
+    const int li = x - p.o, lj = y0 + r - p.o;
+    if (!own[r] || li < 0 || li >= p.bx || lj < 0 || lj >= p.by) continue;
+    double s = 0.0;
 #pragma unroll
-    for (int i = 0; i < K; ++i) {
-      if (i >= jm) break;
-      acc2 += yv[i] * Vr[i][s];
-    }
-    p.z[(size_t)(ibx * p.bx + li) + (size_t)p.nx * (iby * p.by + lj)] = acc2;
+    for (int i = 0; i < K; ++i)
+      if (i < jm) s = fma(yv[i], Vr[i][r], s);
+    p.z[(size_t)(ibx * p.bx + li) + (size_t)p.nx * (iby * p.by + lj)] = s;
   }
 }
 
-size_t ras2d_reg_smem_bytes(int bx, int by, int o, int ntt) {
-  const size_t Ex = bx + 2 * o, Ey = by + 2 * o, n = Ex * Ey, np = (Ex + 6) * (Ey + 6);
-  const size_t nw = ntt / 32;
-  return (n + 3 * np + 2 * nw * 16 + nw * 3 * 16) * sizeof(double);
+size_t ras2d_col_smem_bytes() {
+  return (size_t)(2 * PP * PPY + 2 * NWC * 16 + NWC * 48) * sizeof(double);
 }
 
 typedef void (*ras2d_fn)(RasArgs);
@@ -634,18 +703,35 @@ ras2d_fn pick(int k) {
   return nullptr;
 }
 
-// register-basis instantiations: (SLOTS, threads) covering extended boxes up to SLOTS*threads
-ras2d_fn pick_reg(int k, int n, int* ntt) {
-#define RK(K)                                                                       \
-  case K:                                                                           \
-    if (n <= 256 * 2) { *ntt = 256; return ras2d_reg_kernel<K, 2, 256>; }         \
-    if (n <= 384 * 4) { *ntt = 384; return ras2d_reg_kernel<K, 4, 384>; }         \
+// column-strip instantiations: local GMRES steps K x rows per thread R
+typedef void (*ras2d_col_fn)(const RasColArgs);
+ras2d_col_fn pick_col(int k, int r) {
+#define RC(K)                                              \
+  case K:                                                  \
+    switch (r) {                                           \
+      case 1: return ras2d_col_kernel<K, 1>;               \
+      case 2: return ras2d_col_kernel<K, 2>;               \
+      case 4: return ras2d_col_kernel<K, 4>;               \
+      case 5: return ras2d_col_kernel<K, 5>;               \
+    }                                                      \
     return nullptr;
   switch (k) {
-    RK(1) RK(2) RK(3) RK(4) RK(5) RK(6) RK(7) RK(8) RK(9) RK(10) RK(11) RK(12)
+    RC(4) RC(5) RC(6) RC(8) RC(10) RC(12)
   }
-#undef RK
+#undef RC
   return nullptr;
+}
+
+// rows per thread for the column kernel: the fewest that fit the extended box in NTC threads
+int col_rows(int k, int Ex, int Ey) {
+  if (Ex + 6 > PP || Ey > 42) return 0;
+  const int cand[4] = {1, 2, 4, 5};
+  for (int i = 0; i < 4; ++i) {
+    const int r = cand[i];
+    const int ns = (Ey + r - 1) / r;
+    if (Ex * ns <= NTC && pick_col(k, r)) return r;
+  }
+  return 0;
 }
 
 }  // namespace
@@ -654,42 +740,67 @@ int ras2d_plan(pfc_ctx* ctx) {
   const pfc_config& c = ctx->cfg;
   const int Ex = c.ras_box[0] + 2 * c.ras_overlap, Ey = c.ras_box[1] + 2 * c.ras_overlap;
   if (Ex * Ey > MAXN) return 0;
-  int ntt = 0;
-  if (getenv("PFC_RAS_SMEM_BASIS") == nullptr && pick_reg(c.ras_local_k, Ex * Ey, &ntt)) {
-    ctx->ras_smem = (int)ras2d_reg_smem_bytes(c.ras_box[0], c.ras_box[1], c.ras_overlap, ntt);
-    ctx->ras_threads = ntt;     // register-basis kernel
-    ctx->ras_cluster = 0;
-    return 1;
+  if (getenv("PFC_RAS_SMEM_BASIS") == nullptr) {
+    const int r = col_rows(c.ras_local_k, Ex, Ey);
+    if (r) {
+      const int ns = (Ey + r - 1) / r;
+      ctx->ras_smem = (int)ras2d_col_smem_bytes();
+      ctx->ras_threads = (Ex * ns + 31) / 32 * 32;   // column-strip kernel
+      ctx->ras_rows = r;                             // rows per thread
+      return 1;
+    }
   }
   size_t sm = ras2d_smem_bytes(c.ras_box[0], c.ras_box[1], c.ras_overlap, c.ras_local_k);
   if (sm + 2048 > 227 * 1024) return 0;   // + static shared memory (H, Givens, reductions)
   ctx->ras_smem = (int)sm;
   ctx->ras_threads = NT;        // shared-memory-basis kernel
-  ctx->ras_cluster = 1;
+  ctx->ras_rows = 0;
   return 1;
 }
 
 cudaError_t launch_ras_2d(pfc_ctx* ctx, const double* v, const double* c, double dt, double* z) {
   const pfc_config& cf = ctx->cfg;
   const int Ex = cf.ras_box[0] + 2 * cf.ras_overlap, Ey = cf.ras_box[1] + 2 * cf.ras_overlap;
-  int ntt = NT;
-  ras2d_fn fn = ctx->ras_cluster == 0 ? pick_reg(cf.ras_local_k, Ex * Ey, &ntt)
-                                      : pick(cf.ras_local_k);
-  if (!fn) return cudaErrorInvalidValue;
-  // opt in to the dynamic shared memory once per kernel
-  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       ctx->ras_smem);
-  if (e != cudaSuccess) return e;
-  RasArgs p{v, c, z, cf.n[0], cf.n[1], cf.ras_box[0], cf.ras_box[1], cf.ras_overlap,
-            1.0 / dt, cf.gamma, ctx->ih2};
   const int nb = (cf.n[0] / cf.ras_box[0]) * (cf.n[1] / cf.ras_box[1]);
-  fn<<<nb, ntt, ctx->ras_smem, ctx->stream>>>(p);
+  cudaError_t e;
+  if (ctx->ras_rows > 0) {
+    const int R = ctx->ras_rows;
+    ras2d_col_fn fn = pick_col(cf.ras_local_k, R);
+    if (!fn) return cudaErrorInvalidValue;
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, ctx->ras_smem);
+    if (e != cudaSuccess) return e;
+    RasColArgs p{};
+    p.v = v; p.c = c; p.z = z;
+    p.nx = cf.n[0]; p.ny = cf.n[1]; p.bx = cf.ras_box[0]; p.by = cf.ras_box[1];
+    p.o = cf.ras_overlap; p.Ex = Ex; p.Ey = Ey; p.ns = (Ey + R - 1) / R;
+    // class weights of the linear part v/dt - alpha Delta v - Delta^2 v - Delta^3 v / 2 with
+    // h^2 Delta = L:  L (0,0) -4, (0,1) 1;  L^2 (0,0) 20, (0,1) -8, (0,2) 1, (1,1) 2;
+    // L^3 (0,0) -112, (0,1) 57, (0,2) -12, (1,1) -24, (0,3) 1, (1,2) 3
+    const double ih2 = ctx->ih2, ih4 = ih2 * ih2, ih6 = ih4 * ih2;
+    const double al = 0.5 * (1.0 - cf.gamma);
+    p.W[0] = 1.0 / dt + 4.0 * al * ih2 - 20.0 * ih4 + 56.0 * ih6;
+    p.W[1] = -al * ih2 + 8.0 * ih4 - 28.5 * ih6;
+    p.W[2] = -ih4 + 6.0 * ih6;
+    p.W[3] = -2.0 * ih4 + 12.0 * ih6;
+    p.W[4] = -0.5 * ih6;
+    p.W[5] = -1.5 * ih6;
+    p.ih2 = ih2;
+    fn<<<nb, ctx->ras_threads, ctx->ras_smem, ctx->stream>>>(p);
+  } else {
+    ras2d_fn fn = pick(cf.ras_local_k);
+    if (!fn) return cudaErrorInvalidValue;
+    // opt in to the dynamic shared memory once per kernel
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, ctx->ras_smem);
+    if (e != cudaSuccess) return e;
+    RasArgs p{v, c, z, cf.n[0], cf.n[1], cf.ras_box[0], cf.ras_box[1], cf.ras_overlap,
+              1.0 / dt, cf.gamma, ctx->ih2};
+    fn<<<nb, NT, ctx->ras_smem, ctx->stream>>>(p);
+  }
   ctx->launches++;
   {  // algorithmic: v, c gathered on the extended boxes, z written on owned nodes; flops of
      // k local J v (25/pt) + CGS2 vector work 4k(k+1) + 3k + 3 per ext node + V y
     const double k = cf.ras_local_k;
-    const double next = (double)nb * (cf.ras_box[0] + 2 * cf.ras_overlap) *
-                        (cf.ras_box[1] + 2 * cf.ras_overlap);
+    const double next = (double)nb * Ex * Ey;
     pfc_account(ctx, PFC_K_RAS, 8.0 * (2.0 * next + ctx->N),
                 next * (25.0 * k + 4.0 * k * (k + 1) + 3.0 * k + 3.0) + 2.0 * k * ctx->N);
   }
