@@ -412,13 +412,71 @@ __device__ __forceinline__ void col_allreduce(const double (&acc)[NV], double* r
 
 // Tail of Arnoldi step J (after w = A_k v_J is in registers): CGS2, norm, next basis vector.
 // Returns true when the solve stops (exact breakdown).
+// Hessenberg column J (h1 + h2, hn) reduced by the previous Givens rotations and a new one,
+// in the oracle's incremental order; R column, rotation and 1/R_JJ kept in shared memory.
+// Run by lane 0 of the Givens warp one phase late (during the next step's stencil).
+template <int K, int J>
+__device__ __forceinline__ void col_givens(const double* h1, const double* h2, double hn,
+                                           double* cs, double* sn, double* gv, double* H,
+                                           double* rd) {
+  double col[J + 2];
+  double cp[J + 1], sp[J + 1];
+#pragma unroll
+  for (int i = 0; i < J; ++i) { cp[i] = cs[i]; sp[i] = sn[i]; }
+#pragma unroll
+  for (int i = 0; i <= J; ++i) col[i] = h1[i] + h2[i];
+  col[J + 1] = hn;
+#pragma unroll
+  for (int i = 0; i < J; ++i) {
+    const double a = col[i], b = col[i + 1];
+    col[i] = cp[i] * a + sp[i] * b;
+    col[i + 1] = -sp[i] * a + cp[i] * b;
+  }
+  const double a = col[J], b = col[J + 1];
+  const double rr = sqrt(a * a + b * b);
+  double cc = 1.0, ss = 0.0;
+  if (rr != 0.0) { cc = a / rr; ss = b / rr; }
+  cs[J] = cc; sn[J] = ss;
+  col[J] = cc * a + ss * b;
+  const double g = gv[J];
+  gv[J + 1] = -ss * g;
+  gv[J] = cc * g;
+  rd[J] = 1.0 / col[J];
+#pragma unroll
+  for (int i = 0; i <= J; ++i) H[i + (K + 1) * J] = col[i];
+}
+
+template <int K, int J>
+__device__ __forceinline__ void col_givens_dispatch(int j, const double* h1, const double* h2,
+                                                    double hn, double* cs, double* sn, double* gv,
+                                                    double* H, double* rd) {
+  if constexpr (J < K) {
+    if (j == J) col_givens<K, J>(h1, h2, hn, cs, sn, gv, H, rd);
+    else col_givens_dispatch<K, J + 1>(j, h1, h2, hn, cs, sn, gv, H, rd);
+  }
+}
+
+#ifdef PFC_RAS_PROFILE
+// diagnostic build only: thread 0 of block 0 accumulates clock64() deltas per phase into the
+// global array ras_prof (read back by tools/ras_phase_probe.py)
+__device__ long long ras_prof[8];
+__device__ long long ras_prof_last;
+#define CPROF(i) do { if (blockIdx.x == 0 && threadIdx.x == 0) { long long t_ = clock64(); \
+    ras_prof[i] += t_ - ras_prof_last; ras_prof_last = t_; } } while (0)
+#else
+#define CPROF(i) do {} while (0)
+#endif
+
 template <int K, int R, int J>
 __device__ __forceinline__ bool col_step(double (&Vr)[K][R], double (&w)[R], double (&cvv)[R],
                                          const double (&cr)[R], const bool (&own)[R],
                                          double* red, int& rb, double* h1, double* h2,
                                          double* hx, double* H, double* cs, double* sn,
-                                         double* gv, double* pvb, double* pcvb, double beta,
-                                         int nwt) {
+                                         double* gv, double* rd, double* pvb, double* pcvb,
+                                         double beta, int nwt, bool g0, double& hn_prev) {
+  if constexpr (J > 0) {
+    if (g0) col_givens<K, J - 1>(h1, h2, hn_prev, cs, sn, gv, H, rd);
+  }
   // pass 1: h1 = V^T w
   {
     double acc[J + 1];
@@ -432,6 +490,7 @@ __device__ __forceinline__ bool col_step(double (&Vr)[K][R], double (&w)[R], dou
     col_allreduce<J + 1>(acc, red + rb * NWC * 16, h1, nwt);
     rb ^= 1;
   }
+  CPROF(3);
   // w' = w - V h1 ; pass 2: h2 = V^T w', |w'|^2 in slot J+1
   {
     double hv[J + 1];
@@ -459,6 +518,7 @@ __device__ __forceinline__ bool col_step(double (&Vr)[K][R], double (&w)[R], dou
     col_allreduce<J + 2>(acc, red + rb * NWC * 16, h2, nwt);
     rb ^= 1;
   }
+  CPROF(4);
   double hv[J + 1];
   double h2n = 0.0;
 #pragma unroll
@@ -486,34 +546,7 @@ __device__ __forceinline__ bool col_step(double (&Vr)[K][R], double (&w)[R], dou
     hn2 = hx[0];
   }
   const double hn = sqrt(hn2 > 0.0 ? hn2 : 0.0);
-  if (threadIdx.x == 0) {
-    // Hessenberg column J, reduced at once by the previous Givens rotations and a new one, in
-    // the oracle's incremental order (registers; rotations and the R factor kept in shared)
-    double col[J + 2];
-    double cp[J + 1], sp[J + 1];
-#pragma unroll
-    for (int i = 0; i < J; ++i) { cp[i] = cs[i]; sp[i] = sn[i]; }
-#pragma unroll
-    for (int i = 0; i <= J; ++i) col[i] = h1[i] + h2[i];
-    col[J + 1] = hn;
-#pragma unroll
-    for (int i = 0; i < J; ++i) {
-      const double a = col[i], b = col[i + 1];
-      col[i] = cp[i] * a + sp[i] * b;
-      col[i + 1] = -sp[i] * a + cp[i] * b;
-    }
-    const double a = col[J], b = col[J + 1];
-    const double rr = sqrt(a * a + b * b);
-    double cc = 1.0, ss = 0.0;
-    if (rr != 0.0) { cc = a / rr; ss = b / rr; }
-    cs[J] = cc; sn[J] = ss;
-    col[J] = cc * a + ss * b;
-    const double g = gv[J];
-    gv[J + 1] = -ss * g;
-    gv[J] = cc * g;
-#pragma unroll
-    for (int i = 0; i <= J; ++i) H[i + (K + 1) * J] = col[i];
-  }
+  hn_prev = hn;                     // the Givens warp reduces column J during step J+1
   if (hn <= 1e-14 * beta) return true;               // exact breakdown (uniform)
   if constexpr (J + 1 < K) {
     const double ihn = 1.0 / hn;
@@ -536,14 +569,15 @@ __device__ __forceinline__ bool col_dispatch(int j, double (&Vr)[K][R], double (
                                              double (&cvv)[R], const double (&cr)[R],
                                              const bool (&own)[R], double* red, int& rb,
                                              double* h1, double* h2, double* hx, double* H,
-                                             double* cs, double* sn, double* gv, double* pvb,
-                                             double* pcvb, double beta, int nwt) {
+                                             double* cs, double* sn, double* gv, double* rd,
+                                             double* pvb, double* pcvb, double beta, int nwt,
+                                             bool g0, double& hn_prev) {
   if constexpr (J < K) {
     if (j == J)
-      return col_step<K, R, J>(Vr, w, cvv, cr, own, red, rb, h1, h2, hx, H, cs, sn, gv, pvb,
-                               pcvb, beta, nwt);
+      return col_step<K, R, J>(Vr, w, cvv, cr, own, red, rb, h1, h2, hx, H, cs, sn, gv, rd, pvb,
+                               pcvb, beta, nwt, g0, hn_prev);
     return col_dispatch<K, R, J + 1>(j, Vr, w, cvv, cr, own, red, rb, h1, h2, hx, H, cs, sn, gv,
-                                     pvb, pcvb, beta, nwt);
+                                     rd, pvb, pcvb, beta, nwt, g0, hn_prev);
   } else {
     return true;
   }
@@ -557,9 +591,12 @@ __global__ void __launch_bounds__(NTC, 1) ras2d_col_kernel(const __grid_constant
   double* red = pcv + PP * PPY;              // 2 x NWC x 16
   double* hwall = red + 2 * NWC * 16;        // NWC x 3 x 16
   __shared__ double H[(K + 1) * K];
-  __shared__ double gv[K + 1], cs[K], sn[K], yv[K];
+  __shared__ double gv[K + 1], cs[K], sn[K], yv[K], rd[K];
 
   const int tid = threadIdx.x, nwt = blockDim.x >> 5;
+  const bool gwarp = (tid >> 5) == nwt - 1;     // the Givens warp: no nodes, reduces H
+  const bool g0 = gwarp && (tid & 31) == 0;
+  double hn_prev = 0.0;
   double* h1 = hwall + (tid >> 5) * 48;
   double* h2 = h1 + 16;
   double* hx = h2 + 16;
@@ -620,12 +657,17 @@ __global__ void __launch_bounds__(NTC, 1) ras2d_col_kernel(const __grid_constant
     }
   }
   if (tid == 0) gv[0] = beta;
+#ifdef PFC_RAS_PROFILE
+  if (blockIdx.x == 0 && tid == 0) ras_prof_last = clock64();
+#endif
 
   int jm = 0;
 #pragma unroll 1
   for (int j = 0; j < K; ++j) {
     __syncthreads();                                  // planes hold v_j and c v_j
-    // ---- w = A_k v_j: direct 25-point linear part, column by column
+    CPROF(0);
+    // ---- w = A_k v_j: direct 25-point linear part, column by column (not in the Givens warp)
+    if (!gwarp) {
     double out[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) out[r] = 0.0;
@@ -649,13 +691,20 @@ __global__ void __launch_bounds__(NTC, 1) ras2d_col_kernel(const __grid_constant
       const double lap = (pcvb[r * PP - 1] + pcvb[r * PP + 1]) + (up + dn) - 4.0 * cvv[r];
       w[r] = own[r] ? fma(-p.ih2, lap, out[r]) : 0.0;
     }
+    } else {
+#pragma unroll
+      for (int r = 0; r < R; ++r) w[r] = 0.0;
+    }
+    CPROF(1);
     const bool stop = col_dispatch<K, R, 0>(j, Vr, w, cvv, cr, own, red, rb, h1, h2, hx, H, cs,
-                                            sn, gv, pvb, pcvb, beta, nwt);
+                                            sn, gv, rd, pvb, pcvb, beta, nwt, g0, hn_prev);
+    CPROF(5);
     jm = j + 1;
     if (stop) break;
   }
-  __syncthreads();
-  if (tid == 0) {   // back substitution R yv = g (R already reduced column by column)
+  CPROF(6);
+  if (g0) {   // last Hessenberg column, then back substitution R yv = g
+    col_givens_dispatch<K, 0>(jm - 1, h1, h2, hn_prev, cs, sn, gv, H, rd);
     const int ld = K + 1;
     double y[K];
 #pragma unroll
@@ -665,7 +714,7 @@ __global__ void __launch_bounds__(NTC, 1) ras2d_col_kernel(const __grid_constant
 #pragma unroll
       for (int l = i + 1; l < K; ++l)
         if (l < jm) sacc -= H[i + ld * l] * y[l];
-      y[i] = sacc / H[i + ld * i];
+      y[i] = sacc * rd[i];
       yv[i] = y[i];
     }
   }
@@ -681,8 +730,18 @@ __global__ void __launch_bounds__(NTC, 1) ras2d_col_kernel(const __grid_constant
       if (i < jm) s = fma(yv[i], Vr[i][r], s);
     p.z[(size_t)(ibx * p.bx + li) + (size_t)p.nx * (iby * p.by + lj)] = s;
   }
+  CPROF(7);
 }
 
+#ifdef PFC_RAS_PROFILE
+}  // namespace
+extern "C" void pfc_ras_prof_read(long long* out) {
+  cudaMemcpyFromSymbol(out, ras_prof, sizeof(long long) * 8);
+  long long z[8] = {0};
+  cudaMemcpyToSymbol(ras_prof, z, sizeof(z));
+}
+namespace {
+#endif
 size_t ras2d_col_smem_bytes() {
   return (size_t)(2 * PP * PPY + 2 * NWC * 16 + NWC * 48) * sizeof(double);
 }
@@ -729,7 +788,7 @@ int col_rows(int k, int Ex, int Ey) {
   for (int i = 0; i < 4; ++i) {
     const int r = cand[i];
     const int ns = (Ey + r - 1) / r;
-    if (Ex * ns <= NTC && pick_col(k, r)) return r;
+    if ((Ex * ns + 31) / 32 * 32 + 32 <= NTC && pick_col(k, r)) return r;
   }
   return 0;
 }
@@ -745,7 +804,7 @@ int ras2d_plan(pfc_ctx* ctx) {
     if (r) {
       const int ns = (Ey + r - 1) / r;
       ctx->ras_smem = (int)ras2d_col_smem_bytes();
-      ctx->ras_threads = (Ex * ns + 31) / 32 * 32;   // column-strip kernel
+      ctx->ras_threads = (Ex * ns + 31) / 32 * 32 + 32;   // node warps + the Givens warp
       ctx->ras_rows = r;                             // rows per thread
       return 1;
     }
