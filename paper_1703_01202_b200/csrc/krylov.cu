@@ -5,14 +5,42 @@
 //   fused : w <- w - V h1 ; h2 = V^T w                     (k_axpy_dot: V read once for both)
 //   fused : w <- w - V h2 ; |w|^2                          (k_axpy_norm)
 // Reductions are deterministic: a FIXED grid (blas_nblocks(N)) with grid-stride loops, a
-// per-block shuffle + shared-memory tree in fixed order, then k_finalize sums the per-block
-// partials in fixed order.  Results are bitwise reproducible run to run.
+// per-block shuffle + shared-memory tree in fixed order, then the last block to finish sums the
+// per-block partials in fixed order (finalize_last_block; k_finalize for the stencil partials).
+// Results are bitwise reproducible run to run.
 #include "pfc_device.cuh"
 #include "pfc_internal.h"
 
 namespace {
 
 constexpr int NT = 256;
+
+// Fused fixed-order finalisation: after every block has written its NV partials, the LAST block
+// to finish (atomic ticket; it decides only WHO sums, not the order) adds the partials of all
+// blocks in the same order k_finalize uses (thread-strided over blocks, then the block tree),
+// so the result is bitwise identical to a separate k_finalize launch, without the launch.
+template <int NV>
+__device__ __forceinline__ void finalize_last_block(const double* partials, double* out,
+                                                    unsigned int* ticket, double* red,
+                                                    double* outv) {
+  __shared__ unsigned int last;
+  __threadfence();                       // this block's partials before the ticket
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  double acc[NV];
+#pragma unroll
+  for (int k = 0; k < NV; ++k) acc[k] = 0.0;
+  for (int b = threadIdx.x; b < (int)gridDim.x; b += NT) {
+#pragma unroll
+    for (int k = 0; k < NV; ++k) acc[k] += __ldcg(partials + (size_t)b * NV + k);
+  }
+  block_sum_multi<NV>(acc, red, outv);
+  if (threadIdx.x < NV) out[threadIdx.x] = outv[threadIdx.x];
+  if (threadIdx.x == 0) *ticket = 0u;    // ready for the next reduction on this stream
+}
 
 struct Coef {
   double c[PFC_MAX_RESTART];
@@ -40,7 +68,9 @@ __global__ void k_axpby(double a, const double* x, double b, const double* y, do
 template <int NV>
 __global__ void __launch_bounds__(NT) k_multidot(const double* __restrict__ V, size_t ldv,
                                                  const double* __restrict__ w, size_t N,
-                                                 double* __restrict__ partials) {
+                                                 double* __restrict__ partials,
+                                                 double* __restrict__ out,
+                                                 unsigned int* __restrict__ ticket) {
   __shared__ double red[32 * NV];
   __shared__ double outv[NV];
   double acc[NV];
@@ -53,13 +83,16 @@ __global__ void __launch_bounds__(NT) k_multidot(const double* __restrict__ V, s
   }
   block_sum_multi<NV>(acc, red, outv);
   if (threadIdx.x < NV) partials[blockIdx.x * NV + threadIdx.x] = outv[threadIdx.x];
+  finalize_last_block<NV>(partials, out, ticket, red, outv);
 }
 
 template <int NV>
 __global__ void __launch_bounds__(NT) k_axpy_dot(const double* __restrict__ V, size_t ldv,
                                                  const double* __restrict__ h,
                                                  double* __restrict__ w, size_t N,
-                                                 double* __restrict__ partials) {
+                                                 double* __restrict__ partials,
+                                                 double* __restrict__ out,
+                                                 unsigned int* __restrict__ ticket) {
   __shared__ double red[32 * NV];
   __shared__ double outv[NV];
   double hk[NV], acc[NV];
@@ -76,13 +109,16 @@ __global__ void __launch_bounds__(NT) k_axpy_dot(const double* __restrict__ V, s
   }
   block_sum_multi<NV>(acc, red, outv);
   if (threadIdx.x < NV) partials[blockIdx.x * NV + threadIdx.x] = outv[threadIdx.x];
+  finalize_last_block<NV>(partials, out, ticket, red, outv);
 }
 
 template <int NV>
 __global__ void __launch_bounds__(NT) k_axpy_norm(const double* __restrict__ V, size_t ldv,
                                                   const double* __restrict__ h,
                                                   double* __restrict__ w, size_t N,
-                                                  double* __restrict__ partials) {
+                                                  double* __restrict__ partials,
+                                                  double* __restrict__ out,
+                                                  unsigned int* __restrict__ ticket) {
   __shared__ double red[32];
   __shared__ double outv[1];
   double hk[NV];
@@ -98,10 +134,13 @@ __global__ void __launch_bounds__(NT) k_axpy_norm(const double* __restrict__ V, 
   }
   block_sum_multi<1>(acc, red, outv);
   if (threadIdx.x == 0) partials[blockIdx.x] = outv[0];
+  finalize_last_block<1>(partials, out, ticket, red, outv);
 }
 
 __global__ void __launch_bounds__(NT) k_norm2(const double* __restrict__ x, size_t N,
-                                              double* __restrict__ partials) {
+                                              double* __restrict__ partials,
+                                              double* __restrict__ out,
+                                              unsigned int* __restrict__ ticket) {
   __shared__ double red[32];
   __shared__ double outv[1];
   double acc[1] = {0.0};
@@ -109,6 +148,7 @@ __global__ void __launch_bounds__(NT) k_norm2(const double* __restrict__ x, size
     acc[0] += x[i] * x[i];
   block_sum_multi<1>(acc, red, outv);
   if (threadIdx.x == 0) partials[blockIdx.x] = outv[0];
+  finalize_last_block<1>(partials, out, ticket, red, outv);
 }
 
 // out[v] = sum_b partials[b*nval + v], fixed order; one CTA per value
@@ -170,12 +210,13 @@ cudaError_t launch_axpby(pfc_ctx* ctx, double a, const double* x, double b, cons
 }
 
 cudaError_t launch_multidot(pfc_ctx* ctx, const double* V, int nv, const double* w,
-                            double* partials) {
+                            double* partials, double* out) {
   const int nb = blas_nblocks(ctx->N);
   switch (nv) {
 #define X(K)                                                                        \
   case K:                                                                           \
-    k_multidot<K><<<nb, NT, 0, ctx->stream>>>(V, ctx->N, w, ctx->N, partials);      \
+    k_multidot<K><<<nb, NT, 0, ctx->stream>>>(V, ctx->N, w, ctx->N, partials, out,  \
+                                              ctx->ticket);                         \
     break;
     PFC_NV_CASES(X)
 #undef X
@@ -187,12 +228,13 @@ cudaError_t launch_multidot(pfc_ctx* ctx, const double* V, int nv, const double*
 }
 
 cudaError_t launch_axpy_dot(pfc_ctx* ctx, const double* V, int nv, const double* h, double* w,
-                            double* partials) {
+                            double* partials, double* out) {
   const int nb = blas_nblocks(ctx->N);
   switch (nv) {
 #define X(K)                                                                          \
   case K:                                                                             \
-    k_axpy_dot<K><<<nb, NT, 0, ctx->stream>>>(V, ctx->N, h, w, ctx->N, partials);     \
+    k_axpy_dot<K><<<nb, NT, 0, ctx->stream>>>(V, ctx->N, h, w, ctx->N, partials, out, \
+                                              ctx->ticket);                           \
     break;
     PFC_NV_CASES(X)
 #undef X
@@ -204,12 +246,13 @@ cudaError_t launch_axpy_dot(pfc_ctx* ctx, const double* V, int nv, const double*
 }
 
 cudaError_t launch_axpy_norm(pfc_ctx* ctx, const double* V, int nv, const double* h, double* w,
-                             double* partials) {
+                             double* partials, double* out) {
   const int nb = blas_nblocks(ctx->N);
   switch (nv) {
 #define X(K)                                                                           \
   case K:                                                                              \
-    k_axpy_norm<K><<<nb, NT, 0, ctx->stream>>>(V, ctx->N, h, w, ctx->N, partials);     \
+    k_axpy_norm<K><<<nb, NT, 0, ctx->stream>>>(V, ctx->N, h, w, ctx->N, partials, out, \
+                                               ctx->ticket);                           \
     break;
     PFC_NV_CASES(X)
 #undef X
@@ -220,8 +263,8 @@ cudaError_t launch_axpy_norm(pfc_ctx* ctx, const double* V, int nv, const double
   return cudaGetLastError();
 }
 
-cudaError_t launch_norm2(pfc_ctx* ctx, const double* x, double* partials) {
-  k_norm2<<<blas_nblocks(ctx->N), NT, 0, ctx->stream>>>(x, ctx->N, partials);
+cudaError_t launch_norm2(pfc_ctx* ctx, const double* x, double* partials, double* out) {
+  k_norm2<<<blas_nblocks(ctx->N), NT, 0, ctx->stream>>>(x, ctx->N, partials, out, ctx->ticket);
   ctx->launches++;
   pfc_account(ctx, PFC_K_VECTOR, 8.0 * ctx->N, 2.0 * ctx->N);
   return cudaGetLastError();

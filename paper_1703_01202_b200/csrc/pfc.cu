@@ -179,7 +179,6 @@ static pfc_status fgmres(pfc_ctx* ctx, double dt, double Fnorm, int* its_out) {
   const int m = c.gmres_restart;
   const size_t N = ctx->N;
   const double tol = std::max(c.gmres_rtol * Fnorm, c.gmres_atol);
-  const int nb = blas_nblocks(N);
   std::vector<double> H((m + 1) * m), cs(m), sn(m), g(m + 1), y(m);
   int its = 0;
   CK(cudaMemsetAsync(ctx->S, 0, N * sizeof(double), ctx->stream), "memset S");
@@ -198,12 +197,9 @@ static pfc_status fgmres(pfc_ctx* ctx, double dt, double Fnorm, int* its_out) {
       double* Zj = ctx->Z + (size_t)j * N;
       KL(PFC_K_RAS, launch_ras(ctx, Vj, ctx->c, dt, Zj), "ras");
       KL(PFC_K_JV, launch_jv(ctx, Zj, ctx->c, dt, ctx->w), "jv");
-      KL(PFC_K_ORTH, launch_multidot(ctx, ctx->V, j + 1, ctx->w, ctx->partials), "multidot");
-      KL(PFC_K_FINALIZE, launch_finalize(ctx, ctx->partials, nb, j + 1, ctx->dscal + SC_H1), "finalize");
-      KL(PFC_K_ORTH, launch_axpy_dot(ctx, ctx->V, j + 1, ctx->dscal + SC_H1, ctx->w, ctx->partials), "cgs2");
-      KL(PFC_K_FINALIZE, launch_finalize(ctx, ctx->partials, nb, j + 1, ctx->dscal + SC_H2), "finalize");
-      KL(PFC_K_ORTH, launch_axpy_norm(ctx, ctx->V, j + 1, ctx->dscal + SC_H2, ctx->w, ctx->partials), "cgs2");
-      KL(PFC_K_FINALIZE, launch_finalize(ctx, ctx->partials, nb, 1, ctx->dscal + SC_NRM), "finalize");
+      KL(PFC_K_ORTH, launch_multidot(ctx, ctx->V, j + 1, ctx->w, ctx->partials, ctx->dscal + SC_H1), "multidot");
+      KL(PFC_K_ORTH, launch_axpy_dot(ctx, ctx->V, j + 1, ctx->dscal + SC_H1, ctx->w, ctx->partials, ctx->dscal + SC_H2), "cgs2");
+      KL(PFC_K_ORTH, launch_axpy_norm(ctx, ctx->V, j + 1, ctx->dscal + SC_H2, ctx->w, ctx->partials, ctx->dscal + SC_NRM), "cgs2");
       pfc_status s = fetch(ctx, 0, SC_NRM + 1);
       if (s) return s;
       const double* h1 = ctx->hscal + SC_H1;
@@ -242,8 +238,7 @@ static pfc_status fgmres(pfc_ctx* ctx, double dt, double Fnorm, int* its_out) {
     // restart: r = -F - J S (true residual), V0 = r/|r|
     KL(PFC_K_JV, launch_jv(ctx, ctx->S, ctx->c, dt, ctx->w), "jv");
     KL(PFC_K_VECTOR, launch_axpby(ctx, -1.0, ctx->F, -1.0, ctx->w, ctx->w), "axpby");
-    KL(PFC_K_VECTOR, launch_norm2(ctx, ctx->w, ctx->partials), "norm");
-    KL(PFC_K_FINALIZE, launch_finalize(ctx, ctx->partials, nb, 1, ctx->dscal + SC_NRM), "finalize");
+    KL(PFC_K_VECTOR, launch_norm2(ctx, ctx->w, ctx->partials, ctx->dscal + SC_NRM), "norm");
     pfc_status s = fetch(ctx, SC_NRM, 1);
     if (s) return s;
     beta = sqrt(ctx->hscal[SC_NRM]);
@@ -426,6 +421,8 @@ pfc_status pfc_create(const pfc_config* cfg, void* stream, pfc_ctx** out) {
   ctx->npartials = std::max<size_t>(tiles, (size_t)blas_nblocks(ctx->N) * 32) + 64;
   if (pfc_check_cuda(ctx, cudaMalloc(&ctx->partials, ctx->npartials * sizeof(double)), "partials") ||
       pfc_check_cuda(ctx, cudaMalloc(&ctx->dscal, SC_TOTAL * sizeof(double)), "dscal") ||
+      pfc_check_cuda(ctx, cudaMalloc(&ctx->ticket, sizeof(unsigned int)), "ticket") ||
+      pfc_check_cuda(ctx, cudaMemset(ctx->ticket, 0, sizeof(unsigned int)), "ticket") ||
       pfc_check_cuda(ctx, cudaMallocHost(&ctx->hscal, SC_TOTAL * sizeof(double)), "hscal"))
     return fail(PFC_ENOMEM);
   if (c.ndim == 3) {
@@ -445,6 +442,7 @@ void pfc_destroy(pfc_ctx* ctx) {
                   ctx->dscal, ctx->ras_scratch};
   for (double* f : fs)
     if (f) cudaFree(f);
+  if (ctx->ticket) cudaFree(ctx->ticket);
   if (ctx->hscal) cudaFreeHost(ctx->hscal);
   prof_drain(ctx);
   for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);

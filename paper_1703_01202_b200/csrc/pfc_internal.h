@@ -37,6 +37,7 @@ struct pfc_ctx {
   size_t npartials = 0;
   double* dscal = nullptr;     // device scalars: [0,64) h1, [64,128) h2, [128] |w|^2, ...
   double* hscal = nullptr;     // pinned host mirror of dscal
+  unsigned int* ticket = nullptr;  // last-block ticket of the fused reductions (device, 0)
 
   // RAS launch plan
   int ras_smem = 0;
@@ -99,13 +100,14 @@ int blas_nblocks(size_t N);
 cudaError_t launch_coef(pfc_ctx* ctx, const double* phi, const double* psi, double* c);
 cudaError_t launch_axpby(pfc_ctx* ctx, double a, const double* x, double b, const double* y,
                          double* out);
+// the reductions below finish in their own last block: `out` receives the nv final sums
 cudaError_t launch_multidot(pfc_ctx* ctx, const double* V, int nv, const double* w,
-                            double* partials);
+                            double* partials, double* out);
 cudaError_t launch_axpy_dot(pfc_ctx* ctx, const double* V, int nv, const double* h, double* w,
-                            double* partials);
+                            double* partials, double* out);
 cudaError_t launch_axpy_norm(pfc_ctx* ctx, const double* V, int nv, const double* h, double* w,
-                             double* partials);
-cudaError_t launch_norm2(pfc_ctx* ctx, const double* x, double* partials);
+                             double* partials, double* out);
+cudaError_t launch_norm2(pfc_ctx* ctx, const double* x, double* partials, double* out);
 cudaError_t launch_finalize(pfc_ctx* ctx, const double* partials, int nblk, int nval,
                             double* out);
 cudaError_t launch_lincomb(pfc_ctx* ctx, double* x, const double* Z, int nv, const double* coef);
