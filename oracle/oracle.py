@@ -33,7 +33,10 @@ class Params(C.Structure):
                 ("newton_maxit", C.c_int), ("ls_c1", C.c_double), ("ls_min_lambda", C.c_double),
                 ("gmres_restart", C.c_int), ("gmres_maxit", C.c_int),
                 ("gmres_rtol", C.c_double), ("gmres_atol", C.c_double),
-                ("ras_box", C.c_int * 3), ("ras_overlap", C.c_int), ("ras_local_k", C.c_int)]
+                ("ras_box", C.c_int * 3), ("ras_overlap", C.c_int), ("ras_local_k", C.c_int),
+                ("ras_variant", C.c_int)]
+
+RAS_LEFT, RAS_AS, RAS_RIGHT = 0, 1, 2
 
 
 class NewtonInfo(C.Structure):
@@ -91,18 +94,20 @@ def _shape(a):
 
 def params(gamma=0.25, newton_rtol=1e-10, newton_atol=1e-10, newton_maxit=50, ls_c1=1e-4,
            ls_min_lambda=1e-12, gmres_restart=30, gmres_maxit=300, gmres_rtol=1e-3,
-           gmres_atol=1e-11, ras_box=(16, 16, 1), ras_overlap=2, ras_local_k=10, **_ignored):
+           gmres_atol=1e-11, ras_box=(16, 16, 1), ras_overlap=2, ras_local_k=10, ras_variant=0,
+           **_ignored):
     b = list(ras_box) + [1] * (3 - len(ras_box))
     return Params(gamma, newton_rtol, newton_atol, newton_maxit, ls_c1, ls_min_lambda,
                   gmres_restart, gmres_maxit, gmres_rtol, gmres_atol, (C.c_int * 3)(*b),
-                  ras_overlap, ras_local_k)
+                  ras_overlap, ras_local_k, ras_variant)
 
 
 def params_from_config(cfg, **over):
     kw = dict(gamma=cfg.gamma, newton_rtol=cfg.newton_rtol, newton_atol=cfg.newton_atol,
               newton_maxit=cfg.newton_maxit, gmres_restart=cfg.gmres_restart,
               gmres_maxit=cfg.gmres_maxit, gmres_rtol=cfg.gmres_rtol, gmres_atol=cfg.gmres_atol,
-              ras_box=cfg.ras_box, ras_overlap=cfg.ras_overlap, ras_local_k=cfg.ras_local_k)
+              ras_box=cfg.ras_box, ras_overlap=cfg.ras_overlap, ras_local_k=cfg.ras_local_k,
+              ras_variant=getattr(cfg, "ras_variant", 0))
     kw.update(over)
     return params(**kw)
 
@@ -157,6 +162,7 @@ def local_jacobian_apply(shape, h, prm, dt, c_loc, v_loc):
 
 
 def ras_apply(phi_new, phi_old, v, h, prm, dt):
+    """Schwarz preconditioner apply; prm.ras_variant selects left-RAS / AS / right-RAS."""
     a, b, v = _f(phi_new), _f(phi_old), _f(v); out = np.zeros_like(a)
     lib().or_ras_apply(C.byref(_grid(_shape(a), h)), C.byref(prm), dt, _ptr(a), _ptr(b), _ptr(v),
                        _ptr(out))

@@ -317,11 +317,16 @@ static void local_gmres(const or_grid* g, const or_params* p, double dt, const d
   free(yy); free(V); free(w); free(H); free(cs); free(sn); free(gv); free(h2);
 }
 
-/* Left restricted additive Schwarz, Eq. (eq:ras) P:398-409:
- *   z = sum_k (R_k^0)^T inv(A_k) R_k^delta v
+/* Additive Schwarz preconditioners, selected by p->ras_variant:
+ *   0  left-RAS      z = sum_k (R_k^0)^T     inv(A_k) R_k^delta v    Eq. (eq:ras)
+ *   1  classical AS  z = sum_k (R_k^delta)^T inv(A_k) R_k^delta v    Eq. (invM)
+ *   2  right-RAS     z = sum_k (R_k^delta)^T inv(A_k) R_k^0 v        Eq. (eq:ash)
  * Boxes Omega_k of ras_box nodes in lexicographic (x-fastest) order; Omega_k^delta
  * extends each by ras_overlap mesh layers (R7) with periodic wrap; inv(A_k) is the
- * fixed-work local GMRES (R9); only owned nodes are written (R_k^0)^T. */
+ * fixed-work local GMRES (R9).  R_k^delta keeps the ext-box entries of v, R_k^0 only the
+ * owned ones (zeros elsewhere on the ext box); (R_k^0)^T writes only the owned
+ * nodes (disjoint), (R_k^delta)^T adds the whole ext-box solution into z,
+ * accumulated in box order. */
 void or_ras_apply(const or_grid* g, const or_params* p, double dt, const double* pn,
                   const double* po, const double* v, double* z) {
   int b[3] = {1, 1, 1}, nb[3] = {1, 1, 1}, E[3] = {1, 1, 1}, o[3] = {0, 0, 0};
@@ -331,6 +336,9 @@ void or_ras_apply(const or_grid* g, const or_params* p, double dt, const double*
     o[d] = p->ras_overlap;
     E[d] = b[d] + 2 * o[d];
   }
+  const int restrict_owned = p->ras_variant == 2;     /* R_k^0 restriction */
+  const int extend_owned = p->ras_variant == 0;       /* (R_k^0)^T extension */
+  if (!extend_owned) memset(z, 0, npts(g) * sizeof(double));
   size_t n = (size_t)E[0] * E[1] * E[2];
   double* r = alloc0(n);
   double* c = alloc0(n);
@@ -339,21 +347,32 @@ void or_ras_apply(const or_grid* g, const or_params* p, double dt, const double*
     for (int by = 0; by < nb[1]; ++by)
       for (int bx = 0; bx < nb[0]; ++bx) {
         int x0 = bx * b[0] - o[0], y0 = by * b[1] - o[1], z0 = bz * b[2] - o[2];
-        for (int k = 0; k < E[2]; ++k)          /* R_k^delta: gather with wrap */
+        for (int k = 0; k < E[2]; ++k)          /* R_k^delta or R_k^0: gather with wrap */
           for (int j = 0; j < E[1]; ++j)
             for (int i = 0; i < E[0]; ++i) {
               size_t q = gidx(g, x0 + i, y0 + j, z0 + k);
               size_t l = (size_t)i + (size_t)E[0] * ((size_t)j + (size_t)E[1] * k);
-              r[l] = v[q];
+              int owned = i >= o[0] && i < o[0] + b[0] && j >= o[1] && j < o[1] + b[1] &&
+                          k >= o[2] && k < o[2] + b[2];
+              r[l] = (restrict_owned && !owned) ? 0.0 : v[q];
               c[l] = (3.0 * pn[q] * pn[q] + 2.0 * pn[q] * po[q] + po[q] * po[q]) / 4.0;
             }
         local_gmres(g, p, dt, c, r, y, n);
-        for (int k = o[2]; k < o[2] + b[2]; ++k)   /* (R_k^0)^T: owned nodes only */
-          for (int j = o[1]; j < o[1] + b[1]; ++j)
-            for (int i = o[0]; i < o[0] + b[0]; ++i) {
-              size_t l = (size_t)i + (size_t)E[0] * ((size_t)j + (size_t)E[1] * k);
-              z[gidx(g, x0 + i, y0 + j, z0 + k)] = y[l];
-            }
+        if (extend_owned) {
+          for (int k = o[2]; k < o[2] + b[2]; ++k)   /* (R_k^0)^T: owned nodes only */
+            for (int j = o[1]; j < o[1] + b[1]; ++j)
+              for (int i = o[0]; i < o[0] + b[0]; ++i) {
+                size_t l = (size_t)i + (size_t)E[0] * ((size_t)j + (size_t)E[1] * k);
+                z[gidx(g, x0 + i, y0 + j, z0 + k)] = y[l];
+              }
+        } else {
+          for (int k = 0; k < E[2]; ++k)             /* (R_k^delta)^T: add the ext box */
+            for (int j = 0; j < E[1]; ++j)
+              for (int i = 0; i < E[0]; ++i) {
+                size_t l = (size_t)i + (size_t)E[0] * ((size_t)j + (size_t)E[1] * k);
+                z[gidx(g, x0 + i, y0 + j, z0 + k)] += y[l];
+              }
+        }
       }
   free(r); free(c); free(y);
 }

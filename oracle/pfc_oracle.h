@@ -27,7 +27,8 @@ typedef struct {
   double ls_c1, ls_min_lambda;  /* line search (reading R16) */
   int gmres_restart, gmres_maxit;
   double gmres_rtol, gmres_atol;     /* xi_r, xi_a */
-  int ras_box[3], ras_overlap, ras_local_k;  /* left-RAS, local GMRES(k) (R9) */
+  int ras_box[3], ras_overlap, ras_local_k;  /* Schwarz boxes, local GMRES(k) (R9) */
+  int ras_variant;  /* 0 left-RAS, 1 classical AS, 2 right-RAS */
 } or_params;
 
 typedef struct {
@@ -53,7 +54,7 @@ int or_num_boxes(const or_grid* g, const or_params* p);
 void or_local_jacobian_apply(const or_grid* g, const or_params* p, double dt,
                              const double* c_loc, const double* v_loc, double* w_loc);
 void or_ras_apply(const or_grid* g, const or_params* p, double dt, const double* phi_new,
-                  const double* phi_old, const double* v, double* z);
+                  const double* phi_old, const double* v, double* z);  /* p->ras_variant */
 void or_ras_apply_box(const or_grid* g, const or_params* p, double dt, const double* phi_new,
                       const double* phi_old, const double* v, int box, double* z_owned);
 

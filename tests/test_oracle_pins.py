@@ -295,21 +295,26 @@ def test_local_operator_is_RJRt(shape, box, o):
         assert np.linalg.norm(Aloc - Ak) <= 1e-13 * np.linalg.norm(Ak)
 
 
-@pytest.mark.parametrize("shape,box,o", [((16, 16), (4, 4), 1), ((8, 8, 8), (2, 2, 2), 0)])
-def test_ras_with_exact_local_solve(shape, box, o):
-    """Left-RAS Eq. (eq:ras) P:398-409 with k_loc = #ext-box unknowns (local GMRES is then an
-    exact solve) equals sum_k (R_k^0)^T A_k^{-1} R_k^delta v by dense numpy solves."""
-    rs = tuple(reversed(shape))
+@pytest.mark.parametrize("variant", [O.RAS_LEFT, O.RAS_AS, O.RAS_RIGHT])
+@pytest.mark.parametrize("shape,box,o", [((16, 16), (4, 4), 1), ((8, 8, 8), (2, 2, 2), 1),
+                                         ((12, 12), (6, 6), 2)])
+def test_schwarz_with_exact_local_solve(shape, box, o, variant):
+    """With k_loc = #ext-box unknowns (local GMRES is then an exact solve) the oracle equals
+    the dense-numpy Schwarz operators built from the definitions, box by box:
+      left-RAS  sum_k (R_k^0)^T A_k^{-1} R_k^delta v      Eq. (eq:ras) P:398-409
+      AS        sum_k (R_k^delta)^T A_k^{-1} R_k^delta v  Eq. (invM)
+      right-RAS sum_k (R_k^delta)^T A_k^{-1} R_k^0 v      Eq. (eq:ash) P:410-419"""
     phi = random_field(shape, 71, 0.07, 0.3)
     psi = random_field(shape, 72, 0.07, 0.3)
     v = random_field(shape, 73)
     dt = 0.5
     n = int(np.prod([b + 2 * o for b in box]))
-    prm = O.params(gamma=GAMMA, ras_box=box, ras_overlap=o, ras_local_k=n)
+    prm = O.params(gamma=GAMMA, ras_box=box, ras_overlap=o, ras_local_k=n, ras_variant=variant)
     z = O.ras_apply(phi, psi, v, H, prm, dt).ravel()
     c = _c_of(phi, psi).ravel()
     vf = v.ravel()
-    zref = np.full(vf.shape, np.nan)
+    zref = np.zeros(vf.shape)
+    owner = np.zeros(vf.shape, dtype=int)
     nb = int(np.prod([s // b for s, b in zip(shape, box)]))
     nd = len(shape)
     for bidx in range(nb):
@@ -318,14 +323,35 @@ def test_ras_with_exact_local_solve(shape, box, o):
         for q in range(n):
             e = np.zeros(n); e[q] = 1.0
             A[:, q] = O.local_jacobian_apply(shape, H, prm, dt, c[idx], e)
-        y = np.linalg.solve(A, vf[idx])
         E = [b + 2 * o for b in box]
         loc = np.arange(n).reshape(tuple(reversed(E)))
         own = loc[tuple(slice(o, o + box[d]) for d in reversed(range(nd)))].ravel()
-        assert np.all(np.isnan(zref[idx[own]]))          # each node owned by exactly one box
-        zref[idx[own]] = y[own]
-    assert not np.any(np.isnan(zref))
+        rhs = vf[idx].copy()
+        if variant == O.RAS_RIGHT:                      # R_k^0: owned entries only
+            keep = np.zeros(n, dtype=bool); keep[own] = True
+            rhs[~keep] = 0.0
+        y = np.linalg.solve(A, rhs)
+        if variant == O.RAS_LEFT:                       # (R_k^0)^T: disjoint owned writes
+            zref[idx[own]] = y[own]
+            owner[idx[own]] += 1
+        else:                                           # (R_k^delta)^T: overlap-add
+            np.add.at(zref, idx, y)
+    if variant == O.RAS_LEFT:
+        assert np.all(owner == 1)                       # each node owned by exactly one box
     assert rel(z, zref) < 1e-9
+
+
+@pytest.mark.parametrize("shape,box", [((16, 16), (4, 4)), ((8, 8, 8), (4, 4, 2))])
+def test_schwarz_variants_coincide_without_overlap(shape, box):
+    """With no overlap (delta = 0) R_k^delta = R_k^0, so AS, left-RAS
+    and right-RAS are the same operator (any k_loc)."""
+    phi = random_field(shape, 74, 0.07, 0.3)
+    psi = random_field(shape, 75, 0.07, 0.3)
+    v = random_field(shape, 76)
+    zs = [O.ras_apply(phi, psi, v, H, O.params(gamma=GAMMA, ras_box=box, ras_overlap=0,
+                                                ras_local_k=6, ras_variant=var), 0.5)
+          for var in (O.RAS_LEFT, O.RAS_AS, O.RAS_RIGHT)]
+    assert np.array_equal(zs[0], zs[1]) and np.array_equal(zs[0], zs[2])
 
 
 # ---------------------------------------------------------------- Krylov and Newton
