@@ -32,7 +32,7 @@
 extern "C" {
 #endif
 
-#define PFC_ABI_VERSION 1
+#define PFC_ABI_VERSION 2
 
 typedef struct pfc_ctx pfc_ctx;
 typedef int pfc_status;
@@ -67,7 +67,17 @@ typedef struct pfc_config {
   int ras_box[3];         /* owned subdomain box Omega_k (nodes per axis); must divide n */
   int ras_overlap;        /* overlap o in MESH LAYERS (paper's delta = o/3) */
   int ras_local_k;        /* fixed number of local GMRES steps in each subdomain solve (1..15) */
+  int ras_variant;        /* Schwarz preconditioner (enum below; default PFC_RAS_LEFT) */
 } pfc_config;
+
+/* Schwarz preconditioner variants.  R_k^delta restricts to the extended box
+ * Omega_k^delta, R_k^0 to the owned box Omega_k (zeros elsewhere on the extended box):
+ *   PFC_RAS_LEFT   z = sum_k (R_k^0)^T     inv(A_k) R_k^delta v   Eq. (eq:ras) P:398-409
+ *   PFC_RAS_AS     z = sum_k (R_k^delta)^T inv(A_k) R_k^delta v   Eq. (invM)
+ *   PFC_RAS_RIGHT  z = sum_k (R_k^delta)^T inv(A_k) R_k^0 v       Eq. (eq:ash) P:410-419
+ * The (R_k^delta)^T extension of AS / right-RAS is an overlap-add, done as a fixed-order
+ * gather (deterministic); it needs one extra (#boxes x ext-box) fp64 work array. */
+enum { PFC_RAS_LEFT = 0, PFC_RAS_AS = 1, PFC_RAS_RIGHT = 2 };
 
 /* Per-step report of pfc_step. */
 typedef struct pfc_step_info {

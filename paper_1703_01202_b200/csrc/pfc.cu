@@ -341,6 +341,7 @@ void pfc_config_default(pfc_config* c) {
   c->ras_box[0] = c->ras_box[1] = c->ras_box[2] = 16;
   c->ras_overlap = 2;
   c->ras_local_k = 10;
+  c->ras_variant = PFC_RAS_LEFT;
 }
 
 static pfc_status validate(const pfc_config& c, std::string* why) {
@@ -366,6 +367,8 @@ static pfc_status validate(const pfc_config& c, std::string* why) {
   if (c.adaptive && !(c.dt_min > 0 && c.dt_min <= c.dt_max)) return bad("need 0 < dt_min <= dt_max");
   if (c.adaptive && !(c.eta >= 0)) return bad("eta must be >= 0");
   if (c.ras_local_k < 1 || c.ras_local_k > PFC_MAX_LOCAL_K) return bad("ras_local_k in [1,15]");
+  if (c.ras_variant != PFC_RAS_LEFT && c.ras_variant != PFC_RAS_AS && c.ras_variant != PFC_RAS_RIGHT)
+    return bad("ras_variant must be PFC_RAS_LEFT, PFC_RAS_AS or PFC_RAS_RIGHT");
   if (c.gmres_restart < 1 || c.gmres_restart > PFC_MAX_RESTART) return bad("gmres_restart in [1,32]");
   if (c.gmres_maxit < 1 || c.newton_maxit < 0) return bad("iteration limits must be positive");
   if (!(c.newton_rtol >= 0 && c.newton_atol >= 0 && c.gmres_rtol >= 0 && c.gmres_atol >= 0))
@@ -431,6 +434,10 @@ pfc_status pfc_create(const pfc_config* cfg, void* stream, pfc_ctx** out) {
     if (pfc_check_cuda(ctx, cudaMalloc(&ctx->ras_scratch, d * sizeof(double)), "ras scratch"))
       return fail(PFC_ENOMEM);
   }
+  if (c.ras_variant != PFC_RAS_LEFT &&
+      pfc_check_cuda(ctx, cudaMalloc(&ctx->ras_y, ras_ext_doubles(ctx) * sizeof(double)),
+                     "ras ext-box solutions"))
+    return fail(PFC_ENOMEM);
   *out = ctx;
   return PFC_OK;
 }
@@ -439,7 +446,7 @@ void pfc_destroy(pfc_ctx* ctx) {
   if (!ctx) return;
   double* fs[] = {ctx->phi, ctx->psi,   ctx->F,        ctx->Ft,       ctx->trial, ctx->S,
                   ctx->c,   ctx->w,     ctx->stage,    ctx->V,        ctx->Z,     ctx->partials,
-                  ctx->dscal, ctx->ras_scratch};
+                  ctx->dscal, ctx->ras_scratch, ctx->ras_y};
   for (double* f : fs)
     if (f) cudaFree(f);
   if (ctx->ticket) cudaFree(ctx->ticket);

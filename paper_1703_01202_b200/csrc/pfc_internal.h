@@ -32,6 +32,7 @@ struct pfc_ctx {
   double* V = nullptr;     // (m+1) N  Krylov basis
   double* Z = nullptr;     // m N      preconditioned basis (flexible GMRES)
   double* ras_scratch = nullptr;  // 3D subdomain-solve scratch (L2-resident)
+  double* ras_y = nullptr;        // AS / right-RAS: ext-box solutions [box][ext node]
   double* stage = nullptr;     // staging field for host-pointer calls
   double* partials = nullptr;  // reduction scratch
   size_t npartials = 0;
@@ -80,6 +81,9 @@ cudaError_t launch_jv(pfc_ctx* ctx, const double* v, const double* c, double dt,
 cudaError_t launch_energy_mass(pfc_ctx* ctx, const double* phi, double* partials, int* nparts);
 cudaError_t launch_ras(pfc_ctx* ctx, const double* v, const double* c, double dt, double* z);
 int ras_plan(pfc_ctx* ctx);   // fills ras_smem/threads/cluster; returns 0 if infeasible
+// (R_k^delta)^T overlap-add of ctx->ras_y into z (AS, right-RAS); scratch size in doubles
+cudaError_t launch_ras_extend(pfc_ctx* ctx, double* z);
+size_t ras_ext_doubles(const pfc_ctx* ctx);
 
 // per-dimension kernels
 cudaError_t launch_residual_2d(pfc_ctx*, const double*, const double*, double, double*, double*,

@@ -44,6 +44,8 @@ struct RasArgs {
   int nx, ny;
   int bx, by, o;
   double idt, gamma, ih2;
+  int restrict_owned;   // right-RAS: R_k^0 (v zero outside the owned box)
+  double* y_ext;        // AS / right-RAS: ext-box solutions [box][ext node] for (R_k^delta)^T
 };
 
 constexpr int pow2_at_least(int x) { return x <= 1 ? 1 : 2 * pow2_at_least((x + 1) / 2); }
@@ -154,7 +156,9 @@ __global__ void __launch_bounds__(NT, 1) ras2d_kernel(RasArgs p) {
     if (own[s]) {
       int l = tid + s * NT;
       size_t g = (size_t)wrapi(gx0 + l % Ex, p.nx) + (size_t)p.nx * wrapi(gy0 + l / Ex, p.ny);
-      w[s] = p.v[g];
+      const int li = l % Ex - p.o, lj = l / Ex - p.o;
+      const bool owned = li >= 0 && li < p.bx && lj >= 0 && lj < p.by;
+      w[s] = (p.restrict_owned && !owned) ? 0.0 : p.v[g];
       cl[l] = p.c[g];
       acc[0] += w[s] * w[s];
     }
@@ -164,8 +168,12 @@ __global__ void __launch_bounds__(NT, 1) ras2d_kernel(RasArgs p) {
   rb ^= 1;
   const double beta = sqrt(hx[0]);
   if (beta == 0.0) {
-    for (int l = tid; l < p.bx * p.by; l += NT)
-      p.z[(size_t)(ibx * p.bx + l % p.bx) + (size_t)p.nx * (iby * p.by + l / p.bx)] = 0.0;
+    if (p.y_ext) {
+      for (int l = tid; l < n; l += NT) p.y_ext[(size_t)blockIdx.x * n + l] = 0.0;
+    } else {
+      for (int l = tid; l < p.bx * p.by; l += NT)
+        p.z[(size_t)(ibx * p.bx + l % p.bx) + (size_t)p.nx * (iby * p.by + l / p.bx)] = 0.0;
+    }
     return;
   }
   {
@@ -336,6 +344,14 @@ __global__ void __launch_bounds__(NT, 1) ras2d_kernel(RasArgs p) {
   }
   __syncthreads();
   // (R_k^0)^T: owned nodes only, y = V yv
+  if (p.y_ext) {   // (R_k^delta)^T: the whole ext-box solution, summed by ras_extend
+    for (int l = tid; l < n; l += NT) {
+      double s = 0.0;
+      for (int i = 0; i < jm; ++i) s += yv[i] * V[(size_t)i * n + l];
+      p.y_ext[(size_t)blockIdx.x * n + l] = s;
+    }
+    return;
+  }
   for (int l = tid; l < p.bx * p.by; l += NT) {
     int li = l % p.bx, lj = l / p.bx;
     int ll = (lj + p.o) * Ex + li + p.o;
@@ -373,6 +389,8 @@ struct RasColArgs {
   double* z;
   int nx, ny, bx, by, o;
   int Ex, Ey, ns;               // extended box, strips per column
+  int restrict_owned;           // right-RAS: R_k^0 (v zero outside the owned box)
+  double* y_ext;                // AS / right-RAS: ext-box solutions [box][ext node]
   double W[6];                  // 25-point class weights: (0,0) (0,1) (0,2) (1,1) (0,3) (1,2)
   double ih2;
 };
@@ -625,7 +643,9 @@ __global__ void __launch_bounds__(NTC, 1) ras2d_col_kernel(const __grid_constant
     cr[r] = 0.0;
     if (own[r]) {
       const size_t g = (size_t)wrapi(gx0 + x, p.nx) + (size_t)p.nx * wrapi(gy0 + y0 + r, p.ny);
-      w[r] = p.v[g];
+      const int li = x - p.o, lj = y0 + r - p.o;
+      const bool owned = li >= 0 && li < p.bx && lj >= 0 && lj < p.by;
+      w[r] = (p.restrict_owned && !owned) ? 0.0 : p.v[g];
       cr[r] = p.c[g];
       acc0[0] = fma(w[r], w[r], acc0[0]);
     }
@@ -638,8 +658,11 @@ __global__ void __launch_bounds__(NTC, 1) ras2d_col_kernel(const __grid_constant
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       const int li = x - p.o, lj = y0 + r - p.o;
-      if (own[r] && li >= 0 && li < p.bx && lj >= 0 && lj < p.by)
+      if (p.y_ext) {
+        if (own[r]) p.y_ext[(size_t)blockIdx.x * (Ex * Ey) + (y0 + r) * Ex + x] = 0.0;
+      } else if (own[r] && li >= 0 && li < p.bx && lj >= 0 && lj < p.by) {
         p.z[(size_t)(ibx * p.bx + li) + (size_t)p.nx * (iby * p.by + lj)] = 0.0;
+      }
     }
     return;
   }
@@ -719,16 +742,19 @@ __global__ void __launch_bounds__(NTC, 1) ras2d_col_kernel(const __grid_constant
     }
   }
   __syncthreads();
-  // (R_k^0)^T: the owner thread of each owned node writes y = V yv
+  // (R_k^0)^T: the owner thread of each owned node writes y = V yv; (R_k^delta)^T (AS,
+  // right-RAS): every ext node's value goes to y_ext for the deterministic overlap-add
 #pragma unroll
   for (int r = 0; r < R; ++r) {
     const int li = x - p.o, lj = y0 + r - p.o;
-    if (!own[r] || li < 0 || li >= p.bx || lj < 0 || lj >= p.by) continue;
+    const bool wr = p.y_ext ? own[r] : (own[r] && li >= 0 && li < p.bx && lj >= 0 && lj < p.by);
+    if (!wr) continue;
     double s = 0.0;
 #pragma unroll
     for (int i = 0; i < K; ++i)
       if (i < jm) s = fma(yv[i], Vr[i][r], s);
-    p.z[(size_t)(ibx * p.bx + li) + (size_t)p.nx * (iby * p.by + lj)] = s;
+    if (p.y_ext) p.y_ext[(size_t)blockIdx.x * (Ex * Ey) + (y0 + r) * Ex + x] = s;
+    else p.z[(size_t)(ibx * p.bx + li) + (size_t)p.nx * (iby * p.by + lj)] = s;
   }
   CPROF(7);
 }
@@ -832,6 +858,8 @@ cudaError_t launch_ras_2d(pfc_ctx* ctx, const double* v, const double* c, double
     p.v = v; p.c = c; p.z = z;
     p.nx = cf.n[0]; p.ny = cf.n[1]; p.bx = cf.ras_box[0]; p.by = cf.ras_box[1];
     p.o = cf.ras_overlap; p.Ex = Ex; p.Ey = Ey; p.ns = (Ey + R - 1) / R;
+    p.restrict_owned = cf.ras_variant == PFC_RAS_RIGHT;
+    p.y_ext = cf.ras_variant == PFC_RAS_LEFT ? nullptr : ctx->ras_y;
     // class weights of the linear part v/dt - alpha Delta v - Delta^2 v - Delta^3 v / 2 with
     // h^2 Delta = L:  L (0,0) -4, (0,1) 1;  L^2 (0,0) 20, (0,1) -8, (0,2) 1, (1,1) 2;
     // L^3 (0,0) -112, (0,1) 57, (0,2) -12, (1,1) -24, (0,3) 1, (1,2) 3
@@ -852,7 +880,8 @@ cudaError_t launch_ras_2d(pfc_ctx* ctx, const double* v, const double* c, double
     e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, ctx->ras_smem);
     if (e != cudaSuccess) return e;
     RasArgs p{v, c, z, cf.n[0], cf.n[1], cf.ras_box[0], cf.ras_box[1], cf.ras_overlap,
-              1.0 / dt, cf.gamma, ctx->ih2};
+              1.0 / dt, cf.gamma, ctx->ih2, cf.ras_variant == PFC_RAS_RIGHT,
+              cf.ras_variant == PFC_RAS_LEFT ? nullptr : ctx->ras_y};
     fn<<<nb, NT, ctx->ras_smem, ctx->stream>>>(p);
   }
   ctx->launches++;
@@ -860,8 +889,11 @@ cudaError_t launch_ras_2d(pfc_ctx* ctx, const double* v, const double* c, double
      // k local J v (25/pt) + CGS2 vector work 4k(k+1) + 3k + 3 per ext node + V y
     const double k = cf.ras_local_k;
     const double next = (double)nb * Ex * Ey;
-    pfc_account(ctx, PFC_K_RAS, 8.0 * (2.0 * next + ctx->N),
-                next * (25.0 * k + 4.0 * k * (k + 1) + 3.0 * k + 3.0) + 2.0 * k * ctx->N);
+    const double nout = cf.ras_variant == PFC_RAS_LEFT ? (double)ctx->N : next;
+    pfc_account(ctx, PFC_K_RAS, 8.0 * (2.0 * next + nout),
+                next * (25.0 * k + 4.0 * k * (k + 1) + 3.0 * k + 3.0) + 2.0 * k * nout);
   }
-  return cudaGetLastError();
+  cudaError_t e2 = cudaGetLastError();
+  if (e2 != cudaSuccess || cf.ras_variant == PFC_RAS_LEFT) return e2;
+  return launch_ras_extend(ctx, z);
 }

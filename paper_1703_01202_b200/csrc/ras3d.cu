@@ -1,4 +1,4 @@
-// ras3d.cu -- left restricted additive Schwarz apply (K4), 3D, sm_100a.  First version.
+// ras3d.cu -- restricted / classical additive Schwarz apply (K4), 3D, sm_100a.  First version.
 //
 // Same algorithm as ras2d.cu (Eq. eq:ras P:398-409, modified subdomain BC P:429-437, fixed-work
 // local GMRES, reading R9).  A 16^3 box with overlap 2 has 8000 extended-box unknowns, so the
@@ -24,6 +24,8 @@ struct Ras3Args {
   int bx, by, bz, o;
   int k;
   double idt, gamma, ih2;
+  int restrict_owned;   // right-RAS: R_k^0 (v zero outside the owned box)
+  double* y_ext;        // AS / right-RAS: ext-box solutions [box][ext node] for (R_k^delta)^T
 };
 
 __global__ void __launch_bounds__(NT, 1) ras3d_kernel(Ras3Args p) {
@@ -65,7 +67,9 @@ __global__ void __launch_bounds__(NT, 1) ras3d_kernel(Ras3Args p) {
       int li = l % Ex, lj = (l / Ex) % Ey, lk = l / (Ex * Ey);
       size_t g = (size_t)wrapi(gx0 + li, p.nx) + NX * wrapi(gy0 + lj, p.ny) +
                  NXY * wrapi(gz0 + lk, p.nz);
-      double vv = p.v[g];
+      const bool owned = li >= p.o && li < p.o + p.bx && lj >= p.o && lj < p.o + p.by &&
+                         lk >= p.o && lk < p.o + p.bz;
+      double vv = (p.restrict_owned && !owned) ? 0.0 : p.v[g];
       V[l] = vv;
       cl[l] = p.c[g];
       acc[0] += vv * vv;
@@ -78,6 +82,10 @@ __global__ void __launch_bounds__(NT, 1) ras3d_kernel(Ras3Args p) {
     }
     const double beta = sqrt(scal[0]);
     if (beta == 0.0) {
+      if (p.y_ext) {
+        for (int l = tid; l < n; l += NT) p.y_ext[(size_t)box * n + l] = 0.0;
+        continue;
+      }
       for (int l = tid; l < p.bx * p.by * p.bz; l += NT) {
         int li = l % p.bx, lj = (l / p.bx) % p.by, lk = l / (p.bx * p.by);
         p.z[(size_t)(ibx * p.bx + li) + NX * (iby * p.by + lj) + NXY * (ibz * p.bz + lk)] = 0.0;
@@ -196,6 +204,14 @@ __global__ void __launch_bounds__(NT, 1) ras3d_kernel(Ras3Args p) {
       }
     }
     __syncthreads();
+    if (p.y_ext) {   // (R_k^delta)^T: the whole ext-box solution, summed by ras_extend
+      for (int l = tid; l < n; l += NT) {
+        double s = 0.0;
+        for (int i = 0; i < jm; ++i) s += yv[i] * V[(size_t)i * n + l];
+        p.y_ext[(size_t)box * n + l] = s;
+      }
+      continue;
+    }
     for (int l = tid; l < p.bx * p.by * p.bz; l += NT) {
       int li = l % p.bx, lj = (l / p.bx) % p.by, lk = l / (p.bx * p.by);
       int ll = ((lk + p.o) * Ey + lj + p.o) * Ex + li + p.o;
@@ -239,7 +255,8 @@ cudaError_t launch_ras_3d(pfc_ctx* ctx, const double* v, const double* c, double
   ras3d_scratch_doubles(ctx, &grid);
   Ras3Args p{v, c, z, scratch, ras3d_scratch_per_cta(cf), cf.n[0], cf.n[1], cf.n[2],
              cf.ras_box[0], cf.ras_box[1], cf.ras_box[2], cf.ras_overlap, cf.ras_local_k,
-             1.0 / dt, cf.gamma, ctx->ih2};
+             1.0 / dt, cf.gamma, ctx->ih2, cf.ras_variant == PFC_RAS_RIGHT,
+             cf.ras_variant == PFC_RAS_LEFT ? nullptr : ctx->ras_y};
   ras3d_kernel<<<grid, NT, 0, ctx->stream>>>(p);
   ctx->launches++;
   {
@@ -248,8 +265,11 @@ cudaError_t launch_ras_3d(pfc_ctx* ctx, const double* v, const double* c, double
                       (cf.n[2] / cf.ras_box[2]);
     const double next = nb * (cf.ras_box[0] + 2 * cf.ras_overlap) *
                         (cf.ras_box[1] + 2 * cf.ras_overlap) * (cf.ras_box[2] + 2 * cf.ras_overlap);
-    pfc_account(ctx, PFC_K_RAS, 8.0 * (2.0 * next + ctx->N),
-                next * (31.0 * k + 4.0 * k * (k + 1) + 3.0 * k + 3.0) + 2.0 * k * ctx->N);
+    const double nout = cf.ras_variant == PFC_RAS_LEFT ? (double)ctx->N : next;
+    pfc_account(ctx, PFC_K_RAS, 8.0 * (2.0 * next + nout),
+                next * (31.0 * k + 4.0 * k * (k + 1) + 3.0 * k + 3.0) + 2.0 * k * nout);
   }
-  return cudaGetLastError();
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess || cf.ras_variant == PFC_RAS_LEFT) return e;
+  return launch_ras_extend(ctx, z);
 }

@@ -128,6 +128,7 @@ class PFCConfig:
     ras_box: tuple = (16, 16, 1)
     ras_overlap: int = 2
     ras_local_k: int = 10
+    ras_variant: int = 0            # 0 left-RAS, 1 AS, 2 right-RAS
     ic: dict = field(default_factory=dict)
     seed: int = 1
 

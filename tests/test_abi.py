@@ -49,6 +49,7 @@ def test_struct_layouts_match_header(lib):
     assert c.newton_rtol == 1e-10 and c.newton_atol == 1e-10 and c.newton_maxit == 50
     assert c.gmres_restart == 30 and c.gmres_rtol == 1e-3 and c.gmres_atol == 1e-11
     assert list(c.ras_box) == [16, 16, 16] and c.ras_overlap == 2 and c.ras_local_k == 10
+    assert c.ras_variant == P.PFC_RAS_LEFT
     # offsets of every field as the C compiler lays them out from include/pfc.h
     import subprocess
     import tempfile
@@ -96,6 +97,7 @@ def _create(lib, **over):
     (dict(adaptive=1, dt_min=2.0, dt_max=1.0), "dt_min"),
     (dict(ras_local_k=0), "ras_local_k"),
     (dict(gmres_restart=64), "gmres_restart"),
+    (dict(ras_variant=3), "ras_variant"),
 ])
 def test_create_validates_configuration(lib, over, fragment):
     st, msg = _create(lib, **over)

@@ -141,6 +141,45 @@ def test_ras_apply_parity(shape, box, o, k):
     assert rel(z, zo) <= 1e-12
 
 
+SCHWARZ_VARIANT_CASES = [
+    ((64, 64), (16, 16), 2, 10),           # column kernel
+    ((128, 128), (32, 32), 3, 10),         # column kernel, 5 rows per thread
+    ((48, 36), (12, 12), 1, 5),            # shared-memory-basis kernel (k = 5)
+    ((32, 32, 32), (16, 16, 16), 2, 10),   # 3D: 2 boxes per axis (-1/+1 neighbour coincide)
+    ((24, 24, 30), (8, 8, 10), 1, 4),      # 3D, 3 boxes per axis
+]
+
+
+@pytest.mark.parametrize("variant", [P.PFC_RAS_AS, P.PFC_RAS_RIGHT])
+@pytest.mark.parametrize("shape,box,o,k", SCHWARZ_VARIANT_CASES)
+def test_schwarz_variant_parity(shape, box, o, k, variant):
+    """Classical AS (Eq. invM) and right-RAS (Eq. eq:ash): subdomain
+    solves + deterministic overlap-add gather vs the oracle's box loop."""
+    phi = random_field(shape, 211, 0.07, 0.07)
+    psi = random_field(shape, 212, 0.07, 0.07)
+    v = random_field(shape, 213, 0.0, 1.0)
+    dt = 0.5
+    ctx = ctx_for(shape, box, o=o, k=k, ras_variant=variant)
+    z = host(ctx.ras_apply(dev(phi), dev(psi), dt, dev(v)))
+    prm = O.params(gamma=G, ras_box=box, ras_overlap=o, ras_local_k=k, ras_variant=variant)
+    zo = O.ras_apply(phi, psi, v, H, prm, dt)
+    assert rel(z, zo) <= 1e-12
+    z2 = host(ctx.ras_apply(dev(phi), dev(psi), dt, dev(v)))
+    assert np.array_equal(z, z2)            # the overlap-add is deterministic
+
+
+@pytest.mark.parametrize("variant", [P.PFC_RAS_AS, P.PFC_RAS_RIGHT])
+def test_cfg1_one_step_parity_schwarz_variants(variant):
+    """A full DVD step of config 1 preconditioned by AS / right-RAS vs the oracle's step."""
+    import dataclasses
+    cfg = dataclasses.replace(CONFIGS["cfg1"], ras_variant=variant)
+    phi0 = cfg.initial_condition()
+    one, infos = _run_gpu(cfg, phi0, 1)
+    ref, hist = O.run(cfg, phi0, 1)
+    assert rel(one, ref) <= 1e-10
+    assert infos[0]["gmres_its"] == hist[0][6]
+
+
 def test_ras_apply_parity_cfg2_full_size():
     cfg = CONFIGS["cfg2"]
     ic = cfg.initial_condition()
