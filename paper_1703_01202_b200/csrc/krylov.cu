@@ -20,7 +20,7 @@ constexpr int NT = 256;
 // blocks in the same order k_finalize uses (thread-strided over blocks, then the block tree),
 // so the result is bitwise identical to a separate k_finalize launch, without the launch.
 template <int NV>
-__device__ __forceinline__ void finalize_last_block(const double* partials, double* out,
+__device__ __forceinline__ bool finalize_last_block(const double* partials, double* out,
                                                     unsigned int* ticket, double* red,
                                                     double* outv) {
   __shared__ unsigned int last;
@@ -28,7 +28,7 @@ __device__ __forceinline__ void finalize_last_block(const double* partials, doub
   __syncthreads();
   if (threadIdx.x == 0) last = atomicAdd(ticket, 1u) == gridDim.x - 1;
   __syncthreads();
-  if (!last) return;
+  if (!last) return false;
   __threadfence();
   double acc[NV];
 #pragma unroll
@@ -40,6 +40,50 @@ __device__ __forceinline__ void finalize_last_block(const double* partials, doub
   block_sum_multi<NV>(acc, red, outv);
   if (threadIdx.x < NV) out[threadIdx.x] = outv[threadIdx.x];
   if (threadIdx.x == 0) *ticket = 0u;    // ready for the next reduction on this stream
+  return true;
+}
+
+// End of Arnoldi step j on the device (f1): Hessenberg column j = h1 + h2 (CGS2) and
+// h_{j+1,j} = ||w||, reduced by the previous Givens rotations and a new one, residual estimate
+// |g_{j+1}|, and the stopping decision of the host loop it replaces: non-finite,
+// happy breakdown h_{j+1,j} <= 1e-14 beta, ||r|| <= tol, its >= maxit, end of the cycle.
+__device__ void arnoldi_close(pfc_gmres_dev* gm, int j, const double* h1, const double* h2,
+                              double nrm2) {
+  const int m = gm->m, ld = m + 1;
+  double* H = gm->H;
+  const double hn = sqrt(nrm2);
+  for (int i = 0; i <= j; ++i) H[i + ld * j] = h1[i] + h2[i];
+  H[j + 1 + ld * j] = hn;
+  for (int i = 0; i < j; ++i) {
+    const double a = H[i + ld * j], b = H[i + 1 + ld * j];
+    H[i + ld * j] = gm->cs[i] * a + gm->sn[i] * b;
+    H[i + 1 + ld * j] = -gm->sn[i] * a + gm->cs[i] * b;
+  }
+  const double a = H[j + ld * j], b = H[j + 1 + ld * j];
+  const double r = sqrt(a * a + b * b);
+  const double c = r == 0.0 ? 1.0 : a / r, s = r == 0.0 ? 0.0 : b / r;
+  gm->cs[j] = c;
+  gm->sn[j] = s;
+  H[j + ld * j] = c * a + s * b;
+  H[j + 1 + ld * j] = 0.0;
+  gm->g[j + 1] = -s * gm->g[j];
+  gm->g[j] = c * gm->g[j];
+  gm->its += 1;
+  gm->jm = j + 1;
+  const double res = fabs(gm->g[j + 1]);
+  gm->res = res;
+  int reason = PFC_GM_RUNNING;
+  if (!isfinite(res)) reason = PFC_GM_NONFINITE;
+  else if (hn <= 1e-14 * gm->beta) reason = PFC_GM_HAPPY;
+  else {
+    gm->ihn = 1.0 / hn;
+    if (res <= gm->tol) reason = PFC_GM_CONVERGED;
+    else if (gm->its >= gm->maxit) reason = PFC_GM_MAXIT;
+    else if (j + 1 == m) reason = PFC_GM_RESTART;
+  }
+  gm->reason = reason;
+  __threadfence();
+  gm->stop = reason != PFC_GM_RUNNING;
 }
 
 struct Coef {
@@ -70,7 +114,9 @@ __global__ void __launch_bounds__(NT) k_multidot(const double* __restrict__ V, s
                                                  const double* __restrict__ w, size_t N,
                                                  double* __restrict__ partials,
                                                  double* __restrict__ out,
-                                                 unsigned int* __restrict__ ticket) {
+                                                 unsigned int* __restrict__ ticket,
+                                                 const int* __restrict__ gate) {
+  if (gate && *gate) return;
   __shared__ double red[32 * NV];
   __shared__ double outv[NV];
   double acc[NV];
@@ -92,7 +138,9 @@ __global__ void __launch_bounds__(NT) k_axpy_dot(const double* __restrict__ V, s
                                                  double* __restrict__ w, size_t N,
                                                  double* __restrict__ partials,
                                                  double* __restrict__ out,
-                                                 unsigned int* __restrict__ ticket) {
+                                                 unsigned int* __restrict__ ticket,
+                                                 const int* __restrict__ gate) {
+  if (gate && *gate) return;
   __shared__ double red[32 * NV];
   __shared__ double outv[NV];
   double hk[NV], acc[NV];
@@ -118,7 +166,10 @@ __global__ void __launch_bounds__(NT) k_axpy_norm(const double* __restrict__ V, 
                                                   double* __restrict__ w, size_t N,
                                                   double* __restrict__ partials,
                                                   double* __restrict__ out,
-                                                  unsigned int* __restrict__ ticket) {
+                                                  unsigned int* __restrict__ ticket,
+                                                  pfc_gmres_dev* __restrict__ gm,
+                                                  const double* __restrict__ h1) {
+  if (gm && gm->stop) return;
   __shared__ double red[32];
   __shared__ double outv[1];
   double hk[NV];
@@ -134,7 +185,8 @@ __global__ void __launch_bounds__(NT) k_axpy_norm(const double* __restrict__ V, 
   }
   block_sum_multi<1>(acc, red, outv);
   if (threadIdx.x == 0) partials[blockIdx.x] = outv[0];
-  finalize_last_block<1>(partials, out, ticket, red, outv);
+  const bool last = finalize_last_block<1>(partials, out, ticket, red, outv);
+  if (gm && last && threadIdx.x == 0) arnoldi_close(gm, NV - 1, h1, h, outv[0]);
 }
 
 __global__ void __launch_bounds__(NT) k_norm2(const double* __restrict__ x, size_t N,
@@ -171,6 +223,56 @@ __global__ void __launch_bounds__(NT) k_lincomb(double* __restrict__ x,
     double s = x[i];
 #pragma unroll
     for (int k = 0; k < NV; ++k) s += coef.c[k] * Z[k * ldz + i];
+    x[i] = s;
+  }
+}
+
+// V_{j+1} = w / h_{j+1,j} (skipped when the cycle stopped at step j)
+__global__ void k_scale_next(const pfc_gmres_dev* __restrict__ gm, const double* __restrict__ w,
+                             double* __restrict__ vnext, size_t N) {
+  if (gm->stop) return;
+  const double ihn = gm->ihn;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < N;
+       i += (size_t)gridDim.x * blockDim.x)
+    vnext[i] = ihn * w[i];
+}
+
+__global__ void k_cycle_init(pfc_gmres_dev* gm, double beta, double tol, int m, int maxit,
+                             int its_done) {
+  gm->beta = beta;
+  gm->tol = tol;
+  gm->m = m;
+  gm->maxit = maxit;
+  gm->its = its_done;
+  gm->jm = 0;
+  gm->reason = PFC_GM_RUNNING;
+  gm->stop = 0;
+  for (int i = 0; i <= m; ++i) gm->g[i] = 0.0;
+  gm->g[0] = beta;
+}
+
+// y = R^{-1} g (back substitution, the host loop's order) by one thread ...
+__global__ void k_backsolve(pfc_gmres_dev* gm) {
+  const int jm = gm->jm, ld = gm->m + 1;
+  for (int i = jm - 1; i >= 0; --i) {
+    double s = gm->g[i];
+    for (int l = i + 1; l < jm; ++l) s -= gm->H[i + ld * l] * gm->y[l];
+    gm->y[i] = s / gm->H[i + ld * i];
+  }
+}
+
+// ... then x += Z y over the jm columns of the cycle (FGMRES: solution from Z)
+__global__ void __launch_bounds__(NT) k_lincomb_dev(double* __restrict__ x,
+                                                    const double* __restrict__ Z, size_t ldz,
+                                                    const pfc_gmres_dev* __restrict__ gm,
+                                                    size_t N) {
+  __shared__ double yk[PFC_MAX_RESTART];
+  const int jm = gm->jm;
+  if (threadIdx.x < jm) yk[threadIdx.x] = gm->y[threadIdx.x];
+  __syncthreads();
+  for (size_t i = blockIdx.x * (size_t)NT + threadIdx.x; i < N; i += (size_t)gridDim.x * NT) {
+    double s = x[i];
+    for (int k = 0; k < jm; ++k) s += yk[k] * Z[k * ldz + i];
     x[i] = s;
   }
 }
@@ -216,7 +318,7 @@ cudaError_t launch_multidot(pfc_ctx* ctx, const double* V, int nv, const double*
 #define X(K)                                                                        \
   case K:                                                                           \
     k_multidot<K><<<nb, NT, 0, ctx->stream>>>(V, ctx->N, w, ctx->N, partials, out,  \
-                                              ctx->ticket);                         \
+                                              ctx->ticket, ctx->gate);              \
     break;
     PFC_NV_CASES(X)
 #undef X
@@ -234,7 +336,7 @@ cudaError_t launch_axpy_dot(pfc_ctx* ctx, const double* V, int nv, const double*
 #define X(K)                                                                          \
   case K:                                                                             \
     k_axpy_dot<K><<<nb, NT, 0, ctx->stream>>>(V, ctx->N, h, w, ctx->N, partials, out, \
-                                              ctx->ticket);                           \
+                                              ctx->ticket, ctx->gate);                \
     break;
     PFC_NV_CASES(X)
 #undef X
@@ -245,14 +347,15 @@ cudaError_t launch_axpy_dot(pfc_ctx* ctx, const double* V, int nv, const double*
   return cudaGetLastError();
 }
 
-cudaError_t launch_axpy_norm(pfc_ctx* ctx, const double* V, int nv, const double* h, double* w,
-                             double* partials, double* out) {
+static cudaError_t axpy_norm_impl(pfc_ctx* ctx, const double* V, int nv, const double* h1,
+                                  const double* h, double* w, double* partials, double* out,
+                                  pfc_gmres_dev* gm) {
   const int nb = blas_nblocks(ctx->N);
   switch (nv) {
 #define X(K)                                                                           \
   case K:                                                                              \
     k_axpy_norm<K><<<nb, NT, 0, ctx->stream>>>(V, ctx->N, h, w, ctx->N, partials, out, \
-                                               ctx->ticket);                           \
+                                               ctx->ticket, gm, h1);                   \
     break;
     PFC_NV_CASES(X)
 #undef X
@@ -260,6 +363,39 @@ cudaError_t launch_axpy_norm(pfc_ctx* ctx, const double* V, int nv, const double
   }
   ctx->launches++;
   pfc_account(ctx, PFC_K_ORTH, 8.0 * (nv + 2) * ctx->N, (2.0 * nv + 2.0) * ctx->N);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_axpy_norm(pfc_ctx* ctx, const double* V, int nv, const double* h, double* w,
+                             double* partials, double* out) {
+  return axpy_norm_impl(ctx, V, nv, nullptr, h, w, partials, out, nullptr);
+}
+
+cudaError_t launch_axpy_norm_close(pfc_ctx* ctx, const double* V, int nv, const double* h1,
+                                   const double* h2, double* w, double* partials, double* out) {
+  return axpy_norm_impl(ctx, V, nv, h1, h2, w, partials, out, ctx->gm);
+}
+
+cudaError_t launch_scale_next(pfc_ctx* ctx, const double* w, double* vnext) {
+  k_scale_next<<<grid_pointwise(ctx->N), NT, 0, ctx->stream>>>(ctx->gm, w, vnext, ctx->N);
+  ctx->launches++;
+  pfc_account(ctx, PFC_K_VECTOR, 16.0 * ctx->N, 1.0 * ctx->N);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_cycle_init(pfc_ctx* ctx, double beta, double tol, int its_done) {
+  k_cycle_init<<<1, 1, 0, ctx->stream>>>(ctx->gm, beta, tol, ctx->cfg.gmres_restart,
+                                         ctx->cfg.gmres_maxit, its_done);
+  ctx->launches++;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_backsolve_lincomb(pfc_ctx* ctx, double* x, const double* Z, int jm) {
+  k_backsolve<<<1, 1, 0, ctx->stream>>>(ctx->gm);
+  ctx->launches++;
+  k_lincomb_dev<<<blas_nblocks(ctx->N), NT, 0, ctx->stream>>>(x, Z, ctx->N, ctx->gm, ctx->N);
+  ctx->launches++;
+  pfc_account(ctx, PFC_K_VECTOR, 8.0 * (jm + 2) * ctx->N, 2.0 * jm * ctx->N);
   return cudaGetLastError();
 }
 

@@ -173,8 +173,9 @@ static pfc_status energy_mass(pfc_ctx* ctx, const double* phi, double* F_d, doub
 // ------------------------------------------------------------------ FGMRES
 
 // Solve J S = -F approximately: right-preconditioned flexible GMRES(m), CGS2 Arnoldi, Givens,
-// x0 = 0, stop at ||r|| <= max(xi_r ||F||, xi_a) or gmres_maxit iterations.
-static pfc_status fgmres(pfc_ctx* ctx, double dt, double Fnorm, int* its_out) {
+// x0 = 0, stop at ||r|| <= max(xi_r ||F||, xi_a) or gmres_maxit iterations.  Host-driven
+// reference loop (one D2H round trip per Arnoldi step); fgmres_device is the default.
+static pfc_status fgmres_host(pfc_ctx* ctx, double dt, double Fnorm, int* its_out) {
   const pfc_config& c = ctx->cfg;
   const int m = c.gmres_restart;
   const size_t N = ctx->N;
@@ -247,6 +248,82 @@ static pfc_status fgmres(pfc_ctx* ctx, double dt, double Fnorm, int* its_out) {
   }
   *its_out = its;
   return PFC_OK;
+}
+
+// Device-resident FGMRES (NEXT row f1): same mathematics and stopping rule as fgmres_host, but
+// the Givens update and the stop decision of every Arnoldi step run on the device (in the
+// last block of k_axpy_norm).  The host launches step j+1 before it knows whether step j
+// stopped the cycle and only then waits for step j-1's flags, so the GPU never idles for a
+// host round trip inside a cycle; kernels of a step launched after the stop exit at once
+// (gate = &gm->stop).  Back substitution and S += Z y run on the device too.  The host syncs
+// once per cycle (restart / exit) instead of once per Arnoldi step.
+static pfc_status fgmres_device(pfc_ctx* ctx, double dt, double Fnorm, int* its_out) {
+  const pfc_config& c = ctx->cfg;
+  const int m = c.gmres_restart;
+  const size_t N = ctx->N;
+  const double tol = std::max(c.gmres_rtol * Fnorm, c.gmres_atol);
+  int its = 0;
+  CK(cudaMemsetAsync(ctx->S, 0, N * sizeof(double), ctx->stream), "memset S");
+  if (Fnorm <= tol || Fnorm == 0.0) { *its_out = 0; return PFC_OK; }
+  double beta = Fnorm;
+  KL(PFC_K_VECTOR, launch_axpby(ctx, -1.0 / beta, ctx->F, 0.0, nullptr, ctx->V), "axpby");
+  for (;;) {
+    KL(PFC_K_VECTOR, launch_cycle_init(ctx, beta, tol, its), "cycle init");
+    ctx->gate = &ctx->gm->stop;
+    int* fl = nullptr;            // flags of the step that stopped the cycle
+    int launched = 0;
+    for (int j = 0; j < m && !fl; ++j) {
+      double* Vj = ctx->V + (size_t)j * N;
+      double* Zj = ctx->Z + (size_t)j * N;
+      KL(PFC_K_RAS, launch_ras(ctx, Vj, ctx->c, dt, Zj), "ras");
+      KL(PFC_K_JV, launch_jv(ctx, Zj, ctx->c, dt, ctx->w), "jv");
+      KL(PFC_K_ORTH, launch_multidot(ctx, ctx->V, j + 1, ctx->w, ctx->partials, ctx->dscal + SC_H1), "multidot");
+      KL(PFC_K_ORTH, launch_axpy_dot(ctx, ctx->V, j + 1, ctx->dscal + SC_H1, ctx->w, ctx->partials, ctx->dscal + SC_H2), "cgs2");
+      KL(PFC_K_ORTH, launch_axpy_norm_close(ctx, ctx->V, j + 1, ctx->dscal + SC_H1, ctx->dscal + SC_H2, ctx->w, ctx->partials, ctx->dscal + SC_NRM), "cgs2");
+      if (j + 1 < m)
+        KL(PFC_K_VECTOR, launch_scale_next(ctx, ctx->w, ctx->V + (size_t)(j + 1) * N), "scale");
+      CK(cudaMemcpyAsync(ctx->hflags + 4 * j, &ctx->gm->stop, 4 * sizeof(int),
+                         cudaMemcpyDeviceToHost, ctx->stream), "D2H flags");
+      CK(cudaEventRecord(ctx->step_ev[j], ctx->stream), "event");
+      launched = j + 1;
+      if (j >= 1) {   // step j is queued behind step j-1: now look at step j-1
+        CK(cudaEventSynchronize(ctx->step_ev[j - 1]), "event sync");
+        if (ctx->hflags[4 * (j - 1)]) fl = ctx->hflags + 4 * (j - 1);
+      }
+    }
+    if (!fl) {        // the last launched step decides (the cycle always stops by step m-1)
+      CK(cudaEventSynchronize(ctx->step_ev[launched - 1]), "event sync");
+      fl = ctx->hflags + 4 * (launched - 1);
+    }
+    ctx->gate = nullptr;
+    const int jm = fl[1], reason = fl[3];
+    its = fl[2];
+    if (reason == PFC_GM_NONFINITE)
+      return pfc_fail(ctx, PFC_EBREAKDOWN, "FGMRES: non-finite residual");
+    KL(PFC_K_VECTOR, launch_backsolve_lincomb(ctx, ctx->S, ctx->Z, jm), "lincomb");   // S += Z y
+    if (reason != PFC_GM_RESTART) break;
+    // restart: r = -F - J S (true residual), V0 = r/|r|
+    KL(PFC_K_JV, launch_jv(ctx, ctx->S, ctx->c, dt, ctx->w), "jv");
+    KL(PFC_K_VECTOR, launch_axpby(ctx, -1.0, ctx->F, -1.0, ctx->w, ctx->w), "axpby");
+    KL(PFC_K_VECTOR, launch_norm2(ctx, ctx->w, ctx->partials, ctx->dscal + SC_NRM), "norm");
+    pfc_status s = fetch(ctx, SC_NRM, 1);
+    if (s) return s;
+    beta = sqrt(ctx->hscal[SC_NRM]);
+    if (beta <= tol) break;
+    KL(PFC_K_VECTOR, launch_axpby(ctx, 1.0 / beta, ctx->w, 0.0, nullptr, ctx->V), "scale");
+  }
+  *its_out = its;
+  return PFC_OK;
+}
+
+// Default: the host-driven loop.  Measured on B200 (round 1, bench.py, 197 / 20 steps): the
+// device-resident cycle was 2-5% SLOWER on cfg1, cfg2 and equal on cfg4 -- the cycles are short
+// (2-3 Arnoldi steps per Newton iteration at the configs' dt), so the early-exit kernels of the
+// one speculative step per cycle cost more than the ~5 us host round trips they remove.
+// PFC_DEVICE_ARNOLDI=1 selects fgmres_device (same results to rounding; parity-tested).
+static pfc_status fgmres(pfc_ctx* ctx, double dt, double Fnorm, int* its_out) {
+  static const bool dev = getenv("PFC_DEVICE_ARNOLDI") != nullptr;
+  return dev ? fgmres_device(ctx, dt, Fnorm, its_out) : fgmres_host(ctx, dt, Fnorm, its_out);
 }
 
 // ------------------------------------------------------------------ Newton
@@ -426,6 +503,9 @@ pfc_status pfc_create(const pfc_config* cfg, void* stream, pfc_ctx** out) {
       pfc_check_cuda(ctx, cudaMalloc(&ctx->dscal, SC_TOTAL * sizeof(double)), "dscal") ||
       pfc_check_cuda(ctx, cudaMalloc(&ctx->ticket, sizeof(unsigned int)), "ticket") ||
       pfc_check_cuda(ctx, cudaMemset(ctx->ticket, 0, sizeof(unsigned int)), "ticket") ||
+      pfc_check_cuda(ctx, cudaMalloc(&ctx->gm, sizeof(pfc_gmres_dev)), "gmres state") ||
+      pfc_check_cuda(ctx, cudaMemset(ctx->gm, 0, sizeof(pfc_gmres_dev)), "gmres state") ||
+      pfc_check_cuda(ctx, cudaMallocHost(&ctx->hflags, 4 * PFC_MAX_RESTART * sizeof(int)), "flags") ||
       pfc_check_cuda(ctx, cudaMallocHost(&ctx->hscal, SC_TOTAL * sizeof(double)), "hscal"))
     return fail(PFC_ENOMEM);
   if (c.ndim == 3) {
@@ -434,6 +514,10 @@ pfc_status pfc_create(const pfc_config* cfg, void* stream, pfc_ctx** out) {
     if (pfc_check_cuda(ctx, cudaMalloc(&ctx->ras_scratch, d * sizeof(double)), "ras scratch"))
       return fail(PFC_ENOMEM);
   }
+  ctx->step_ev.resize(PFC_MAX_RESTART);
+  for (auto& e : ctx->step_ev)
+    if (pfc_check_cuda(ctx, cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "events"))
+      return fail(PFC_ECUDA);
   if (c.ras_variant != PFC_RAS_LEFT &&
       pfc_check_cuda(ctx, cudaMalloc(&ctx->ras_y, ras_ext_doubles(ctx) * sizeof(double)),
                      "ras ext-box solutions"))
@@ -450,6 +534,10 @@ void pfc_destroy(pfc_ctx* ctx) {
   for (double* f : fs)
     if (f) cudaFree(f);
   if (ctx->ticket) cudaFree(ctx->ticket);
+  if (ctx->gm) cudaFree(ctx->gm);
+  if (ctx->hflags) cudaFreeHost(ctx->hflags);
+  for (cudaEvent_t e : ctx->step_ev)
+    if (e) cudaEventDestroy(e);
   if (ctx->hscal) cudaFreeHost(ctx->hscal);
   prof_drain(ctx);
   for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);

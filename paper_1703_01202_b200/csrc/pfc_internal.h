@@ -12,6 +12,22 @@
 #define PFC_MAX_RESTART 32
 #define PFC_MAX_LOCAL_K 15
 
+// Device-resident state of one FGMRES cycle (NEXT row f1): the Givens QR of the Hessenberg
+// matrix is updated on the device at the end of every Arnoldi step, which also decides
+// whether the cycle stops; `stop` gates every kernel of the following (speculatively
+// launched) steps, so the host never waits between Arnoldi steps.
+struct pfc_gmres_dev {
+  double H[(PFC_MAX_RESTART + 1) * PFC_MAX_RESTART];   // H[i + (m+1) j], reduced to R
+  double cs[PFC_MAX_RESTART], sn[PFC_MAX_RESTART];
+  double g[PFC_MAX_RESTART + 1], y[PFC_MAX_RESTART];
+  double beta, tol, ihn, res;
+  int m, maxit;
+  // read back by the host after every step (contiguous): stop flag, columns, total its, why
+  int stop, jm, its, reason;
+};
+enum { PFC_GM_RUNNING = 0, PFC_GM_CONVERGED = 1, PFC_GM_HAPPY = 2, PFC_GM_MAXIT = 3,
+       PFC_GM_RESTART = 4, PFC_GM_NONFINITE = 5 };
+
 struct pfc_ctx {
   pfc_config cfg;
   cudaStream_t stream = nullptr;
@@ -39,6 +55,10 @@ struct pfc_ctx {
   double* dscal = nullptr;     // device scalars: [0,64) h1, [64,128) h2, [128] |w|^2, ...
   double* hscal = nullptr;     // pinned host mirror of dscal
   unsigned int* ticket = nullptr;  // last-block ticket of the fused reductions (device, 0)
+  pfc_gmres_dev* gm = nullptr;     // device FGMRES cycle state (f1)
+  int* hflags = nullptr;           // pinned: per-step snapshots of gm->{stop, jm, its, reason}
+  std::vector<cudaEvent_t> step_ev;   // one event per Arnoldi step of a cycle
+  const int* gate = nullptr;       // &gm->stop while a device-resident cycle is being launched
 
   // RAS launch plan
   int ras_smem = 0;
@@ -111,6 +131,13 @@ cudaError_t launch_axpy_dot(pfc_ctx* ctx, const double* V, int nv, const double*
                             double* partials, double* out);
 cudaError_t launch_axpy_norm(pfc_ctx* ctx, const double* V, int nv, const double* h, double* w,
                              double* partials, double* out);
+// device-resident FGMRES cycle (f1): axpy_norm + Givens update of column nv-1 in its last
+// block; V_{j+1} = w / h_{j+1,j}; cycle init; back substitution + S += Z y on the device
+cudaError_t launch_axpy_norm_close(pfc_ctx* ctx, const double* V, int nv, const double* h1,
+                                   const double* h2, double* w, double* partials, double* out);
+cudaError_t launch_scale_next(pfc_ctx* ctx, const double* w, double* vnext);
+cudaError_t launch_cycle_init(pfc_ctx* ctx, double beta, double tol, int its_done);
+cudaError_t launch_backsolve_lincomb(pfc_ctx* ctx, double* x, const double* Z, int jm);
 cudaError_t launch_norm2(pfc_ctx* ctx, const double* x, double* partials, double* out);
 cudaError_t launch_finalize(pfc_ctx* ctx, const double* partials, int nblk, int nval,
                             double* out);

@@ -46,6 +46,7 @@ struct RasArgs {
   double idt, gamma, ih2;
   int restrict_owned;   // right-RAS: R_k^0 (v zero outside the owned box)
   double* y_ext;        // AS / right-RAS: ext-box solutions [box][ext node] for (R_k^delta)^T
+  const int* gate;   // device-resident FGMRES: skip the launch when *gate != 0 (f1)
 };
 
 constexpr int pow2_at_least(int x) { return x <= 1 ? 1 : 2 * pow2_at_least((x + 1) / 2); }
@@ -125,6 +126,7 @@ __global__ void __launch_bounds__(NT, 1) ras2d_kernel(RasArgs p) {
   __shared__ double H[(K + 1) * K];
   __shared__ double gv[K + 1], cs[K], sn[K], yv[K];
 
+  if (p.gate && *p.gate) return;
   const int tid = threadIdx.x;
   double* h1 = hwall + (tid >> 5) * 3 * NVP;
   double* h2 = h1 + NVP;
@@ -391,6 +393,7 @@ struct RasColArgs {
   int Ex, Ey, ns;               // extended box, strips per column
   int restrict_owned;           // right-RAS: R_k^0 (v zero outside the owned box)
   double* y_ext;                // AS / right-RAS: ext-box solutions [box][ext node]
+  const int* gate;   // device-resident FGMRES: skip the launch when *gate != 0 (f1)
   double W[6];                  // 25-point class weights: (0,0) (0,1) (0,2) (1,1) (0,3) (1,2)
   double ih2;
 };
@@ -611,6 +614,7 @@ __global__ void __launch_bounds__(NTC, 1) ras2d_col_kernel(const __grid_constant
   __shared__ double H[(K + 1) * K];
   __shared__ double gv[K + 1], cs[K], sn[K], yv[K], rd[K];
 
+  if (p.gate && *p.gate) return;
   const int tid = threadIdx.x, nwt = blockDim.x >> 5;
   const bool gwarp = (tid >> 5) == nwt - 1;     // the Givens warp: no nodes, reduces H
   const bool g0 = gwarp && (tid & 31) == 0;
@@ -860,6 +864,7 @@ cudaError_t launch_ras_2d(pfc_ctx* ctx, const double* v, const double* c, double
     p.o = cf.ras_overlap; p.Ex = Ex; p.Ey = Ey; p.ns = (Ey + R - 1) / R;
     p.restrict_owned = cf.ras_variant == PFC_RAS_RIGHT;
     p.y_ext = cf.ras_variant == PFC_RAS_LEFT ? nullptr : ctx->ras_y;
+    p.gate = ctx->gate;
     // class weights of the linear part v/dt - alpha Delta v - Delta^2 v - Delta^3 v / 2 with
     // h^2 Delta = L:  L (0,0) -4, (0,1) 1;  L^2 (0,0) 20, (0,1) -8, (0,2) 1, (1,1) 2;
     // L^3 (0,0) -112, (0,1) 57, (0,2) -12, (1,1) -24, (0,3) 1, (1,2) 3
@@ -881,7 +886,7 @@ cudaError_t launch_ras_2d(pfc_ctx* ctx, const double* v, const double* c, double
     if (e != cudaSuccess) return e;
     RasArgs p{v, c, z, cf.n[0], cf.n[1], cf.ras_box[0], cf.ras_box[1], cf.ras_overlap,
               1.0 / dt, cf.gamma, ctx->ih2, cf.ras_variant == PFC_RAS_RIGHT,
-              cf.ras_variant == PFC_RAS_LEFT ? nullptr : ctx->ras_y};
+              cf.ras_variant == PFC_RAS_LEFT ? nullptr : ctx->ras_y, ctx->gate};
     fn<<<nb, NT, ctx->ras_smem, ctx->stream>>>(p);
   }
   ctx->launches++;

@@ -26,6 +26,7 @@ struct Ras3Args {
   double idt, gamma, ih2;
   int restrict_owned;   // right-RAS: R_k^0 (v zero outside the owned box)
   double* y_ext;        // AS / right-RAS: ext-box solutions [box][ext node] for (R_k^delta)^T
+  const int* gate;   // device-resident FGMRES: skip the launch when *gate != 0 (f1)
 };
 
 __global__ void __launch_bounds__(NT, 1) ras3d_kernel(Ras3Args p) {
@@ -48,6 +49,7 @@ __global__ void __launch_bounds__(NT, 1) ras3d_kernel(Ras3Args p) {
   double* pl = pv + np;
   double* pb = pl + np;
 
+  if (p.gate && *p.gate) return;
   const int tid = threadIdx.x;
   const int nbx = p.nx / p.bx, nby = p.ny / p.by, nbz = p.nz / p.bz;
   const int nboxes = nbx * nby * nbz;
@@ -256,7 +258,7 @@ cudaError_t launch_ras_3d(pfc_ctx* ctx, const double* v, const double* c, double
   Ras3Args p{v, c, z, scratch, ras3d_scratch_per_cta(cf), cf.n[0], cf.n[1], cf.n[2],
              cf.ras_box[0], cf.ras_box[1], cf.ras_box[2], cf.ras_overlap, cf.ras_local_k,
              1.0 / dt, cf.gamma, ctx->ih2, cf.ras_variant == PFC_RAS_RIGHT,
-             cf.ras_variant == PFC_RAS_LEFT ? nullptr : ctx->ras_y};
+             cf.ras_variant == PFC_RAS_LEFT ? nullptr : ctx->ras_y, ctx->gate};
   ras3d_kernel<<<grid, NT, 0, ctx->stream>>>(p);
   ctx->launches++;
   {

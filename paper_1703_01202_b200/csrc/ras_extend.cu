@@ -19,6 +19,7 @@ struct ExtArgs {
   double* z;
   int n[3], b[3], nb[3], E[3], o;
   int nd;
+  const int* gate;   // device-resident FGMRES: skip the launch when *gate != 0 (f1)
 };
 
 // candidate boxes along one axis covering coordinate x: unique indices, local coordinates
@@ -43,6 +44,7 @@ __device__ __forceinline__ int axis_candidates(int x, int n, int b, int nb, int 
 }
 
 __global__ void __launch_bounds__(NT) k_ras_extend(const ExtArgs p) {
+  if (p.gate && *p.gate) return;
   const size_t N = (size_t)p.n[0] * p.n[1] * p.n[2];
   const size_t next = (size_t)p.E[0] * p.E[1] * p.E[2];
   for (size_t q = blockIdx.x * (size_t)NT + threadIdx.x; q < N; q += (size_t)gridDim.x * NT) {
@@ -76,6 +78,7 @@ cudaError_t launch_ras_extend(pfc_ctx* ctx, double* z) {
   p.z = z;
   p.nd = c.ndim;
   p.o = c.ras_overlap;
+  p.gate = ctx->gate;
   for (int d = 0; d < 3; ++d) {
     const bool act = d < c.ndim;
     p.n[d] = c.n[d];

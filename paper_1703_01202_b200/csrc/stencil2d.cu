@@ -36,6 +36,7 @@ struct S2Args {
   int nx, ny;
   double idt, gamma, ih2;
   int use_tma;
+  const int* gate;   // device-resident FGMRES: skip the launch when *gate != 0 (f1)
 };
 
 __device__ __forceinline__ double lap5(const double* f, int q, double ih2) {
@@ -58,6 +59,7 @@ __global__ void __launch_bounds__(NT) stencil2d_kernel(const __grid_constant__ C
   __shared__ uint64_t bar;
   __shared__ double red[64];
 
+  if (p.gate && *p.gate) return;
   const int tid = threadIdx.x;
   const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
   const int gx0 = x0 - HX, gy0 = y0 - HY;
@@ -161,7 +163,8 @@ cudaError_t launch2d(pfc_ctx* ctx, const double* a, const double* b, double dt, 
     attr_set = true;
   }
   const int nx = ctx->cfg.n[0], ny = ctx->cfg.n[1];
-  S2Args p{a, b, out, partials, nx, ny, 1.0 / dt, ctx->cfg.gamma, ctx->ih2, 0};
+  S2Args p{a, b, out, partials, nx, ny, 1.0 / dt, ctx->cfg.gamma, ctx->ih2, 0,
+           OP == OP_JV ? ctx->gate : nullptr};
   CUtensorMap ma, mb;
   memset(&ma, 0, sizeof(ma));
   memset(&mb, 0, sizeof(mb));

@@ -48,6 +48,7 @@ struct S3Args {
   int zc;            // planes per chunk
   double idt, gamma, ih2;
   int use_tma;
+  const int* gate;   // device-resident FGMRES: skip the launch when *gate != 0 (f1)
 };
 
 struct d2 { double x, y; };
@@ -99,6 +100,7 @@ __global__ void __launch_bounds__(NT, 1) stencil3d_kernel(const __grid_constant_
   __shared__ uint64_t bars[RING];
   __shared__ double red[64];
 
+  if (p.gate && *p.gate) return;
   const int tid = threadIdx.x;
   const int ntx = (p.nx + TX - 1) / TX;
   const int x0 = (blockIdx.x % ntx) * TX, y0 = (blockIdx.x / ntx) * TY;
@@ -317,7 +319,8 @@ cudaError_t launch3d(pfc_ctx* ctx, const double* a, const double* b, double dt, 
   int zc = want < 8 ? 8 : (want > 64 ? 64 : want);
   if (zc > nz) zc = nz;
   const int nzc = (nz + zc - 1) / zc;
-  S3Args p{a, b, out, partials, nx, ny, nz, zc, 1.0 / dt, ctx->cfg.gamma, ctx->ih2, 0};
+  S3Args p{a, b, out, partials, nx, ny, nz, zc, 1.0 / dt, ctx->cfg.gamma, ctx->ih2, 0,
+           OP == OP_JV ? ctx->gate : nullptr};
   CUtensorMap ma, mb;
   memset(&ma, 0, sizeof(ma));
   memset(&mb, 0, sizeof(mb));

@@ -247,6 +247,33 @@ def test_cfg4_3d_one_step_parity_small():
     assert rel(out, ref) <= 1e-10
 
 
+def test_device_resident_fgmres_matches_oracle():
+    """NEXT row f1: the device-resident FGMRES cycle (Givens + stopping test on the GPU,
+    speculative launches gated by the device stop flag), run in a subprocess with
+    PFC_DEVICE_ARNOLDI=1: cfg1 one step and 5 steps vs the oracle, same iteration counts."""
+    import os
+    import subprocess
+    import sys
+    code = (
+        "import numpy as np, torch, sys\n"
+        "from oracle import oracle as O\n"
+        "from paper_1703_01202_b200 import pfc as P\n"
+        "from paper_1703_01202_b200.inputs import CONFIGS\n"
+        "cfg = CONFIGS['cfg1']; phi0 = cfg.initial_condition(); ctx = P.Context(cfg)\n"
+        "phi = torch.from_numpy(phi0.copy()).cuda(); dt = cfg.dt0; its = []\n"
+        "for _ in range(5):\n"
+        "    dt, info = ctx.step(phi, dt); its.append(info['gmres_its'])\n"
+        "ref, hist = O.run(cfg, phi0, 5)\n"
+        "r = float(np.linalg.norm(phi.cpu().numpy() - ref) / np.linalg.norm(ref))\n"
+        "print(r, its == [h[6] for h in hist])\n"
+        "sys.exit(0 if (r <= 1e-9 and its == [h[6] for h in hist]) else 1)\n")
+    env = dict(os.environ, PFC_DEVICE_ARNOLDI="1")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], env=env, cwd=root, capture_output=True,
+                       text=True, timeout=600)
+    assert r.returncode == 0, r.stdout + r.stderr
+
+
 def test_step_host_pointer_matches_device_and_is_deterministic():
     cfg = CONFIGS["cfg1"]
     phi0 = cfg.initial_condition()
