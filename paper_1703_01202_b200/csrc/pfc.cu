@@ -6,6 +6,7 @@
 #include <math.h>
 #include <stdio.h>
 #include <string.h>
+#include <stdlib.h>
 
 #include <cudaTypedefs.h>
 
@@ -131,8 +132,9 @@ cudaError_t launch_jv(pfc_ctx* ctx, const double* v, const double* c, double dt,
 int ras_plan(pfc_ctx* ctx) { return ctx->cfg.ndim == 2 ? ras2d_plan(ctx) : ras3d_plan(ctx); }
 
 cudaError_t launch_ras(pfc_ctx* ctx, const double* v, const double* c, double dt, double* z) {
-  return ctx->cfg.ndim == 2 ? launch_ras_2d(ctx, v, c, dt, z)
-                            : launch_ras_3d(ctx, v, c, dt, z, ctx->ras_scratch);
+  if (ctx->cfg.ndim == 2) return launch_ras_2d(ctx, v, c, dt, z);
+  return ctx->ras3_col ? launch_ras_3d_col(ctx, v, c, dt, z, ctx->ras_scratch)
+                       : launch_ras_3d(ctx, v, c, dt, z, ctx->ras_scratch);
 }
 
 // ------------------------------------------------------------------ scalars
@@ -510,7 +512,9 @@ pfc_status pfc_create(const pfc_config* cfg, void* stream, pfc_ctx** out) {
     return fail(PFC_ENOMEM);
   if (c.ndim == 3) {
     int grid = 0;
-    size_t d = ras3d_scratch_doubles(ctx, &grid);
+    size_t d = 0;
+    ctx->ras3_col = getenv("PFC_RAS3D_V1") == nullptr && ras3d_col_plan(ctx, &d, &grid);
+    if (!ctx->ras3_col) d = ras3d_scratch_doubles(ctx, &grid);
     if (pfc_check_cuda(ctx, cudaMalloc(&ctx->ras_scratch, d * sizeof(double)), "ras scratch"))
       return fail(PFC_ENOMEM);
   }

@@ -64,7 +64,8 @@ struct pfc_ctx {
   int ras_smem = 0;
   int ras_threads = 0;
   int ras_cluster = 1;
-  int ras_rows = 0;        // 2D column-strip RAS kernel: node rows per thread (0: other kernel)
+  int ras_rows = 0;
+  int ras3_col = 0;        // 3D: on-chip column kernel (ras3d_col.cu) instead of ras3d.cu
 
   long long launches = 0;
   std::string err;
@@ -118,6 +119,9 @@ size_t ras3d_scratch_doubles(pfc_ctx* ctx, int* grid);
 cudaError_t launch_ras_2d(pfc_ctx*, const double* v, const double* c, double dt, double* z);
 cudaError_t launch_ras_3d(pfc_ctx*, const double* v, const double* c, double dt, double* z,
                           double* scratch);
+int ras3d_col_plan(pfc_ctx* ctx, size_t* scratch_doubles, int* grid);
+cudaError_t launch_ras_3d_col(pfc_ctx*, const double* v, const double* c, double dt, double* z,
+                              double* scratch);
 
 // Krylov / pointwise (krylov.cu)
 int blas_nblocks(size_t N);

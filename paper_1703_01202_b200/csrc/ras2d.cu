@@ -27,6 +27,7 @@
 //    loop depends on it).  Five barriers per Arnoldi step.
 #include "pfc_device.cuh"
 #include "pfc_internal.h"
+#include "ras_common.cuh"
 
 #include <stdlib.h>
 
@@ -48,39 +49,6 @@ struct RasArgs {
   double* y_ext;        // AS / right-RAS: ext-box solutions [box][ext node] for (R_k^delta)^T
   const int* gate;   // device-resident FGMRES: skip the launch when *gate != 0 (f1)
 };
-
-constexpr int pow2_at_least(int x) { return x <= 1 ? 1 : 2 * pow2_at_least((x + 1) / 2); }
-
-// One reduce-scatter step: lanes exchange the half they do not keep across lane offset `off`
-// (HALF is a template parameter so every array index is compile-time: registers only).
-template <int NVP, int HALF>
-__device__ __forceinline__ void rs_step(double (&a)[NVP], int lane, int off) {
-  const bool upper = (lane & off) != 0;
-#pragma unroll
-  for (int i = 0; i < HALF; ++i) {
-    const double lo = a[i], hi = a[i + HALF];      // compile-time indices: registers
-    const double send = upper ? lo : hi, keep = upper ? hi : lo;
-    a[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
-  }
-  if constexpr (HALF > 1) rs_step<NVP, HALF / 2>(a, lane, off >> 1);
-}
-
-// Warp reduce-scatter of NVP (power of two, <= 32) values: afterwards lane l holds the warp
-// sum of value (l >> (5 - log2 NVP)).  Fixed shuffle tree, deterministic.
-template <int NVP>
-__device__ __forceinline__ double warp_reduce_scatter(double (&a)[NVP]) {
-  const int lane = threadIdx.x & 31;
-  int off = 16;
-  if constexpr (NVP > 1) {
-    rs_step<NVP, NVP / 2>(a, lane, 16);
-    off = 16 / (NVP / 2) / 2;
-  }
-  double s = a[0];
-#pragma unroll
-  for (int o = 16; o >= 1; o >>= 1)
-    if (o <= off) s += __shfl_xor_sync(0xffffffffu, s, o);
-  return s;
-}
 
 // Block sum of nv (runtime, <= NVP) values held by every thread in acc[]: the sums are left in
 // this warp's private copy hw[0..nv) (valid after return for every lane of the warp).  One

@@ -123,8 +123,9 @@ RAS_CASES = [
     ((128, 128), (32, 32), 3, 10),
     ((128, 128), (32, 32), 4, 10),
     ((48, 36), (12, 12), 1, 5),
-    ((32, 32, 32), (16, 16, 16), 2, 10),
-    ((24, 24, 20), (8, 8, 10), 1, 4),
+    ((32, 32, 32), (16, 16, 16), 2, 10),   # on-chip 3D column kernel, E = 20
+    ((32, 32, 32), (8, 8, 8), 2, 4),       # on-chip 3D column kernel, E = 12
+    ((24, 24, 20), (8, 8, 10), 1, 4),      # non-cubic box: global-scratch 3D kernel
 ]
 
 
