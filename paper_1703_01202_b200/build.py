@@ -34,8 +34,17 @@ def build(force: bool = False, verbose: bool = False) -> str:
     os.makedirs(objdir, exist_ok=True)
     os.makedirs(LIBDIR, exist_ok=True)
 
+    # diagnostic variants (PFC_LIB_NAME + PFC_EXTRA_NVCC_FLAGS) may recompile only the sources
+    # listed in PFC_VARIANT_SOURCES and reuse the default build's objects for the rest
+    only = [f for f in os.environ.get("PFC_VARIANT_SOURCES", "").split(",") if f]
+    basedir = os.path.join(HERE, "..", "build", "obj")
+
     def compile_one(src):
         obj = os.path.join(objdir, src.replace(".cu", ".o"))
+        if only and src not in only:
+            base = os.path.join(basedir, src.replace(".cu", ".o"))
+            if os.path.exists(base):
+                return base, ""
         cmd = [NVCC, *FLAGS, "-c", os.path.join(CSRC, src), "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:

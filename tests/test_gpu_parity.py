@@ -63,6 +63,8 @@ OPERATOR_CASES = [
     ((32, 32, 32), (16, 16, 16)),
     ((40, 24, 20), (8, 8, 4)),
     ((27, 21, 15), (9, 7, 3)),
+    ((96, 72, 20), (16, 8, 10)),      # TMA path: edge tiles on every side, ragged y tail
+    ((66, 50, 20), (11, 10, 10)),     # TMA path: ragged x and y tails
     ((128, 128, 128), (16, 16, 16)),
 ]
 
