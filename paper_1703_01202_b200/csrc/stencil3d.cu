@@ -9,13 +9,17 @@
 //   jv:    B = ((1-gamma)/2 + c) v + ih2 Lt v + ih2^2/2 Lt Lt v,   Jv = v/dt - ih2 Lt B
 //
 // 2.5D z-march.  A CTA owns a 32 x 32 column of outputs and a chunk of z-planes; input planes
-// z0-3 .. z0+zc+2 stream through a RING-slot ring per field (one 42 x 40 TMA box per field and
-// plane, cp.async.bulk.tensor.3d, PF planes in flight).  Warp specialisation:
-//  * the producer warp issues every TMA load and makes the periodic wrap: TMA zero-fills
-//    out-of-range cells and has no wrap mode, so edge tiles also load small x-strip, y-strip and
-//    corner boxes at the wrapped coordinates into a staging area and the producer copies those
-//    cells into the window (ragged grids: wrapped global re-reads; no-TMA grids: every cell);
-//    full / fixd / empty mbarriers per slot order TMA -> wrap -> compute -> re-fill;
+// z0-3 .. z0+zc+2 stream through a RING-slot ring per field.  The input window of a plane is
+// loaded by TMA (cp.async.bulk.tensor.3d) as two 42 x 20 boxes (rows 0..19 | 20..39).
+// Periodic wrap without any fix-up: when n_x, n_y are multiples of 32 the tile origins are
+// shifted to x0 = 32k - 18, y0 = 32j - 16, so the periodic seam y = 0 falls on the boxes' row
+// boundary (row 20), and in the one tile column that straddles x = 0 the window is loaded as
+// four 22 x 20 boxes split at col 22, where the seam x = 0 falls: every box is one in-range
+// rectangle at wrapped coordinates (TMA has no wrap mode).  Other grids (ragged or too small
+// for TMA) use unshifted tiles, and the producer warp re-reads the out-of-range cells (or all
+// cells) with wrapped indices.  Warp specialisation:
+//  * the producer warp issues every TMA load (full / empty mbarriers per slot) and, on such
+//    grids, makes the periodic fix-up (fixd mbarrier);
 //  * compute thread i < 324 owns the 2 x 2 point block (pair column p, row strip s), p, s in
 //    1..18, of the window, i.e. the halo-2 region; at streamed plane t it computes
 //        Lt s|v (t-1)  ->  A|B (t-2)  ->  F|Jv (t-3)
@@ -23,38 +27,46 @@
 //    queue has period 3, so the 3x-unrolled loop rotates it by register renaming) and only the
 //    block's 8 outside neighbours read from shared memory.  The intermediate planes Lt and A|B
 //    are kept in an even/odd-column split layout with a row pitch of 25 doubles, which makes
-//    every shared access of a warp conflict-free; the input window uses a row pitch of 42 for the
-//    same reason.  Each stage reads planes written in the previous iteration: a split-phase
-//    mbarrier (arrive after the plane stores, wait before the neighbour loads) separates
-//    iterations, and the neighbour-free parts of the three Laplacians are computed before the
-//    wait.  Optional fused ||F||^2 partial per CTA.
+//    every shared access of a warp conflict-free.  Each stage reads planes written in the
+//    previous iteration: a split-phase mbarrier (arrive after the plane stores, wait before the
+//    neighbour loads) separates iterations, and the neighbour-free parts of the three Laplacians
+//    are computed before the wait.  Optional fused ||F||^2 partial per CTA.
 #include "pfc_device.cuh"
 #include "pfc_internal.h"
 
 namespace {
 
 constexpr int TX = 32, TY = 32;
-constexpr int WX = 42, WY = 40;     // window: cols x0-4 .. x0+37, rows y0-4 .. y0+35
-constexpr int WS = WX * WY;         // doubles per ring slot (13440 B, a multiple of 128)
+constexpr int WY = 40;              // window rows y0-4 .. y0+35
+constexpr int BH = 20;              // TMA box rows (upper / lower half of the window)
+// natural layout (every tile except the x-seam column): two 42 x 20 boxes, row pitch 42
+constexpr int NW = 42, NYB = 848;   // box width; offset of the lower box (128-B aligned)
+// split layout (x-seam tiles): four 22 x 20 boxes, cols 0..21 | 22..43, row pitch 22
+constexpr int BW = 22, BOXN = 448;  // box width; doubles per box incl. padding (22 x 20 = 440)
+constexpr int XB = BOXN, YB = 2 * BOXN;    // offsets of the right-hand and lower boxes
+constexpr int WS = 4 * BOXN;        // doubles per ring slot (14336 B), either layout
 constexpr int NPB = 18;             // stage region: pair columns 1..18 x strips 1..18
 constexpr int NBLK = NPB * NPB;     // 324 blocks
-constexpr int NTC = 352;            // 11 compute warps (324 blocks)
+constexpr int NTC = 352;            // 11 compute warps
 constexpr int NWC = NTC / 32;
-constexpr int NT = NTC + 32;        // + 1 producer warp (TMA issue, periodic wrap)
-#ifndef ST3_RING                    // diagnostic builds may override the ring depth
-#define ST3_RING 5
-#define ST3_PF 3
-#endif
-constexpr int RING = ST3_RING, PF = ST3_PF;   // PF <= RING - 2: re-fill after the last reader
+constexpr int NT = NTC + 32;        // + 1 producer warp (TMA issue, periodic fix-up)
+constexpr int RING = 5, PF = 3;     // PF <= RING - 2
 constexpr int SP = 25;              // split-plane row pitch (doubles)
 constexpr int SROWS = WY;
 constexpr int SO = SROWS * SP;      // offset of the odd-column half
 constexpr int SPLANE = 2 * SO;      // doubles per split plane
-// wrap staging (mode 2): per field and slot an x-strip box 4 x 40, a y-strip box 42 x 4 (padded
-// to 176 for 128-B aligned TMA destinations) and a corner box 4 x 4
-constexpr int XS_N = 4 * WY, YS_N = WX * 4, YS_PAD = 176, CS_N = 16;
-constexpr int STG = XS_N + YS_PAD + CS_N;   // 352 doubles per field and slot
-constexpr int SMEM_BYTES = (2 * RING * WS + 4 * SPLANE + 2 * RING * STG) * (int)sizeof(double);
+constexpr int SMEM_BYTES = (2 * RING * WS + 4 * SPLANE) * (int)sizeof(double);   // 207360
+
+// slot offset of window cell (row r, col c)
+__host__ __device__ constexpr int woff_nat(int r, int c) {
+  return (r < BH ? r * NW : NYB + (r - BH) * NW) + c;
+}
+__host__ __device__ constexpr int woff_split(int r, int c) {
+  return (r < BH ? r * BW : YB + (r - BH) * BW) + (c < BW ? c : XB + (c - BW));
+}
+__device__ __forceinline__ int woff(bool split, int r, int c) {
+  return split ? woff_split(r, c) : woff_nat(r, c);
+}
 
 enum { OP_RESID = 0, OP_JV = 1 };
 
@@ -66,7 +78,7 @@ struct S3Args {
   int nx, ny, nz;
   int zc;            // planes per chunk
   double idt, k0, k1, k2, kout;   // (1-gamma)/2, ih2, ih2^2/2, -ih2
-  int mode;          // 0: plain loads; 1: TMA + wrapped global re-reads; 2: TMA + staged wrap
+  int mode;          // 0: plain loads; 1: TMA + wrapped re-reads; 2: seam-aligned TMA tiles
   const int* gate;   // device-resident FGMRES: skip the launch when *gate != 0 (f1)
 };
 
@@ -79,18 +91,21 @@ __device__ __forceinline__ void stg2(double* p, double x, double y) {
   *reinterpret_cast<double2*>(p) = make_double2(x, y);
 }
 
-// sums of the outside xy neighbours of the block, natural (ring) layout, qa = row-0 offset
-__device__ __forceinline__ q4 out_ring(const double* f, int qa) {
-  const double L0 = f[qa - 1], R0 = f[qa + 2], L1 = f[qa + WX - 1], R1 = f[qa + WX + 2];
-  const double2 T = lds2(f + qa - WX), D = lds2(f + qa + 2 * WX);
+// window-relative offsets of one block's accesses; row 1 of a pair / scalar: + pitch
+struct boff { int own, l, r, t, d, pitch; };
+
+// sums of the outside xy neighbours of the block from a ring slot
+__device__ __forceinline__ q4 out_ring(const double* f, const boff& o) {
+  const double L0 = f[o.l], R0 = f[o.r], L1 = f[o.l + o.pitch], R1 = f[o.r + o.pitch];
+  const double2 T = lds2(f + o.t), D = lds2(f + o.d);
   return {L0 + T.x, R0 + T.y, L1 + D.x, R1 + D.y};
 }
 // same for Phi + psi from both rings (resid stage 1)
-__device__ __forceinline__ q4 out_ring2(const double* f, const double* g, int qa) {
-  const double L0 = f[qa - 1] + g[qa - 1], R0 = f[qa + 2] + g[qa + 2];
-  const double L1 = f[qa + WX - 1] + g[qa + WX - 1], R1 = f[qa + WX + 2] + g[qa + WX + 2];
-  const double2 T = lds2(f + qa - WX), D = lds2(f + qa + 2 * WX);
-  const double2 Tg = lds2(g + qa - WX), Dg = lds2(g + qa + 2 * WX);
+__device__ __forceinline__ q4 out_ring2(const double* f, const double* g, const boff& o) {
+  const double L0 = f[o.l] + g[o.l], R0 = f[o.r] + g[o.r];
+  const double L1 = f[o.l + o.pitch] + g[o.l + o.pitch], R1 = f[o.r + o.pitch] + g[o.r + o.pitch];
+  const double2 T = lds2(f + o.t), D = lds2(f + o.d);
+  const double2 Tg = lds2(g + o.t), Dg = lds2(g + o.d);
   return {L0 + (T.x + Tg.x), R0 + (T.y + Tg.y), L1 + (D.x + Dg.x), R1 + (D.y + Dg.y)};
 }
 // split layout: E(r,k) = P[r*SP + k] (window col 2k), O(r,k) = P[SO + r*SP + k] (col 2k+1)
@@ -129,8 +144,8 @@ __device__ __forceinline__ q4 add4(const q4& x, const q4& y) {
   return {x.a + y.a, x.b + y.b, x.c + y.c, x.d + y.d};
 }
 
-struct S3Maps {   // main window box, x-strip, y-strip and corner boxes, per field
-  CUtensorMap a, b, xa, xb, ya, yb, ca, cb;
+struct S3Maps {   // 42 x 20 (natural) and 22 x 20 (split) boxes of both fields
+  CUtensorMap a, b, a22, b22;
 };
 
 template <int OP>
@@ -141,9 +156,8 @@ __global__ void __launch_bounds__(NT, 1) stencil3d_kernel(const __grid_constant_
   double* ringB = ringA + RING * WS;        // RING slots: psi | c
   double* Lsp = ringB + RING * WS;          // 2 split planes: Lt s | Lt v
   double* Bsp = Lsp + 2 * SPLANE;           // 2 split planes: A | B
-  double* stg = Bsp + 2 * SPLANE;           // RING x (field a, field b) wrap staging
   __shared__ uint64_t full[RING];   // the slot's TMA boxes landed (transaction bytes)
-  __shared__ uint64_t fixd[RING];   // the producer finished the periodic wrap of the slot
+  __shared__ uint64_t fixd[RING];   // the producer finished the periodic fix-up of the slot
   __shared__ uint64_t empty[RING];  // every compute warp finished reading the slot
   __shared__ uint64_t itbar;        // compute warps: split-phase iteration barrier
   __shared__ double red[64];
@@ -152,20 +166,20 @@ __global__ void __launch_bounds__(NT, 1) stencil3d_kernel(const __grid_constant_
   const int tid = threadIdx.x, lane = tid & 31;
   const int nx = p.nx, ny = p.ny, nz = p.nz;
   const int ntx = (nx + TX - 1) / TX;
-  const int x0 = (blockIdx.x % ntx) * TX, y0 = (blockIdx.x / ntx) * TY;
+  const bool tma = p.mode != 0, seam = p.mode == 2;
+  // seam-aligned tiles (mode 2): the periodic seam lies on the boxes' shared edge; only the
+  // tile column that straddles x = 0 needs the split (four-box) layout
+  const bool split = seam && blockIdx.x % ntx == 0;
+  const int x0 = (blockIdx.x % ntx) * TX - (seam ? 18 : 0);
+  const int y0 = (blockIdx.x / ntx) * TY - (seam ? 16 : 0);
   const int z0 = blockIdx.y * p.zc;
   const int zc = min(p.zc, nz - z0);
   const int gx0 = x0 - 4, gy0 = y0 - 4;     // global coordinates of window cell (0,0)
   const size_t plane = (size_t)nx * ny;
   const int T = zc + 6;
   const int Tp = (T + 2) / 3 * 3;           // padded to the unroll factor; extra planes are inert
-  const bool tma = p.mode != 0, staged = p.mode == 2;
-  // does a window cell the stencil reads (rows and cols 1..38) lie outside the grid?
-#ifdef ST3_NOEDGE   // diagnostic timing build: no periodic wrap at all (wrong edge values)
-  const bool edge = false;
-#else
-  const bool edge = !tma || x0 < 3 || y0 < 3 || x0 + 34 >= nx || y0 + 34 >= ny;
-#endif
+  // does a window cell the stencil reads (rows and cols 1..38) need a fix-up?
+  const bool edge = !tma || (!seam && (x0 < 3 || y0 < 3 || x0 + 34 >= nx || y0 + 34 >= ny));
 
   if (tid == 0) {
     for (int i = 0; i < RING; ++i) {
@@ -180,13 +194,9 @@ __global__ void __launch_bounds__(NT, 1) stencil3d_kernel(const __grid_constant_
   double nrm = 0.0;
 
   if (tid >= NTC) {
-    // ================= producer warp: TMA issue and periodic wrap of every plane =================
-    const bool xl = x0 == 0, xr = x0 + TX >= nx, yt = y0 == 0, yb = y0 + TY >= ny;
-    const bool xe = edge && staged && (xl || xr), ye = edge && staged && (yt || yb);
-    const int xs = xl ? nx - 4 : 0, cb0 = xl ? 0 : 36;   // strip origins: global x, window col
-    const int ys = yt ? ny - 4 : 0, rb0 = yt ? 0 : 36;
-    const uint32_t tx_bytes = 2u * sizeof(double) *
-        (WS + (xe ? XS_N : 0) + (ye ? YS_N : 0) + (xe && ye ? CS_N : 0));
+    // ================= producer warp: TMA issue (and periodic fix-up) of every plane =========
+    const int xa = seam ? wrapi(gx0, nx) : gx0, xb = seam ? wrapi(x0 + 18, nx) : x0 + 18;
+    const int ya = seam ? wrapi(gy0, ny) : gy0, yb = seam ? wrapi(y0 + 16, ny) : y0 + 16;
     auto zof = [&](int q) { return wrapi(z0 - 3 + q, nz); };
     auto wait_empty = [&](int q) {   // plane q - RING released by every compute warp
       if (q >= RING) mbar_wait(&empty[q % RING], (uint32_t)((q / RING - 1) & 1));
@@ -195,85 +205,49 @@ __global__ void __launch_bounds__(NT, 1) stencil3d_kernel(const __grid_constant_
       const int sl = q % RING, zi = zof(q);
       wait_empty(q);
       if (lane == 0) {
-        mbar_expect_tx(&full[sl], tx_bytes);
-        tma_load_3d(ringA + sl * WS, &m.a, &full[sl], gx0, gy0, zi);
-        tma_load_3d(ringB + sl * WS, &m.b, &full[sl], gx0, gy0, zi);
-        double* sa = stg + sl * 2 * STG;
-        double* sb = sa + STG;
-        if (xe) {
-          tma_load_3d(sa, &m.xa, &full[sl], xs, gy0, zi);
-          tma_load_3d(sb, &m.xb, &full[sl], xs, gy0, zi);
-        }
-        if (ye) {
-          tma_load_3d(sa + XS_N, &m.ya, &full[sl], gx0, ys, zi);
-          tma_load_3d(sb + XS_N, &m.yb, &full[sl], gx0, ys, zi);
-        }
-        if (xe && ye) {
-          tma_load_3d(sa + XS_N + YS_PAD, &m.ca, &full[sl], xs, ys, zi);
-          tma_load_3d(sb + XS_N + YS_PAD, &m.cb, &full[sl], xs, ys, zi);
+        double* da = ringA + sl * WS;
+        double* db = ringB + sl * WS;
+        if (split) {
+          mbar_expect_tx(&full[sl], 2u * 4u * BW * BH * (uint32_t)sizeof(double));
+          tma_load_3d(da, &m.a22, &full[sl], xa, ya, zi);
+          tma_load_3d(da + XB, &m.a22, &full[sl], xb, ya, zi);
+          tma_load_3d(da + YB, &m.a22, &full[sl], xa, yb, zi);
+          tma_load_3d(da + YB + XB, &m.a22, &full[sl], xb, yb, zi);
+          tma_load_3d(db, &m.b22, &full[sl], xa, ya, zi);
+          tma_load_3d(db + XB, &m.b22, &full[sl], xb, ya, zi);
+          tma_load_3d(db + YB, &m.b22, &full[sl], xa, yb, zi);
+          tma_load_3d(db + YB + XB, &m.b22, &full[sl], xb, yb, zi);
+        } else {
+          mbar_expect_tx(&full[sl], 2u * 2u * NW * BH * (uint32_t)sizeof(double));
+          tma_load_3d(da, &m.a, &full[sl], xa, ya, zi);
+          tma_load_3d(da + NYB, &m.a, &full[sl], xa, yb, zi);
+          tma_load_3d(db, &m.b, &full[sl], xa, ya, zi);
+          tma_load_3d(db + NYB, &m.b, &full[sl], xa, yb, zi);
         }
       }
     };
-    // periodic wrap of plane q: every cell of rows/cols 1..38 outside the grid.  Mode 2: copied
-    // from the slot's staging boxes, (window, staging) offsets precomputed per lane (<= 7 cells:
-    // at most 3 x 38 + 3 x 35 = 219 per tile); mode 1: re-read with wrapped indices; mode 0:
-    // every cell re-read (the last two only on ragged or small grids)
-    constexpr int MAXC = 7;
-    int cdst[MAXC], csrc[MAXC];
-    {
-      const int nxc = xe ? 3 : 0, nyr = ye ? 3 : 0, w = 38 - nxc;
-      const int cnt = nxc * 38 + nyr * w;
-#pragma unroll
-      for (int k = 0; k < MAXC; ++k) {
-        const int i = lane + 32 * k;
-        int r = 0, c = 0;
-        if (i < nxc * 38) { r = 1 + i / nxc; c = (xl ? 1 : 36) + i % nxc; }
-        else if (i < cnt) {
-          const int j = i - nxc * 38;
-          r = (yt ? 1 : 36) + j / w;
-          c = (xe && xl ? 4 : 1) + j % w;
-        }
-        const bool ix = xe && (xl ? c < 4 : c >= 36), iy = ye && (yt ? r < 4 : r >= 36);
-        cdst[k] = i < cnt ? r * WX + c : -1;
-        csrc[k] = (ix && iy) ? XS_N + YS_PAD + (r - rb0) * 4 + (c - cb0)
-                  : ix ? r * 4 + (c - cb0) : XS_N + (r - rb0) * WX + c;
-      }
-    }
-    auto fix_body = [&](int q) {
+    // periodic fix-up of plane q (ragged / small grids only): every cell of rows/cols 1..38
+    // outside the grid (no TMA: every cell) re-read with wrapped indices
+    auto fix = [&](int q) {
       const int sl = q % RING;
+      if (tma) mbar_wait(&full[sl], (uint32_t)((q / RING) & 1));
+      else wait_empty(q);
       double* ra = ringA + sl * WS;
       double* rb = ringB + sl * WS;
-      if (staged) {
-        const double* sa = stg + sl * 2 * STG;
-        const double* sb = sa + STG;
-        double va[MAXC], vb[MAXC];
-#pragma unroll
-        for (int k = 0; k < MAXC; ++k)
-          if (cdst[k] >= 0) { va[k] = sa[csrc[k]]; vb[k] = sb[csrc[k]]; }
-#pragma unroll
-        for (int k = 0; k < MAXC; ++k)
-          if (cdst[k] >= 0) { ra[cdst[k]] = va[k]; rb[cdst[k]] = vb[k]; }
-      } else {
-        const size_t zo = plane * (size_t)zof(q);
+      const size_t zo = plane * (size_t)zof(q);
 #pragma unroll 4
-        for (int i = lane; i < 38 * 38; i += 32) {
-          const int r = 1 + i / 38, c = 1 + i % 38;
-          const int x = gx0 + c, y = gy0 + r;
-          if (!tma || x < 0 || x >= nx || y < 0 || y >= ny) {
-            const size_t g = (size_t)wrapi(x, nx) + (size_t)nx * wrapi(y, ny) + zo;
-            ra[r * WX + c] = p.a[g];
-            rb[r * WX + c] = p.b[g];
-          }
+      for (int i = lane; i < 38 * 38; i += 32) {
+        const int r = 1 + i / 38, c = 1 + i % 38;
+        const int x = gx0 + c, y = gy0 + r;
+        if (!tma || x < 0 || x >= nx || y < 0 || y >= ny) {
+          const size_t g = (size_t)wrapi(x, nx) + (size_t)nx * wrapi(y, ny) + zo;
+          ra[woff_nat(r, c)] = p.a[g];
+          rb[woff_nat(r, c)] = p.b[g];
         }
       }
       if (tma) fence_proxy_async();   // generic writes before a later TMA overwrite
       __syncwarp();
       if (lane == 0) mbar_arrive(&fixd[sl]);
-    };
-    auto fix = [&](int q) {   // blocking
-      if (tma) mbar_wait(&full[q % RING], (uint32_t)((q / RING) & 1));
-      else wait_empty(q);
-      fix_body(q);
     };
     if (tma)
       for (int q = 0; q < PF && q < Tp; ++q) issue(q);
@@ -282,20 +256,10 @@ __global__ void __launch_bounds__(NT, 1) stencil3d_kernel(const __grid_constant_
     } else if (!tma) {
       for (int q = 0; q < Tp; ++q) fix(q);
     } else {
-      // issue and wrap decoupled: whichever is ready first (never block the TMA pipeline
-      // behind a plane that has not landed yet)
       fix(0);
-      int qi = PF, qf = 1;
-      while (qi < Tp || qf < Tp) {
-        if (qi < Tp && (qi < RING || mbar_test(&empty[qi % RING], (uint32_t)((qi / RING - 1) & 1)))) {
-          issue(qi);
-          ++qi;
-        } else if (qf < qi && qf < Tp && mbar_test(&full[qf % RING], (uint32_t)((qf / RING) & 1))) {
-          fix_body(qf);
-          ++qf;
-        } else {
-          __nanosleep(64);
-        }
+      for (int t = 0; t < Tp; ++t) {
+        if (t + PF < Tp) issue(t + PF);
+        if (t + 1 < Tp) fix(t + 1);
       }
     }
   } else {
@@ -304,18 +268,21 @@ __global__ void __launch_bounds__(NT, 1) stencil3d_kernel(const __grid_constant_
     const bool valid = tid < NBLK;
     const int bi = valid ? tid : 0;
     const int pc = 1 + bi % NPB, sr = 1 + bi / NPB;
-    const int qa = 2 * sr * WX + 2 * pc;      // ring offset of (row 2sr, col 2pc)
-    const int e0 = 2 * sr * SP + pc;          // split offset of the same point
-    const int xa = gx0 + 2 * pc, ya = gy0 + 2 * sr;   // global coords of point a
-    // outputs: pair columns / strips 2..17 inside the (possibly ragged) grid
+    const boff bo{woff(split, 2 * sr, 2 * pc), woff(split, 2 * sr, 2 * pc - 1),
+                  woff(split, 2 * sr, 2 * pc + 2), woff(split, 2 * sr - 1, 2 * pc),
+                  woff(split, 2 * sr + 2, 2 * pc), split ? BW : NW};
+    const int e0 = 2 * sr * SP + pc;          // split offset of the block's point a
+    const int xg = gx0 + 2 * pc, yg = gy0 + 2 * sr;   // global coords of point a (unwrapped)
+    // outputs: pair columns / strips 2..17 inside the (possibly ragged) grid; a pair never
+    // straddles the seam (x, y0 even)
     const bool outblk = valid && pc >= 2 && pc <= 17 && sr >= 2 && sr <= 17;
-    const bool o_a = outblk && xa < nx && ya < ny, o_b = outblk && xa + 1 < nx && ya < ny;
-    const bool o_c = outblk && xa < nx && ya + 1 < ny, o_d = outblk && xa + 1 < nx && ya + 1 < ny;
-    const size_t ga = (size_t)xa + (size_t)nx * ya;   // meaningful only for output points
-    const bool vec0 = o_a && o_b && (nx % 2 == 0) && ((reinterpret_cast<uintptr_t>(p.out + ga) & 15u) == 0);
-    const bool vec1 = o_c && o_d && (nx % 2 == 0) &&
-                      ((reinterpret_cast<uintptr_t>(p.out + ga + nx) & 15u) == 0);
-    uint64_t* wbar = edge ? fixd : full;      // plane ready: wrapped (edge tiles) or just landed
+    const bool o_a = outblk && xg < nx && yg < ny, o_b = outblk && xg + 1 < nx && yg < ny;
+    const bool o_c = outblk && xg < nx && yg + 1 < ny, o_d = outblk && xg + 1 < nx && yg + 1 < ny;
+    const size_t g0 = (size_t)wrapi(xg, nx) + (size_t)nx * wrapi(yg, ny);
+    const size_t g1 = (size_t)wrapi(xg, nx) + (size_t)nx * wrapi(yg + 1, ny);
+    const bool vec0 = o_a && o_b && (nx % 2 == 0) && ((reinterpret_cast<uintptr_t>(p.out + g0) & 15u) == 0);
+    const bool vec1 = o_c && o_d && (nx % 2 == 0) && ((reinterpret_cast<uintptr_t>(p.out + g1) & 15u) == 0);
+    uint64_t* wbar = edge ? fixd : full;      // plane ready: fixed up (edge tiles) or landed
 
     int slot = 0;
     uint32_t phase = 0;
@@ -323,7 +290,8 @@ __global__ void __launch_bounds__(NT, 1) stencil3d_kernel(const __grid_constant_
     // queues (period 3):  A1,A2 = Phi|v at t-1,t-2;  B1,B2 = psi|c at t-1,t-2;
     // L2,L3 = Lt at t-2,t-3;  M3,M4 = A|B at t-3,t-4;  P2,P3 = (Phi-psi)/dt | v/dt at t-2,t-3
     q4 A1 = Z, A2 = Z, B1 = Z, B2 = Z, L2 = Z, L3 = Z, M3 = Z, M4 = Z, P2 = Z, P3 = Z;
-    double* outp = p.out + plane * (size_t)z0 + ga;
+    double* out0 = p.out + plane * (size_t)z0 + g0;
+    const ptrdiff_t d1 = (ptrdiff_t)g1 - (ptrdiff_t)g0;
 
 #pragma unroll 3
     for (int t = 0; t < Tp; ++t) {
@@ -338,8 +306,8 @@ __global__ void __launch_bounds__(NT, 1) stencil3d_kernel(const __grid_constant_
 
       q4 A0, B0;   // own inputs of plane t
       {
-        const double2 a0 = lds2(ra + qa), a1 = lds2(ra + qa + WX);
-        const double2 b0 = lds2(rb + qa), b1 = lds2(rb + qa + WX);
+        const double2 a0 = lds2(ra + bo.own), a1 = lds2(ra + bo.own + bo.pitch);
+        const double2 b0 = lds2(rb + bo.own), b1 = lds2(rb + bo.own + bo.pitch);
         A0 = {a0.x, a0.y, a1.x, a1.y};
         B0 = {b0.x, b0.y, b1.x, b1.y};
       }
@@ -373,8 +341,8 @@ __global__ void __launch_bounds__(NT, 1) stencil3d_kernel(const __grid_constant_
       // ---- every compute warp has finished iteration t-1 (its reads and its plane stores)
       if (t > 0) mbar_wait(&itbar, (uint32_t)((t - 1) & 1));
       // outside neighbours of the planes produced in iteration t-1 (all loads before any store)
-      const q4 x1 = (OP == OP_RESID) ? out_ring2(ringA + prv * WS, ringB + prv * WS, qa)
-                                     : out_ring(ringA + prv * WS, qa);
+      const q4 x1 = (OP == OP_RESID) ? out_ring2(ringA + prv * WS, ringB + prv * WS, bo)
+                                     : out_ring(ringA + prv * WS, bo);
       const q4 x2 = out_split(Lr, e0);
       const q4 x3 = out_split(Mr, e0);
       // ---- stage 1: Lt s | Lt v at plane t-1
@@ -403,7 +371,7 @@ __global__ void __launch_bounds__(NT, 1) stencil3d_kernel(const __grid_constant_
       M4 = M3; M3 = Mnew;
       P3 = P2; P2 = Pnew;
       if (t >= 6 && t - 6 < zc) {
-        double* o = outp + plane * (size_t)(t - 6);
+        double* o = out0 + plane * (size_t)(t - 6);
         if (vec0) {
           stg2(o, oa, ob);
           nrm += oa * oa + ob * ob;
@@ -412,11 +380,11 @@ __global__ void __launch_bounds__(NT, 1) stencil3d_kernel(const __grid_constant_
           if (o_b) { o[1] = ob; nrm += ob * ob; }
         }
         if (vec1) {
-          stg2(o + nx, oc, od);
+          stg2(o + d1, oc, od);
           nrm += oc * oc + od * od;
         } else {
-          if (o_c) { o[nx] = oc; nrm += oc * oc; }
-          if (o_d) { o[nx + 1] = od; nrm += od * od; }
+          if (o_c) { o[d1] = oc; nrm += oc * oc; }
+          if (o_d) { o[d1 + 1] = od; nrm += od * od; }
         }
       }
       slot = slot + 1 == RING ? 0 : slot + 1;
@@ -467,17 +435,12 @@ cudaError_t launch3d(pfc_ctx* ctx, const double* a, const double* b, double dt, 
            0.5 * ih2 * ih2, -ih2, 0, OP == OP_JV ? ctx->gate : nullptr};
   S3Maps m;
   memset(&m, 0, sizeof(m));
-  const int* n = ctx->cfg.n;
-  const int box[3] = {WX, WY, 1}, xbox[3] = {4, WY, 1}, ybox[3] = {WX, 4, 1}, cbox[3] = {4, 4, 1};
-  if (nx % 2 == 0 && nx >= WX && ny >= WY && tma_usable(a) && tma_usable(b) &&
-      tma_encode(&m.a, a, 3, n, box) && tma_encode(&m.b, b, 3, n, box)) {
-    p.mode = 1;
-    if (nx % TX == 0 && ny % TY == 0 && nx >= 2 * TX && ny >= 2 * TY &&
-        tma_encode(&m.xa, a, 3, n, xbox) && tma_encode(&m.xb, b, 3, n, xbox) &&
-        tma_encode(&m.ya, a, 3, n, ybox) && tma_encode(&m.yb, b, 3, n, ybox) &&
-        tma_encode(&m.ca, a, 3, n, cbox) && tma_encode(&m.cb, b, 3, n, cbox))
-      p.mode = 2;
-  }
+  const int box[3] = {NW, BH, 1}, box22[3] = {BW, BH, 1};
+  // TMA: 16-B aligned rows and base; a box must fit the grid
+  if (nx % 2 == 0 && nx >= NW && ny >= BH && tma_usable(a) && tma_usable(b) &&
+      tma_encode(&m.a, a, 3, ctx->cfg.n, box) && tma_encode(&m.b, b, 3, ctx->cfg.n, box) &&
+      tma_encode(&m.a22, a, 3, ctx->cfg.n, box22) && tma_encode(&m.b22, b, 3, ctx->cfg.n, box22))
+    p.mode = (nx % TX == 0 && ny % TY == 0) ? 2 : 1;
   dim3 grid(ntiles, nzc);
   if (nparts) *nparts = grid.x * grid.y;
   stencil3d_kernel<OP><<<grid, NT, SMEM_BYTES, ctx->stream>>>(m, p);
