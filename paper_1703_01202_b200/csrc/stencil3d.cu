@@ -50,12 +50,15 @@ constexpr int NBLK = NPB * NPB;     // 324 blocks
 constexpr int NTC = 352;            // 11 compute warps
 constexpr int NWC = NTC / 32;
 constexpr int NT = NTC + 32;        // + 1 producer warp (TMA issue, periodic fix-up)
-constexpr int RING = 5, PF = 3;     // PF <= RING - 2
+// ring depth per operator (PF <= RING - 2): the residual also keeps s = Phi + psi in split planes
+template <int OP> struct Cfg { static constexpr int RING = 5, PF = 3, NSPL = 4; };
 constexpr int SP = 25;              // split-plane row pitch (doubles)
 constexpr int SROWS = WY;
 constexpr int SO = SROWS * SP;      // offset of the odd-column half
 constexpr int SPLANE = 2 * SO;      // doubles per split plane
-constexpr int SMEM_BYTES = (2 * RING * WS + 4 * SPLANE) * (int)sizeof(double);   // 207360
+template <int OP> constexpr int smem_bytes() {
+  return (2 * Cfg<OP>::RING * WS + Cfg<OP>::NSPL * SPLANE) * (int)sizeof(double);
+}
 
 // slot offset of window cell (row r, col c)
 __host__ __device__ constexpr int woff_nat(int r, int c) {
@@ -69,6 +72,7 @@ __device__ __forceinline__ int woff(bool split, int r, int c) {
 }
 
 enum { OP_RESID = 0, OP_JV = 1 };
+template <> struct Cfg<OP_RESID> { static constexpr int RING = 4, PF = 2, NSPL = 6; };
 
 struct S3Args {
   const double* a;   // Phi | v
@@ -99,14 +103,6 @@ __device__ __forceinline__ q4 out_ring(const double* f, const boff& o) {
   const double L0 = f[o.l], R0 = f[o.r], L1 = f[o.l + o.pitch], R1 = f[o.r + o.pitch];
   const double2 T = lds2(f + o.t), D = lds2(f + o.d);
   return {L0 + T.x, R0 + T.y, L1 + D.x, R1 + D.y};
-}
-// same for Phi + psi from both rings (resid stage 1)
-__device__ __forceinline__ q4 out_ring2(const double* f, const double* g, const boff& o) {
-  const double L0 = f[o.l] + g[o.l], R0 = f[o.r] + g[o.r];
-  const double L1 = f[o.l + o.pitch] + g[o.l + o.pitch], R1 = f[o.r + o.pitch] + g[o.r + o.pitch];
-  const double2 T = lds2(f + o.t), D = lds2(f + o.d);
-  const double2 Tg = lds2(g + o.t), Dg = lds2(g + o.d);
-  return {L0 + (T.x + Tg.x), R0 + (T.y + Tg.y), L1 + (D.x + Dg.x), R1 + (D.y + Dg.y)};
 }
 // split layout: E(r,k) = P[r*SP + k] (window col 2k), O(r,k) = P[SO + r*SP + k] (col 2k+1)
 __device__ __forceinline__ q4 out_split(const double* P, int e0) {
@@ -151,11 +147,13 @@ struct S3Maps {   // 42 x 20 (natural) and 22 x 20 (split) boxes of both fields
 template <int OP>
 __global__ void __launch_bounds__(NT, 1) stencil3d_kernel(const __grid_constant__ S3Maps m,
                                                           const __grid_constant__ S3Args p) {
+  constexpr int RING = Cfg<OP>::RING, PF = Cfg<OP>::PF;
   extern __shared__ __align__(128) double smem_dyn[];
   double* ringA = smem_dyn;                 // RING slots: Phi | v
   double* ringB = ringA + RING * WS;        // RING slots: psi | c
   double* Lsp = ringB + RING * WS;          // 2 split planes: Lt s | Lt v
   double* Bsp = Lsp + 2 * SPLANE;           // 2 split planes: A | B
+  double* Ssp = Bsp + 2 * SPLANE;           // resid: 2 split planes of s = Phi + psi
   __shared__ uint64_t full[RING];   // the slot's TMA boxes landed (transaction bytes)
   __shared__ uint64_t fixd[RING];   // the producer finished the periodic fix-up of the slot
   __shared__ uint64_t empty[RING];  // every compute warp finished reading the slot
@@ -272,6 +270,16 @@ __global__ void __launch_bounds__(NT, 1) stencil3d_kernel(const __grid_constant_
                   woff(split, 2 * sr, 2 * pc + 2), woff(split, 2 * sr - 1, 2 * pc),
                   woff(split, 2 * sr + 2, 2 * pc), split ? BW : NW};
     const int e0 = 2 * sr * SP + pc;          // split offset of the block's point a
+    // resid: s = Phi + psi of one outer-ring cell of the window (rows / cols 1 and 38, which no
+    // block owns) per thread tid < 148, written with the block values into the s plane
+    int rc_q = 0, rc_e = -1;
+    if (OP == OP_RESID && tid < 2 * 38 + 2 * 36) {
+      int rr, cc;
+      if (tid < 76) { rr = tid < 38 ? 1 : 38; cc = 1 + tid % 38; }
+      else { const int k = tid - 76; cc = k < 36 ? 1 : 38; rr = 2 + k % 36; }
+      rc_q = woff(split, rr, cc);
+      rc_e = ((cc & 1) ? SO : 0) + rr * SP + (cc >> 1);
+    }
     const int xg = gx0 + 2 * pc, yg = gy0 + 2 * sr;   // global coords of point a (unwrapped)
     // outputs: pair columns / strips 2..17 inside the (possibly ragged) grid; a pair never
     // straddles the seam (x, y0 even)
@@ -321,6 +329,8 @@ __global__ void __launch_bounds__(NT, 1) stencil3d_kernel(const __grid_constant_
       // the centre and z parts of the three Laplacians and the pointwise part of A|B
       const q4 c1 = (OP == OP_RESID) ? lap_own(add4(A1, B1), add4(A2, B2), add4(A0, B0))
                                      : lap_own(A1, A2, A0);
+      double srng = 0.0;   // resid: s at this thread's outer-ring cell of plane t
+      if (OP == OP_RESID && rc_e >= 0) srng = ra[rc_q] + rb[rc_q];
       const q4 c2 = lap_own(L2, L3), c3 = lap_own(M3, M4);
       q4 r2;       // pointwise part of A|B at t-2 plus ih2 Lt at t-2
       {
@@ -341,7 +351,7 @@ __global__ void __launch_bounds__(NT, 1) stencil3d_kernel(const __grid_constant_
       // ---- every compute warp has finished iteration t-1 (its reads and its plane stores)
       if (t > 0) mbar_wait(&itbar, (uint32_t)((t - 1) & 1));
       // outside neighbours of the planes produced in iteration t-1 (all loads before any store)
-      const q4 x1 = (OP == OP_RESID) ? out_ring2(ringA + prv * WS, ringB + prv * WS, bo)
+      const q4 x1 = (OP == OP_RESID) ? out_split(Ssp + ((t - 1) & 1) * SPLANE, e0)
                                      : out_ring(ringA + prv * WS, bo);
       const q4 x2 = out_split(Lr, e0);
       const q4 x3 = out_split(Mr, e0);
@@ -359,7 +369,9 @@ __global__ void __launch_bounds__(NT, 1) stencil3d_kernel(const __grid_constant_
       if (valid) {
         st_split(Lw, e0, Lnew);
         st_split(Mw, e0, Mnew);
+        if (OP == OP_RESID) st_split(Ssp + (t & 1) * SPLANE, e0, add4(A0, B0));
       }
+      if (OP == OP_RESID && rc_e >= 0) Ssp[(t & 1) * SPLANE + rc_e] = srng;
       __syncwarp();
       if (lane == 0) {
         mbar_arrive(&itbar);
@@ -418,7 +430,8 @@ cudaError_t launch3d(pfc_ctx* ctx, const double* a, const double* b, double dt, 
   static int nsm = 148;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(stencil3d_kernel<OP>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         smem_bytes<OP>());
     if (e != cudaSuccess) return e;
     int dev = 0, v = 0;
     if (cudaGetDevice(&dev) == cudaSuccess &&
@@ -443,7 +456,7 @@ cudaError_t launch3d(pfc_ctx* ctx, const double* a, const double* b, double dt, 
     p.mode = (nx % TX == 0 && ny % TY == 0) ? 2 : 1;
   dim3 grid(ntiles, nzc);
   if (nparts) *nparts = grid.x * grid.y;
-  stencil3d_kernel<OP><<<grid, NT, SMEM_BYTES, ctx->stream>>>(m, p);
+  stencil3d_kernel<OP><<<grid, NT, smem_bytes<OP>(), ctx->stream>>>(m, p);
   ctx->launches++;
   pfc_account(ctx, OP == OP_RESID ? PFC_K_RESIDUAL : PFC_K_JV, 24.0 * ctx->N,
               (OP == OP_RESID ? 42.0 : 31.0) * ctx->N);
