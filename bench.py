@@ -39,6 +39,19 @@ def dist_env():
     return ws, rank, local
 
 
+def ncu_traffic(pattern):
+    """DRAM bytes per launch of a kernel from the committed ncu --set full summary
+    (profiles/ncu_traffic.json, written by tools/ncu_traffic.py from the captures of
+    tools/gpu_evidence.sh: ras2d on the config-2 shape, stencil3d at 512^3)."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if not os.path.exists(p):
+        return None
+    for k in json.load(open(p)):
+        if pattern in k["kernel"]:
+            return k["traffic_bytes"]
+    return None
+
+
 def load_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -206,9 +219,12 @@ def bench_cuda(args):
                 clk_mhz = clocks.get("sm_mhz") or 1965.0
                 peak, kind = 148 * 64 * 2 * clk_mhz * 1e6 / 1e12, "derived: 148 SM x 64 DFMA/clk x 2 x clock"
             ach = v["flops"] / (v["ms"] * 1e-3) / 1e12
+            tr = ncu_traffic("ras2d_col_kernel" if cfg.ndim == 2 else "ras3d_col_kernel")
             return {"kernel": "ras_apply", "bound": "alu", "achieved": round(ach, 3),
                     "peak": round(peak, 2), "unit": "TFLOP/s", "frac": round(ach / peak, 4),
-                    "peak_kind": kind, "traffic": None}
+                    "peak_kind": kind, "traffic": tr,
+                    "traffic_note": "dram read+write bytes per launch, ncu --set full "
+                                    "(profiles/ncu_traffic.json)"}
         ach = v["bytes"] / (v["ms"] * 1e-3) / 1e9
         return {"kernel": name, "bound": "hbm", "achieved": round(ach, 1), "peak": hbm_peak,
                 "unit": "GB/s", "frac": round(ach / hbm_peak, 4), "peak_kind": peak_kind,
@@ -245,6 +261,7 @@ def bench_cuda(args):
               "ms_per_apply": round(pr["jv"]["ms"] / reps, 4),
               "residual_GBps": round(rs_gbs, 1), "residual_frac": round(rs_gbs / hbm_peak, 4),
               "algo_bytes_per_apply": 24 * n ** 3, "peak": hbm_peak, "peak_kind": peak_kind,
+              "traffic": ncu_traffic("stencil3d_kernel<1>") if n == 512 else None,
               "l2": "fields 1 GiB each >> 126 MB L2"}
         del cj, a, v, out
 

@@ -1,6 +1,6 @@
 """Launch each hot kernel a few times on its benchmark shape (for ncu / timing probes).
 
-usage: python tools/kernel_probe.py [ras2d|jv3d|res3d|jv2d|res2d|ras3d|all] [reps]
+usage: python tools/kernel_probe.py [ras2d|jv3d|res3d|st3d|jv2d|res2d|ras3d|all] [reps]
 """
 import os
 import sys
@@ -41,7 +41,7 @@ def run(which, reps):
                 ctx.residual(a, v, 0.5, z)
         out["2d"] = ctx.profile_report()
         del ctx
-    if which in ("jv3d", "res3d", "all"):
+    if which in ("jv3d", "res3d", "st3d", "all"):
         n = 512
         ctx = P.Context(None, ndim=3, n=(n, n, n), h=h, gamma=0.25, ras_box=(16, 16, 16),
                         ras_overlap=2, gmres_restart=1)
@@ -50,9 +50,9 @@ def run(which, reps):
         z = torch.empty_like(v)
         ctx.profile(True)
         for _ in range(reps):
-            if which in ("jv3d", "all"):
+            if which in ("jv3d", "st3d", "all"):
                 ctx.jacobian_apply(a, a, 1.0, v, z)
-            if which in ("res3d", "all"):
+            if which in ("res3d", "st3d", "all"):
                 ctx.residual(a, v, 1.0, z)
         out["3d"] = ctx.profile_report()
         del ctx
