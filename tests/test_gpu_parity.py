@@ -87,6 +87,24 @@ def test_residual_jacobian_energy_parity(shape, box):
     assert abs(M - Mo) <= 1e-12 * np.sum(np.abs(phi)) * H ** len(shape)
 
 
+@pytest.mark.parametrize("kernel", ["strip", "tile"])
+@pytest.mark.parametrize("shape,box", [((64, 64), (16, 16)), ((100, 36), (10, 12)),
+                                       ((45, 27), (15, 9)), ((12, 12), (4, 4)),
+                                       ((130, 70), (13, 14))])
+def test_2d_stencil_kernels_both_paths(shape, box, kernel, monkeypatch):
+    """Both 2D kernels (strip march: large grids; tile: small grids) on ragged, odd and tiny
+    shapes, forced through PFC_ST2_KERNEL."""
+    monkeypatch.setenv("PFC_ST2_KERNEL", kernel)
+    phi = random_field(shape, 111, 0.0, 1.0)
+    psi = random_field(shape, 112, 0.0, 1.0)
+    v = random_field(shape, 113, 0.0, 1.0)
+    ctx = ctx_for(shape, box, o=1)
+    F = host(ctx.residual(dev(phi), dev(psi), 0.5))
+    assert rel(F, O.residual(phi, psi, H, G, 0.5)) <= 1e-12
+    Jv = host(ctx.jacobian_apply(dev(phi), dev(psi), 0.5, dev(v)))
+    assert rel(Jv, O.jacobian_apply(phi, psi, v, H, G, 0.5)) <= 1e-12
+
+
 @pytest.mark.parametrize("name", ["cfg1", "cfg2", "cfg3", "cfg4"])
 def test_operator_parity_on_config_ics(name):
     """Each config's own initial condition as Phi with psi = IC + perturbation (R20: inputs

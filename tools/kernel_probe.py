@@ -1,6 +1,6 @@
 """Launch each hot kernel a few times on its benchmark shape (for ncu / timing probes).
 
-usage: python tools/kernel_probe.py [ras2d|jv3d|res3d|st3d|jv2d|res2d|ras3d|all] [reps]
+usage: python tools/kernel_probe.py [ras2d|jv3d|res3d|st3d|st2dbig|st2dsz|jv2d|res2d|ras3d|all] [reps]
 """
 import os
 import sys
@@ -40,6 +40,34 @@ def run(which, reps):
             if which in ("res2d", "all"):
                 ctx.residual(a, v, 0.5, z)
         out["2d"] = ctx.profile_report()
+        del ctx
+    if which == "st2dsz":       # 2D stencils over grid sizes (kernel choice crossover)
+        for n in (1024, 2048, 4096, 8192):
+            ctx = P.Context(None, ndim=2, n=(n, n), h=h, gamma=0.25, ras_box=(32, 32),
+                            ras_overlap=2, gmres_restart=1)
+            a = field((n, n), 7, 0.07, 0.07)
+            v = field((n, n), 8)
+            z = torch.empty_like(v)
+            for _ in range(2):
+                ctx.jacobian_apply(a, a, 0.5, v, z)
+            ctx.profile(True)
+            for _ in range(max(reps, 1)):
+                ctx.jacobian_apply(a, a, 0.5, v, z)
+                ctx.residual(a, v, 0.5, z)
+            out[f"2d{n}"] = ctx.profile_report()
+            del ctx, a, v, z
+    if which in ("st2dbig",):   # 2D stencils on an HBM-sized grid (inputs >> L2)
+        n = 8192
+        ctx = P.Context(None, ndim=2, n=(n, n), h=h, gamma=0.25, ras_box=(32, 32), ras_overlap=2,
+                        gmres_restart=1)
+        a = field((n, n), 7, 0.07, 0.07)
+        v = field((n, n), 8)
+        z = torch.empty_like(v)
+        ctx.profile(True)
+        for _ in range(reps):
+            ctx.jacobian_apply(a, a, 0.5, v, z)
+            ctx.residual(a, v, 0.5, z)
+        out["2dbig"] = ctx.profile_report()
         del ctx
     if which in ("jv3d", "res3d", "st3d", "all"):
         n = 512
