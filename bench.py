@@ -233,18 +233,20 @@ def bench_cuda(args):
     roofline = roofline_for(dom, prof[dom])
     roofline["share_of_step"] = round(prof[dom]["ms"] / total_ms, 4)
 
-    # ---- isolated Jacobian apply at the config-5 size (inputs >> L2)
-    jv = None
-    if args.jv_size > 0:
-        n = args.jv_size
-        del ctx
-        torch.cuda.empty_cache()
-        cj = P.Context(None, ndim=3, n=(n, n, n), h=cfg.h, gamma=cfg.gamma, ras_box=(16, 16, 16),
-                       ras_overlap=2, gmres_restart=1)
+    # ---- isolated Jacobian apply / residual on HBM-sized grids (inputs >> L2): the config-5
+    # size 512^3 and a 2D 8192^2 grid (the 2D configs are L2-resident)
+    del ctx
+    torch.cuda.empty_cache()
+
+    def stencil_sweep(shape, pattern):
+        nd = len(shape)
+        cj = P.Context(None, ndim=nd, n=shape, h=cfg.h, gamma=cfg.gamma,
+                       ras_box=(16,) * nd, ras_overlap=2, gmres_restart=1)
         g = torch.Generator(device="cuda").manual_seed(5)
-        a = (-0.35 + 0.05 * (2 * torch.rand((n, n, n), dtype=torch.float64, device="cuda",
-                                             generator=g) - 1))
-        v = torch.rand((n, n, n), dtype=torch.float64, device="cuda", generator=g)
+        tshape = tuple(reversed(shape))
+        a = -0.35 + 0.05 * (2 * torch.rand(tshape, dtype=torch.float64, device="cuda",
+                                           generator=g) - 1)
+        v = torch.rand(tshape, dtype=torch.float64, device="cuda", generator=g)
         out = torch.empty_like(v)
         for _ in range(3):
             cj.jacobian_apply(a, a, 1.0, v, out)
@@ -255,15 +257,26 @@ def bench_cuda(args):
             cj.residual(a, v, 1.0, out)
         pr = cj.profile_report()
         cj.profile(False)
+        npts = 1
+        for d in shape:
+            npts *= d
         jv_gbs = pr["jv"]["bytes"] / (pr["jv"]["ms"] * 1e-3) / 1e9
         rs_gbs = pr["residual"]["bytes"] / (pr["residual"]["ms"] * 1e-3) / 1e9
-        jv = {"grid": [n, n, n], "GBps": round(jv_gbs, 1), "frac": round(jv_gbs / hbm_peak, 4),
-              "ms_per_apply": round(pr["jv"]["ms"] / reps, 4),
-              "residual_GBps": round(rs_gbs, 1), "residual_frac": round(rs_gbs / hbm_peak, 4),
-              "algo_bytes_per_apply": 24 * n ** 3, "peak": hbm_peak, "peak_kind": peak_kind,
-              "traffic": ncu_traffic("stencil3d_kernel<1>") if n == 512 else None,
-              "l2": "fields 1 GiB each >> 126 MB L2"}
+        res = {"grid": list(shape), "GBps": round(jv_gbs, 1), "frac": round(jv_gbs / hbm_peak, 4),
+               "ms_per_apply": round(pr["jv"]["ms"] / reps, 4),
+               "residual_GBps": round(rs_gbs, 1), "residual_frac": round(rs_gbs / hbm_peak, 4),
+               "algo_bytes_per_apply": 24 * npts, "peak": hbm_peak, "peak_kind": peak_kind,
+               "traffic": ncu_traffic(pattern),
+               "l2": f"fields {8 * npts / 2**30:.2f} GiB each >> 126 MB L2"}
         del cj, a, v, out
+        torch.cuda.empty_cache()
+        return res
+
+    jv = jv2 = None
+    if args.jv_size > 0:
+        n = args.jv_size
+        jv = stencil_sweep((n, n, n), "stencil3d_kernel<1>" if n == 512 else "@none")
+        jv2 = stencil_sweep((8192, 8192), "stencil2d_kernel<1>")
 
     newton = sum(i["newton_its"] for i in infos)
     gmres = sum(i["gmres_its"] for i in infos)
@@ -284,6 +297,7 @@ def bench_cuda(args):
         "newton_its": newton, "gmres_its": gmres,
         "clocks": clocks, "e2e": e2e, "gpu_launches": launches,
         "roofline": roofline, "kernel_classes": classes, "jacobian_apply": jv,
+        "jacobian_apply_2d": jv2,
     }
     if ws == 1 and rank == 0 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(cfg, phi0, W, args.cpu_steps)
