@@ -34,9 +34,10 @@ class Params(C.Structure):
                 ("gmres_restart", C.c_int), ("gmres_maxit", C.c_int),
                 ("gmres_rtol", C.c_double), ("gmres_atol", C.c_double),
                 ("ras_box", C.c_int * 3), ("ras_overlap", C.c_int), ("ras_local_k", C.c_int),
-                ("ras_variant", C.c_int)]
+                ("ras_variant", C.c_int), ("mobility", C.c_int)]
 
 RAS_LEFT, RAS_AS, RAS_RIGHT = 0, 1, 2
+MOB_ONE, MOB_QUADRATIC = 0, 1           # M = 1; M(phi) = 1 - phi^2
 
 
 class NewtonInfo(C.Structure):
@@ -69,6 +70,10 @@ def lib():
         L.or_ras_apply_box.argtypes = [G, PR, C.c_double, _P, _P, _P, C.c_int, _P]
         L.or_fgmres.argtypes = [G, PR, C.c_double, _P, _P, _P, _P, C.c_int, C.POINTER(C.c_int)]
         L.or_newton.argtypes = [G, PR, C.c_double, _P, _P, _P, C.POINTER(NewtonInfo)]
+        L.or_div_mgrad.argtypes = [G, _P, _P, _P]
+        L.or_mobility.argtypes = [G, C.c_int, _P, _P, _P]
+        L.or_residual_p.argtypes = [G, PR, C.c_double, _P, _P, _P]
+        L.or_jacobian_apply_p.argtypes = [G, PR, C.c_double, _P, _P, _P, _P]
         L.or_next_dt.argtypes = [C.c_double] * 6
         L.or_next_dt.restype = C.c_double
     return _lib
@@ -95,11 +100,11 @@ def _shape(a):
 def params(gamma=0.25, newton_rtol=1e-10, newton_atol=1e-10, newton_maxit=50, ls_c1=1e-4,
            ls_min_lambda=1e-12, gmres_restart=30, gmres_maxit=300, gmres_rtol=1e-3,
            gmres_atol=1e-11, ras_box=(16, 16, 1), ras_overlap=2, ras_local_k=10, ras_variant=0,
-           **_ignored):
+           mobility=0, **_ignored):
     b = list(ras_box) + [1] * (3 - len(ras_box))
     return Params(gamma, newton_rtol, newton_atol, newton_maxit, ls_c1, ls_min_lambda,
                   gmres_restart, gmres_maxit, gmres_rtol, gmres_atol, (C.c_int * 3)(*b),
-                  ras_overlap, ras_local_k, ras_variant)
+                  ras_overlap, ras_local_k, ras_variant, mobility)
 
 
 def params_from_config(cfg, **over):
@@ -107,7 +112,7 @@ def params_from_config(cfg, **over):
               newton_maxit=cfg.newton_maxit, gmres_restart=cfg.gmres_restart,
               gmres_maxit=cfg.gmres_maxit, gmres_rtol=cfg.gmres_rtol, gmres_atol=cfg.gmres_atol,
               ras_box=cfg.ras_box, ras_overlap=cfg.ras_overlap, ras_local_k=cfg.ras_local_k,
-              ras_variant=getattr(cfg, "ras_variant", 0))
+              ras_variant=getattr(cfg, "ras_variant", 0), mobility=getattr(cfg, "mobility", 0))
     kw.update(over)
     return params(**kw)
 
@@ -134,6 +139,33 @@ def jacobian_apply(phi_new, phi_old, v, h, gamma, dt):
     a, b, v = _f(phi_new), _f(phi_old), _f(v); out = np.empty_like(a)
     lib().or_jacobian_apply(C.byref(_grid(_shape(a), h)), gamma, dt, _ptr(a), _ptr(b), _ptr(v),
                             _ptr(out))
+    return out
+
+
+def div_mgrad(M, f, h):
+    """(grad . M grad)_d f with edge-averaged M."""
+    m, f = _f(M), _f(f); out = np.empty_like(f)
+    lib().or_div_mgrad(C.byref(_grid(_shape(f), h)), _ptr(m), _ptr(f), _ptr(out))
+    return out
+
+
+def mobility_field(phi_new, phi_old, h, mobility):
+    a, b = _f(phi_new), _f(phi_old); out = np.empty_like(a)
+    lib().or_mobility(C.byref(_grid(_shape(a), h)), int(mobility), _ptr(a), _ptr(b), _ptr(out))
+    return out
+
+
+def residual_p(phi_new, phi_old, h, prm, dt):
+    """Residual of Eq. NSOP with prm.mobility."""
+    a, b = _f(phi_new), _f(phi_old); out = np.empty_like(a)
+    lib().or_residual_p(C.byref(_grid(_shape(a), h)), C.byref(prm), dt, _ptr(a), _ptr(b), _ptr(out))
+    return out
+
+
+def jacobian_apply_p(phi_new, phi_old, v, h, prm, dt):
+    a, b, v = _f(phi_new), _f(phi_old), _f(v); out = np.empty_like(a)
+    lib().or_jacobian_apply_p(C.byref(_grid(_shape(a), h)), C.byref(prm), dt, _ptr(a), _ptr(b),
+                              _ptr(v), _ptr(out))
     return out
 
 

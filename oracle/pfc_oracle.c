@@ -173,6 +173,88 @@ double or_mass(const or_grid* g, const double* f) {
   return sum_compensated(npts(g), f) * pow(g->h, g->nd);
 }
 
+/* ------------------------------------------ variable mobility P:208-212 */
+
+/* (grad . M grad)_d f = D_x M D_x f + D_y M D_y f (+ D_z M D_z f), with the value of
+ * M on the midpoint of an edge the average of its two end nodes:
+ *   (D_x M D_x f)_i = [M_{i+1/2} (f_{i+1} - f_i) - M_{i-1/2} (f_i - f_{i-1})] / dx^2,
+ *   M_{i+1/2} = (M_i + M_{i+1}) / 2.  Periodic. */
+void or_div_mgrad(const or_grid* g, const double* M, const double* f, double* out) {
+  const double ih2 = 1.0 / (g->h * g->h);
+  for (int k = 0; k < g->n[2]; ++k)
+    for (int j = 0; j < g->n[1]; ++j)
+      for (int i = 0; i < g->n[0]; ++i) {
+        size_t c = gidx(g, i, j, k);
+        size_t nb[3][2] = {{gidx(g, i + 1, j, k), gidx(g, i - 1, j, k)},
+                           {gidx(g, i, j + 1, k), gidx(g, i, j - 1, k)},
+                           {gidx(g, i, j, k + 1), gidx(g, i, j, k - 1)}};
+        double s = 0.0;
+        for (int d = 0; d < g->nd; ++d) {
+          double mp = (M[c] + M[nb[d][0]]) / 2.0, mm = (M[c] + M[nb[d][1]]) / 2.0;
+          s += (mp * (f[nb[d][0]] - f[c]) - mm * (f[c] - f[nb[d][1]])) * ih2;
+        }
+        out[c] = s;
+      }
+}
+
+/* M_d = M((phi_new + phi_old)/2), M(phi) = 1 - phi^2 or M = 1. */
+void or_mobility(const or_grid* g, int mobility, const double* pn, const double* po, double* M) {
+  size_t N = npts(g);
+  for (size_t q = 0; q < N; ++q) {
+    double u = (pn[q] + po[q]) / 2.0;
+    M[q] = mobility ? 1.0 - u * u : 1.0;
+  }
+}
+
+/* Residual of Eq. (NSOP) P:257-263 with the mobility of p:
+ *   F(Phi) = (Phi - psi)/dt - (grad . M_d grad)_d A(Phi, psi).
+ * With M = 1 it is or_residual (whose Delta_d is the M = 1 case of P:208-212, R3). */
+void or_residual_p(const or_grid* g, const or_params* p, double dt, const double* pn,
+                   const double* po, double* F) {
+  if (!p->mobility) { or_residual(g, p->gamma, dt, pn, po, F); return; }
+  size_t N = npts(g);
+  double* A = alloc0(N);
+  double* M = alloc0(N);
+  double* D = alloc0(N);
+  or_dvd_derivative(g, p->gamma, pn, po, A);
+  or_mobility(g, p->mobility, pn, po, M);
+  or_div_mgrad(g, M, A, D);
+  for (size_t q = 0; q < N; ++q) F[q] = (pn[q] - po[q]) / dt - D[q];
+  free(A); free(M); free(D);
+}
+
+/* J v = dF/dPhi v (Eq. Jacobi) with the mobility of p: the product rule on
+ * (grad . M_d grad) A with both factors depending on Phi,
+ *   J v = v/dt - (grad . M_d grad)(dA/dPhi v) - (grad . (dM_d/dPhi v) grad) A,
+ *   dA/dPhi v as in or_jacobian_apply, dM_d/dPhi v = M'(u) v / 2 = -u v for M = 1 - u^2. */
+void or_jacobian_apply_p(const or_grid* g, const or_params* p, double dt, const double* pn,
+                         const double* po, const double* v, double* Jv) {
+  if (!p->mobility) { or_jacobian_apply(g, p->gamma, dt, pn, po, v, Jv); return; }
+  size_t N = npts(g);
+  double* L1 = alloc0(N);
+  double* L2 = alloc0(N);
+  double* dA = alloc0(N);
+  double* A = alloc0(N);
+  double* M = alloc0(N);
+  double* Mv = alloc0(N);
+  double* T1 = alloc0(N);
+  double* T2 = alloc0(N);
+  or_laplacian(g, v, L1);
+  or_laplacian(g, L1, L2);
+  for (size_t q = 0; q < N; ++q) {
+    double a = pn[q], b = po[q];
+    double c = (3.0 * a * a + 2.0 * a * b + b * b) / 4.0;
+    dA[q] = 0.5 * ((1.0 - p->gamma) * v[q] + 2.0 * L1[q] + L2[q]) + c * v[q];
+    Mv[q] = -((a + b) / 2.0) * v[q];
+  }
+  or_dvd_derivative(g, p->gamma, pn, po, A);
+  or_mobility(g, p->mobility, pn, po, M);
+  or_div_mgrad(g, M, dA, T1);
+  or_div_mgrad(g, Mv, A, T2);
+  for (size_t q = 0; q < N; ++q) Jv[q] = v[q] / dt - T1[q] - T2[q];
+  free(L1); free(L2); free(dA); free(A); free(M); free(Mv); free(T1); free(T2);
+}
+
 /* ----------------------------------------------- Schwarz preconditioner P:381-437 */
 
 int or_num_boxes(const or_grid* g, const or_params* p) {
@@ -258,11 +340,42 @@ static void givens(double a, double b, double* c, double* s) {
   *c = a / r; *s = b / r;
 }
 
+/* The subdomain operator of one box.  M = 1: or_local_jacobian_apply (zero ring on the
+ * padded grid, R8).  Variable mobility: A_k = R_k^delta J (R_k^delta)^T, the "directly
+ * generated" subdomain matrix of Eq. (Ak) P:422-428 (reading R8b): v_loc extended by zero to
+ * the whole grid, the global J of or_jacobian_apply_p, restricted to the ext box. */
+typedef struct {
+  const or_grid* g; const or_params* p; double dt; const double* c_loc;
+  const double* pn; const double* po; int x0, y0, z0, E[3];
+} local_op;
+
+static void local_apply(const local_op* L, const double* v_loc, double* w_loc) {
+  if (!L->p->mobility) {
+    or_local_jacobian_apply(L->g, L->p, L->dt, L->c_loc, v_loc, w_loc);
+    return;
+  }
+  size_t N = npts(L->g);
+  double* vg = alloc0(N);
+  double* wg = alloc0(N);
+  for (int k = 0; k < L->E[2]; ++k)                  /* (R_k^delta)^T v_loc */
+    for (int j = 0; j < L->E[1]; ++j)
+      for (int i = 0; i < L->E[0]; ++i)
+        vg[gidx(L->g, L->x0 + i, L->y0 + j, L->z0 + k)] =
+            v_loc[(size_t)i + (size_t)L->E[0] * ((size_t)j + (size_t)L->E[1] * k)];
+  or_jacobian_apply_p(L->g, L->p, L->dt, L->pn, L->po, vg, wg);
+  for (int k = 0; k < L->E[2]; ++k)                  /* R_k^delta */
+    for (int j = 0; j < L->E[1]; ++j)
+      for (int i = 0; i < L->E[0]; ++i)
+        w_loc[(size_t)i + (size_t)L->E[0] * ((size_t)j + (size_t)L->E[1] * k)] =
+            wg[gidx(L->g, L->x0 + i, L->y0 + j, L->z0 + k)];
+  free(vg); free(wg);
+}
+
 /* Fixed-work local solve (reading R9): exactly k steps of GMRES on A_k y = r with zero
  * initial guess, classical Gram-Schmidt applied twice (CGS2), Givens least squares;
  * early exit only on exact breakdown H(j+1,j) <= 1e-14 beta. */
-static void local_gmres(const or_grid* g, const or_params* p, double dt, const double* c_loc,
-                        const double* r, double* y, size_t n) {
+static void local_gmres(const local_op* L, const double* r, double* y, size_t n) {
+  const or_params* p = L->p;
   int k = p->ras_local_k;
   memset(y, 0, n * sizeof(double));
   double beta = or_norm2(n, r);
@@ -278,7 +391,7 @@ static void local_gmres(const or_grid* g, const or_params* p, double dt, const d
   gv[0] = beta;
   int jm = 0;
   for (int j = 0; j < k; ++j) {
-    or_local_jacobian_apply(g, p, dt, c_loc, V + (size_t)j * n, w);
+    local_apply(L, V + (size_t)j * n, w);
     for (int pass = 0; pass < 2; ++pass) {         /* CGS2 */
       for (int i = 0; i <= j; ++i) {
         double s = 0.0;
@@ -357,7 +470,8 @@ void or_ras_apply(const or_grid* g, const or_params* p, double dt, const double*
               r[l] = (restrict_owned && !owned) ? 0.0 : v[q];
               c[l] = (3.0 * pn[q] * pn[q] + 2.0 * pn[q] * po[q] + po[q] * po[q]) / 4.0;
             }
-        local_gmres(g, p, dt, c, r, y, n);
+        local_op L = {g, p, dt, c, pn, po, x0, y0, z0, {E[0], E[1], E[2]}};
+        local_gmres(&L, r, y, n);
         if (extend_owned) {
           for (int k = o[2]; k < o[2] + b[2]; ++k)   /* (R_k^0)^T: owned nodes only */
             for (int j = o[1]; j < o[1] + b[1]; ++j)
@@ -404,7 +518,8 @@ void or_ras_apply_box(const or_grid* g, const or_params* p, double dt, const dou
         r[l] = v[q];
         c[l] = (3.0 * pn[q] * pn[q] + 2.0 * pn[q] * po[q] + po[q] * po[q]) / 4.0;
       }
-  local_gmres(g, p, dt, c, r, y, n);
+  local_op L = {g, p, dt, c, pn, po, x0, y0, z0, {E[0], E[1], E[2]}};
+  local_gmres(&L, r, y, n);
   for (int k = 0; k < b[2]; ++k)
     for (int j = 0; j < b[1]; ++j)
       for (int i = 0; i < b[0]; ++i) {
@@ -453,7 +568,7 @@ int or_fgmres(const or_grid* g, const or_params* p, double dt, const double* pn,
       double* zj = Z + (size_t)j * N;
       if (precondition) or_ras_apply(g, p, dt, pn, po, V + (size_t)j * N, zj);
       else memcpy(zj, V + (size_t)j * N, N * sizeof(double));
-      or_jacobian_apply(g, p->gamma, dt, pn, po, zj, w);
+      or_jacobian_apply_p(g, p, dt, pn, po, zj, w);
       for (int pass = 0; pass < 2; ++pass) {
         for (int i = 0; i <= j; ++i) {
           double s = 0.0;
@@ -493,7 +608,7 @@ int or_fgmres(const or_grid* g, const or_params* p, double dt, const double* pn,
     for (int i = 0; i < jm; ++i)                      /* x += Z y (flexible form) */
       for (size_t q = 0; q < N; ++q) x[q] += yy[i] * Z[(size_t)i * N + q];
     if (stop) break;
-    or_jacobian_apply(g, p->gamma, dt, pn, po, x, w);  /* true residual at restart */
+    or_jacobian_apply_p(g, p, dt, pn, po, x, w);       /* true residual at restart */
     for (size_t q = 0; q < N; ++q) r[q] = b[q] - w[q];
   }
   if (its_out) *its_out = its;
@@ -517,7 +632,7 @@ int or_newton(const or_grid* g, const or_params* p, double dt, const double* po,
   double* b = alloc0(N);
   double* trial = alloc0(N);
   memcpy(pn, po, N * sizeof(double));
-  or_residual(g, p->gamma, dt, pn, po, F);
+  or_residual_p(g, p, dt, pn, po, F);
   if (source) for (size_t q = 0; q < N; ++q) F[q] -= source[q];
   double n0 = or_norm2(N, F), nrm = n0;
   double stop = fmax(p->newton_rtol * n0, p->newton_atol);
@@ -533,7 +648,7 @@ int or_newton(const or_grid* g, const or_params* p, double dt, const double* po,
     int accepted = 0;
     for (int t = 0; t <= 40 && lambda >= p->ls_min_lambda; ++t) {
       for (size_t q = 0; q < N; ++q) trial[q] = pn[q] + lambda * S[q];
-      or_residual(g, p->gamma, dt, trial, po, Ft);
+      or_residual_p(g, p, dt, trial, po, Ft);
       if (source) for (size_t q = 0; q < N; ++q) Ft[q] -= source[q];
       double nt = or_norm2(N, Ft);
       if (nt <= (1.0 - p->ls_c1 * lambda) * nrm) { accepted = 1; nrm = nt; break; }

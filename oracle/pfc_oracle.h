@@ -29,6 +29,7 @@ typedef struct {
   double gmres_rtol, gmres_atol;     /* xi_r, xi_a */
   int ras_box[3], ras_overlap, ras_local_k;  /* Schwarz boxes, local GMRES(k) (R9) */
   int ras_variant;  /* 0 left-RAS, 1 classical AS, 2 right-RAS */
+  int mobility;     /* 0: M = 1 (the configs); 1: M(phi) = 1 - phi^2 */
 } or_params;
 
 typedef struct {
@@ -48,6 +49,15 @@ void or_local_energy(const or_grid* g, double gamma, const double* phi, double* 
 double or_free_energy(const or_grid* g, double gamma, const double* phi);
 double or_mass(const or_grid* g, const double* phi);
 double or_norm2(size_t n, const double* x);
+
+/* variable mobility */
+void or_div_mgrad(const or_grid* g, const double* M, const double* f, double* out);
+void or_mobility(const or_grid* g, int mobility, const double* phi_new, const double* phi_old,
+                 double* M);
+void or_residual_p(const or_grid* g, const or_params* p, double dt, const double* phi_new,
+                   const double* phi_old, double* F);
+void or_jacobian_apply_p(const or_grid* g, const or_params* p, double dt, const double* phi_new,
+                         const double* phi_old, const double* v, double* Jv);
 
 /* Schwarz preconditioner */
 int or_num_boxes(const or_grid* g, const or_params* p);
