@@ -1,0 +1,181 @@
+// mobility.cu -- variable-mobility residual and Jacobian-vector product, 2D (NEXT row f3).
+//
+// Eq. (NSOP) P:257-263 with M_d = M((Phi+psi)/2), M(phi) = 1 - phi^2 (Test B
+// variants) and (grad . M grad)_d of P:208-212 (edge midpoint value = average of
+// the two end nodes):
+//   F    = (Phi - psi)/dt - (grad . M grad)_d A,   A of Eq. (discretedG)
+//   J v  = v/dt - (grad . M grad)_d (dA v) - (grad . (dM v) grad)_d A,
+//          dA v = (1/2)[(1-gamma) + 2 Delta_d + Delta_d^2] v + c v,  dM v = -u v,
+//          u = (Phi+psi)/2, c = (3Phi^2 + 2Phi psi + psi^2)/4.
+// Each operator is a chain of three radius-1 kernels over global memory (neighbours through
+// L1/L2): Laplacian, Laplacian + pointwise combine, divergence form.  This is the
+// correctness-first path of the row (DESIGN.md §6 gives its measured rate); the M = 1
+// configurations run the fused single-pass stencils of stencil2d.cu / stencil3d.cu.
+#include "pfc_device.cuh"
+#include "pfc_internal.h"
+
+#include <algorithm>
+
+namespace {
+
+constexpr int NT = 256;
+
+__device__ __forceinline__ void nbrs(int i, int j, int nx, int ny, size_t& c, size_t& xm,
+                                     size_t& xp, size_t& ym, size_t& yp) {
+  const int im = i == 0 ? nx - 1 : i - 1, ip = i + 1 == nx ? 0 : i + 1;
+  const int jm = j == 0 ? ny - 1 : j - 1, jp = j + 1 == ny ? 0 : j + 1;
+  c = (size_t)i + (size_t)nx * j;
+  xm = (size_t)im + (size_t)nx * j;
+  xp = (size_t)ip + (size_t)nx * j;
+  ym = (size_t)i + (size_t)nx * jm;
+  yp = (size_t)i + (size_t)nx * jp;
+}
+
+// L = Delta_d f, where f = (a + b) * s (a 2-field average when b != nullptr, s = 1/2)
+__global__ void k_lap(const double* __restrict__ a, const double* __restrict__ b, double s,
+                      double* __restrict__ L, int nx, int ny, double ih2) {
+  const size_t N = (size_t)nx * ny;
+  for (size_t q = blockIdx.x * (size_t)blockDim.x + threadIdx.x; q < N;
+       q += (size_t)gridDim.x * blockDim.x) {
+    size_t c, xm, xp, ym, yp;
+    nbrs((int)(q % nx), (int)(q / nx), nx, ny, c, xm, xp, ym, yp);
+    auto f = [&](size_t k) { return b ? (a[k] + b[k]) * s : a[k]; };
+    L[c] = ih2 * ((f(xm) + f(xp)) + (f(ym) + f(yp)) - 4.0 * f(c));
+  }
+}
+
+// residual / state: A = (1-gamma) u + 2 L1 + Delta L1 + (Phi^3 + Phi^2 psi + Phi psi^2 + psi^3)/4
+// J v:              dA = (1/2)[(1-gamma) v + 2 L1 + Delta L1] + c v
+template <bool JV>
+__global__ void k_combine(const double* __restrict__ a, const double* __restrict__ b,
+                          const double* __restrict__ L1, double* __restrict__ out, int nx,
+                          int ny, double ih2, double gamma) {
+  const size_t N = (size_t)nx * ny;
+  for (size_t q = blockIdx.x * (size_t)blockDim.x + threadIdx.x; q < N;
+       q += (size_t)gridDim.x * blockDim.x) {
+    size_t c, xm, xp, ym, yp;
+    nbrs((int)(q % nx), (int)(q / nx), nx, ny, c, xm, xp, ym, yp);
+    const double LL = ih2 * ((L1[xm] + L1[xp]) + (L1[ym] + L1[yp]) - 4.0 * L1[c]);
+    if (JV) {            // a = v, b = c
+      out[c] = 0.5 * ((1.0 - gamma) * a[c] + 2.0 * L1[c] + LL) + b[c] * a[c];
+    } else {             // a = Phi, b = psi
+      const double p = a[c], s = b[c];
+      out[c] = (1.0 - gamma) * 0.5 * (p + s) + 2.0 * L1[c] + LL +
+               0.25 * (p * p * p + p * p * s + p * s * s + s * s * s);
+    }
+  }
+}
+
+// (grad . M grad)_d g at node c, M given by the function m(k)
+template <class MF>
+__device__ __forceinline__ double div_mgrad(const MF& m, const double* __restrict__ g, size_t c,
+                                            size_t xm, size_t xp, size_t ym, size_t yp,
+                                            double ih2) {
+  const double mc = m(c), gc = g[c];
+  return ih2 * (0.5 * (mc + m(xp)) * (g[xp] - gc) - 0.5 * (mc + m(xm)) * (gc - g[xm]) +
+                0.5 * (mc + m(yp)) * (g[yp] - gc) - 0.5 * (mc + m(ym)) * (gc - g[ym]));
+}
+
+// residual: F = (Phi - psi)/dt - (grad . M grad) A, M = 1 - u^2; fixed-grid per-block ||F||^2
+__global__ void k_resid_out(const double* __restrict__ phi, const double* __restrict__ psi,
+                            const double* __restrict__ A, double* __restrict__ F,
+                            double* __restrict__ partials, int nx, int ny, double ih2,
+                            double idt) {
+  __shared__ double red[64];
+  const size_t N = (size_t)nx * ny;
+  auto m = [&](size_t k) { const double u = 0.5 * (phi[k] + psi[k]); return 1.0 - u * u; };
+  double nrm = 0.0;
+  for (size_t q = blockIdx.x * (size_t)blockDim.x + threadIdx.x; q < N;
+       q += (size_t)gridDim.x * blockDim.x) {
+    size_t c, xm, xp, ym, yp;
+    nbrs((int)(q % nx), (int)(q / nx), nx, ny, c, xm, xp, ym, yp);
+    const double o = (phi[c] - psi[c]) * idt - div_mgrad(m, A, c, xm, xp, ym, yp, ih2);
+    F[c] = o;
+    nrm += o * o;
+  }
+  if (partials) {
+    const double s = block_sum(nrm, red);
+    if (threadIdx.x == 0) partials[blockIdx.x] = s;
+  }
+}
+
+// J v = v/dt - (grad . M grad) dA - (grad . (-u v) grad) A
+__global__ void k_jv_out(const double* __restrict__ v, const double* __restrict__ dA,
+                         const double* __restrict__ phi, const double* __restrict__ psi,
+                         const double* __restrict__ A, double* __restrict__ out, int nx, int ny,
+                         double ih2, double idt, const int* gate) {
+  if (gate && *gate) return;
+  const size_t N = (size_t)nx * ny;
+  auto m = [&](size_t k) { const double u = 0.5 * (phi[k] + psi[k]); return 1.0 - u * u; };
+  auto dm = [&](size_t k) { return -0.5 * (phi[k] + psi[k]) * v[k]; };
+  for (size_t q = blockIdx.x * (size_t)blockDim.x + threadIdx.x; q < N;
+       q += (size_t)gridDim.x * blockDim.x) {
+    size_t c, xm, xp, ym, yp;
+    nbrs((int)(q % nx), (int)(q / nx), nx, ny, c, xm, xp, ym, yp);
+    out[c] = v[c] * idt - div_mgrad(m, dA, c, xm, xp, ym, yp, ih2) -
+             div_mgrad(dm, A, c, xm, xp, ym, yp, ih2);
+  }
+}
+
+int grid_for(size_t N) {
+  static int nsm = 0;
+  if (!nsm) {
+    int dev = 0, v = 0;
+    nsm = (cudaGetDevice(&dev) == cudaSuccess &&
+           cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess && v > 0)
+              ? v : 148;
+  }
+  const size_t want = (N + NT - 1) / NT;
+  return (int)std::min<size_t>(want, (size_t)nsm * 8);   // fixed for a given N: deterministic
+}
+
+// A(Phi, psi) into `A` through the work field t0
+cudaError_t a_field(pfc_ctx* ctx, const double* phi, const double* psi, double* A, double* t0) {
+  const int nx = ctx->cfg.n[0], ny = ctx->cfg.n[1];
+  const int g = grid_for(ctx->N);
+  k_lap<<<g, NT, 0, ctx->stream>>>(phi, psi, 0.5, t0, nx, ny, ctx->ih2);
+  k_combine<false><<<g, NT, 0, ctx->stream>>>(phi, psi, t0, A, nx, ny, ctx->ih2, ctx->cfg.gamma);
+  ctx->launches += 2;
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t launch_mob_state(pfc_ctx* ctx, const double* phi, const double* psi) {
+  ctx->mob_phi = phi;
+  ctx->mob_psi = psi;
+  cudaError_t e = a_field(ctx, phi, psi, ctx->mob_A, ctx->mob_t[0]);
+  pfc_account(ctx, PFC_K_COEF, 48.0 * ctx->N, 30.0 * ctx->N);
+  return e;
+}
+
+cudaError_t launch_residual_mob(pfc_ctx* ctx, const double* phi, const double* psi, double dt,
+                                double* F, double* partials, int* nparts) {
+  const int nx = ctx->cfg.n[0], ny = ctx->cfg.n[1];
+  cudaError_t e = a_field(ctx, phi, psi, ctx->mob_t[1], ctx->mob_t[0]);
+  if (e != cudaSuccess) return e;
+  const int g = grid_for(ctx->N);
+  k_resid_out<<<g, NT, 0, ctx->stream>>>(phi, psi, ctx->mob_t[1], F, partials, nx, ny,
+                                          ctx->ih2, 1.0 / dt);
+  ctx->launches++;
+  if (nparts) *nparts = g;
+  // algorithmic: Phi, psi in, F out (the two intermediate fields are work of this path)
+  pfc_account(ctx, PFC_K_RESIDUAL, 24.0 * ctx->N, 50.0 * ctx->N);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_jv_mob(pfc_ctx* ctx, const double* v, const double* c, double dt,
+                          double* out) {
+  const int nx = ctx->cfg.n[0], ny = ctx->cfg.n[1];
+  const int g = grid_for(ctx->N);
+  // device-resident FGMRES (f1): only the final write is gated; the two producer kernels
+  // run unconditionally into work fields nobody reads when the gate is set
+  k_lap<<<g, NT, 0, ctx->stream>>>(v, nullptr, 1.0, ctx->mob_t[0], nx, ny, ctx->ih2);
+  k_combine<true><<<g, NT, 0, ctx->stream>>>(v, c, ctx->mob_t[0], ctx->mob_t[1], nx, ny, ctx->ih2,
+                                             ctx->cfg.gamma);
+  k_jv_out<<<g, NT, 0, ctx->stream>>>(v, ctx->mob_t[1], ctx->mob_phi, ctx->mob_psi, ctx->mob_A,
+                                       out, nx, ny, ctx->ih2, 1.0 / dt, ctx->gate);
+  ctx->launches += 3;
+  pfc_account(ctx, PFC_K_JV, 24.0 * ctx->N, 45.0 * ctx->N);
+  return cudaGetLastError();
+}

@@ -121,12 +121,20 @@ bool tma_usable(const void* ptr) { return (reinterpret_cast<uintptr_t>(ptr) & 15
 
 cudaError_t launch_residual(pfc_ctx* ctx, const double* a, const double* b, double dt, double* F,
                             double* partials, int* nparts) {
+  if (ctx->cfg.mobility) return launch_residual_mob(ctx, a, b, dt, F, partials, nparts);
   return ctx->cfg.ndim == 2 ? launch_residual_2d(ctx, a, b, dt, F, partials, nparts)
                             : launch_residual_3d(ctx, a, b, dt, F, partials, nparts);
 }
 
 cudaError_t launch_jv(pfc_ctx* ctx, const double* v, const double* c, double dt, double* out) {
+  if (ctx->cfg.mobility) return launch_jv_mob(ctx, v, c, dt, out);
   return ctx->cfg.ndim == 2 ? launch_jv_2d(ctx, v, c, dt, out) : launch_jv_3d(ctx, v, c, dt, out);
+}
+
+cudaError_t launch_jac_state(pfc_ctx* ctx, const double* phi_new, const double* phi_old) {
+  cudaError_t e = launch_coef(ctx, phi_new, phi_old, ctx->c);
+  if (e != cudaSuccess || !ctx->cfg.mobility) return e;
+  return launch_mob_state(ctx, phi_new, phi_old);
 }
 
 int ras_plan(pfc_ctx* ctx) { return ctx->cfg.ndim == 2 ? ras2d_plan(ctx) : ras3d_plan(ctx); }
@@ -359,7 +367,7 @@ static pfc_status newton(pfc_ctx* ctx, double dt, pfc_step_info* inf) {
       inf->res_final = nrm;
       return pfc_fail(ctx, PFC_ENOCONV, "Newton: newton_maxit reached");
     }
-    KL(PFC_K_COEF, launch_coef(ctx, ctx->phi, ctx->psi, ctx->c), "coef");
+    KL(PFC_K_COEF, launch_jac_state(ctx, ctx->phi, ctx->psi), "coef");
     int its = 0;
     s = fgmres(ctx, dt, nrm, &its);
     if (s) return s;
@@ -421,6 +429,7 @@ void pfc_config_default(pfc_config* c) {
   c->ras_overlap = 2;
   c->ras_local_k = 10;
   c->ras_variant = PFC_RAS_LEFT;
+  c->mobility = PFC_MOBILITY_ONE;
 }
 
 static pfc_status validate(const pfc_config& c, std::string* why) {
@@ -448,6 +457,10 @@ static pfc_status validate(const pfc_config& c, std::string* why) {
   if (c.ras_local_k < 1 || c.ras_local_k > PFC_MAX_LOCAL_K) return bad("ras_local_k in [1,15]");
   if (c.ras_variant != PFC_RAS_LEFT && c.ras_variant != PFC_RAS_AS && c.ras_variant != PFC_RAS_RIGHT)
     return bad("ras_variant must be PFC_RAS_LEFT, PFC_RAS_AS or PFC_RAS_RIGHT");
+  if (c.mobility != PFC_MOBILITY_ONE && c.mobility != PFC_MOBILITY_QUADRATIC)
+    return bad("mobility must be PFC_MOBILITY_ONE or PFC_MOBILITY_QUADRATIC");
+  if (c.mobility == PFC_MOBILITY_QUADRATIC && c.ndim != 2)
+    return bad("PFC_MOBILITY_QUADRATIC is built for ndim == 2 only");
   if (c.gmres_restart < 1 || c.gmres_restart > PFC_MAX_RESTART) return bad("gmres_restart in [1,32]");
   if (c.gmres_maxit < 1 || c.newton_maxit < 0) return bad("iteration limits must be positive");
   if (!(c.newton_rtol >= 0 && c.newton_atol >= 0 && c.gmres_rtol >= 0 && c.gmres_atol >= 0))
@@ -493,6 +506,11 @@ pfc_status pfc_create(const pfc_config* cfg, void* stream, pfc_ctx** out) {
                        &ctx->S,   &ctx->c,   &ctx->w, &ctx->stage};
   for (double** f : fields)
     if (pfc_check_cuda(ctx, cudaMalloc(f, bytes), "cudaMalloc field")) return fail(PFC_ENOMEM);
+  if (c.mobility) {
+    double** mf[] = {&ctx->mob_A, &ctx->mob_t[0], &ctx->mob_t[1], &ctx->mob_t[2]};
+    for (double** f : mf)
+      if (pfc_check_cuda(ctx, cudaMalloc(f, bytes), "cudaMalloc mobility field")) return fail(PFC_ENOMEM);
+  }
   if (pfc_check_cuda(ctx, cudaMalloc(&ctx->V, bytes * (m + 1)), "cudaMalloc V") ||
       pfc_check_cuda(ctx, cudaMalloc(&ctx->Z, bytes * m), "cudaMalloc Z"))
     return fail(PFC_ENOMEM);
@@ -534,7 +552,8 @@ void pfc_destroy(pfc_ctx* ctx) {
   if (!ctx) return;
   double* fs[] = {ctx->phi, ctx->psi,   ctx->F,        ctx->Ft,       ctx->trial, ctx->S,
                   ctx->c,   ctx->w,     ctx->stage,    ctx->V,        ctx->Z,     ctx->partials,
-                  ctx->dscal, ctx->ras_scratch, ctx->ras_y};
+                  ctx->dscal, ctx->ras_scratch, ctx->ras_y, ctx->mob_A, ctx->mob_t[0],
+                  ctx->mob_t[1], ctx->mob_t[2]};
   for (double* f : fs)
     if (f) cudaFree(f);
   if (ctx->ticket) cudaFree(ctx->ticket);
@@ -602,7 +621,7 @@ pfc_status pfc_jacobian_apply(pfc_ctx* ctx, const double* phi_new, const double*
                               double dt, const double* v, double* Jv) {
   pfc_status s = check_fields(ctx, dt, {phi_new, phi_old, v}, Jv);
   if (s) return s;
-  KL(PFC_K_COEF, launch_coef(ctx, phi_new, phi_old, ctx->c), "pfc_jacobian_apply coef");
+  KL(PFC_K_COEF, launch_jac_state(ctx, phi_new, phi_old), "pfc_jacobian_apply coef");
   KL(PFC_K_JV, launch_jv(ctx, v, ctx->c, dt, Jv), "pfc_jacobian_apply");
   return PFC_OK;
 }
@@ -611,7 +630,7 @@ pfc_status pfc_ras_apply(pfc_ctx* ctx, const double* phi_new, const double* phi_
                          const double* v, double* z) {
   pfc_status s = check_fields(ctx, dt, {phi_new, phi_old, v}, z);
   if (s) return s;
-  KL(PFC_K_COEF, launch_coef(ctx, phi_new, phi_old, ctx->c), "pfc_ras_apply coef");
+  KL(PFC_K_COEF, launch_jac_state(ctx, phi_new, phi_old), "pfc_ras_apply coef");
   KL(PFC_K_RAS, launch_ras(ctx, v, ctx->c, dt, z), "pfc_ras_apply");
   return PFC_OK;
 }

@@ -50,6 +50,12 @@ struct pfc_ctx {
   double* ras_scratch = nullptr;  // 3D subdomain-solve scratch (L2-resident)
   double* ras_y = nullptr;        // AS / right-RAS: ext-box solutions [box][ext node]
   double* stage = nullptr;     // staging field for host-pointer calls
+  // variable mobility (row f3): the Jacobian state A(Phi, psi) and the iterate it belongs to,
+  // plus three work fields for the composed stencils
+  double* mob_A = nullptr;
+  double* mob_t[3] = {nullptr, nullptr, nullptr};
+  const double* mob_phi = nullptr;
+  const double* mob_psi = nullptr;
   double* partials = nullptr;  // reduction scratch
   size_t npartials = 0;
   double* dscal = nullptr;     // device scalars: [0,64) h1, [64,128) h2, [128] |w|^2, ...
@@ -99,6 +105,14 @@ pfc_status pfc_check_cuda(pfc_ctx* ctx, cudaError_t e, const char* where);
 cudaError_t launch_residual(pfc_ctx* ctx, const double* phi_new, const double* phi_old, double dt,
                             double* F, double* norm_partials, int* nparts);
 cudaError_t launch_jv(pfc_ctx* ctx, const double* v, const double* c, double dt, double* out);
+// Jacobian state of (phi_new, phi_old): c (k_coef) and, with variable mobility, A and the
+// iterate pointers used by the mobility J v and the subdomain solves
+cudaError_t launch_jac_state(pfc_ctx* ctx, const double* phi_new, const double* phi_old);
+// variable-mobility operators (mobility.cu, 2D)
+cudaError_t launch_residual_mob(pfc_ctx*, const double* phi_new, const double* phi_old, double dt,
+                                double* F, double* partials, int* nparts);
+cudaError_t launch_jv_mob(pfc_ctx*, const double* v, const double* c, double dt, double* out);
+cudaError_t launch_mob_state(pfc_ctx*, const double* phi_new, const double* phi_old);
 cudaError_t launch_energy_mass(pfc_ctx* ctx, const double* phi, double* partials, int* nparts);
 cudaError_t launch_ras(pfc_ctx* ctx, const double* v, const double* c, double dt, double* z);
 int ras_plan(pfc_ctx* ctx);   // fills ras_smem/threads/cluster; returns 0 if infeasible

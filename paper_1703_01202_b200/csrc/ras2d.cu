@@ -48,6 +48,12 @@ struct RasArgs {
   int restrict_owned;   // right-RAS: R_k^0 (v zero outside the owned box)
   double* y_ext;        // AS / right-RAS: ext-box solutions [box][ext node] for (R_k^delta)^T
   const int* gate;   // device-resident FGMRES: skip the launch when *gate != 0 (f1)
+  // variable mobility (row f3): the Jacobian state Phi, psi, A of the current iterate; the
+  // local operator is then A_k = R_k^delta J (R_k^delta)^T (reading R8b)
+  const double* phi;
+  const double* psi;
+  const double* A;
+  int mobility;
 };
 
 // Block sum of nv (runtime, <= NVP) values held by every thread in acc[]: the sums are left in
@@ -91,6 +97,9 @@ __global__ void __launch_bounds__(NT, 1) ras2d_kernel(RasArgs p) {
   double* pb = pl + np;                  // np
   double* red = pb + np;                 // 2 x NW x NVP
   double* hwall = red + 2 * NW * NVP;    // NW x 3 NVP: per-warp copies of h1 | h2 | misc
+  double* pm = hwall + NW * 3 * NVP;     // mobility: M, A, u on the padded plane (np each)
+  double* pa = pm + np;
+  double* pu = pa + np;
   __shared__ double H[(K + 1) * K];
   __shared__ double gv[K + 1], cs[K], sn[K], yv[K];
 
@@ -116,6 +125,19 @@ __global__ void __launch_bounds__(NT, 1) ras2d_kernel(RasArgs p) {
 
   // zero the padded planes (ring stays zero), gather R_k^delta v and c with periodic wrap
   for (int q = tid; q < 3 * np; q += NT) pv[q] = 0.0;
+  if (p.mobility) {   // M = 1 - u^2, A and u of the iterate on the ext box and its +1 ring
+    for (int q = tid; q < np; q += NT) {
+      const int pi = q % Px, pj = q / Px;
+      double m = 0.0, a = 0.0, u = 0.0;
+      if (pi >= 2 && pi < Px - 2 && pj >= 2 && pj < Py - 2) {
+        const size_t g = (size_t)wrapi(gx0 + pi - 3, p.nx) + (size_t)p.nx * wrapi(gy0 + pj - 3, p.ny);
+        u = 0.5 * (p.phi[g] + p.psi[g]);
+        m = 1.0 - u * u;
+        a = p.A[g];
+      }
+      pm[q] = m; pa[q] = a; pu[q] = u;
+    }
+  }
   double w[SLOTS];
   double acc[NVP];
 #pragma unroll
@@ -199,8 +221,21 @@ __global__ void __launch_bounds__(NT, 1) ras2d_kernel(RasArgs p) {
     for (int s = 0; s < SLOTS; ++s) {
       if (own[s]) {
         const int f = pidx[s], l = tid + s * NT;
-        double lapb = ih2 * ((pb[f - 1] + pb[f + 1]) + (pb[f - Px] + pb[f + Px]) - 4.0 * pb[f]);
-        double ww = pv[f] * idt - lapb;
+        double ww;
+        if (p.mobility) {   // v/dt - (grad . M grad) B - (grad . (-u v) grad) A
+          auto dmg = [&](const double* m, const double* g, const double* s2) {
+            auto mm = [&](int k) { return s2 ? -pu[k] * s2[k] : m[k]; };
+            const double mc = mm(f), gc = g[f];
+            return ih2 * (0.5 * (mc + mm(f + 1)) * (g[f + 1] - gc) -
+                          0.5 * (mc + mm(f - 1)) * (gc - g[f - 1]) +
+                          0.5 * (mc + mm(f + Px)) * (g[f + Px] - gc) -
+                          0.5 * (mc + mm(f - Px)) * (gc - g[f - Px]));
+          };
+          ww = pv[f] * idt - dmg(pm, pb, nullptr) - dmg(nullptr, pa, pv);
+        } else {
+          double lapb = ih2 * ((pb[f - 1] + pb[f + 1]) + (pb[f - Px] + pb[f + Px]) - 4.0 * pb[f]);
+          ww = pv[f] * idt - lapb;
+        }
         w[s] = ww;
 #pragma unroll
         for (int i = 0; i < K; ++i) {
@@ -745,9 +780,9 @@ size_t ras2d_col_smem_bytes() {
 }
 
 typedef void (*ras2d_fn)(RasArgs);
-size_t ras2d_smem_bytes(int bx, int by, int o, int k) {
+size_t ras2d_smem_bytes(int bx, int by, int o, int k, int mobility) {
   const size_t Ex = bx + 2 * o, Ey = by + 2 * o, n = Ex * Ey, np = (Ex + 6) * (Ey + 6);
-  size_t d = (size_t)k * n + n + 3 * np + 2 * NW * 16 + NW * 3 * 16;
+  size_t d = (size_t)k * n + n + 3 * np + 2 * NW * 16 + NW * 3 * 16 + (mobility ? 3 * np : 0);
   return d * sizeof(double) + 128;
 }
 
@@ -797,7 +832,7 @@ int ras2d_plan(pfc_ctx* ctx) {
   const pfc_config& c = ctx->cfg;
   const int Ex = c.ras_box[0] + 2 * c.ras_overlap, Ey = c.ras_box[1] + 2 * c.ras_overlap;
   if (Ex * Ey > MAXN) return 0;
-  if (getenv("PFC_RAS_SMEM_BASIS") == nullptr) {
+  if (getenv("PFC_RAS_SMEM_BASIS") == nullptr && !c.mobility) {
     const int r = col_rows(c.ras_local_k, Ex, Ey);
     if (r) {
       const int ns = (Ey + r - 1) / r;
@@ -807,7 +842,8 @@ int ras2d_plan(pfc_ctx* ctx) {
       return 1;
     }
   }
-  size_t sm = ras2d_smem_bytes(c.ras_box[0], c.ras_box[1], c.ras_overlap, c.ras_local_k);
+  size_t sm = ras2d_smem_bytes(c.ras_box[0], c.ras_box[1], c.ras_overlap, c.ras_local_k,
+                               c.mobility);
   if (sm + 2048 > 227 * 1024) return 0;   // + static shared memory (H, Givens, reductions)
   ctx->ras_smem = (int)sm;
   ctx->ras_threads = NT;        // shared-memory-basis kernel
@@ -854,7 +890,8 @@ cudaError_t launch_ras_2d(pfc_ctx* ctx, const double* v, const double* c, double
     if (e != cudaSuccess) return e;
     RasArgs p{v, c, z, cf.n[0], cf.n[1], cf.ras_box[0], cf.ras_box[1], cf.ras_overlap,
               1.0 / dt, cf.gamma, ctx->ih2, cf.ras_variant == PFC_RAS_RIGHT,
-              cf.ras_variant == PFC_RAS_LEFT ? nullptr : ctx->ras_y, ctx->gate};
+              cf.ras_variant == PFC_RAS_LEFT ? nullptr : ctx->ras_y, ctx->gate,
+              ctx->mob_phi, ctx->mob_psi, ctx->mob_A, cf.mobility};
     fn<<<nb, NT, ctx->ras_smem, ctx->stream>>>(p);
   }
   ctx->launches++;
