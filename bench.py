@@ -146,6 +146,11 @@ def bench_cuda(args):
     if ws > 1:
         dist.barrier()
     cfg = CONFIGS[args.config]
+    if args.mobility or args.ras_variant:   # NEXT-row measurements (not the headline line)
+        import dataclasses
+        cfg = dataclasses.replace(cfg, mobility=args.mobility, ras_variant=args.ras_variant,
+                                  name=cfg.name + (f"_mobility{args.mobility}" if args.mobility else "")
+                                  + (f"_ras{args.ras_variant}" if args.ras_variant else ""))
     W, K = args.warmup, args.steps
     phi0 = cfg.initial_condition()
     ctx = P.Context(cfg)
@@ -338,6 +343,11 @@ def bench_reference(args):
     from paper_1703_01202_b200.inputs import CONFIGS
     O.build()
     cfg = CONFIGS[args.config]
+    if args.mobility or args.ras_variant:   # NEXT-row measurements (not the headline line)
+        import dataclasses
+        cfg = dataclasses.replace(cfg, mobility=args.mobility, ras_variant=args.ras_variant,
+                                  name=cfg.name + (f"_mobility{args.mobility}" if args.mobility else "")
+                                  + (f"_ras{args.ras_variant}" if args.ras_variant else ""))
     W, K = args.warmup, args.steps
     phi = cfg.initial_condition()
     prm = O.params_from_config(cfg)
@@ -379,6 +389,8 @@ def main():
     ap.add_argument("--jv-size", type=int, default=512)
     ap.add_argument("--cpu-steps", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--mobility", type=int, default=0, help="1: M = 1 - phi^2 (row f3, 2D)")
+    ap.add_argument("--ras-variant", type=int, default=0, help="0 left-RAS, 1 AS, 2 right-RAS")
     args = ap.parse_args()
     if args.warmup < 3:
         print("note: --warmup < 3 is below the timing contract", file=sys.stderr)

@@ -129,6 +129,7 @@ class PFCConfig:
     ras_overlap: int = 2
     ras_local_k: int = 10
     ras_variant: int = 0            # 0 left-RAS, 1 AS, 2 right-RAS
+    mobility: int = 0               # 0 M = 1 (all five configs); 1 M = 1 - phi^2 (row f3)
     ic: dict = field(default_factory=dict)
     seed: int = 1
 
