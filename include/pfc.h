@@ -74,7 +74,7 @@ typedef struct pfc_config {
 /* Mobility of Eq. (PFCeq) P:137-150 in the scheme's (grad . M_d grad)_d, P:208-212 (edge
  * midpoint value = average of the two end nodes), M_d = M((phi_new + phi_old)/2):
  *   PFC_MOBILITY_ONE        M = 1: (grad . M grad)_d = Delta_d (the five configurations);
- *   PFC_MOBILITY_QUADRATIC  M(phi) = 1 - phi^2 (Test B variants; 2D only).  The
+ *   PFC_MOBILITY_QUADRATIC  M(phi) = 1 - phi^2 (Test B variants).  The
  *   Jacobian then carries the mobility derivative, J v = v/dt - (grad . M grad)(dA v)
  *   - (grad . (dM v) grad) A with dM v = -(phi_new+phi_old)/2 v, and the Schwarz subdomain
  *   matrix is A_k = R_k^delta J (R_k^delta)^T (Eq. Ak, reading R8b). */
@@ -115,8 +115,8 @@ void pfc_config_default(pfc_config* cfg);
  * 0 < dt_min <= dt_max when adaptive; n_d % ras_box_d == 0; 0 <= ras_overlap < ras_box_d and
  * ras_box_d + 2 ras_overlap + 6 <= n_d (the zero ring of P:429-437 must not wrap onto the box);
  * the ext box fits the subdomain kernel's shared-memory plan; 1 <= ras_local_k <= 15;
- * 1 <= gmres_restart <= 32; mobility is PFC_MOBILITY_ONE, or PFC_MOBILITY_QUADRATIC with
- * ndim == 2 and an ext box of at most 38^2 nodes.  Allocates the Krylov workspace (2m+1 fields
+ * 1 <= gmres_restart <= 32; mobility is PFC_MOBILITY_ONE or PFC_MOBILITY_QUADRATIC (2D: the
+ * ext box must fit the shared-memory subdomain kernel, at most 38^2 nodes).  Allocates the Krylov workspace (2m+1 fields
  * + 8 work fields; + 4 with PFC_MOBILITY_QUADRATIC). */
 pfc_status pfc_create(const pfc_config* cfg, void* cuda_stream, pfc_ctx** out);
 void pfc_destroy(pfc_ctx* ctx);

@@ -1,4 +1,4 @@
-// mobility.cu -- variable-mobility residual and Jacobian-vector product, 2D (NEXT row f3).
+// mobility.cu -- variable-mobility residual and Jacobian-vector product, 2D/3D (NEXT row f3).
 //
 // Eq. (NSOP) P:257-263 with M_d = M((Phi+psi)/2), M(phi) = 1 - phi^2 (Test B
 // variants) and (grad . M grad)_d of P:208-212 (edge midpoint value = average of
@@ -20,27 +20,42 @@ namespace {
 
 constexpr int NT = 256;
 
-__device__ __forceinline__ void nbrs(int i, int j, int nx, int ny, size_t& c, size_t& xm,
-                                     size_t& xp, size_t& ym, size_t& yp) {
-  const int im = i == 0 ? nx - 1 : i - 1, ip = i + 1 == nx ? 0 : i + 1;
-  const int jm = j == 0 ? ny - 1 : j - 1, jp = j + 1 == ny ? 0 : j + 1;
-  c = (size_t)i + (size_t)nx * j;
-  xm = (size_t)im + (size_t)nx * j;
-  xp = (size_t)ip + (size_t)nx * j;
-  ym = (size_t)i + (size_t)nx * jm;
-  yp = (size_t)i + (size_t)nx * jp;
+struct Grid { int nx, ny, nz, nd; };
+
+// the node q and its 2*nd periodic neighbours (x-, x+, y-, y+, z-, z+)
+struct Nb {
+  size_t c, m[3], p[3];
+};
+__device__ __forceinline__ Nb nbrs(size_t q, const Grid& G) {
+  const size_t nxy = (size_t)G.nx * G.ny;
+  const int i = (int)(q % G.nx), j = (int)((q / G.nx) % G.ny), k = (int)(q / nxy);
+  const int im = i == 0 ? G.nx - 1 : i - 1, ip = i + 1 == G.nx ? 0 : i + 1;
+  const int jm = j == 0 ? G.ny - 1 : j - 1, jp = j + 1 == G.ny ? 0 : j + 1;
+  const int km = k == 0 ? G.nz - 1 : k - 1, kp = k + 1 == G.nz ? 0 : k + 1;
+  const size_t row = (size_t)G.nx * j + nxy * k;
+  Nb n;
+  n.c = q;
+  n.m[0] = row + im; n.p[0] = row + ip;
+  n.m[1] = (size_t)G.nx * jm + nxy * k + i; n.p[1] = (size_t)G.nx * jp + nxy * k + i;
+  n.m[2] = (size_t)G.nx * j + nxy * km + i; n.p[2] = (size_t)G.nx * j + nxy * kp + i;
+  return n;
+}
+template <class F>
+__device__ __forceinline__ double lapf(const F& f, const Nb& n, int nd, double ih2) {
+  double s = 0.0;
+  for (int d = 0; d < nd; ++d) s += f(n.m[d]) + f(n.p[d]);
+  return ih2 * (s - 2.0 * nd * f(n.c));
 }
 
 // L = Delta_d f, where f = (a + b) * s (a 2-field average when b != nullptr, s = 1/2)
 __global__ void k_lap(const double* __restrict__ a, const double* __restrict__ b, double s,
-                      double* __restrict__ L, int nx, int ny, double ih2) {
-  const size_t N = (size_t)nx * ny;
+                      double* __restrict__ L, Grid G, double ih2) {
+  const size_t N = (size_t)G.nx * G.ny * G.nz;
   for (size_t q = blockIdx.x * (size_t)blockDim.x + threadIdx.x; q < N;
        q += (size_t)gridDim.x * blockDim.x) {
-    size_t c, xm, xp, ym, yp;
-    nbrs((int)(q % nx), (int)(q / nx), nx, ny, c, xm, xp, ym, yp);
+    const Nb n = nbrs(q, G);
     auto f = [&](size_t k) { return b ? (a[k] + b[k]) * s : a[k]; };
-    L[c] = ih2 * ((f(xm) + f(xp)) + (f(ym) + f(yp)) - 4.0 * f(c));
+    L[q] = lapf(f, n, G.nd, ih2);
   }
 }
 
@@ -48,14 +63,14 @@ __global__ void k_lap(const double* __restrict__ a, const double* __restrict__ b
 // J v:              dA = (1/2)[(1-gamma) v + 2 L1 + Delta L1] + c v
 template <bool JV>
 __global__ void k_combine(const double* __restrict__ a, const double* __restrict__ b,
-                          const double* __restrict__ L1, double* __restrict__ out, int nx,
-                          int ny, double ih2, double gamma) {
-  const size_t N = (size_t)nx * ny;
+                          const double* __restrict__ L1, double* __restrict__ out, Grid G,
+                          double ih2, double gamma) {
+  const size_t N = (size_t)G.nx * G.ny * G.nz;
   for (size_t q = blockIdx.x * (size_t)blockDim.x + threadIdx.x; q < N;
        q += (size_t)gridDim.x * blockDim.x) {
-    size_t c, xm, xp, ym, yp;
-    nbrs((int)(q % nx), (int)(q / nx), nx, ny, c, xm, xp, ym, yp);
-    const double LL = ih2 * ((L1[xm] + L1[xp]) + (L1[ym] + L1[yp]) - 4.0 * L1[c]);
+    const Nb n = nbrs(q, G);
+    const size_t c = q;
+    const double LL = lapf([&](size_t k) { return L1[k]; }, n, G.nd, ih2);
     if (JV) {            // a = v, b = c
       out[c] = 0.5 * ((1.0 - gamma) * a[c] + 2.0 * L1[c] + LL) + b[c] * a[c];
     } else {             // a = Phi, b = psi
@@ -66,31 +81,30 @@ __global__ void k_combine(const double* __restrict__ a, const double* __restrict
   }
 }
 
-// (grad . M grad)_d g at node c, M given by the function m(k)
+// (grad . M grad)_d g at node n.c, M given by the function m(k)
 template <class MF>
-__device__ __forceinline__ double div_mgrad(const MF& m, const double* __restrict__ g, size_t c,
-                                            size_t xm, size_t xp, size_t ym, size_t yp,
-                                            double ih2) {
-  const double mc = m(c), gc = g[c];
-  return ih2 * (0.5 * (mc + m(xp)) * (g[xp] - gc) - 0.5 * (mc + m(xm)) * (gc - g[xm]) +
-                0.5 * (mc + m(yp)) * (g[yp] - gc) - 0.5 * (mc + m(ym)) * (gc - g[ym]));
+__device__ __forceinline__ double div_mgrad(const MF& m, const double* __restrict__ g, const Nb& n,
+                                            int nd, double ih2) {
+  const double mc = m(n.c), gc = g[n.c];
+  double s = 0.0;
+  for (int d = 0; d < nd; ++d)
+    s += 0.5 * (mc + m(n.p[d])) * (g[n.p[d]] - gc) - 0.5 * (mc + m(n.m[d])) * (gc - g[n.m[d]]);
+  return ih2 * s;
 }
 
 // residual: F = (Phi - psi)/dt - (grad . M grad) A, M = 1 - u^2; fixed-grid per-block ||F||^2
 __global__ void k_resid_out(const double* __restrict__ phi, const double* __restrict__ psi,
                             const double* __restrict__ A, double* __restrict__ F,
-                            double* __restrict__ partials, int nx, int ny, double ih2,
-                            double idt) {
+                            double* __restrict__ partials, Grid G, double ih2, double idt) {
   __shared__ double red[64];
-  const size_t N = (size_t)nx * ny;
+  const size_t N = (size_t)G.nx * G.ny * G.nz;
   auto m = [&](size_t k) { const double u = 0.5 * (phi[k] + psi[k]); return 1.0 - u * u; };
   double nrm = 0.0;
   for (size_t q = blockIdx.x * (size_t)blockDim.x + threadIdx.x; q < N;
        q += (size_t)gridDim.x * blockDim.x) {
-    size_t c, xm, xp, ym, yp;
-    nbrs((int)(q % nx), (int)(q / nx), nx, ny, c, xm, xp, ym, yp);
-    const double o = (phi[c] - psi[c]) * idt - div_mgrad(m, A, c, xm, xp, ym, yp, ih2);
-    F[c] = o;
+    const Nb n = nbrs(q, G);
+    const double o = (phi[q] - psi[q]) * idt - div_mgrad(m, A, n, G.nd, ih2);
+    F[q] = o;
     nrm += o * o;
   }
   if (partials) {
@@ -102,18 +116,16 @@ __global__ void k_resid_out(const double* __restrict__ phi, const double* __rest
 // J v = v/dt - (grad . M grad) dA - (grad . (-u v) grad) A
 __global__ void k_jv_out(const double* __restrict__ v, const double* __restrict__ dA,
                          const double* __restrict__ phi, const double* __restrict__ psi,
-                         const double* __restrict__ A, double* __restrict__ out, int nx, int ny,
+                         const double* __restrict__ A, double* __restrict__ out, Grid G,
                          double ih2, double idt, const int* gate) {
   if (gate && *gate) return;
-  const size_t N = (size_t)nx * ny;
+  const size_t N = (size_t)G.nx * G.ny * G.nz;
   auto m = [&](size_t k) { const double u = 0.5 * (phi[k] + psi[k]); return 1.0 - u * u; };
   auto dm = [&](size_t k) { return -0.5 * (phi[k] + psi[k]) * v[k]; };
   for (size_t q = blockIdx.x * (size_t)blockDim.x + threadIdx.x; q < N;
        q += (size_t)gridDim.x * blockDim.x) {
-    size_t c, xm, xp, ym, yp;
-    nbrs((int)(q % nx), (int)(q / nx), nx, ny, c, xm, xp, ym, yp);
-    out[c] = v[c] * idt - div_mgrad(m, dA, c, xm, xp, ym, yp, ih2) -
-             div_mgrad(dm, A, c, xm, xp, ym, yp, ih2);
+    const Nb n = nbrs(q, G);
+    out[q] = v[q] * idt - div_mgrad(m, dA, n, G.nd, ih2) - div_mgrad(dm, A, n, G.nd, ih2);
   }
 }
 
@@ -130,11 +142,16 @@ int grid_for(size_t N) {
 }
 
 // A(Phi, psi) into `A` through the work field t0
+Grid grid_of(const pfc_ctx* ctx) {
+  const pfc_config& c = ctx->cfg;
+  return Grid{c.n[0], c.n[1], c.ndim == 3 ? c.n[2] : 1, c.ndim};
+}
+
 cudaError_t a_field(pfc_ctx* ctx, const double* phi, const double* psi, double* A, double* t0) {
-  const int nx = ctx->cfg.n[0], ny = ctx->cfg.n[1];
+  const Grid G = grid_of(ctx);
   const int g = grid_for(ctx->N);
-  k_lap<<<g, NT, 0, ctx->stream>>>(phi, psi, 0.5, t0, nx, ny, ctx->ih2);
-  k_combine<false><<<g, NT, 0, ctx->stream>>>(phi, psi, t0, A, nx, ny, ctx->ih2, ctx->cfg.gamma);
+  k_lap<<<g, NT, 0, ctx->stream>>>(phi, psi, 0.5, t0, G, ctx->ih2);
+  k_combine<false><<<g, NT, 0, ctx->stream>>>(phi, psi, t0, A, G, ctx->ih2, ctx->cfg.gamma);
   ctx->launches += 2;
   return cudaGetLastError();
 }
@@ -151,12 +168,12 @@ cudaError_t launch_mob_state(pfc_ctx* ctx, const double* phi, const double* psi)
 
 cudaError_t launch_residual_mob(pfc_ctx* ctx, const double* phi, const double* psi, double dt,
                                 double* F, double* partials, int* nparts) {
-  const int nx = ctx->cfg.n[0], ny = ctx->cfg.n[1];
+  const Grid G = grid_of(ctx);
   cudaError_t e = a_field(ctx, phi, psi, ctx->mob_t[1], ctx->mob_t[0]);
   if (e != cudaSuccess) return e;
   const int g = grid_for(ctx->N);
-  k_resid_out<<<g, NT, 0, ctx->stream>>>(phi, psi, ctx->mob_t[1], F, partials, nx, ny,
-                                          ctx->ih2, 1.0 / dt);
+  k_resid_out<<<g, NT, 0, ctx->stream>>>(phi, psi, ctx->mob_t[1], F, partials, G, ctx->ih2,
+                                          1.0 / dt);
   ctx->launches++;
   if (nparts) *nparts = g;
   // algorithmic: Phi, psi in, F out (the two intermediate fields are work of this path)
@@ -166,15 +183,15 @@ cudaError_t launch_residual_mob(pfc_ctx* ctx, const double* phi, const double* p
 
 cudaError_t launch_jv_mob(pfc_ctx* ctx, const double* v, const double* c, double dt,
                           double* out) {
-  const int nx = ctx->cfg.n[0], ny = ctx->cfg.n[1];
+  const Grid G = grid_of(ctx);
   const int g = grid_for(ctx->N);
   // device-resident FGMRES (f1): only the final write is gated; the two producer kernels
   // run unconditionally into work fields nobody reads when the gate is set
-  k_lap<<<g, NT, 0, ctx->stream>>>(v, nullptr, 1.0, ctx->mob_t[0], nx, ny, ctx->ih2);
-  k_combine<true><<<g, NT, 0, ctx->stream>>>(v, c, ctx->mob_t[0], ctx->mob_t[1], nx, ny, ctx->ih2,
+  k_lap<<<g, NT, 0, ctx->stream>>>(v, nullptr, 1.0, ctx->mob_t[0], G, ctx->ih2);
+  k_combine<true><<<g, NT, 0, ctx->stream>>>(v, c, ctx->mob_t[0], ctx->mob_t[1], G, ctx->ih2,
                                              ctx->cfg.gamma);
   k_jv_out<<<g, NT, 0, ctx->stream>>>(v, ctx->mob_t[1], ctx->mob_phi, ctx->mob_psi, ctx->mob_A,
-                                       out, nx, ny, ctx->ih2, 1.0 / dt, ctx->gate);
+                                       out, G, ctx->ih2, 1.0 / dt, ctx->gate);
   ctx->launches += 3;
   pfc_account(ctx, PFC_K_JV, 24.0 * ctx->N, 45.0 * ctx->N);
   return cudaGetLastError();

@@ -459,8 +459,6 @@ static pfc_status validate(const pfc_config& c, std::string* why) {
     return bad("ras_variant must be PFC_RAS_LEFT, PFC_RAS_AS or PFC_RAS_RIGHT");
   if (c.mobility != PFC_MOBILITY_ONE && c.mobility != PFC_MOBILITY_QUADRATIC)
     return bad("mobility must be PFC_MOBILITY_ONE or PFC_MOBILITY_QUADRATIC");
-  if (c.mobility == PFC_MOBILITY_QUADRATIC && c.ndim != 2)
-    return bad("PFC_MOBILITY_QUADRATIC is built for ndim == 2 only");
   if (c.gmres_restart < 1 || c.gmres_restart > PFC_MAX_RESTART) return bad("gmres_restart in [1,32]");
   if (c.gmres_maxit < 1 || c.newton_maxit < 0) return bad("iteration limits must be positive");
   if (!(c.newton_rtol >= 0 && c.newton_atol >= 0 && c.gmres_rtol >= 0 && c.gmres_atol >= 0))
@@ -531,7 +529,8 @@ pfc_status pfc_create(const pfc_config* cfg, void* stream, pfc_ctx** out) {
   if (c.ndim == 3) {
     int grid = 0;
     size_t d = 0;
-    ctx->ras3_col = getenv("PFC_RAS3D_V1") == nullptr && ras3d_col_plan(ctx, &d, &grid);
+    ctx->ras3_col = getenv("PFC_RAS3D_V1") == nullptr && !c.mobility &&
+                    ras3d_col_plan(ctx, &d, &grid);
     if (!ctx->ras3_col) d = ras3d_scratch_doubles(ctx, &grid);
     if (pfc_check_cuda(ctx, cudaMalloc(&ctx->ras_scratch, d * sizeof(double)), "ras scratch"))
       return fail(PFC_ENOMEM);

@@ -27,6 +27,11 @@ struct Ras3Args {
   int restrict_owned;   // right-RAS: R_k^0 (v zero outside the owned box)
   double* y_ext;        // AS / right-RAS: ext-box solutions [box][ext node] for (R_k^delta)^T
   const int* gate;   // device-resident FGMRES: skip the launch when *gate != 0 (f1)
+  // variable mobility (row f3): iterate Phi, psi and its A; A_k = R J R^T (reading R8b)
+  const double* phi;
+  const double* psi;
+  const double* A;
+  int mobility;
 };
 
 __global__ void __launch_bounds__(NT, 1) ras3d_kernel(Ras3Args p) {
@@ -48,6 +53,9 @@ __global__ void __launch_bounds__(NT, 1) ras3d_kernel(Ras3Args p) {
   double* pv = w + n;
   double* pl = pv + np;
   double* pb = pl + np;
+  double* pm = pb + np;      // mobility: M, A, u on the padded grid (scratch sized for them)
+  double* pa = pm + np;
+  double* pu = pa + np;
 
   if (p.gate && *p.gate) return;
   const int tid = threadIdx.x;
@@ -75,6 +83,20 @@ __global__ void __launch_bounds__(NT, 1) ras3d_kernel(Ras3Args p) {
       V[l] = vv;
       cl[l] = p.c[g];
       acc[0] += vv * vv;
+    }
+    if (p.mobility) {   // M = 1 - u^2, A, u of the iterate on the ext box and its +1 ring
+      for (int q = tid; q < np; q += NT) {
+        const int pi = q % Px, pj = (q / Px) % Py, pk = q / PP;
+        double m = 0.0, a = 0.0, u = 0.0;
+        if (pi >= 2 && pi < Px - 2 && pj >= 2 && pj < Py - 2 && pk >= 2 && pk < Pz - 2) {
+          const size_t g = (size_t)wrapi(gx0 + pi - 3, p.nx) + NX * wrapi(gy0 + pj - 3, p.ny) +
+                           NXY * wrapi(gz0 + pk - 3, p.nz);
+          u = 0.5 * (p.phi[g] + p.psi[g]);
+          m = 1.0 - u * u;
+          a = p.A[g];
+        }
+        pm[q] = m; pa[q] = a; pu[q] = u;
+      }
     }
     for (int q = tid; q < (k + 1) * k; q += NT) H[q] = 0.0;
     for (int q = tid; q < k + 1; q += NT) gv[q] = 0.0;
@@ -136,9 +158,24 @@ __global__ void __launch_bounds__(NT, 1) ras3d_kernel(Ras3Args p) {
       for (int l = tid; l < n; l += NT) {
         int li = l % Ex, lj = (l / Ex) % Ey, lk = l / (Ex * Ey);
         int f = (lk + 3) * PP + (lj + 3) * Px + li + 3;
-        double lapb = ih2 * ((pb[f - 1] + pb[f + 1]) + (pb[f - Px] + pb[f + Px]) +
-                             (pb[f - PP] + pb[f + PP]) - 6.0 * pb[f]);
-        double ww = pv[f] * idt - lapb;
+        double ww;
+        if (p.mobility) {   // v/dt - (grad . M grad) B - (grad . (-u v) grad) A
+          auto dmg = [&](const double* mm0, const double* g, bool dm) {
+            auto mm = [&](int q) { return dm ? -pu[q] * pv[q] : mm0[q]; };
+            const double mc = mm(f), gc = g[f];
+            double s = 0.0;
+            const int off[3] = {1, Px, PP};
+            for (int d = 0; d < 3; ++d)
+              s += 0.5 * (mc + mm(f + off[d])) * (g[f + off[d]] - gc) -
+                   0.5 * (mc + mm(f - off[d])) * (gc - g[f - off[d]]);
+            return ih2 * s;
+          };
+          ww = pv[f] * idt - dmg(pm, pb, false) - dmg(nullptr, pa, true);
+        } else {
+          double lapb = ih2 * ((pb[f - 1] + pb[f + 1]) + (pb[f - Px] + pb[f + Px]) +
+                               (pb[f - PP] + pb[f + PP]) - 6.0 * pb[f]);
+          ww = pv[f] * idt - lapb;
+        }
         w[l] = ww;
 #pragma unroll
         for (int i = 0; i <= KMAX; ++i)
@@ -228,7 +265,7 @@ size_t ras3d_scratch_per_cta(const pfc_config& c) {
   const size_t Ex = c.ras_box[0] + 2 * c.ras_overlap, Ey = c.ras_box[1] + 2 * c.ras_overlap,
                Ez = c.ras_box[2] + 2 * c.ras_overlap;
   const size_t n = Ex * Ey * Ez, np = (Ex + 6) * (Ey + 6) * (Ez + 6);
-  size_t d = (size_t)(c.ras_local_k + 1) * n + 2 * n + 3 * np;
+  size_t d = (size_t)(c.ras_local_k + 1) * n + 2 * n + (c.mobility ? 6 : 3) * np;
   return (d + 31) & ~size_t(31);
 }
 
@@ -258,7 +295,8 @@ cudaError_t launch_ras_3d(pfc_ctx* ctx, const double* v, const double* c, double
   Ras3Args p{v, c, z, scratch, ras3d_scratch_per_cta(cf), cf.n[0], cf.n[1], cf.n[2],
              cf.ras_box[0], cf.ras_box[1], cf.ras_box[2], cf.ras_overlap, cf.ras_local_k,
              1.0 / dt, cf.gamma, ctx->ih2, cf.ras_variant == PFC_RAS_RIGHT,
-             cf.ras_variant == PFC_RAS_LEFT ? nullptr : ctx->ras_y, ctx->gate};
+             cf.ras_variant == PFC_RAS_LEFT ? nullptr : ctx->ras_y, ctx->gate,
+             ctx->mob_phi, ctx->mob_psi, ctx->mob_A, cf.mobility};
   ras3d_kernel<<<grid, NT, 0, ctx->stream>>>(p);
   ctx->launches++;
   {

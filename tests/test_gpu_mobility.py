@@ -100,9 +100,49 @@ def test_mobility_one_step_parity_energy_mass():
     assert np.linalg.norm(O.residual_p(new, phi0, H, prm_m((16, 16)), dt)) <= 1e-8
 
 
+def ctx_m3(shape, box, o=1, k=4, **kw):
+    return P.Context(None, ndim=3, n=shape, h=H, gamma=G, ras_box=box, ras_overlap=o,
+                     ras_local_k=k, mobility=P.PFC_MOBILITY_QUADRATIC, **kw)
+
+
+@pytest.mark.parametrize("shape,box", [((32, 32, 32), (16, 16, 16)), ((24, 20, 18), (12, 10, 9))])
+def test_mobility_3d_operator_parity(shape, box):
+    phi = random_field(shape, 421, 0.07, 0.3)
+    psi = random_field(shape, 422, 0.07, 0.3)
+    v = random_field(shape, 423, 0.0, 1.0)
+    dt = 0.5
+    ctx = ctx_m3(shape, box)
+    prm = prm_m(box, o=1, k=4)
+    F = host(ctx.residual(dev(phi), dev(psi), dt))
+    assert rel(F, O.residual_p(phi, psi, H, prm, dt)) <= 1e-12
+    Jv = host(ctx.jacobian_apply(dev(phi), dev(psi), dt, dev(v)))
+    assert rel(Jv, O.jacobian_apply_p(phi, psi, v, H, prm, dt)) <= 1e-12
+
+
+@pytest.mark.parametrize("variant", [P.PFC_RAS_LEFT, P.PFC_RAS_AS])
+def test_mobility_3d_schwarz_parity(variant):
+    shape, box = (24, 24, 24), (8, 8, 8)
+    phi = random_field(shape, 431, -0.35, 0.05)
+    psi = random_field(shape, 432, -0.35, 0.05)
+    v = random_field(shape, 433, 0.0, 1.0)
+    ctx = ctx_m3(shape, box, ras_variant=variant)
+    z = host(ctx.ras_apply(dev(phi), dev(psi), 1.0, dev(v)))
+    zo = O.ras_apply(phi, psi, v, H, prm_m(box, o=1, k=4, ras_variant=variant), 1.0)
+    assert rel(z, zo) <= 1e-12
+
+
+def test_mobility_3d_one_step_parity():
+    shape, box = (16, 16, 16), (8, 8, 8)
+    phi0 = random_field(shape, 4, -0.35, 0.05)
+    ctx = ctx_m3(shape, box, k=10)
+    phi = dev(phi0)
+    _, info = ctx.step(phi, 1.0)
+    ref, ok, _ = O.newton(phi0, H, prm_m(box, o=1, k=10), 1.0)
+    assert ok and info["converged"]
+    assert rel(host(phi), ref) <= 1e-10
+    assert info["energy"] <= info["energy_old"]
+
+
 def test_mobility_argument_errors():
-    with pytest.raises(P.PfcError):   # built for 2D only
-        P.Context(None, ndim=3, n=(32, 32, 32), h=H, gamma=G, ras_box=(16, 16, 16),
-                  ras_overlap=2, mobility=P.PFC_MOBILITY_QUADRATIC)
     with pytest.raises(P.PfcError):
         P.Context(None, ndim=2, n=(64, 64), h=H, gamma=G, ras_box=(16, 16, 1), mobility=7)
