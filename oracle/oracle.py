@@ -34,10 +34,12 @@ class Params(C.Structure):
                 ("gmres_restart", C.c_int), ("gmres_maxit", C.c_int),
                 ("gmres_rtol", C.c_double), ("gmres_atol", C.c_double),
                 ("ras_box", C.c_int * 3), ("ras_overlap", C.c_int), ("ras_local_k", C.c_int),
-                ("ras_variant", C.c_int), ("mobility", C.c_int)]
+                ("ras_variant", C.c_int), ("mobility", C.c_int), ("ras_local_solver", C.c_int),
+                ("ras_ilu_level", C.c_int), ("ras_ilu_reuse", C.c_int)]
 
 RAS_LEFT, RAS_AS, RAS_RIGHT = 0, 1, 2
 MOB_ONE, MOB_QUADRATIC = 0, 1           # M = 1; M(phi) = 1 - phi^2
+LOCAL_GMRES, LOCAL_ILU = 0, 1           # R9; ILU(k) / LU (row f2)
 
 
 class NewtonInfo(C.Structure):
@@ -74,6 +76,7 @@ def lib():
         L.or_mobility.argtypes = [G, C.c_int, _P, _P, _P]
         L.or_residual_p.argtypes = [G, PR, C.c_double, _P, _P, _P]
         L.or_jacobian_apply_p.argtypes = [G, PR, C.c_double, _P, _P, _P, _P]
+        L.or_ilu_dense.argtypes = [C.c_int, _P, C.c_int, _P]
         L.or_next_dt.argtypes = [C.c_double] * 6
         L.or_next_dt.restype = C.c_double
     return _lib
@@ -100,11 +103,12 @@ def _shape(a):
 def params(gamma=0.25, newton_rtol=1e-10, newton_atol=1e-10, newton_maxit=50, ls_c1=1e-4,
            ls_min_lambda=1e-12, gmres_restart=30, gmres_maxit=300, gmres_rtol=1e-3,
            gmres_atol=1e-11, ras_box=(16, 16, 1), ras_overlap=2, ras_local_k=10, ras_variant=0,
-           mobility=0, **_ignored):
+           mobility=0, ras_local_solver=0, ras_ilu_level=0, ras_ilu_reuse=0, **_ignored):
     b = list(ras_box) + [1] * (3 - len(ras_box))
     return Params(gamma, newton_rtol, newton_atol, newton_maxit, ls_c1, ls_min_lambda,
                   gmres_restart, gmres_maxit, gmres_rtol, gmres_atol, (C.c_int * 3)(*b),
-                  ras_overlap, ras_local_k, ras_variant, mobility)
+                  ras_overlap, ras_local_k, ras_variant, mobility, ras_local_solver,
+                  ras_ilu_level, ras_ilu_reuse)
 
 
 def params_from_config(cfg, **over):
@@ -112,7 +116,10 @@ def params_from_config(cfg, **over):
               newton_maxit=cfg.newton_maxit, gmres_restart=cfg.gmres_restart,
               gmres_maxit=cfg.gmres_maxit, gmres_rtol=cfg.gmres_rtol, gmres_atol=cfg.gmres_atol,
               ras_box=cfg.ras_box, ras_overlap=cfg.ras_overlap, ras_local_k=cfg.ras_local_k,
-              ras_variant=getattr(cfg, "ras_variant", 0), mobility=getattr(cfg, "mobility", 0))
+              ras_variant=getattr(cfg, "ras_variant", 0), mobility=getattr(cfg, "mobility", 0),
+              ras_local_solver=getattr(cfg, "ras_local_solver", 0),
+              ras_ilu_level=getattr(cfg, "ras_ilu_level", 0),
+              ras_ilu_reuse=getattr(cfg, "ras_ilu_reuse", 0))
     kw.update(over)
     return params(**kw)
 
@@ -167,6 +174,15 @@ def jacobian_apply_p(phi_new, phi_old, v, h, prm, dt):
     lib().or_jacobian_apply_p(C.byref(_grid(_shape(a), h)), C.byref(prm), dt, _ptr(a), _ptr(b),
                               _ptr(v), _ptr(out))
     return out
+
+
+def ilu_dense(A, level):
+    """ILU(level) of a dense matrix on the pattern of its nonzeros (combined L\\U factors)."""
+    A = np.ascontiguousarray(A, dtype=np.float64)
+    n = A.shape[0]
+    LU = np.empty_like(A)
+    lib().or_ilu_dense(n, _ptr(A), int(level), _ptr(LU))
+    return LU
 
 
 def local_energy(phi, h, gamma):

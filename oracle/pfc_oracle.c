@@ -333,6 +333,72 @@ void or_local_jacobian_apply(const or_grid* g, const or_params* p, double dt,
   free(pv); free(L1); free(L2); free(dA); free(L3);
 }
 
+/* --------------------------------------------- ILU(k) subdomain solves, row f2
+ * The paper's subdomain solvers (Table 1): incomplete LU with fill level
+ * k of the subdomain matrix A_k in the natural (x-fastest) order of the ext box, LU being the
+ * unlimited-fill case; the preconditioner applies U^{-1} L^{-1} per box.  Fill levels by the
+ * standard rule lev(i,j) = min over k < min(i,j) of lev(i,k) + lev(k,j) + 1, nonzeros of A at
+ * level 0; entries with lev <= k are kept.  The numeric factorisation is the IKJ variant. */
+
+/* factor pattern of a sparse matrix given by a dense nonzero mask (row-major n x n): returns
+ * lev[n*n] (-1 = not in the pattern) */
+static int* ilu_levels(int n, const unsigned char* nz, int level) {
+  int* lev = (int*)malloc((size_t)n * n * sizeof(int));
+  for (size_t q = 0; q < (size_t)n * n; ++q) lev[q] = nz[q] ? 0 : -1;
+  for (int i = 0; i < n; ++i)
+    for (int k = 0; k < i; ++k) {
+      int lik = lev[(size_t)i * n + k];
+      if (lik < 0) continue;
+      for (int j = k + 1; j < n; ++j) {
+        int lkj = lev[(size_t)k * n + j];
+        if (lkj < 0) continue;
+        int l = lik + lkj + 1;
+        if (l > level) continue;
+        int* lij = &lev[(size_t)i * n + j];
+        if (*lij < 0 || l < *lij) *lij = l;
+      }
+    }
+  return lev;
+}
+
+/* IKJ incomplete LU on the kept pattern, in place on a dense row-major copy */
+static void ilu_numeric(int n, const int* lev, double* a) {
+  for (int i = 1; i < n; ++i)
+    for (int k = 0; k < i; ++k) {
+      if (lev[(size_t)i * n + k] < 0) continue;
+      a[(size_t)i * n + k] /= a[(size_t)k * n + k];
+      double lik = a[(size_t)i * n + k];
+      for (int j = k + 1; j < n; ++j)
+        if (lev[(size_t)i * n + j] >= 0 && lev[(size_t)k * n + j] >= 0)
+          a[(size_t)i * n + j] -= lik * a[(size_t)k * n + j];
+    }
+  for (size_t q = 0; q < (size_t)n * n; ++q)
+    if (lev[q] < 0) a[q] = 0.0;
+}
+
+void or_ilu_dense(int n, const double* A, int level, double* LU) {
+  unsigned char* nz = (unsigned char*)malloc((size_t)n * n);
+  for (size_t q = 0; q < (size_t)n * n; ++q) nz[q] = A[q] != 0.0;
+  int* lev = ilu_levels(n, nz, level);
+  memcpy(LU, A, (size_t)n * n * sizeof(double));
+  ilu_numeric(n, lev, LU);
+  free(lev); free(nz);
+}
+
+/* y = U^{-1} L^{-1} r with the combined dense factors */
+static void ilu_solve(int n, const double* LU, const double* r, double* y) {
+  for (int i = 0; i < n; ++i) {
+    double s = r[i];
+    for (int k = 0; k < i; ++k) s -= LU[(size_t)i * n + k] * y[k];
+    y[i] = s;
+  }
+  for (int i = n - 1; i >= 0; --i) {
+    double s = y[i];
+    for (int j = i + 1; j < n; ++j) s -= LU[(size_t)i * n + j] * y[j];
+    y[i] = s / LU[(size_t)i * n + i];
+  }
+}
+
 /* Givens rotation zeroing b in (a, b): r = sqrt(a^2 + b^2), c = a/r, s = b/r. */
 static void givens(double a, double b, double* c, double* s) {
   double r = sqrt(a * a + b * b);
@@ -430,6 +496,30 @@ static void local_gmres(const local_op* L, const double* r, double* y, size_t n)
   free(yy); free(V); free(w); free(H); free(cs); free(sn); free(gv); free(h2);
 }
 
+/* inv(A_k) r by ILU(level) of the assembled A_k (row f2): A_k column q = the local operator
+ * applied to the unit vector e_q (Eq. Ak P:422-428 with the modified BC, or R J R^T with
+ * variable mobility), dense storage (test sizes). */
+static void local_ilu(const local_op* L, const double* r, double* y, size_t n) {
+  double* A = alloc0(n * n);
+  double* e = alloc0(n);
+  double* col = alloc0(n);
+  for (size_t q = 0; q < n; ++q) {
+    e[q] = 1.0;
+    local_apply(L, e, col);
+    for (size_t i = 0; i < n; ++i) A[i * n + q] = col[i];
+    e[q] = 0.0;
+  }
+  double* LU = alloc0(n * n);
+  or_ilu_dense((int)n, A, L->p->ras_ilu_level, LU);
+  ilu_solve((int)n, LU, r, y);
+  free(A); free(e); free(col); free(LU);
+}
+
+static void local_solve(const local_op* L, const double* r, double* y, size_t n) {
+  if (L->p->ras_local_solver == 1) local_ilu(L, r, y, n);
+  else local_gmres(L, r, y, n);
+}
+
 /* Additive Schwarz preconditioners, selected by p->ras_variant:
  *   0  left-RAS      z = sum_k (R_k^0)^T     inv(A_k) R_k^delta v    Eq. (eq:ras)
  *   1  classical AS  z = sum_k (R_k^delta)^T inv(A_k) R_k^delta v    Eq. (invM)
@@ -471,7 +561,7 @@ void or_ras_apply(const or_grid* g, const or_params* p, double dt, const double*
               c[l] = (3.0 * pn[q] * pn[q] + 2.0 * pn[q] * po[q] + po[q] * po[q]) / 4.0;
             }
         local_op L = {g, p, dt, c, pn, po, x0, y0, z0, {E[0], E[1], E[2]}};
-        local_gmres(&L, r, y, n);
+        local_solve(&L, r, y, n);
         if (extend_owned) {
           for (int k = o[2]; k < o[2] + b[2]; ++k)   /* (R_k^0)^T: owned nodes only */
             for (int j = o[1]; j < o[1] + b[1]; ++j)
@@ -519,7 +609,7 @@ void or_ras_apply_box(const or_grid* g, const or_params* p, double dt, const dou
         c[l] = (3.0 * pn[q] * pn[q] + 2.0 * pn[q] * po[q] + po[q] * po[q]) / 4.0;
       }
   local_op L = {g, p, dt, c, pn, po, x0, y0, z0, {E[0], E[1], E[2]}};
-  local_gmres(&L, r, y, n);
+  local_solve(&L, r, y, n);
   for (int k = 0; k < b[2]; ++k)
     for (int j = 0; j < b[1]; ++j)
       for (int i = 0; i < b[0]; ++i) {
@@ -566,7 +656,10 @@ int or_fgmres(const or_grid* g, const or_params* p, double dt, const double* pn,
     int jm = 0, stop = 0;
     for (int j = 0; j < m; ++j) {
       double* zj = Z + (size_t)j * N;
-      if (precondition) or_ras_apply(g, p, dt, pn, po, V + (size_t)j * N, zj);
+      /* ILU with reuse (R10): the subdomain matrices of the step's first Newton
+       * iteration, Phi_0 = psi */
+      const double* pre = (p->ras_local_solver == 1 && p->ras_ilu_reuse) ? po : pn;
+      if (precondition) or_ras_apply(g, p, dt, pre, po, V + (size_t)j * N, zj);
       else memcpy(zj, V + (size_t)j * N, N * sizeof(double));
       or_jacobian_apply_p(g, p, dt, pn, po, zj, w);
       for (int pass = 0; pass < 2; ++pass) {

@@ -30,6 +30,9 @@ typedef struct {
   int ras_box[3], ras_overlap, ras_local_k;  /* Schwarz boxes, local GMRES(k) (R9) */
   int ras_variant;  /* 0 left-RAS, 1 classical AS, 2 right-RAS */
   int mobility;     /* 0: M = 1 (the configs); 1: M(phi) = 1 - phi^2 */
+  int ras_local_solver;  /* 0: fixed-work local GMRES (R9); 1: ILU(level) (row f2) */
+  int ras_ilu_level;     /* fill level k of ILU(k) (Table 1); >= n gives LU */
+  int ras_ilu_reuse;     /* 1: subdomain factors of the step's first Newton iteration */
 } or_params;
 
 typedef struct {
@@ -67,6 +70,10 @@ void or_ras_apply(const or_grid* g, const or_params* p, double dt, const double*
                   const double* phi_old, const double* v, double* z);  /* p->ras_variant */
 void or_ras_apply_box(const or_grid* g, const or_params* p, double dt, const double* phi_new,
                       const double* phi_old, const double* v, int box, double* z_owned);
+
+/* ILU(k) of a dense n x n matrix with the pattern of its nonzeros (tests of row f2): the
+ * combined factors (unit-lower L below the diagonal, U on and above) written to LU. */
+void or_ilu_dense(int n, const double* A, int level, double* LU);
 
 /* Krylov, Newton and time step control */
 int or_fgmres(const or_grid* g, const or_params* p, double dt, const double* phi_new,
