@@ -146,11 +146,16 @@ def bench_cuda(args):
     if ws > 1:
         dist.barrier()
     cfg = CONFIGS[args.config]
-    if args.mobility or args.ras_variant:   # NEXT-row measurements (not the headline line)
+    if args.mobility or args.ras_variant or args.ilu >= 0:   # NEXT-row measurements
         import dataclasses
+        ilu = args.ilu >= 0
         cfg = dataclasses.replace(cfg, mobility=args.mobility, ras_variant=args.ras_variant,
+                                  ras_local_solver=1 if ilu else 0,
+                                  ras_ilu_level=max(args.ilu, 0), ras_ilu_reuse=args.ilu_reuse,
                                   name=cfg.name + (f"_mobility{args.mobility}" if args.mobility else "")
-                                  + (f"_ras{args.ras_variant}" if args.ras_variant else ""))
+                                  + (f"_ras{args.ras_variant}" if args.ras_variant else "")
+                                  + (f"_ilu{args.ilu}" + ("reuse" if args.ilu_reuse else "")
+                                     if ilu else ""))
     W, K = args.warmup, args.steps
     phi0 = cfg.initial_condition()
     ctx = P.Context(cfg)
@@ -343,11 +348,16 @@ def bench_reference(args):
     from paper_1703_01202_b200.inputs import CONFIGS
     O.build()
     cfg = CONFIGS[args.config]
-    if args.mobility or args.ras_variant:   # NEXT-row measurements (not the headline line)
+    if args.mobility or args.ras_variant or args.ilu >= 0:   # NEXT-row measurements
         import dataclasses
+        ilu = args.ilu >= 0
         cfg = dataclasses.replace(cfg, mobility=args.mobility, ras_variant=args.ras_variant,
+                                  ras_local_solver=1 if ilu else 0,
+                                  ras_ilu_level=max(args.ilu, 0), ras_ilu_reuse=args.ilu_reuse,
                                   name=cfg.name + (f"_mobility{args.mobility}" if args.mobility else "")
-                                  + (f"_ras{args.ras_variant}" if args.ras_variant else ""))
+                                  + (f"_ras{args.ras_variant}" if args.ras_variant else "")
+                                  + (f"_ilu{args.ilu}" + ("reuse" if args.ilu_reuse else "")
+                                     if ilu else ""))
     W, K = args.warmup, args.steps
     phi = cfg.initial_condition()
     prm = O.params_from_config(cfg)
@@ -391,6 +401,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--mobility", type=int, default=0, help="1: M = 1 - phi^2 (row f3, 2D)")
     ap.add_argument("--ras-variant", type=int, default=0, help="0 left-RAS, 1 AS, 2 right-RAS")
+    ap.add_argument("--ilu", type=int, default=-1, help="k >= 0: ILU(k) subdomain solves (row f2)")
+    ap.add_argument("--ilu-reuse", type=int, default=0, help="1: factors reused over a step")
     args = ap.parse_args()
     if args.warmup < 3:
         print("note: --warmup < 3 is below the timing contract", file=sys.stderr)

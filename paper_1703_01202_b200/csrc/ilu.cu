@@ -1,0 +1,397 @@
+// ilu.cu -- ILU(k) subdomain solves of the Schwarz preconditioner (NEXT row f2), sm_100a.
+//
+// The paper's subdomain solvers (Table 1): incomplete LU with fill level
+// k of A_k in the natural (x-fastest) order of the extended box, with the option of reusing
+// the factors of the step's first Newton iteration (reading R10).  A_k is the
+// zero-ring subdomain matrix (= R J R^T for M = 1, reading R8):
+//   A_ij = W[class(x_j - x_i)] + (j == i ? 2d h^-2 c_i : |x_j - x_i|_1 == 1 ? -h^-2 c_j : 0)
+// with W the class weights of v/dt - alpha Delta v - Delta^2 v - Delta^3 v / 2 (the 25 / 63
+// point radius-3 stencil truncated at the box) and the second term from -Delta(c v).
+//
+// Everything structural is built once on the host at pfc_create, identical for every box: the
+// pattern of A (the truncated stencil), the ILU(k) fill pattern by the standard level rule,
+// the IKJ operation list of each row (divide a_ik by a_kk, then a_ij -= a_ik a_kj for the kept
+// j > k), and the level schedules of the factorisation / forward solve (a row depends on its
+// L entries) and of the backward solve (on its U entries).  The device then runs, one CTA per
+// box, (1) the numeric factorisation into the box's value array, level by level, one warp per
+// row (lane 0 divides, the lanes apply that k's updates in parallel: distinct a_ij), and (2) per
+// preconditioner apply, the forward and backward solves, level by level, one thread per row,
+// in shared memory.  Same operations as the oracle (or_ilu_dense / ilu_solve) per entry; the
+// parallel order only regroups independent updates and the triangular-solve dot products.
+#include "pfc_device.cuh"
+#include "pfc_internal.h"
+
+#include <algorithm>
+#include <map>
+#include <vector>
+
+namespace {
+
+constexpr int NT = 512;
+
+int wclass(int a, int b, int c) {   // class of the sorted |offset|: 000 001 002 011 003 012 111
+  const int s = a + b + c;
+  if (s == 0) return 0;
+  if (s == 1) return 1;
+  if (s == 2) return (a == 2 || b == 2 || c == 2) ? 2 : 3;
+  if (a == 3 || b == 3 || c == 3) return 4;
+  return (a == 1 && b == 1 && c == 1) ? 6 : 5;
+}
+
+struct IluArgs {
+  const double* v;      // apply: input field
+  const double* c;      // factor: Jacobian coefficient field
+  double* z;            // apply: output (owned nodes) or nullptr with y_ext
+  double* y_ext;        // AS / right-RAS: ext-box solutions [box][ext node]
+  double* vals;         // [box][nnz] factor values
+  const int* rowptr;    // CSR of the factor pattern
+  const int* col;
+  const int* diag;      // position of a_ii
+  const int* ecls;      // per entry: linear-weight class, -1 for fill
+  const int* ectype;    // per entry: 0 none, 1 -h^-2 c_j, 2 +2d h^-2 c_i
+  const int* opptr;     // per row: ops [opptr[i], opptr[i+1])
+  const int* opk;       // op: k (divide a_ik by a_kk) ...
+  const int* oppos;     // ... pos_ik for the divide, then pairs (pos_kj, pos_ij)
+  const int* flev_ptr;  // forward / factorisation levels
+  const int* flev_row;
+  const int* blev_ptr;  // backward levels
+  const int* blev_row;
+  int nflev, nblev, n, nnz;
+  int nx, ny, nz, bx, by, bz, o, nd;
+  double W[7];
+  double ih2;
+  int restrict_owned;
+  const int* gate;
+};
+
+__device__ __forceinline__ void box_origin(const IluArgs& p, int box, int& gx0, int& gy0,
+                                           int& gz0, int& ibx, int& iby, int& ibz) {
+  const int nbx = p.nx / p.bx, nby = p.ny / p.by;
+  ibx = box % nbx; iby = (box / nbx) % nby; ibz = box / (nbx * nby);
+  gx0 = ibx * p.bx - p.o; gy0 = iby * p.by - p.o; gz0 = p.nd == 3 ? ibz * p.bz - p.o : 0;
+}
+
+__device__ __forceinline__ size_t gnode(const IluArgs& p, int l, int gx0, int gy0, int gz0) {
+  const int Ex = p.bx + 2 * p.o, Ey = p.by + 2 * p.o;
+  const int li = l % Ex, lj = (l / Ex) % Ey, lk = l / (Ex * Ey);
+  return (size_t)wrapi(gx0 + li, p.nx) + (size_t)p.nx * wrapi(gy0 + lj, p.ny) +
+         (size_t)p.nx * p.ny * (p.nd == 3 ? wrapi(gz0 + lk, p.nz) : 0);
+}
+
+// numeric ILU(k) of every box: A values from the class weights and c, then IKJ by levels
+__global__ void __launch_bounds__(NT) k_ilu_factor(const IluArgs p) {
+  const int box = blockIdx.x;
+  int gx0, gy0, gz0, ibx, iby, ibz;
+  box_origin(p, box, gx0, gy0, gz0, ibx, iby, ibz);
+  double* a = p.vals + (size_t)box * p.nnz;
+  const int d2 = 2 * p.nd;
+  for (int i = threadIdx.x; i < p.n; i += NT) {
+    const double ci = p.c[gnode(p, i, gx0, gy0, gz0)];
+    for (int q = p.rowptr[i]; q < p.rowptr[i + 1]; ++q) {
+      const int cl = p.ecls[q], ct = p.ectype[q];
+      double val = cl >= 0 ? p.W[cl] : 0.0;
+      if (ct == 2) val += d2 * p.ih2 * ci;
+      else if (ct == 1) val -= p.ih2 * p.c[gnode(p, p.col[q], gx0, gy0, gz0)];
+      a[q] = val;
+    }
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int L = 0; L < p.nflev; ++L) {
+    for (int r = p.flev_ptr[L] + wid; r < p.flev_ptr[L + 1]; r += NT / 32) {
+      const int i = p.flev_row[r];
+      int q = p.opptr[i];
+      const int qe = p.opptr[i + 1];
+      while (q < qe) {                 // one k: [k, pos_ik, nupd, (pos_kj, pos_ij) x nupd]
+        const int k = p.opk[q];
+        const int pik = p.oppos[q];
+        const int nup = p.opk[q + 1];
+        double lik = 0.0;
+        if (lane == 0) {
+          lik = a[pik] / a[p.diag[k]];
+          a[pik] = lik;
+        }
+        lik = __shfl_sync(0xffffffffu, lik, 0);
+        for (int u = lane; u < nup; u += 32) {
+          const int pkj = p.oppos[q + 1 + 2 * u], pij = p.oppos[q + 2 + 2 * u];
+          a[pij] -= lik * a[pkj];
+        }
+        __syncwarp();
+        q += 2 + 2 * nup;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// z = sum_k (R_k^0)^T U^{-1} L^{-1} R_k^delta v (left-RAS) or the ext-box solutions
+__global__ void __launch_bounds__(NT) k_ilu_apply(const IluArgs p) {
+  extern __shared__ double y[];
+  if (p.gate && *p.gate) return;
+  const int box = blockIdx.x;
+  int gx0, gy0, gz0, ibx, iby, ibz;
+  box_origin(p, box, gx0, gy0, gz0, ibx, iby, ibz);
+  const double* a = p.vals + (size_t)box * p.nnz;
+  const int Ex = p.bx + 2 * p.o, Ey = p.by + 2 * p.o;
+  for (int l = threadIdx.x; l < p.n; l += NT) {
+    const int li = l % Ex, lj = (l / Ex) % Ey, lk = l / (Ex * Ey);
+    const bool owned = li >= p.o && li < p.o + p.bx && lj >= p.o && lj < p.o + p.by &&
+                       (p.nd == 2 || (lk >= p.o && lk < p.o + p.bz));
+    y[l] = (p.restrict_owned && !owned) ? 0.0 : p.v[gnode(p, l, gx0, gy0, gz0)];
+  }
+  __syncthreads();
+  for (int L = 0; L < p.nflev; ++L) {          // L y = r (unit lower)
+    for (int r = p.flev_ptr[L] + threadIdx.x; r < p.flev_ptr[L + 1]; r += NT) {
+      const int i = p.flev_row[r];
+      double s = y[i];
+      for (int q = p.rowptr[i]; q < p.diag[i]; ++q) s -= a[q] * y[p.col[q]];
+      y[i] = s;
+    }
+    __syncthreads();
+  }
+  for (int L = 0; L < p.nblev; ++L) {          // U x = y
+    for (int r = p.blev_ptr[L] + threadIdx.x; r < p.blev_ptr[L + 1]; r += NT) {
+      const int i = p.blev_row[r];
+      double s = y[i];
+      for (int q = p.diag[i] + 1; q < p.rowptr[i + 1]; ++q) s -= a[q] * y[p.col[q]];
+      y[i] = s / a[p.diag[i]];
+    }
+    __syncthreads();
+  }
+  if (p.y_ext) {
+    for (int l = threadIdx.x; l < p.n; l += NT) p.y_ext[(size_t)box * p.n + l] = y[l];
+    return;
+  }
+  const int nown = p.bx * p.by * (p.nd == 3 ? p.bz : 1);
+  for (int l = threadIdx.x; l < nown; l += NT) {
+    const int li = l % p.bx, lj = (l / p.bx) % p.by, lk = l / (p.bx * p.by);
+    const int e = (li + p.o) + Ex * ((lj + p.o) + Ey * (p.nd == 3 ? lk + p.o : 0));
+    p.z[(size_t)(ibx * p.bx + li) + (size_t)p.nx * (iby * p.by + lj) +
+        (size_t)p.nx * p.ny * (p.nd == 3 ? ibz * p.bz + lk : 0)] = y[e];
+  }
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------- host: symbolic setup
+
+struct pfc_ilu {
+  int n = 0, nnz = 0, nflev = 0, nblev = 0;
+  int* d_rowptr = nullptr; int* d_col = nullptr; int* d_diag = nullptr;
+  int* d_ecls = nullptr; int* d_ectype = nullptr;
+  int* d_opptr = nullptr; int* d_opk = nullptr; int* d_oppos = nullptr;
+  int* d_flev_ptr = nullptr; int* d_flev_row = nullptr;
+  int* d_blev_ptr = nullptr; int* d_blev_row = nullptr;
+  double* d_vals = nullptr;
+  size_t nbox = 0;
+};
+
+static bool up(pfc_ctx* ctx, int** d, const std::vector<int>& h) {
+  if (cudaMalloc(d, std::max<size_t>(h.size(), 1) * sizeof(int)) != cudaSuccess) return false;
+  return cudaMemcpy(*d, h.data(), h.size() * sizeof(int), cudaMemcpyHostToDevice) == cudaSuccess;
+}
+
+pfc_status ilu_setup(pfc_ctx* ctx) {
+  const pfc_config& c = ctx->cfg;
+  const int nd = c.ndim;
+  int E[3] = {1, 1, 1};
+  for (int d = 0; d < nd; ++d) E[d] = c.ras_box[d] + 2 * c.ras_overlap;
+  const int n = E[0] * E[1] * E[2];
+  auto pos = [&](int i, int j, int k) { return i + E[0] * (j + E[1] * k); };
+  // pattern of A: the radius-3 L1 stencil truncated at the box, per row a map col -> level
+  std::vector<std::map<int, int>> rows(n);
+  std::vector<std::map<int, std::pair<int, int>>> meta(n);   // col -> (class, ctype)
+  const int R = 3;
+  for (int k = 0; k < E[2]; ++k)
+    for (int j = 0; j < E[1]; ++j)
+      for (int i = 0; i < E[0]; ++i) {
+        const int r = pos(i, j, k);
+        for (int dz = (nd == 3 ? -R : 0); dz <= (nd == 3 ? R : 0); ++dz)
+          for (int dy = -R; dy <= R; ++dy)
+            for (int dx = -R; dx <= R; ++dx) {
+              const int ax = std::abs(dx), ay = std::abs(dy), az = std::abs(dz);
+              if (ax + ay + az > R) continue;
+              const int ii = i + dx, jj = j + dy, kk = k + dz;
+              if (ii < 0 || ii >= E[0] || jj < 0 || jj >= E[1] || kk < 0 || kk >= E[2]) continue;
+              int s[3] = {ax, ay, az};
+              std::sort(s, s + 3);
+              const int cl = wclass(s[0], s[1], s[2]);
+              const int ct = (ax + ay + az == 0) ? 2 : (ax + ay + az == 1) ? 1 : 0;
+              rows[r][pos(ii, jj, kk)] = 0;
+              meta[r][pos(ii, jj, kk)] = {cl, ct};
+            }
+      }
+  // ILU(k) fill levels, row by row (rows k < i are final when row i is processed)
+  const int level = c.ras_ilu_level;
+  for (int i = 0; i < n; ++i) {
+    auto& ri = rows[i];
+    for (auto it = ri.begin(); it != ri.end() && it->first < i; ++it) {
+      const int kk = it->first, lik = it->second;
+      for (auto jt = rows[kk].upper_bound(kk); jt != rows[kk].end(); ++jt) {
+        const int l = lik + jt->second + 1;
+        if (l > level) continue;
+        auto f = ri.find(jt->first);
+        if (f == ri.end()) ri[jt->first] = l;          // new fill (j > k: visited later if < i)
+        else if (l < f->second) f->second = l;
+      }
+    }
+  }
+  // CSR
+  std::vector<int> rowptr(n + 1, 0), col, diag(n), ecls, ectype;
+  std::vector<std::map<int, int>> where(n);
+  for (int i = 0; i < n; ++i) {
+    for (auto& e : rows[i]) {
+      where[i][e.first] = (int)col.size();
+      if (e.first == i) diag[i] = (int)col.size();
+      col.push_back(e.first);
+      auto m = meta[i].find(e.first);
+      ecls.push_back(m == meta[i].end() ? -1 : m->second.first);
+      ectype.push_back(m == meta[i].end() ? 0 : m->second.second);
+    }
+    rowptr[i + 1] = (int)col.size();
+  }
+  const int nnz = (int)col.size();
+  // IKJ op list per row: [k, pos_ik] + [nupd] then pairs (pos_kj, pos_ij) -- encoded in two
+  // parallel arrays opk / oppos: opk[q] = k, oppos[q] = pos_ik, opk[q+1] = nupd, then oppos
+  // holds the pairs from q+1 on
+  std::vector<int> opptr(n + 1, 0), opk, oppos;
+  std::vector<int> flev(n, 0), blev(n, 0);
+  for (int i = 0; i < n; ++i) {
+    for (auto it = rows[i].begin(); it != rows[i].end() && it->first < i; ++it) {
+      const int kk = it->first;
+      flev[i] = std::max(flev[i], flev[kk] + 1);
+      std::vector<int> pairs;
+      for (auto jt = rows[kk].upper_bound(kk); jt != rows[kk].end(); ++jt) {
+        auto w = where[i].find(jt->first);
+        if (w == where[i].end()) continue;
+        pairs.push_back(where[kk][jt->first]);
+        pairs.push_back(w->second);
+      }
+      const size_t q = opk.size();
+      const int nup = (int)pairs.size() / 2;
+      opk.resize(q + 2 + 2 * nup, 0);
+      oppos.resize(q + 2 + 2 * nup, 0);
+      opk[q] = kk;
+      oppos[q] = where[i][kk];
+      opk[q + 1] = nup;
+      for (int u = 0; u < 2 * nup; ++u) oppos[q + 1 + u] = pairs[u];
+    }
+    opptr[i + 1] = (int)opk.size();
+  }
+  for (int i = n - 1; i >= 0; --i)
+    for (auto jt = rows[i].upper_bound(i); jt != rows[i].end(); ++jt)
+      blev[i] = std::max(blev[i], blev[jt->first] + 1);
+  auto group = [&](const std::vector<int>& lev, std::vector<int>& ptr, std::vector<int>& rr) {
+    const int nl = *std::max_element(lev.begin(), lev.end()) + 1;
+    ptr.assign(nl + 1, 0);
+    for (int i = 0; i < n; ++i) ptr[lev[i] + 1]++;
+    for (int l = 0; l < nl; ++l) ptr[l + 1] += ptr[l];
+    rr.assign(n, 0);
+    std::vector<int> fill(ptr.begin(), ptr.end() - 1);
+    for (int i = 0; i < n; ++i) rr[fill[lev[i]]++] = i;
+    return nl;
+  };
+  std::vector<int> fptr, frow, bptr, brow;
+  pfc_ilu* I = new pfc_ilu();
+  ctx->ilu = I;
+  I->n = n; I->nnz = nnz;
+  I->nflev = group(flev, fptr, frow);
+  I->nblev = group(blev, bptr, brow);
+  I->nbox = 1;
+  for (int d = 0; d < nd; ++d) I->nbox *= (size_t)(c.n[d] / c.ras_box[d]);
+  if (!up(ctx, &I->d_rowptr, rowptr) || !up(ctx, &I->d_col, col) || !up(ctx, &I->d_diag, diag) ||
+      !up(ctx, &I->d_ecls, ecls) || !up(ctx, &I->d_ectype, ectype) ||
+      !up(ctx, &I->d_opptr, opptr) || !up(ctx, &I->d_opk, opk) || !up(ctx, &I->d_oppos, oppos) ||
+      !up(ctx, &I->d_flev_ptr, fptr) || !up(ctx, &I->d_flev_row, frow) ||
+      !up(ctx, &I->d_blev_ptr, bptr) || !up(ctx, &I->d_blev_row, brow) ||
+      cudaMalloc(&I->d_vals, I->nbox * nnz * sizeof(double)) != cudaSuccess)
+    return pfc_fail(ctx, PFC_ENOMEM, "ILU structures");
+  if ((size_t)n * sizeof(double) > 200 * 1024)
+    return pfc_fail(ctx, PFC_EINVAL, "ILU: ext box too large for the shared-memory solve");
+  return PFC_OK;
+}
+
+void ilu_free(pfc_ctx* ctx) {
+  pfc_ilu* I = ctx->ilu;
+  if (!I) return;
+  int* a[] = {I->d_rowptr, I->d_col, I->d_diag, I->d_ecls, I->d_ectype, I->d_opptr, I->d_opk,
+              I->d_oppos, I->d_flev_ptr, I->d_flev_row, I->d_blev_ptr, I->d_blev_row};
+  for (int* p : a)
+    if (p) cudaFree(p);
+  if (I->d_vals) cudaFree(I->d_vals);
+  delete I;
+  ctx->ilu = nullptr;
+}
+
+static IluArgs ilu_args(pfc_ctx* ctx, double dt) {
+  const pfc_config& cf = ctx->cfg;
+  pfc_ilu* I = ctx->ilu;
+  IluArgs p{};
+  p.vals = I->d_vals; p.rowptr = I->d_rowptr; p.col = I->d_col; p.diag = I->d_diag;
+  p.ecls = I->d_ecls; p.ectype = I->d_ectype; p.opptr = I->d_opptr; p.opk = I->d_opk;
+  p.oppos = I->d_oppos; p.flev_ptr = I->d_flev_ptr; p.flev_row = I->d_flev_row;
+  p.blev_ptr = I->d_blev_ptr; p.blev_row = I->d_blev_row;
+  p.nflev = I->nflev; p.nblev = I->nblev; p.n = I->n; p.nnz = I->nnz;
+  p.nx = cf.n[0]; p.ny = cf.n[1]; p.nz = cf.ndim == 3 ? cf.n[2] : 1;
+  p.bx = cf.ras_box[0]; p.by = cf.ras_box[1]; p.bz = cf.ndim == 3 ? cf.ras_box[2] : 1;
+  p.o = cf.ras_overlap; p.nd = cf.ndim;
+  const double ih2 = ctx->ih2, ih4 = ih2 * ih2, ih6 = ih4 * ih2, al = 0.5 * (1.0 - cf.gamma);
+  if (cf.ndim == 2) {   // class weights of the linear part (as in ras2d.cu)
+    p.W[0] = 1.0 / dt + 4.0 * al * ih2 - 20.0 * ih4 + 56.0 * ih6;
+    p.W[1] = -al * ih2 + 8.0 * ih4 - 28.5 * ih6;
+    p.W[2] = -ih4 + 6.0 * ih6;
+    p.W[3] = -2.0 * ih4 + 12.0 * ih6;
+    p.W[4] = -0.5 * ih6;
+    p.W[5] = -1.5 * ih6;
+    p.W[6] = 0.0;
+  } else {              // as in ras3d_col.cu
+    p.W[0] = 1.0 / dt + 6.0 * al * ih2 - 42.0 * ih4 + 162.0 * ih6;
+    p.W[1] = -al * ih2 + 12.0 * ih4 - 61.5 * ih6;
+    p.W[2] = -ih4 + 9.0 * ih6;
+    p.W[3] = -2.0 * ih4 + 18.0 * ih6;
+    p.W[4] = -0.5 * ih6;
+    p.W[5] = -1.5 * ih6;
+    p.W[6] = -3.0 * ih6;
+  }
+  p.ih2 = ih2;
+  p.restrict_owned = cf.ras_variant == PFC_RAS_RIGHT;
+  return p;
+}
+
+cudaError_t launch_ilu_factor(pfc_ctx* ctx, const double* c, double dt) {
+  IluArgs p = ilu_args(ctx, dt);
+  p.c = c;
+  k_ilu_factor<<<(int)ctx->ilu->nbox, NT, 0, ctx->stream>>>(p);
+  ctx->launches++;
+  ctx->ilu_dt = dt;
+  pfc_account(ctx, PFC_K_RAS, 8.0 * ctx->N + 8.0 * ctx->ilu->nbox * ctx->ilu->nnz,
+              2.0 * ctx->ilu->nbox * ctx->ilu->nnz);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_ras_ilu(pfc_ctx* ctx, const double* v, double* z) {
+  const pfc_config& cf = ctx->cfg;
+  IluArgs p = ilu_args(ctx, ctx->ilu_dt);
+  p.v = v;
+  p.z = z;
+  p.y_ext = cf.ras_variant == PFC_RAS_LEFT ? nullptr : ctx->ras_y;
+  p.gate = ctx->gate;
+  const size_t sm = (size_t)p.n * sizeof(double);
+  static size_t attr = 0;
+  if (sm > 48 * 1024 && sm > attr) {
+    cudaError_t e = cudaFuncSetAttribute(k_ilu_apply, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)sm);
+    if (e != cudaSuccess) return e;
+    attr = sm;
+  }
+  k_ilu_apply<<<(int)ctx->ilu->nbox, NT, sm, ctx->stream>>>(p);
+  ctx->launches++;
+  {
+    const double next = (double)ctx->ilu->nbox * ctx->ilu->n;
+    pfc_account(ctx, PFC_K_RAS, 8.0 * (next + ctx->N) + 8.0 * ctx->ilu->nbox * ctx->ilu->nnz,
+                4.0 * ctx->ilu->nbox * ctx->ilu->nnz);
+  }
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess || cf.ras_variant == PFC_RAS_LEFT) return e;
+  return launch_ras_extend(ctx, z);
+}

@@ -28,6 +28,8 @@ struct pfc_gmres_dev {
 enum { PFC_GM_RUNNING = 0, PFC_GM_CONVERGED = 1, PFC_GM_HAPPY = 2, PFC_GM_MAXIT = 3,
        PFC_GM_RESTART = 4, PFC_GM_NONFINITE = 5 };
 
+struct pfc_ilu;   // ILU(k) subdomain-solve structures (ilu.cu, row f2)
+
 struct pfc_ctx {
   pfc_config cfg;
   cudaStream_t stream = nullptr;
@@ -56,6 +58,8 @@ struct pfc_ctx {
   double* mob_t[3] = {nullptr, nullptr, nullptr};
   const double* mob_phi = nullptr;
   const double* mob_psi = nullptr;
+  pfc_ilu* ilu = nullptr;          // PFC_LOCAL_ILU: pattern, schedules and per-box factors
+  double ilu_dt = 0.0;             // dt the current factors were built with
   double* partials = nullptr;  // reduction scratch
   size_t npartials = 0;
   double* dscal = nullptr;     // device scalars: [0,64) h1, [64,128) h2, [128] |w|^2, ...
@@ -113,6 +117,11 @@ cudaError_t launch_residual_mob(pfc_ctx*, const double* phi_new, const double* p
                                 double* F, double* partials, int* nparts);
 cudaError_t launch_jv_mob(pfc_ctx*, const double* v, const double* c, double dt, double* out);
 cudaError_t launch_mob_state(pfc_ctx*, const double* phi_new, const double* phi_old);
+// ILU(k) subdomain solves (ilu.cu)
+pfc_status ilu_setup(pfc_ctx* ctx);
+void ilu_free(pfc_ctx* ctx);
+cudaError_t launch_ilu_factor(pfc_ctx* ctx, const double* c, double dt);
+cudaError_t launch_ras_ilu(pfc_ctx* ctx, const double* v, double* z);
 cudaError_t launch_energy_mass(pfc_ctx* ctx, const double* phi, double* partials, int* nparts);
 cudaError_t launch_ras(pfc_ctx* ctx, const double* v, const double* c, double dt, double* z);
 int ras_plan(pfc_ctx* ctx);   // fills ras_smem/threads/cluster; returns 0 if infeasible

@@ -130,6 +130,9 @@ class PFCConfig:
     ras_local_k: int = 10
     ras_variant: int = 0            # 0 left-RAS, 1 AS, 2 right-RAS
     mobility: int = 0               # 0 M = 1 (all five configs); 1 M = 1 - phi^2 (row f3)
+    ras_local_solver: int = 0       # 0 local GMRES(k) (R9); 1 ILU(k) (row f2)
+    ras_ilu_level: int = 0
+    ras_ilu_reuse: int = 0          # factors of the step's first Newton iteration
     ic: dict = field(default_factory=dict)
     seed: int = 1
 

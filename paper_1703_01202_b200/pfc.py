@@ -29,11 +29,13 @@ class PfcConfig(C.Structure):
                 ("gmres_restart", C.c_int), ("gmres_maxit", C.c_int),
                 ("gmres_rtol", C.c_double), ("gmres_atol", C.c_double),
                 ("ras_box", C.c_int * 3), ("ras_overlap", C.c_int), ("ras_local_k", C.c_int),
-                ("ras_variant", C.c_int), ("mobility", C.c_int)]
+                ("ras_variant", C.c_int), ("mobility", C.c_int), ("ras_local_solver", C.c_int),
+                ("ras_ilu_level", C.c_int), ("ras_ilu_reuse", C.c_int)]
 
 
 PFC_RAS_LEFT, PFC_RAS_AS, PFC_RAS_RIGHT = 0, 1, 2   # include/pfc.h
 PFC_MOBILITY_ONE, PFC_MOBILITY_QUADRATIC = 0, 1     # include/pfc.h (M = 1; M = 1 - phi^2)
+PFC_LOCAL_GMRES, PFC_LOCAL_ILU = 0, 1               # include/pfc.h (R9; ILU(k))
 
 
 class PfcStepInfo(C.Structure):
@@ -104,7 +106,10 @@ def make_config(cfg=None, **over) -> PfcConfig:
                   gmres_maxit=cfg.gmres_maxit, gmres_rtol=cfg.gmres_rtol,
                   gmres_atol=cfg.gmres_atol, ras_box=cfg.ras_box, ras_overlap=cfg.ras_overlap,
                   ras_local_k=cfg.ras_local_k, ras_variant=getattr(cfg, "ras_variant", 0),
-                  mobility=getattr(cfg, "mobility", 0))
+                  mobility=getattr(cfg, "mobility", 0),
+                  ras_local_solver=getattr(cfg, "ras_local_solver", 0),
+                  ras_ilu_level=getattr(cfg, "ras_ilu_level", 0),
+                  ras_ilu_reuse=getattr(cfg, "ras_ilu_reuse", 0))
     kw.update(over)
     for k, v in kw.items():
         if k in ("n", "ras_box"):

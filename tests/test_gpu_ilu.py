@@ -1,0 +1,89 @@
+"""GPU parity of the ILU(k) subdomain solves (NEXT row f2, Table 1 P:872-915,
+factor reuse P:910-915) through the C ABI against the pinned oracle (-m gpu).  Small dt: at
+the configurations' h, ILU(0) of A_k keeps positive pivots only for dt of order 0.01-0.1
+(consistent with the paper's "n/c" entries)."""
+import math
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from oracle import oracle as O  # noqa: E402
+from paper_1703_01202_b200 import build as B  # noqa: E402
+from paper_1703_01202_b200 import pfc as P  # noqa: E402
+from paper_1703_01202_b200.inputs import random_field  # noqa: E402
+
+H = math.pi / 4
+G = 0.25
+
+
+def rel(a, b):
+    a = np.asarray(a).ravel(); b = np.asarray(b).ravel()
+    return np.linalg.norm(a - b) / np.linalg.norm(b)
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    B.build()
+    yield
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def host(t):
+    torch.cuda.synchronize()
+    return t.cpu().numpy()
+
+
+def ctx_ilu(shape, box, o, level, **kw):
+    nd = len(shape)
+    b = list(box) + [1] * (3 - nd)
+    return P.Context(None, ndim=nd, n=shape, h=H, gamma=G, ras_box=b, ras_overlap=o,
+                     ras_local_solver=P.PFC_LOCAL_ILU, ras_ilu_level=level, **kw)
+
+
+def prm_ilu(box, o, level, **kw):
+    return O.params(gamma=G, ras_box=box, ras_overlap=o, ras_local_solver=O.LOCAL_ILU,
+                    ras_ilu_level=level, **kw)
+
+
+@pytest.mark.parametrize("variant", [P.PFC_RAS_LEFT, P.PFC_RAS_AS, P.PFC_RAS_RIGHT])
+@pytest.mark.parametrize("shape,box,o,level", [((64, 64), (16, 16), 2, 0), ((64, 64), (16, 16), 2, 1),
+                                               ((48, 36), (12, 12), 1, 2),
+                                               ((24, 24, 24), (8, 8, 8), 1, 0)])
+def test_ilu_schwarz_parity(shape, box, o, level, variant):
+    phi = random_field(shape, 601, 0.07, 0.07)
+    psi = random_field(shape, 602, 0.07, 0.07)
+    v = random_field(shape, 603, 0.0, 1.0)
+    dt = 0.05
+    ctx = ctx_ilu(shape, box, o, level, ras_variant=variant)
+    z = host(ctx.ras_apply(dev(phi), dev(psi), dt, dev(v)))
+    zo = O.ras_apply(phi, psi, v, H, prm_ilu(box, o, level, ras_variant=variant), dt)
+    assert rel(z, zo) <= 1e-12
+
+
+@pytest.mark.parametrize("reuse", [0, 1])
+def test_ilu_one_step_parity(reuse):
+    shape = (64, 64)
+    phi0 = random_field(shape, 1, 0.07, 0.07)
+    dt = 0.02
+    ctx = ctx_ilu(shape, (16, 16), 2, 0, ras_ilu_reuse=reuse)
+    phi = dev(phi0)
+    _, info = ctx.step(phi, dt)
+    ref, ok, oinfo = O.newton(phi0, H, prm_ilu((16, 16), 2, 0, ras_ilu_reuse=reuse), dt)
+    assert ok and info["converged"]
+    assert info["newton_its"] == oinfo.newton_its and info["gmres_its"] == oinfo.gmres_its
+    assert rel(host(phi), ref) <= 1e-10
+
+
+def test_ilu_argument_errors():
+    with pytest.raises(P.PfcError):
+        ctx_ilu((64, 64), (16, 16), 2, 5)
+    with pytest.raises(P.PfcError):
+        ctx_ilu((64, 64), (16, 16), 2, 0, mobility=P.PFC_MOBILITY_QUADRATIC)
