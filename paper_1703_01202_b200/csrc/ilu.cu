@@ -15,9 +15,11 @@
 // L entries) and of the backward solve (on its U entries).  The device then runs, one CTA per
 // box, (1) the numeric factorisation into the box's value array, level by level, one warp per
 // row (lane 0 divides, the lanes apply that k's updates in parallel: distinct a_ij), and (2) per
-// preconditioner apply, the forward and backward solves, level by level, one thread per row,
-// in shared memory.  Same operations as the oracle (or_ilu_dense / ilu_solve) per entry; the
-// parallel order only regroups independent updates and the triangular-solve dot products.
+// preconditioner apply, the forward and backward solves, one WARP per box, the rows of each
+// level on the lanes (warp-synchronous; many boxes per SM hide the factor-read latency); the
+// value array is laid out as [L block | U block].
+// Same operations as the oracle (or_ilu_dense / ilu_solve) per entry; the parallel order only
+// regroups independent updates and the triangular-solve dot products.
 #include "pfc_device.cuh"
 #include "pfc_internal.h"
 
@@ -44,9 +46,11 @@ struct IluArgs {
   double* z;            // apply: output (owned nodes) or nullptr with y_ext
   double* y_ext;        // AS / right-RAS: ext-box solutions [box][ext node]
   double* vals;         // [box][nnz] factor values
-  const int* rowptr;    // CSR of the factor pattern
-  const int* col;
-  const int* diag;      // position of a_ii
+  const int* lptr;      // factor pattern, L block (strictly lower entries of every row) ...
+  const int* lcol;
+  const int* uptr;      // ... then the U block (diagonal first, then the upper entries)
+  const int* ucol;
+  int nL, nU;           // value position of U entry t of row i: nL + uptr[i] + t
   const int* ecls;      // per entry: linear-weight class, -1 for fill
   const int* ectype;    // per entry: 0 none, 1 -h^-2 c_j, 2 +2d h^-2 c_i
   const int* opptr;     // per row: ops [opptr[i], opptr[i+1])
@@ -87,13 +91,15 @@ __global__ void __launch_bounds__(NT) k_ilu_factor(const IluArgs p) {
   const int d2 = 2 * p.nd;
   for (int i = threadIdx.x; i < p.n; i += NT) {
     const double ci = p.c[gnode(p, i, gx0, gy0, gz0)];
-    for (int q = p.rowptr[i]; q < p.rowptr[i + 1]; ++q) {
+    auto set = [&](int q, int col) {
       const int cl = p.ecls[q], ct = p.ectype[q];
       double val = cl >= 0 ? p.W[cl] : 0.0;
       if (ct == 2) val += d2 * p.ih2 * ci;
-      else if (ct == 1) val -= p.ih2 * p.c[gnode(p, p.col[q], gx0, gy0, gz0)];
+      else if (ct == 1) val -= p.ih2 * p.c[gnode(p, col, gx0, gy0, gz0)];
       a[q] = val;
-    }
+    };
+    for (int q = p.lptr[i]; q < p.lptr[i + 1]; ++q) set(q, p.lcol[q]);
+    for (int t = p.uptr[i]; t < p.uptr[i + 1]; ++t) set(p.nL + t, p.ucol[t]);
   }
   __syncthreads();
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -108,7 +114,7 @@ __global__ void __launch_bounds__(NT) k_ilu_factor(const IluArgs p) {
         const int nup = p.opk[q + 1];
         double lik = 0.0;
         if (lane == 0) {
-          lik = a[pik] / a[p.diag[k]];
+          lik = a[pik] / a[p.nL + p.uptr[k]];
           a[pik] = lik;
         }
         lik = __shfl_sync(0xffffffffu, lik, 0);
@@ -124,46 +130,79 @@ __global__ void __launch_bounds__(NT) k_ilu_factor(const IluArgs p) {
   }
 }
 
-// z = sum_k (R_k^0)^T U^{-1} L^{-1} R_k^delta v (left-RAS) or the ext-box solutions
-__global__ void __launch_bounds__(NT) k_ilu_apply(const IluArgs p) {
-  extern __shared__ double y[];
+// z = sum_k (R_k^0)^T U^{-1} L^{-1} R_k^delta v (left-RAS) or the ext-box solutions.
+// One WARP per box, warp-synchronous (no block barriers): the sweeps are chains of levels with
+// a few rows each, so the rows of a level go to the lanes and many boxes per SM hide the
+// latency of the (L2 / HBM) factor reads.  y of each warp's box lives in shared memory.
+constexpr int AWMAX = 4;   // boxes (warps) per CTA at most (shared memory: one y per warp)
+__global__ void __launch_bounds__(AWMAX * 32) k_ilu_apply(const IluArgs p, int nbox) {
+  extern __shared__ double ysh[];
   if (p.gate && *p.gate) return;
-  const int box = blockIdx.x;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int box = blockIdx.x * (blockDim.x >> 5) + wid;
+  if (box >= nbox) return;                     // whole warps only
+  double* y = ysh + (size_t)wid * p.n;
   int gx0, gy0, gz0, ibx, iby, ibz;
   box_origin(p, box, gx0, gy0, gz0, ibx, iby, ibz);
   const double* a = p.vals + (size_t)box * p.nnz;
   const int Ex = p.bx + 2 * p.o, Ey = p.by + 2 * p.o;
-  for (int l = threadIdx.x; l < p.n; l += NT) {
+  for (int l = lane; l < p.n; l += 32) {
     const int li = l % Ex, lj = (l / Ex) % Ey, lk = l / (Ex * Ey);
     const bool owned = li >= p.o && li < p.o + p.bx && lj >= p.o && lj < p.o + p.by &&
                        (p.nd == 2 || (lk >= p.o && lk < p.o + p.bz));
     y[l] = (p.restrict_owned && !owned) ? 0.0 : p.v[gnode(p, l, gx0, gy0, gz0)];
   }
-  __syncthreads();
+  __syncwarp();
   for (int L = 0; L < p.nflev; ++L) {          // L y = r (unit lower)
-    for (int r = p.flev_ptr[L] + threadIdx.x; r < p.flev_ptr[L + 1]; r += NT) {
+    for (int r = p.flev_ptr[L] + lane; r < p.flev_ptr[L + 1]; r += 32) {
       const int i = p.flev_row[r];
+      const int q0 = __ldg(p.lptr + i), q1 = __ldg(p.lptr + i + 1);
       double s = y[i];
-      for (int q = p.rowptr[i]; q < p.diag[i]; ++q) s -= a[q] * y[p.col[q]];
+      for (int q = q0; q < q1; q += 8) {       // 8 independent loads in flight, then the
+        double av[8];                          // subtractions in ascending order
+        int cv[8];
+#pragma unroll
+        for (int t = 0; t < 8; ++t) {
+          av[t] = q + t < q1 ? a[q + t] : 0.0;
+          cv[t] = q + t < q1 ? __ldg(p.lcol + q + t) : i;
+        }
+#pragma unroll
+        for (int t = 0; t < 8; ++t)
+          if (q + t < q1) s -= av[t] * y[cv[t]];
+      }
       y[i] = s;
     }
-    __syncthreads();
+    __syncwarp();
   }
+  const double* u = a + p.nL;
   for (int L = 0; L < p.nblev; ++L) {          // U x = y
-    for (int r = p.blev_ptr[L] + threadIdx.x; r < p.blev_ptr[L + 1]; r += NT) {
+    for (int r = p.blev_ptr[L] + lane; r < p.blev_ptr[L + 1]; r += 32) {
       const int i = p.blev_row[r];
+      const int t0 = __ldg(p.uptr + i), t1 = __ldg(p.uptr + i + 1);
+      const double dii = u[t0];
       double s = y[i];
-      for (int q = p.diag[i] + 1; q < p.rowptr[i + 1]; ++q) s -= a[q] * y[p.col[q]];
-      y[i] = s / a[p.diag[i]];
+      for (int t = t0 + 1; t < t1; t += 8) {
+        double av[8];
+        int cv[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          av[k] = t + k < t1 ? u[t + k] : 0.0;
+          cv[k] = t + k < t1 ? __ldg(p.ucol + t + k) : i;
+        }
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          if (t + k < t1) s -= av[k] * y[cv[k]];
+      }
+      y[i] = s / dii;
     }
-    __syncthreads();
+    __syncwarp();
   }
   if (p.y_ext) {
-    for (int l = threadIdx.x; l < p.n; l += NT) p.y_ext[(size_t)box * p.n + l] = y[l];
+    for (int l = lane; l < p.n; l += 32) p.y_ext[(size_t)box * p.n + l] = y[l];
     return;
   }
   const int nown = p.bx * p.by * (p.nd == 3 ? p.bz : 1);
-  for (int l = threadIdx.x; l < nown; l += NT) {
+  for (int l = lane; l < nown; l += 32) {
     const int li = l % p.bx, lj = (l / p.bx) % p.by, lk = l / (p.bx * p.by);
     const int e = (li + p.o) + Ex * ((lj + p.o) + Ey * (p.nd == 3 ? lk + p.o : 0));
     p.z[(size_t)(ibx * p.bx + li) + (size_t)p.nx * (iby * p.by + lj) +
@@ -177,7 +216,8 @@ __global__ void __launch_bounds__(NT) k_ilu_apply(const IluArgs p) {
 
 struct pfc_ilu {
   int n = 0, nnz = 0, nflev = 0, nblev = 0;
-  int* d_rowptr = nullptr; int* d_col = nullptr; int* d_diag = nullptr;
+  int nL = 0, nU = 0;
+  int* d_lptr = nullptr; int* d_lcol = nullptr; int* d_uptr = nullptr; int* d_ucol = nullptr;
   int* d_ecls = nullptr; int* d_ectype = nullptr;
   int* d_opptr = nullptr; int* d_opk = nullptr; int* d_oppos = nullptr;
   int* d_flev_ptr = nullptr; int* d_flev_row = nullptr;
@@ -236,21 +276,30 @@ pfc_status ilu_setup(pfc_ctx* ctx) {
       }
     }
   }
-  // CSR
-  std::vector<int> rowptr(n + 1, 0), col, diag(n), ecls, ectype;
+  // value positions: the L block (strictly lower entries of every row, in row order), then the
+  // U block (diagonal first, then the upper entries, in row order)
+  std::vector<int> lptr(n + 1, 0), uptr(n + 1, 0), lcol, ucol, ecls, ectype;
   std::vector<std::map<int, int>> where(n);
   for (int i = 0; i < n; ++i) {
-    for (auto& e : rows[i]) {
-      where[i][e.first] = (int)col.size();
-      if (e.first == i) diag[i] = (int)col.size();
-      col.push_back(e.first);
-      auto m = meta[i].find(e.first);
-      ecls.push_back(m == meta[i].end() ? -1 : m->second.first);
-      ectype.push_back(m == meta[i].end() ? 0 : m->second.second);
-    }
-    rowptr[i + 1] = (int)col.size();
+    for (auto& e : rows[i])
+      if (e.first < i) lcol.push_back(e.first);
+    lptr[i + 1] = (int)lcol.size();
+    ucol.push_back(i);
+    for (auto& e : rows[i])
+      if (e.first > i) ucol.push_back(e.first);
+    uptr[i + 1] = (int)ucol.size();
   }
-  const int nnz = (int)col.size();
+  const int nL = (int)lcol.size(), nU = (int)ucol.size(), nnz = nL + nU;
+  ecls.assign(nnz, -1);
+  ectype.assign(nnz, 0);
+  for (int i = 0; i < n; ++i) {
+    for (int q = lptr[i]; q < lptr[i + 1]; ++q) where[i][lcol[q]] = q;
+    for (int t = uptr[i]; t < uptr[i + 1]; ++t) where[i][ucol[t]] = nL + t;
+    for (auto& w : where[i]) {
+      auto m = meta[i].find(w.first);
+      if (m != meta[i].end()) { ecls[w.second] = m->second.first; ectype[w.second] = m->second.second; }
+    }
+  }
   // IKJ op list per row: [k, pos_ik] + [nupd] then pairs (pos_kj, pos_ij) -- encoded in two
   // parallel arrays opk / oppos: opk[q] = k, oppos[q] = pos_ik, opk[q+1] = nupd, then oppos
   // holds the pairs from q+1 on
@@ -294,12 +343,13 @@ pfc_status ilu_setup(pfc_ctx* ctx) {
   std::vector<int> fptr, frow, bptr, brow;
   pfc_ilu* I = new pfc_ilu();
   ctx->ilu = I;
-  I->n = n; I->nnz = nnz;
+  I->n = n; I->nnz = nnz; I->nL = nL; I->nU = nU;
   I->nflev = group(flev, fptr, frow);
   I->nblev = group(blev, bptr, brow);
   I->nbox = 1;
   for (int d = 0; d < nd; ++d) I->nbox *= (size_t)(c.n[d] / c.ras_box[d]);
-  if (!up(ctx, &I->d_rowptr, rowptr) || !up(ctx, &I->d_col, col) || !up(ctx, &I->d_diag, diag) ||
+  if (!up(ctx, &I->d_lptr, lptr) || !up(ctx, &I->d_lcol, lcol) || !up(ctx, &I->d_uptr, uptr) ||
+      !up(ctx, &I->d_ucol, ucol) ||
       !up(ctx, &I->d_ecls, ecls) || !up(ctx, &I->d_ectype, ectype) ||
       !up(ctx, &I->d_opptr, opptr) || !up(ctx, &I->d_opk, opk) || !up(ctx, &I->d_oppos, oppos) ||
       !up(ctx, &I->d_flev_ptr, fptr) || !up(ctx, &I->d_flev_row, frow) ||
@@ -314,7 +364,7 @@ pfc_status ilu_setup(pfc_ctx* ctx) {
 void ilu_free(pfc_ctx* ctx) {
   pfc_ilu* I = ctx->ilu;
   if (!I) return;
-  int* a[] = {I->d_rowptr, I->d_col, I->d_diag, I->d_ecls, I->d_ectype, I->d_opptr, I->d_opk,
+  int* a[] = {I->d_lptr, I->d_lcol, I->d_uptr, I->d_ucol, I->d_ecls, I->d_ectype, I->d_opptr, I->d_opk,
               I->d_oppos, I->d_flev_ptr, I->d_flev_row, I->d_blev_ptr, I->d_blev_row};
   for (int* p : a)
     if (p) cudaFree(p);
@@ -327,7 +377,8 @@ static IluArgs ilu_args(pfc_ctx* ctx, double dt) {
   const pfc_config& cf = ctx->cfg;
   pfc_ilu* I = ctx->ilu;
   IluArgs p{};
-  p.vals = I->d_vals; p.rowptr = I->d_rowptr; p.col = I->d_col; p.diag = I->d_diag;
+  p.vals = I->d_vals; p.lptr = I->d_lptr; p.lcol = I->d_lcol; p.uptr = I->d_uptr;
+  p.ucol = I->d_ucol; p.nL = I->nL; p.nU = I->nU;
   p.ecls = I->d_ecls; p.ectype = I->d_ectype; p.opptr = I->d_opptr; p.opk = I->d_opk;
   p.oppos = I->d_oppos; p.flev_ptr = I->d_flev_ptr; p.flev_row = I->d_flev_row;
   p.blev_ptr = I->d_blev_ptr; p.blev_row = I->d_blev_row;
@@ -376,7 +427,8 @@ cudaError_t launch_ras_ilu(pfc_ctx* ctx, const double* v, double* z) {
   p.z = z;
   p.y_ext = cf.ras_variant == PFC_RAS_LEFT ? nullptr : ctx->ras_y;
   p.gate = ctx->gate;
-  const size_t sm = (size_t)p.n * sizeof(double);
+  const int aw = std::max(1, std::min<int>(AWMAX, (int)((200 * 1024) / ((size_t)p.n * 8))));
+  const size_t sm = (size_t)aw * p.n * sizeof(double);
   static size_t attr = 0;
   if (sm > 48 * 1024 && sm > attr) {
     cudaError_t e = cudaFuncSetAttribute(k_ilu_apply, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -384,7 +436,8 @@ cudaError_t launch_ras_ilu(pfc_ctx* ctx, const double* v, double* z) {
     if (e != cudaSuccess) return e;
     attr = sm;
   }
-  k_ilu_apply<<<(int)ctx->ilu->nbox, NT, sm, ctx->stream>>>(p);
+  const int nbox = (int)ctx->ilu->nbox;
+  k_ilu_apply<<<(nbox + aw - 1) / aw, aw * 32, sm, ctx->stream>>>(p, nbox);
   ctx->launches++;
   {
     const double next = (double)ctx->ilu->nbox * ctx->ilu->n;
