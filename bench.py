@@ -52,6 +52,24 @@ def ncu_traffic(pattern):
     return None
 
 
+def max_over_ranks(x, ws, device="cuda"):
+    """The max of a per-rank float over all ranks (the timing contract: the job's time is its
+    slowest replica).  NCCL on the GPU path, gloo in the CPU tests."""
+    if ws == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def replica_value(ms_max, steps, ws):
+    """Whole-job steps/s of ws independent replicas (weak scaling): every rank
+    advances its own copy of the workload by `steps`, so the job did ws*steps in ms_max."""
+    return ws * steps / (ms_max / 1e3)
+
+
 def load_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -166,13 +184,6 @@ def bench_cuda(args):
             dist.barrier()
         torch.cuda.synchronize()
 
-    def max_over_ranks(x):
-        if ws == 1:
-            return x
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
-
     # ---- device-resident timed run
     phi = torch.from_numpy(phi0.copy()).cuda()
     dt, _ = run_steps(ctx, phi, cfg.dt0, W, cfg.dt_min)
@@ -186,9 +197,9 @@ def bench_cuda(args):
         e1.record(stream)
         barrier()
     launches = ctx.launches - l0
-    ms = max_over_ranks(e0.elapsed_time(e1))
+    ms = max_over_ranks(e0.elapsed_time(e1), ws)
     clocks = clk.summary()
-    value = ws * K / (ms / 1e3)
+    value = replica_value(ms, K, ws)
 
     # ---- end to end through the C ABI with a pinned host buffer (same trajectory)
     ph = torch.from_numpy(phi0.copy()).pin_memory()
@@ -198,8 +209,8 @@ def bench_cuda(args):
     run_steps(ctx, ph, dt, K, cfg.dt_min)
     e1.record(stream)
     barrier()
-    ms_e2e = max_over_ranks(e0.elapsed_time(e1))
-    e2e = {"value": ws * K / (ms_e2e / 1e3), "unit": "steps/s",
+    ms_e2e = max_over_ranks(e0.elapsed_time(e1), ws)
+    e2e = {"value": replica_value(ms_e2e, K, ws), "unit": "steps/s",
            "h2d_bytes_per_step": cfg.N * 8, "d2h_bytes_per_step": cfg.N * 8}
 
     # ---- per-kernel-class profile of the same K steps (separate pass; events per launch)
