@@ -14,7 +14,8 @@
 // j > k), and the level schedules of the factorisation / forward solve (a row depends on its
 // L entries) and of the backward solve (on its U entries).  The device then runs, one CTA per
 // box, (1) the numeric factorisation into the box's value array, level by level, one warp per
-// row (lane 0 divides, the lanes apply that k's updates in parallel: distinct a_ij), and (2) per
+// row: its values, pivots and every a_kj it needs fetched in one round trip, then the IKJ loop
+// in shared memory (lane 0 divides, the lanes apply that k's distinct updates), and (2) per
 // preconditioner apply, the forward and backward solves, one WARP per box, the rows of each
 // level on the lanes (warp-synchronous; many boxes per SM hide the factor-read latency); the
 // value array is laid out as [L block | U block].
@@ -53,14 +54,14 @@ struct IluArgs {
   int nL, nU;           // value position of U entry t of row i: nL + uptr[i] + t
   const int* ecls;      // per entry: linear-weight class, -1 for fill
   const int* ectype;    // per entry: 0 none, 1 -h^-2 c_j, 2 +2d h^-2 c_i
-  const int* opptr;     // per row: ops [opptr[i], opptr[i+1])
-  const int* opk;       // op: k (divide a_ik by a_kk) ...
-  const int* oppos;     // ... pos_ik for the divide, then pairs (pos_kj, pos_ij)
+  const int* ukptr;     // updates of L entry q: [ukptr[q], ukptr[q+1]) of ...
+  const int* usrc;      // ... the value position of a_kj (final row k)
+  const int* udst;      // ... and the slot of a_ij within row i
   const int* flev_ptr;  // forward / factorisation levels
   const int* flev_row;
   const int* blev_ptr;  // backward levels
   const int* blev_row;
-  int nflev, nblev, n, nnz;
+  int nflev, nblev, n, nnz, maxrow, maxupd;
   int nx, ny, nz, bx, by, bz, o, nd;
   double W[7];
   double ih2;
@@ -89,7 +90,7 @@ __global__ void __launch_bounds__(NT) k_ilu_factor(const IluArgs p) {
   box_origin(p, box, gx0, gy0, gz0, ibx, iby, ibz);
   double* a = p.vals + (size_t)box * p.nnz;
   const int d2 = 2 * p.nd;
-  for (int i = threadIdx.x; i < p.n; i += NT) {
+  for (int i = threadIdx.x; i < p.n; i += blockDim.x) {
     const double ci = p.c[gnode(p, i, gx0, gy0, gz0)];
     auto set = [&](int q, int col) {
       const int cl = p.ecls[q], ct = p.ectype[q];
@@ -102,29 +103,47 @@ __global__ void __launch_bounds__(NT) k_ilu_factor(const IluArgs p) {
     for (int t = p.uptr[i]; t < p.uptr[i + 1]; ++t) set(p.nL + t, p.ucol[t]);
   }
   __syncthreads();
+  // IKJ by levels, one warp per row.  Everything the row needs is read in one round trip:
+  // its own values, the pivots a_kk and every a_kj of its updates (rows k are final: earlier
+  // levels); then the k loop runs in shared memory (lane 0 divides a_ik, the lanes apply the
+  // distinct updates a_ij -= a_ik a_kj) and the row is written back.
+  extern __shared__ double fsm[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  double* rb = fsm + (size_t)wid * (2 * p.maxrow + p.maxupd);
+  double* piv = rb + p.maxrow;
+  double* us = piv + p.maxrow;
+  // the row's index data too (the k loop must not wait on global loads)
+  const int nw = blockDim.x >> 5;     // warps of this launch (fewer when the rows are long)
+  int* ibase = reinterpret_cast<int*>(fsm + (size_t)nw * (2 * p.maxrow + p.maxupd));
+  int* uk = ibase + (size_t)wid * (p.maxrow + 1 + p.maxupd);
+  int* ud = uk + p.maxrow + 1;
   for (int L = 0; L < p.nflev; ++L) {
-    for (int r = p.flev_ptr[L] + wid; r < p.flev_ptr[L + 1]; r += NT / 32) {
+    for (int r = p.flev_ptr[L] + wid; r < p.flev_ptr[L + 1]; r += nw) {
       const int i = p.flev_row[r];
-      int q = p.opptr[i];
-      const int qe = p.opptr[i + 1];
-      while (q < qe) {                 // one k: [k, pos_ik, nupd, (pos_kj, pos_ij) x nupd]
-        const int k = p.opk[q];
-        const int pik = p.oppos[q];
-        const int nup = p.opk[q + 1];
-        double lik = 0.0;
-        if (lane == 0) {
-          lik = a[pik] / a[p.nL + p.uptr[k]];
-          a[pik] = lik;
-        }
-        lik = __shfl_sync(0xffffffffu, lik, 0);
-        for (int u = lane; u < nup; u += 32) {
-          const int pkj = p.oppos[q + 1 + 2 * u], pij = p.oppos[q + 2 + 2 * u];
-          a[pij] -= lik * a[pkj];
-        }
-        __syncwarp();
-        q += 2 + 2 * nup;
+      const int l0 = p.lptr[i], nLi = p.lptr[i + 1] - l0;
+      const int u0 = p.nL + p.uptr[i], nUi = p.uptr[i + 1] - p.uptr[i];
+      const int g0 = p.ukptr[l0], ng = p.ukptr[l0 + nLi] - g0;
+      for (int t = lane; t < nLi + nUi; t += 32) rb[t] = t < nLi ? a[l0 + t] : a[u0 + t - nLi];
+      for (int t = lane; t < nLi; t += 32) piv[t] = a[p.nL + p.uptr[p.lcol[l0 + t]]];
+      for (int u = lane; u < ng; u += 32) {
+        us[u] = a[p.usrc[g0 + u]];
+        ud[u] = p.udst[g0 + u];
       }
+      for (int t = lane; t <= nLi; t += 32) uk[t] = p.ukptr[l0 + t] - g0;
+      __syncwarp();
+      for (int t = 0; t < nLi; ++t) {
+        if (lane == 0) rb[t] = rb[t] / piv[t];
+        __syncwarp();
+        const double lik = rb[t];
+        const int e1 = uk[t + 1];
+        for (int u = uk[t] + lane; u < e1; u += 32) rb[ud[u]] -= lik * us[u];
+        __syncwarp();
+      }
+      for (int t = lane; t < nLi + nUi; t += 32) {
+        if (t < nLi) a[l0 + t] = rb[t];
+        else a[u0 + t - nLi] = rb[t];
+      }
+      __syncwarp();
     }
     __syncthreads();
   }
@@ -216,10 +235,10 @@ __global__ void __launch_bounds__(AWMAX * 32) k_ilu_apply(const IluArgs p, int n
 
 struct pfc_ilu {
   int n = 0, nnz = 0, nflev = 0, nblev = 0;
-  int nL = 0, nU = 0;
+  int nL = 0, nU = 0, maxrow = 0, maxupd = 0;
+  int* d_ukptr = nullptr; int* d_usrc = nullptr; int* d_udst = nullptr;
   int* d_lptr = nullptr; int* d_lcol = nullptr; int* d_uptr = nullptr; int* d_ucol = nullptr;
   int* d_ecls = nullptr; int* d_ectype = nullptr;
-  int* d_opptr = nullptr; int* d_opk = nullptr; int* d_oppos = nullptr;
   int* d_flev_ptr = nullptr; int* d_flev_row = nullptr;
   int* d_blev_ptr = nullptr; int* d_blev_row = nullptr;
   double* d_vals = nullptr;
@@ -300,32 +319,30 @@ pfc_status ilu_setup(pfc_ctx* ctx) {
       if (m != meta[i].end()) { ecls[w.second] = m->second.first; ectype[w.second] = m->second.second; }
     }
   }
-  // IKJ op list per row: [k, pos_ik] + [nupd] then pairs (pos_kj, pos_ij) -- encoded in two
-  // parallel arrays opk / oppos: opk[q] = k, oppos[q] = pos_ik, opk[q+1] = nupd, then oppos
-  // holds the pairs from q+1 on
-  std::vector<int> opptr(n + 1, 0), opk, oppos;
+  // IKJ updates per row: for the L entry q of row i (column k, ascending), the updates
+  // a_ij -= a_ik a_kj over the kept j > k are [ukptr[q], ukptr[q+1]) of the flat lists usrc
+  // (value position of a_kj in the final row k) and udst (slot of a_ij in row i: L entries
+  // 0..nLi-1, then the U entries)
+  std::vector<int> ukptr(nL + 1, 0), usrc, udst;
   std::vector<int> flev(n, 0), blev(n, 0);
+  int maxupd = 0;
   for (int i = 0; i < n; ++i) {
-    for (auto it = rows[i].begin(); it != rows[i].end() && it->first < i; ++it) {
-      const int kk = it->first;
+    const int nLi = lptr[i + 1] - lptr[i];
+    int rowupd = 0;
+    for (int q = lptr[i]; q < lptr[i + 1]; ++q) {
+      const int kk = lcol[q];
       flev[i] = std::max(flev[i], flev[kk] + 1);
-      std::vector<int> pairs;
       for (auto jt = rows[kk].upper_bound(kk); jt != rows[kk].end(); ++jt) {
         auto w = where[i].find(jt->first);
         if (w == where[i].end()) continue;
-        pairs.push_back(where[kk][jt->first]);
-        pairs.push_back(w->second);
+        usrc.push_back(where[kk][jt->first]);
+        const int pos = w->second;
+        udst.push_back(pos < nL ? pos - lptr[i] : nLi + (pos - nL - uptr[i]));
       }
-      const size_t q = opk.size();
-      const int nup = (int)pairs.size() / 2;
-      opk.resize(q + 2 + 2 * nup, 0);
-      oppos.resize(q + 2 + 2 * nup, 0);
-      opk[q] = kk;
-      oppos[q] = where[i][kk];
-      opk[q + 1] = nup;
-      for (int u = 0; u < 2 * nup; ++u) oppos[q + 1 + u] = pairs[u];
+      ukptr[q + 1] = (int)usrc.size();
+      rowupd += ukptr[q + 1] - ukptr[q];
     }
-    opptr[i + 1] = (int)opk.size();
+    maxupd = std::max(maxupd, rowupd);
   }
   for (int i = n - 1; i >= 0; --i)
     for (auto jt = rows[i].upper_bound(i); jt != rows[i].end(); ++jt)
@@ -343,7 +360,9 @@ pfc_status ilu_setup(pfc_ctx* ctx) {
   std::vector<int> fptr, frow, bptr, brow;
   pfc_ilu* I = new pfc_ilu();
   ctx->ilu = I;
-  I->n = n; I->nnz = nnz; I->nL = nL; I->nU = nU;
+  I->n = n; I->nnz = nnz; I->nL = nL; I->nU = nU; I->maxupd = maxupd;
+  for (int i = 0; i < n; ++i)
+    I->maxrow = std::max(I->maxrow, (lptr[i + 1] - lptr[i]) + (uptr[i + 1] - uptr[i]));
   I->nflev = group(flev, fptr, frow);
   I->nblev = group(blev, bptr, brow);
   I->nbox = 1;
@@ -351,21 +370,22 @@ pfc_status ilu_setup(pfc_ctx* ctx) {
   if (!up(ctx, &I->d_lptr, lptr) || !up(ctx, &I->d_lcol, lcol) || !up(ctx, &I->d_uptr, uptr) ||
       !up(ctx, &I->d_ucol, ucol) ||
       !up(ctx, &I->d_ecls, ecls) || !up(ctx, &I->d_ectype, ectype) ||
-      !up(ctx, &I->d_opptr, opptr) || !up(ctx, &I->d_opk, opk) || !up(ctx, &I->d_oppos, oppos) ||
+      !up(ctx, &I->d_ukptr, ukptr) || !up(ctx, &I->d_usrc, usrc) || !up(ctx, &I->d_udst, udst) ||
       !up(ctx, &I->d_flev_ptr, fptr) || !up(ctx, &I->d_flev_row, frow) ||
       !up(ctx, &I->d_blev_ptr, bptr) || !up(ctx, &I->d_blev_row, brow) ||
       cudaMalloc(&I->d_vals, I->nbox * nnz * sizeof(double)) != cudaSuccess)
     return pfc_fail(ctx, PFC_ENOMEM, "ILU structures");
-  if ((size_t)n * sizeof(double) > 200 * 1024)
-    return pfc_fail(ctx, PFC_EINVAL, "ILU: ext box too large for the shared-memory solve");
+  if ((size_t)n * sizeof(double) > 200 * 1024 ||
+      (size_t)(2 * I->maxrow + I->maxupd) * 8 + (I->maxrow + 1 + I->maxupd) * 4 > 200 * 1024)
+    return pfc_fail(ctx, PFC_EINVAL, "ILU: rows or ext box too large for the shared-memory plan");
   return PFC_OK;
 }
 
 void ilu_free(pfc_ctx* ctx) {
   pfc_ilu* I = ctx->ilu;
   if (!I) return;
-  int* a[] = {I->d_lptr, I->d_lcol, I->d_uptr, I->d_ucol, I->d_ecls, I->d_ectype, I->d_opptr, I->d_opk,
-              I->d_oppos, I->d_flev_ptr, I->d_flev_row, I->d_blev_ptr, I->d_blev_row};
+  int* a[] = {I->d_lptr, I->d_lcol, I->d_uptr, I->d_ucol, I->d_ecls, I->d_ectype, I->d_ukptr,
+              I->d_usrc, I->d_udst, I->d_flev_ptr, I->d_flev_row, I->d_blev_ptr, I->d_blev_row};
   for (int* p : a)
     if (p) cudaFree(p);
   if (I->d_vals) cudaFree(I->d_vals);
@@ -379,8 +399,9 @@ static IluArgs ilu_args(pfc_ctx* ctx, double dt) {
   IluArgs p{};
   p.vals = I->d_vals; p.lptr = I->d_lptr; p.lcol = I->d_lcol; p.uptr = I->d_uptr;
   p.ucol = I->d_ucol; p.nL = I->nL; p.nU = I->nU;
-  p.ecls = I->d_ecls; p.ectype = I->d_ectype; p.opptr = I->d_opptr; p.opk = I->d_opk;
-  p.oppos = I->d_oppos; p.flev_ptr = I->d_flev_ptr; p.flev_row = I->d_flev_row;
+  p.ecls = I->d_ecls; p.ectype = I->d_ectype; p.ukptr = I->d_ukptr; p.usrc = I->d_usrc;
+  p.udst = I->d_udst; p.maxrow = I->maxrow; p.maxupd = I->maxupd;
+  p.flev_ptr = I->d_flev_ptr; p.flev_row = I->d_flev_row;
   p.blev_ptr = I->d_blev_ptr; p.blev_row = I->d_blev_row;
   p.nflev = I->nflev; p.nblev = I->nblev; p.n = I->n; p.nnz = I->nnz;
   p.nx = cf.n[0]; p.ny = cf.n[1]; p.nz = cf.ndim == 3 ? cf.n[2] : 1;
@@ -412,7 +433,18 @@ static IluArgs ilu_args(pfc_ctx* ctx, double dt) {
 cudaError_t launch_ilu_factor(pfc_ctx* ctx, const double* c, double dt) {
   IluArgs p = ilu_args(ctx, dt);
   p.c = c;
-  k_ilu_factor<<<(int)ctx->ilu->nbox, NT, 0, ctx->stream>>>(p);
+  const size_t per_warp = (2 * p.maxrow + p.maxupd) * sizeof(double) +
+                          (p.maxrow + 1 + p.maxupd) * sizeof(int);
+  const int nw = (int)std::max<size_t>(1, std::min<size_t>(NT / 32, (200 * 1024) / per_warp));
+  const size_t sm = (size_t)nw * per_warp;
+  static size_t attr = 0;
+  if (sm > 48 * 1024 && sm > attr) {
+    cudaError_t e = cudaFuncSetAttribute(k_ilu_factor, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)sm);
+    if (e != cudaSuccess) return e;
+    attr = sm;
+  }
+  k_ilu_factor<<<(int)ctx->ilu->nbox, nw * 32, sm, ctx->stream>>>(p);
   ctx->launches++;
   ctx->ilu_dt = dt;
   pfc_account(ctx, PFC_K_RAS, 8.0 * ctx->N + 8.0 * ctx->ilu->nbox * ctx->ilu->nnz,
