@@ -50,8 +50,10 @@ constexpr int NBLK = NPB * NPB;     // 324 blocks
 constexpr int NTC = 352;            // 11 compute warps
 constexpr int NWC = NTC / 32;
 constexpr int NT = NTC + 32;        // + 1 producer warp (TMA issue, periodic fix-up)
-// ring depth per operator (PF <= RING - 2): the residual also keeps s = Phi + psi in split planes
-template <int OP> struct Cfg { static constexpr int RING = 5, PF = 3, NSPL = 4; };
+// ring depth per operator.  LAG: a plane's slot is released LAG iterations after the plane's
+// own iteration (J v reads the input ring's plane t-1 for the stage-1 neighbours: LAG 1; the
+// residual takes them from its s = Phi + psi split planes: LAG 0); PF <= RING - 1 - LAG.
+template <int OP> struct Cfg { static constexpr int RING = 5, PF = 3, NSPL = 4, LAG = 1; };
 constexpr int SP = 25;              // split-plane row pitch (doubles)
 constexpr int SROWS = WY;
 constexpr int SO = SROWS * SP;      // offset of the odd-column half
@@ -72,7 +74,7 @@ __device__ __forceinline__ int woff(bool split, int r, int c) {
 }
 
 enum { OP_RESID = 0, OP_JV = 1 };
-template <> struct Cfg<OP_RESID> { static constexpr int RING = 4, PF = 2, NSPL = 6; };
+template <> struct Cfg<OP_RESID> { static constexpr int RING = 4, PF = 3, NSPL = 6, LAG = 0; };
 
 struct S3Args {
   const double* a;   // Phi | v
@@ -147,7 +149,7 @@ struct S3Maps {   // 42 x 20 (natural) and 22 x 20 (split) boxes of both fields
 template <int OP>
 __global__ void __launch_bounds__(NT, 1) stencil3d_kernel(const __grid_constant__ S3Maps m,
                                                           const __grid_constant__ S3Args p) {
-  constexpr int RING = Cfg<OP>::RING, PF = Cfg<OP>::PF;
+  constexpr int RING = Cfg<OP>::RING, PF = Cfg<OP>::PF, LAG = Cfg<OP>::LAG;
   extern __shared__ __align__(128) double smem_dyn[];
   double* ringA = smem_dyn;                 // RING slots: Phi | v
   double* ringB = ringA + RING * WS;        // RING slots: psi | c
@@ -375,7 +377,8 @@ __global__ void __launch_bounds__(NT, 1) stencil3d_kernel(const __grid_constant_
       __syncwarp();
       if (lane == 0) {
         mbar_arrive(&itbar);
-        if (t > 0) mbar_arrive(&empty[prv]);
+        if (LAG == 0) mbar_arrive(&empty[slot]);
+        else if (t > 0) mbar_arrive(&empty[prv]);
       }
       // ---- queue rotation (renames under the 3x unroll)
       A2 = A1; A1 = A0; B2 = B1; B1 = B0;
@@ -464,8 +467,6 @@ cudaError_t launch3d(pfc_ctx* ctx, const double* a, const double* b, double dt, 
 }
 
 }  // namespace
-
-int stencil3d_tiles(int nx, int ny) { return ((nx + TX - 1) / TX) * ((ny + TY - 1) / TY); }
 
 cudaError_t launch_residual_3d(pfc_ctx* ctx, const double* phi_new, const double* phi_old,
                                double dt, double* F, double* partials, int* nparts) {
