@@ -93,7 +93,12 @@ def load():
 
 
 def make_config(cfg=None, **over) -> PfcConfig:
-    """pfc_config from a paper_1703_01202_b200.inputs.PFCConfig and/or keyword overrides."""
+    """pfc_config from a paper_1703_01202_b200.inputs.PFCConfig and/or keyword overrides.
+
+    Keyword overrides use the field names of include/pfc.h, e.g. ndim, n, h, gamma, adaptive,
+    dt_min, dt_max, eta, newton_rtol, gmres_restart, ras_box, ras_overlap, ras_local_k,
+    ras_variant (PFC_RAS_LEFT / _AS / _RIGHT), mobility (PFC_MOBILITY_ONE / _QUADRATIC),
+    ras_local_solver (PFC_LOCAL_GMRES / _ILU), ras_ilu_level, ras_ilu_reuse."""
     L = load()
     c = PfcConfig()
     L.pfc_config_default(C.byref(c))
