@@ -328,3 +328,36 @@ def test_constant_state_is_a_fixed_point():
     phi = torch.full((64, 64), 0.07, dtype=torch.float64, device="cuda")
     dt, info = ctx.step(phi, 0.5)
     assert info["newton_its"] == 0 and torch.all(phi == 0.07)
+
+
+@pytest.mark.parametrize("name,boxes", [("cfg4", (0, 7, 63, 511)), ("cfg5", (0, 31, 16383, 32767))])
+def test_ras_apply_parity_3d_full_size_sampled(name, boxes):
+    """The 3D subdomain solves at the full config sizes (128^3: 512 boxes; 512^3: 32768
+    boxes) in the launch configuration of the step: sampled boxes (first, last, x/y/z edge
+    boxes with periodic wrap) against the oracle's per-box output (or_ras_apply_box)."""
+    cfg = CONFIGS[name]
+    n = cfg.n
+    phi = random_field(n, 901, -0.35, 0.05)
+    v = random_field(n, 902, 0.0, 1.0)
+    ctx = P.Context(cfg)
+    z = host(ctx.ras_apply(dev(phi), dev(phi), 1.0, dev(v)))
+    prm = O.params_from_config(cfg)
+    b = cfg.ras_box
+    nb = [n[d] // b[d] for d in range(3)]
+    for box in boxes:
+        bx, by, bz = box % nb[0], (box // nb[0]) % nb[1], box // (nb[0] * nb[1])
+        zo = O.ras_apply_box(phi, phi, v, H, prm, 1.0, box)
+        zg = z[bz * b[2]:(bz + 1) * b[2], by * b[1]:(by + 1) * b[1], bx * b[0]:(bx + 1) * b[0]]
+        assert rel(zg, zo) <= 1e-12, box
+
+
+def test_cfg3_one_step_parity():
+    """Config 3 (2048^2 hexagonal crystallites, adaptive dt from dt_min): one step from the
+    IC against the oracle (R18: one-step parity is the bar where dynamics amplify)."""
+    cfg = CONFIGS["cfg3"]
+    phi0 = cfg.initial_condition()
+    ctx = P.Context(cfg)
+    phi = dev(phi0)
+    ctx.step(phi, cfg.dt0)
+    ref, _ = O.run(cfg, phi0, 1)
+    assert rel(host(phi), ref) <= 1e-10
