@@ -95,6 +95,14 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
+// Ampere-style asynchronous 8-byte global -> shared copy (per thread), commit, wait
+__device__ __forceinline__ void cp_async8(double* smem, const double* gmem) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(smem)), "l"(gmem)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
 // Deterministic block sum of NV values per thread; result valid in out[0..NV) for ALL threads
 // after return (broadcast through shared memory).  `red` needs 32*NV doubles.
 template <int NV>

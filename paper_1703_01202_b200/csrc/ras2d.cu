@@ -614,6 +614,7 @@ __global__ void __launch_bounds__(NTC, 1) ras2d_col_kernel(const __grid_constant
   double* pcv = pv + PP * PPY;               // PP x PPY padded c v
   double* red = pcv + PP * PPY;              // 2 x NWC x 16
   double* hwall = red + 2 * NWC * 16;        // NWC x 3 x 16
+  double* stg = hwall + NWC * 48;            // next box's v, c of each thread's nodes (2 x NTC x R)
   __shared__ double H[(K + 1) * K];
   __shared__ double gv[K + 1], cs[K], sn[K], yv[K], rd[K];
 
@@ -627,8 +628,7 @@ __global__ void __launch_bounds__(NTC, 1) ras2d_col_kernel(const __grid_constant
   double* hx = h2 + 16;
   const int Ex = p.Ex, Ey = p.Ey;
   const int nbx = p.nx / p.bx;
-  const int ibx = blockIdx.x % nbx, iby = blockIdx.x / nbx;
-  const int gx0 = ibx * p.bx - p.o, gy0 = iby * p.by - p.o;
+  const int nboxes = nbx * (p.ny / p.by);
 
   const int xs = tid % Ex, ss = tid / Ex;
   const bool active = ss < p.ns;
@@ -639,8 +639,28 @@ __global__ void __launch_bounds__(NTC, 1) ras2d_col_kernel(const __grid_constant
   double* pvb = pv + (y0 + 3) * PP + x + 3;
   double* pcvb = pcv + (y0 + 3) * PP + x + 3;
 
-  for (int q = tid; q < 2 * PP * PPY; q += blockDim.x) pv[q] = 0.0;
-  // gather R_k^delta v and c (periodic wrap)
+  for (int q = tid; q < 2 * PP * PPY; q += blockDim.x) pv[q] = 0.0;   // the ring stays zero
+  double* sv = stg + tid * R;
+  double* sc = stg + NTC * R + tid * R;
+  // R_k^delta v and c of a box (periodic wrap) into this thread's staging slots, asynchronously
+  auto prefetch = [&](int box) {
+    if (box >= nboxes) return;
+    const int gx0 = (box % nbx) * p.bx - p.o, gy0 = (box / nbx) * p.by - p.o;
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+      if (own[r]) {
+        const size_t g = (size_t)wrapi(gx0 + x, p.nx) + (size_t)p.nx * wrapi(gy0 + y0 + r, p.ny);
+        cp_async8(sv + r, p.v + g);
+        cp_async8(sc + r, p.c + g);
+      }
+    cp_async_commit();
+  };
+  prefetch(blockIdx.x);
+  // persistent CTA: boxes blockIdx.x, + gridDim.x, ...; the next box's inputs load while the
+  // current box is solved
+  for (int box = blockIdx.x; box < nboxes; box += gridDim.x) {
+  const int ibx = box % nbx, iby = box / nbx;
+  cp_async_wait_all();
   double Vr[K][R];
   double w[R], cr[R], cvv[R];
   double acc0[1] = {0.0};
@@ -649,14 +669,15 @@ __global__ void __launch_bounds__(NTC, 1) ras2d_col_kernel(const __grid_constant
     w[r] = 0.0;
     cr[r] = 0.0;
     if (own[r]) {
-      const size_t g = (size_t)wrapi(gx0 + x, p.nx) + (size_t)p.nx * wrapi(gy0 + y0 + r, p.ny);
       const int li = x - p.o, lj = y0 + r - p.o;
       const bool owned = li >= 0 && li < p.bx && lj >= 0 && lj < p.by;
-      w[r] = (p.restrict_owned && !owned) ? 0.0 : p.v[g];
-      cr[r] = p.c[g];
+      w[r] = (p.restrict_owned && !owned) ? 0.0 : sv[r];
+      cr[r] = sc[r];
       acc0[0] = fma(w[r], w[r], acc0[0]);
     }
   }
+  prefetch(box + gridDim.x);   // this thread's slots are free again
+  hn_prev = 0.0;
   int rb = 0;
   col_allreduce<1>(acc0, red + rb * NWC * 16, hx, nwt);   // also orders the zero fill
   rb ^= 1;
@@ -666,12 +687,12 @@ __global__ void __launch_bounds__(NTC, 1) ras2d_col_kernel(const __grid_constant
     for (int r = 0; r < R; ++r) {
       const int li = x - p.o, lj = y0 + r - p.o;
       if (p.y_ext) {
-        if (own[r]) p.y_ext[(size_t)blockIdx.x * (Ex * Ey) + (y0 + r) * Ex + x] = 0.0;
+        if (own[r]) p.y_ext[(size_t)box * (Ex * Ey) + (y0 + r) * Ex + x] = 0.0;
       } else if (own[r] && li >= 0 && li < p.bx && lj >= 0 && lj < p.by) {
         p.z[(size_t)(ibx * p.bx + li) + (size_t)p.nx * (iby * p.by + lj)] = 0.0;
       }
     }
-    return;
+    continue;   // uniform: every thread saw beta = 0
   }
   {
     const double ib = 1.0 / beta;
@@ -760,10 +781,12 @@ __global__ void __launch_bounds__(NTC, 1) ras2d_col_kernel(const __grid_constant
 #pragma unroll
     for (int i = 0; i < K; ++i)
       if (i < jm) s = fma(yv[i], Vr[i][r], s);
-    if (p.y_ext) p.y_ext[(size_t)blockIdx.x * (Ex * Ey) + (y0 + r) * Ex + x] = s;
+    if (p.y_ext) p.y_ext[(size_t)box * (Ex * Ey) + (y0 + r) * Ex + x] = s;
     else p.z[(size_t)(ibx * p.bx + li) + (size_t)p.nx * (iby * p.by + lj)] = s;
   }
   CPROF(7);
+  __syncthreads();   // yv, H and the planes are reused by the next box
+  }
 }
 
 #ifdef PFC_RAS_PROFILE
@@ -775,8 +798,8 @@ extern "C" void pfc_ras_prof_read(long long* out) {
 }
 namespace {
 #endif
-size_t ras2d_col_smem_bytes() {
-  return (size_t)(2 * PP * PPY + 2 * NWC * 16 + NWC * 48) * sizeof(double);
+size_t ras2d_col_smem_bytes(int R) {
+  return (size_t)(2 * PP * PPY + 2 * NWC * 16 + NWC * 48 + 2 * NTC * R) * sizeof(double);
 }
 
 typedef void (*ras2d_fn)(RasArgs);
@@ -836,7 +859,7 @@ int ras2d_plan(pfc_ctx* ctx) {
     const int r = col_rows(c.ras_local_k, Ex, Ey);
     if (r) {
       const int ns = (Ey + r - 1) / r;
-      ctx->ras_smem = (int)ras2d_col_smem_bytes();
+      ctx->ras_smem = (int)ras2d_col_smem_bytes(r);
       ctx->ras_threads = (Ex * ns + 31) / 32 * 32 + 32;   // node warps + the Givens warp
       ctx->ras_rows = r;                             // rows per thread
       return 1;
@@ -881,7 +904,14 @@ cudaError_t launch_ras_2d(pfc_ctx* ctx, const double* v, const double* c, double
     p.W[4] = -0.5 * ih6;
     p.W[5] = -1.5 * ih6;
     p.ih2 = ih2;
-    fn<<<nb, ctx->ras_threads, ctx->ras_smem, ctx->stream>>>(p);
+    static int nsm = 0;
+    if (!nsm) {
+      int dev = 0;
+      if (cudaGetDevice(&dev) != cudaSuccess ||
+          cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+        nsm = 148;
+    }
+    fn<<<std::min(nb, nsm), ctx->ras_threads, ctx->ras_smem, ctx->stream>>>(p);   // persistent
   } else {
     ras2d_fn fn = pick(cf.ras_local_k);
     if (!fn) return cudaErrorInvalidValue;
