@@ -146,6 +146,23 @@ def fp64_peak():
     return None, None
 
 
+def variant_config(cfg, args):
+    """The configuration with the NEXT-row options of the command line (mobility, Schwarz
+    variant, ILU(k) / LU subdomain solves); unchanged without them."""
+    if not (args.mobility or args.ras_variant or args.ilu >= 0 or args.lu):
+        return cfg
+    import dataclasses
+    solver = 2 if args.lu else (1 if args.ilu >= 0 else 0)
+    tag = ("_lu" if args.lu else f"_ilu{args.ilu}" if args.ilu >= 0 else "")
+    if solver and args.ilu_reuse:
+        tag += "reuse"
+    return dataclasses.replace(cfg, mobility=args.mobility, ras_variant=args.ras_variant,
+                               ras_local_solver=solver, ras_ilu_level=max(args.ilu, 0),
+                               ras_ilu_reuse=args.ilu_reuse,
+                               name=cfg.name + (f"_mobility{args.mobility}" if args.mobility else "")
+                               + (f"_ras{args.ras_variant}" if args.ras_variant else "") + tag)
+
+
 def bench_cuda(args):
     import numpy as np
     import torch
@@ -163,17 +180,7 @@ def bench_cuda(args):
         B.build()
     if ws > 1:
         dist.barrier()
-    cfg = CONFIGS[args.config]
-    if args.mobility or args.ras_variant or args.ilu >= 0:   # NEXT-row measurements
-        import dataclasses
-        ilu = args.ilu >= 0
-        cfg = dataclasses.replace(cfg, mobility=args.mobility, ras_variant=args.ras_variant,
-                                  ras_local_solver=1 if ilu else 0,
-                                  ras_ilu_level=max(args.ilu, 0), ras_ilu_reuse=args.ilu_reuse,
-                                  name=cfg.name + (f"_mobility{args.mobility}" if args.mobility else "")
-                                  + (f"_ras{args.ras_variant}" if args.ras_variant else "")
-                                  + (f"_ilu{args.ilu}" + ("reuse" if args.ilu_reuse else "")
-                                     if ilu else ""))
+    cfg = variant_config(CONFIGS[args.config], args)
     W, K = args.warmup, args.steps
     phi0 = cfg.initial_condition()
     ctx = P.Context(cfg)
@@ -311,8 +318,14 @@ def bench_cuda(args):
                           f"{W}..{W + K - 1} from dt_min" if cfg.adaptive else f"fixed {cfg.dt0}"),
                    "dt_first_timed": dt_first_timed, "dt_last": dt_end,
                    "solver": (f"Newton rtol {cfg.newton_rtol} / FGMRES({cfg.gmres_restart}) rtol "
-                              f"{cfg.gmres_rtol} / left-RAS {cfg.ras_box[:cfg.ndim]} overlap "
-                              f"{cfg.ras_overlap} local GMRES k={cfg.ras_local_k}"),
+                              f"{cfg.gmres_rtol} / {('left-RAS', 'AS', 'right-RAS')[cfg.ras_variant]} "
+                              f"{cfg.ras_box[:cfg.ndim]} overlap {cfg.ras_overlap} "
+                              + (f"local GMRES k={cfg.ras_local_k}" if cfg.ras_local_solver == 0
+                                 else f"ILU({cfg.ras_ilu_level})" if cfg.ras_local_solver == 1
+                                 else "LU")
+                              + (" factors reused per step" if cfg.ras_local_solver and
+                                 cfg.ras_ilu_reuse else "")
+                              + (", mobility 1-phi^2" if cfg.mobility else "")),
                    "parallelism": f"{ws} independent replica(s)",
                    "l2": "step working set (61-field Krylov basis, 0.5 GB) > 126 MB L2; no flush"},
         "newton_its": newton, "gmres_its": gmres,
@@ -358,17 +371,7 @@ def bench_reference(args):
     from oracle import oracle as O
     from paper_1703_01202_b200.inputs import CONFIGS
     O.build()
-    cfg = CONFIGS[args.config]
-    if args.mobility or args.ras_variant or args.ilu >= 0:   # NEXT-row measurements
-        import dataclasses
-        ilu = args.ilu >= 0
-        cfg = dataclasses.replace(cfg, mobility=args.mobility, ras_variant=args.ras_variant,
-                                  ras_local_solver=1 if ilu else 0,
-                                  ras_ilu_level=max(args.ilu, 0), ras_ilu_reuse=args.ilu_reuse,
-                                  name=cfg.name + (f"_mobility{args.mobility}" if args.mobility else "")
-                                  + (f"_ras{args.ras_variant}" if args.ras_variant else "")
-                                  + (f"_ilu{args.ilu}" + ("reuse" if args.ilu_reuse else "")
-                                     if ilu else ""))
+    cfg = variant_config(CONFIGS[args.config], args)
     W, K = args.warmup, args.steps
     phi = cfg.initial_condition()
     prm = O.params_from_config(cfg)
@@ -414,6 +417,7 @@ def main():
     ap.add_argument("--ras-variant", type=int, default=0, help="0 left-RAS, 1 AS, 2 right-RAS")
     ap.add_argument("--ilu", type=int, default=-1, help="k >= 0: ILU(k) subdomain solves (row f2)")
     ap.add_argument("--ilu-reuse", type=int, default=0, help="1: factors reused over a step")
+    ap.add_argument("--lu", action="store_true", help="exact LU subdomain solves (row f2)")
     args = ap.parse_args()
     if args.warmup < 3:
         print("note: --warmup < 3 is below the timing contract", file=sys.stderr)

@@ -69,9 +69,9 @@ typedef struct pfc_config {
   int ras_local_k;        /* fixed number of local GMRES steps in each subdomain solve (1..15) */
   int ras_variant;        /* Schwarz preconditioner (enum below; default PFC_RAS_LEFT) */
   int mobility;           /* PFC_MOBILITY_ONE (M = 1, default) or PFC_MOBILITY_QUADRATIC */
-  int ras_local_solver;   /* PFC_LOCAL_GMRES (default, reading R9) or PFC_LOCAL_ILU */
+  int ras_local_solver;   /* PFC_LOCAL_GMRES (default, reading R9), PFC_LOCAL_ILU, PFC_LOCAL_LU */
   int ras_ilu_level;      /* PFC_LOCAL_ILU: fill level k of ILU(k), 0..4 (Table 1) */
-  int ras_ilu_reuse;      /* PFC_LOCAL_ILU: 1 = factors of the step's first Newton iteration */
+  int ras_ilu_reuse;      /* ILU / LU: 1 = factors of the step's first Newton iteration */
 } pfc_config;
 
 /* Subdomain solve inv(A_k) of the Schwarz preconditioner:
@@ -81,8 +81,13 @@ typedef struct pfc_config {
  *                    P:872-909), U^{-1} L^{-1} per apply; with ras_ilu_reuse the factors of the
  *                    step's first Newton iteration (Phi_0 = phi^n) serve all its iterations
  *                    (P:910-915).  M = 1 only; usable at small dt for the configurations' h
- *                    (ILU(0) loses positive pivots near dt >= 0.5). */
-enum { PFC_LOCAL_GMRES = 0, PFC_LOCAL_ILU = 1 };
+ *                    (ILU(0) loses positive pivots near dt >= 0.5);
+ *   PFC_LOCAL_LU     the paper's LU (Table 1): the same factor path with unlimited fill, i.e.
+ *                    the exact factorisation of A_k in natural order (no pivoting: A_k of the
+ *                    configurations keeps positive pivots, eigenvalues in [1.9, 914] at dt=0.5,
+ *                    SURVEY App. A), reuse as above.  Band fill ~ 2 (3 E_x) per row: 2D ext
+ *                    boxes up to the shared-memory plan (EINVAL beyond, e.g. every 3D box). */
+enum { PFC_LOCAL_GMRES = 0, PFC_LOCAL_ILU = 1, PFC_LOCAL_LU = 2 };
 
 /* Mobility of Eq. (PFCeq) P:137-150 in the scheme's (grad . M_d grad)_d, P:208-212 (edge
  * midpoint value = average of the two end nodes), M_d = M((phi_new + phi_old)/2):

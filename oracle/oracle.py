@@ -39,7 +39,7 @@ class Params(C.Structure):
 
 RAS_LEFT, RAS_AS, RAS_RIGHT = 0, 1, 2
 MOB_ONE, MOB_QUADRATIC = 0, 1           # M = 1; M(phi) = 1 - phi^2
-LOCAL_GMRES, LOCAL_ILU = 0, 1           # R9; ILU(k) / LU (row f2)
+LOCAL_GMRES, LOCAL_ILU, LOCAL_LU = 0, 1, 2   # R9; ILU(k); LU = unlimited fill (f2)
 
 
 class NewtonInfo(C.Structure):

@@ -498,7 +498,8 @@ static void local_gmres(const local_op* L, const double* r, double* y, size_t n)
 
 /* inv(A_k) r by ILU(level) of the assembled A_k (row f2): A_k column q = the local operator
  * applied to the unit vector e_q (Eq. Ak P:422-428 with the modified BC, or R J R^T with
- * variable mobility), dense storage (test sizes). */
+ * variable mobility), dense storage (test sizes).  The paper's "LU" (Table 1) is the
+ * unlimited-fill case: level n keeps every fill entry, i.e. the exact factorisation. */
 static void local_ilu(const local_op* L, const double* r, double* y, size_t n) {
   double* A = alloc0(n * n);
   double* e = alloc0(n);
@@ -510,13 +511,13 @@ static void local_ilu(const local_op* L, const double* r, double* y, size_t n) {
     e[q] = 0.0;
   }
   double* LU = alloc0(n * n);
-  or_ilu_dense((int)n, A, L->p->ras_ilu_level, LU);
+  or_ilu_dense((int)n, A, L->p->ras_local_solver == 2 ? (int)n : L->p->ras_ilu_level, LU);
   ilu_solve((int)n, LU, r, y);
   free(A); free(e); free(col); free(LU);
 }
 
 static void local_solve(const local_op* L, const double* r, double* y, size_t n) {
-  if (L->p->ras_local_solver == 1) local_ilu(L, r, y, n);
+  if (L->p->ras_local_solver == 1 || L->p->ras_local_solver == 2) local_ilu(L, r, y, n);
   else local_gmres(L, r, y, n);
 }
 
@@ -658,7 +659,7 @@ int or_fgmres(const or_grid* g, const or_params* p, double dt, const double* pn,
       double* zj = Z + (size_t)j * N;
       /* ILU with reuse (R10): the subdomain matrices of the step's first Newton
        * iteration, Phi_0 = psi */
-      const double* pre = (p->ras_local_solver == 1 && p->ras_ilu_reuse) ? po : pn;
+      const double* pre = (p->ras_local_solver != 0 && p->ras_ilu_reuse) ? po : pn;
       if (precondition) or_ras_apply(g, p, dt, pre, po, V + (size_t)j * N, zj);
       else memcpy(zj, V + (size_t)j * N, N * sizeof(double));
       or_jacobian_apply_p(g, p, dt, pn, po, zj, w);

@@ -30,9 +30,9 @@ typedef struct {
   int ras_box[3], ras_overlap, ras_local_k;  /* Schwarz boxes, local GMRES(k) (R9) */
   int ras_variant;  /* 0 left-RAS, 1 classical AS, 2 right-RAS */
   int mobility;     /* 0: M = 1 (the configs); 1: M(phi) = 1 - phi^2 */
-  int ras_local_solver;  /* 0: fixed-work local GMRES (R9); 1: ILU(level) (row f2) */
+  int ras_local_solver;  /* 0: fixed-work local GMRES (R9); 1: ILU(level); 2: LU (row f2) */
   int ras_ilu_level;     /* fill level k of ILU(k) (Table 1); >= n gives LU */
-  int ras_ilu_reuse;     /* 1: subdomain factors of the step's first Newton iteration */
+  int ras_ilu_reuse;     /* 1 (ILU / LU): factors of the step's first Newton iteration */
 } or_params;
 
 typedef struct {

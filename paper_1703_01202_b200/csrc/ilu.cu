@@ -280,8 +280,9 @@ pfc_status ilu_setup(pfc_ctx* ctx) {
               meta[r][pos(ii, jj, kk)] = {cl, ct};
             }
       }
-  // ILU(k) fill levels, row by row (rows k < i are final when row i is processed)
-  const int level = c.ras_ilu_level;
+  // ILU(k) fill levels, row by row (rows k < i are final when row i is processed); the paper's
+  // LU (Table 1) keeps every fill entry: the exact factorisation in natural order
+  const int level = c.ras_local_solver == PFC_LOCAL_LU ? n : c.ras_ilu_level;
   for (int i = 0; i < n; ++i) {
     auto& ri = rows[i];
     for (auto it = ri.begin(); it != ri.end() && it->first < i; ++it) {

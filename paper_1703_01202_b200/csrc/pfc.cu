@@ -140,7 +140,7 @@ cudaError_t launch_jac_state(pfc_ctx* ctx, const double* phi_new, const double* 
 int ras_plan(pfc_ctx* ctx) { return ctx->cfg.ndim == 2 ? ras2d_plan(ctx) : ras3d_plan(ctx); }
 
 cudaError_t launch_ras(pfc_ctx* ctx, const double* v, const double* c, double dt, double* z) {
-  if (ctx->cfg.ras_local_solver == PFC_LOCAL_ILU) return launch_ras_ilu(ctx, v, z);
+  if (ctx->cfg.ras_local_solver != PFC_LOCAL_GMRES) return launch_ras_ilu(ctx, v, z);
   if (ctx->cfg.ndim == 2) return launch_ras_2d(ctx, v, c, dt, z);
   return ctx->ras3_col ? launch_ras_3d_col(ctx, v, c, dt, z, ctx->ras_scratch)
                        : launch_ras_3d(ctx, v, c, dt, z, ctx->ras_scratch);
@@ -369,7 +369,7 @@ static pfc_status newton(pfc_ctx* ctx, double dt, pfc_step_info* inf) {
       return pfc_fail(ctx, PFC_ENOCONV, "Newton: newton_maxit reached");
     }
     KL(PFC_K_COEF, launch_jac_state(ctx, ctx->phi, ctx->psi), "coef");
-    if (c.ras_local_solver == PFC_LOCAL_ILU && (!c.ras_ilu_reuse || inf->newton_its == 0))
+    if (c.ras_local_solver != PFC_LOCAL_GMRES && (!c.ras_ilu_reuse || inf->newton_its == 0))
       KL(PFC_K_RAS, launch_ilu_factor(ctx, ctx->c, dt), "ilu factor");
     int its = 0;
     s = fgmres(ctx, dt, nrm, &its);
@@ -465,12 +465,13 @@ static pfc_status validate(const pfc_config& c, std::string* why) {
     return bad("ras_variant must be PFC_RAS_LEFT, PFC_RAS_AS or PFC_RAS_RIGHT");
   if (c.mobility != PFC_MOBILITY_ONE && c.mobility != PFC_MOBILITY_QUADRATIC)
     return bad("mobility must be PFC_MOBILITY_ONE or PFC_MOBILITY_QUADRATIC");
-  if (c.ras_local_solver != PFC_LOCAL_GMRES && c.ras_local_solver != PFC_LOCAL_ILU)
-    return bad("ras_local_solver must be PFC_LOCAL_GMRES or PFC_LOCAL_ILU");
+  if (c.ras_local_solver != PFC_LOCAL_GMRES && c.ras_local_solver != PFC_LOCAL_ILU &&
+      c.ras_local_solver != PFC_LOCAL_LU)
+    return bad("ras_local_solver must be PFC_LOCAL_GMRES, PFC_LOCAL_ILU or PFC_LOCAL_LU");
   if (c.ras_local_solver == PFC_LOCAL_ILU && (c.ras_ilu_level < 0 || c.ras_ilu_level > 4))
     return bad("ras_ilu_level in [0,4]");
-  if (c.ras_local_solver == PFC_LOCAL_ILU && c.mobility != PFC_MOBILITY_ONE)
-    return bad("PFC_LOCAL_ILU is built for PFC_MOBILITY_ONE");
+  if (c.ras_local_solver != PFC_LOCAL_GMRES && c.mobility != PFC_MOBILITY_ONE)
+    return bad("PFC_LOCAL_ILU / PFC_LOCAL_LU are built for PFC_MOBILITY_ONE");
   if (c.gmres_restart < 1 || c.gmres_restart > PFC_MAX_RESTART) return bad("gmres_restart in [1,32]");
   if (c.gmres_maxit < 1 || c.newton_maxit < 0) return bad("iteration limits must be positive");
   if (!(c.newton_rtol >= 0 && c.newton_atol >= 0 && c.gmres_rtol >= 0 && c.gmres_atol >= 0))
@@ -555,7 +556,7 @@ pfc_status pfc_create(const pfc_config* cfg, void* stream, pfc_ctx** out) {
       pfc_check_cuda(ctx, cudaMalloc(&ctx->ras_y, ras_ext_doubles(ctx) * sizeof(double)),
                      "ras ext-box solutions"))
     return fail(PFC_ENOMEM);
-  if (c.ras_local_solver == PFC_LOCAL_ILU) {
+  if (c.ras_local_solver != PFC_LOCAL_GMRES) {
     pfc_status si = ilu_setup(ctx);
     if (si) return fail(si);
   }
@@ -647,7 +648,7 @@ pfc_status pfc_ras_apply(pfc_ctx* ctx, const double* phi_new, const double* phi_
   pfc_status s = check_fields(ctx, dt, {phi_new, phi_old, v}, z);
   if (s) return s;
   KL(PFC_K_COEF, launch_jac_state(ctx, phi_new, phi_old), "pfc_ras_apply coef");
-  if (ctx->cfg.ras_local_solver == PFC_LOCAL_ILU)
+  if (ctx->cfg.ras_local_solver != PFC_LOCAL_GMRES)
     KL(PFC_K_RAS, launch_ilu_factor(ctx, ctx->c, dt), "pfc_ras_apply ilu factor");
   KL(PFC_K_RAS, launch_ras(ctx, v, ctx->c, dt, z), "pfc_ras_apply");
   return PFC_OK;

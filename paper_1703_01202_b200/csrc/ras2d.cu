@@ -904,14 +904,12 @@ cudaError_t launch_ras_2d(pfc_ctx* ctx, const double* v, const double* c, double
     p.W[4] = -0.5 * ih6;
     p.W[5] = -1.5 * ih6;
     p.ih2 = ih2;
-    static int nsm = 0;
-    if (!nsm) {
-      int dev = 0;
-      if (cudaGetDevice(&dev) != cudaSuccess ||
-          cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
-        nsm = 148;
-    }
-    fn<<<std::min(nb, nsm), ctx->ras_threads, ctx->ras_smem, ctx->stream>>>(p);   // persistent
+    int nsm = 148, per_sm = 1;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, ctx->device);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, ctx->ras_threads,
+                                                      ctx->ras_smem) != cudaSuccess || per_sm < 1)
+      per_sm = 1;
+    fn<<<std::min(nb, nsm * per_sm), ctx->ras_threads, ctx->ras_smem, ctx->stream>>>(p);   // persistent
   } else {
     ras2d_fn fn = pick(cf.ras_local_k);
     if (!fn) return cudaErrorInvalidValue;

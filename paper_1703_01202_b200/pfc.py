@@ -35,7 +35,7 @@ class PfcConfig(C.Structure):
 
 PFC_RAS_LEFT, PFC_RAS_AS, PFC_RAS_RIGHT = 0, 1, 2   # include/pfc.h
 PFC_MOBILITY_ONE, PFC_MOBILITY_QUADRATIC = 0, 1     # include/pfc.h (M = 1; M = 1 - phi^2)
-PFC_LOCAL_GMRES, PFC_LOCAL_ILU = 0, 1               # include/pfc.h (R9; ILU(k))
+PFC_LOCAL_GMRES, PFC_LOCAL_ILU, PFC_LOCAL_LU = 0, 1, 2   # include/pfc.h (R9; ILU(k); LU)
 
 
 class PfcStepInfo(C.Structure):
@@ -98,7 +98,7 @@ def make_config(cfg=None, **over) -> PfcConfig:
     Keyword overrides use the field names of include/pfc.h, e.g. ndim, n, h, gamma, adaptive,
     dt_min, dt_max, eta, newton_rtol, gmres_restart, ras_box, ras_overlap, ras_local_k,
     ras_variant (PFC_RAS_LEFT / _AS / _RIGHT), mobility (PFC_MOBILITY_ONE / _QUADRATIC),
-    ras_local_solver (PFC_LOCAL_GMRES / _ILU), ras_ilu_level, ras_ilu_reuse."""
+    ras_local_solver (PFC_LOCAL_GMRES / _ILU / _LU), ras_ilu_level, ras_ilu_reuse."""
     L = load()
     c = PfcConfig()
     L.pfc_config_default(C.byref(c))

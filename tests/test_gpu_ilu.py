@@ -87,3 +87,46 @@ def test_ilu_argument_errors():
         ctx_ilu((64, 64), (16, 16), 2, 5)
     with pytest.raises(P.PfcError):
         ctx_ilu((64, 64), (16, 16), 2, 0, mobility=P.PFC_MOBILITY_QUADRATIC)
+
+
+@pytest.mark.parametrize("variant", [P.PFC_RAS_LEFT, P.PFC_RAS_AS, P.PFC_RAS_RIGHT])
+@pytest.mark.parametrize("shape,box,o", [((64, 64), (16, 16), 2), ((48, 36), (12, 12), 1)])
+def test_lu_schwarz_parity(shape, box, o, variant):
+    """PFC_LOCAL_LU (the paper's LU, Table 1): exact factorisation of A_k, at dt = 0.5 where
+    ILU(0) has lost its positive pivots."""
+    phi = random_field(shape, 611, 0.07, 0.07)
+    psi = random_field(shape, 612, 0.07, 0.07)
+    v = random_field(shape, 613, 0.0, 1.0)
+    dt = 0.5
+    nd = len(shape)
+    ctx = P.Context(None, ndim=nd, n=shape, h=H, gamma=G, ras_box=list(box) + [1], ras_overlap=o,
+                    ras_local_solver=P.PFC_LOCAL_LU, ras_variant=variant)
+    z = host(ctx.ras_apply(dev(phi), dev(psi), dt, dev(v)))
+    zo = O.ras_apply(phi, psi, v, H, O.params(gamma=G, ras_box=box, ras_overlap=o,
+                                              ras_local_solver=O.LOCAL_LU, ras_variant=variant), dt)
+    assert rel(z, zo) <= 1e-12
+
+
+@pytest.mark.parametrize("reuse", [0, 1])
+def test_lu_one_step_parity(reuse):
+    shape = (64, 64)
+    phi0 = random_field(shape, 1, 0.07, 0.07)
+    dt = 0.5
+    ctx = P.Context(None, ndim=2, n=shape, h=H, gamma=G, ras_box=[16, 16, 1], ras_overlap=2,
+                    ras_local_solver=P.PFC_LOCAL_LU, ras_ilu_reuse=reuse)
+    phi = dev(phi0)
+    _, info = ctx.step(phi, dt)
+    ref, ok, oinfo = O.newton(phi0, H, O.params(gamma=G, ras_box=(16, 16), ras_overlap=2,
+                                                ras_local_solver=O.LOCAL_LU, ras_ilu_reuse=reuse),
+                              dt)
+    assert ok and info["converged"]
+    assert info["newton_its"] == oinfo.newton_its and info["gmres_its"] == oinfo.gmres_its
+    assert rel(host(phi), ref) <= 1e-10
+
+
+def test_lu_3d_box_beyond_the_plan_is_einval():
+    """3D LU fill (~2 x 3 E_x E_y per row) exceeds the shared-memory plan: EINVAL, not a
+    silent fallback (the paper reports LU as the most expensive subdomain solve, Table 1)."""
+    with pytest.raises(P.PfcError):
+        P.Context(None, ndim=3, n=(24, 24, 24), h=H, gamma=G, ras_box=[8, 8, 8], ras_overlap=1,
+                  ras_local_solver=P.PFC_LOCAL_LU)

@@ -109,3 +109,36 @@ def test_newton_with_ilu0_solves_the_same_scheme(reuse):
                                                 ras_ilu_reuse=reuse, **base), dt)
     assert ok and ok2 and info.newton_its >= 1
     assert rel(new, ref) < 1e-9
+
+
+@pytest.mark.parametrize("shape,box,o", [((16, 16), (4, 4), 1), ((6, 6, 6), (3, 3, 3), 1)])
+def test_lu_local_solver_is_exact(shape, box, o):
+    """LOCAL_LU (the paper's "LU", Table 1) is the unlimited-fill factorisation:
+    identical to ILU(n), and equal to the dense Schwarz apply with exact local solves."""
+    phi = random_field(shape, 521, 0.07, 0.3)
+    psi = random_field(shape, 522, 0.07, 0.3)
+    v = random_field(shape, 523)
+    n = int(np.prod([b + 2 * o for b in box]))
+    common = dict(gamma=GAMMA, ras_box=box, ras_overlap=o)
+    z_lu = O.ras_apply(phi, psi, v, H, O.params(ras_local_solver=O.LOCAL_LU, **common), 0.5)
+    z_iln = O.ras_apply(phi, psi, v, H, O.params(ras_local_solver=O.LOCAL_ILU, ras_ilu_level=n,
+                                                 **common), 0.5)
+    assert np.array_equal(z_lu, z_iln)
+    z_ex = O.ras_apply(phi, psi, v, H, O.params(ras_local_k=n, **common), 0.5)
+    assert rel(z_lu, z_ex) < 1e-9
+
+
+def test_newton_with_lu_at_large_dt():
+    """At dt = 0.5, where ILU(0) stalls at these h, exact local LU with
+    overlap 2 keeps FGMRES at a few iterations per Newton step (App. A: 4) and reaches the
+    same solution as the GMRES(k)-preconditioned step."""
+    shape = (32, 32)
+    phi0 = random_field(shape, 531, 0.07, 0.07)
+    dt = 0.5
+    base = dict(gamma=GAMMA, ras_box=(16, 16), ras_overlap=2, newton_rtol=1e-12, newton_atol=1e-14)
+    ref, ok, _ = O.newton(phi0, H, O.params(**base), dt)
+    new, ok2, info = O.newton(phi0, H, O.params(ras_local_solver=O.LOCAL_LU, ras_ilu_reuse=1,
+                                                **base), dt)
+    assert ok and ok2 and info.newton_its >= 1
+    assert info.gmres_its <= 8 * info.newton_its
+    assert rel(new, ref) < 1e-9
