@@ -25,7 +25,7 @@ def build(force: bool = False) -> str:
 
 
 class Grid(C.Structure):
-    _fields_ = [("nd", C.c_int), ("n", C.c_int * 3), ("h", C.c_double)]
+    _fields_ = [("nd", C.c_int), ("n", C.c_int * 3), ("h", C.c_double), ("bc", C.c_int)]
 
 
 class Params(C.Structure):
@@ -40,6 +40,7 @@ class Params(C.Structure):
 RAS_LEFT, RAS_AS, RAS_RIGHT = 0, 1, 2
 MOB_ONE, MOB_QUADRATIC = 0, 1           # M = 1; M(phi) = 1 - phi^2
 LOCAL_GMRES, LOCAL_ILU, LOCAL_LU = 0, 1, 2   # R9; ILU(k); LU = unlimited fill (f2)
+BC_PERIODIC, BC_MIRROR = 0, 1           # P:125; Neumann-type mirror ghosts (row f3, R23)
 
 
 class NewtonInfo(C.Structure):
@@ -82,9 +83,9 @@ def lib():
     return _lib
 
 
-def _grid(shape, h):
+def _grid(shape, h, bc=0):
     n = list(shape) + [1] * (3 - len(shape))
-    return Grid(len(shape), (C.c_int * 3)(*n), h)
+    return Grid(len(shape), (C.c_int * 3)(*n), h, int(bc))
 
 
 def _ptr(a):
@@ -103,12 +104,16 @@ def _shape(a):
 def params(gamma=0.25, newton_rtol=1e-10, newton_atol=1e-10, newton_maxit=50, ls_c1=1e-4,
            ls_min_lambda=1e-12, gmres_restart=30, gmres_maxit=300, gmres_rtol=1e-3,
            gmres_atol=1e-11, ras_box=(16, 16, 1), ras_overlap=2, ras_local_k=10, ras_variant=0,
-           mobility=0, ras_local_solver=0, ras_ilu_level=0, ras_ilu_reuse=0, **_ignored):
+           mobility=0, ras_local_solver=0, ras_ilu_level=0, ras_ilu_reuse=0, bc=0, **_ignored):
+    """bc (BC_PERIODIC / BC_MIRROR) travels with the parameters into the grid of every call
+    that takes them (or_grid.bc, reading R23)."""
     b = list(ras_box) + [1] * (3 - len(ras_box))
-    return Params(gamma, newton_rtol, newton_atol, newton_maxit, ls_c1, ls_min_lambda,
-                  gmres_restart, gmres_maxit, gmres_rtol, gmres_atol, (C.c_int * 3)(*b),
-                  ras_overlap, ras_local_k, ras_variant, mobility, ras_local_solver,
-                  ras_ilu_level, ras_ilu_reuse)
+    p = Params(gamma, newton_rtol, newton_atol, newton_maxit, ls_c1, ls_min_lambda,
+               gmres_restart, gmres_maxit, gmres_rtol, gmres_atol, (C.c_int * 3)(*b),
+               ras_overlap, ras_local_k, ras_variant, mobility, ras_local_solver,
+               ras_ilu_level, ras_ilu_reuse)
+    p.bc = int(bc)
+    return p
 
 
 def params_from_config(cfg, **over):
@@ -119,59 +124,59 @@ def params_from_config(cfg, **over):
               ras_variant=getattr(cfg, "ras_variant", 0), mobility=getattr(cfg, "mobility", 0),
               ras_local_solver=getattr(cfg, "ras_local_solver", 0),
               ras_ilu_level=getattr(cfg, "ras_ilu_level", 0),
-              ras_ilu_reuse=getattr(cfg, "ras_ilu_reuse", 0))
+              ras_ilu_reuse=getattr(cfg, "ras_ilu_reuse", 0), bc=getattr(cfg, "bc", 0))
     kw.update(over)
     return params(**kw)
 
 
-def laplacian(f, h):
+def laplacian(f, h, bc=0):
     f = _f(f); out = np.empty_like(f)
-    lib().or_laplacian(C.byref(_grid(_shape(f), h)), _ptr(f), _ptr(out))
+    lib().or_laplacian(C.byref(_grid(_shape(f), h, bc)), _ptr(f), _ptr(out))
     return out
 
 
-def dvd_derivative(phi_new, phi_old, h, gamma):
+def dvd_derivative(phi_new, phi_old, h, gamma, bc=0):
     a, b = _f(phi_new), _f(phi_old); out = np.empty_like(a)
-    lib().or_dvd_derivative(C.byref(_grid(_shape(a), h)), gamma, _ptr(a), _ptr(b), _ptr(out))
+    lib().or_dvd_derivative(C.byref(_grid(_shape(a), h, bc)), gamma, _ptr(a), _ptr(b), _ptr(out))
     return out
 
 
-def residual(phi_new, phi_old, h, gamma, dt):
+def residual(phi_new, phi_old, h, gamma, dt, bc=0):
     a, b = _f(phi_new), _f(phi_old); out = np.empty_like(a)
-    lib().or_residual(C.byref(_grid(_shape(a), h)), gamma, dt, _ptr(a), _ptr(b), _ptr(out))
+    lib().or_residual(C.byref(_grid(_shape(a), h, bc)), gamma, dt, _ptr(a), _ptr(b), _ptr(out))
     return out
 
 
-def jacobian_apply(phi_new, phi_old, v, h, gamma, dt):
+def jacobian_apply(phi_new, phi_old, v, h, gamma, dt, bc=0):
     a, b, v = _f(phi_new), _f(phi_old), _f(v); out = np.empty_like(a)
-    lib().or_jacobian_apply(C.byref(_grid(_shape(a), h)), gamma, dt, _ptr(a), _ptr(b), _ptr(v),
+    lib().or_jacobian_apply(C.byref(_grid(_shape(a), h, bc)), gamma, dt, _ptr(a), _ptr(b), _ptr(v),
                             _ptr(out))
     return out
 
 
-def div_mgrad(M, f, h):
+def div_mgrad(M, f, h, bc=0):
     """(grad . M grad)_d f with edge-averaged M."""
     m, f = _f(M), _f(f); out = np.empty_like(f)
-    lib().or_div_mgrad(C.byref(_grid(_shape(f), h)), _ptr(m), _ptr(f), _ptr(out))
+    lib().or_div_mgrad(C.byref(_grid(_shape(f), h, bc)), _ptr(m), _ptr(f), _ptr(out))
     return out
 
 
-def mobility_field(phi_new, phi_old, h, mobility):
+def mobility_field(phi_new, phi_old, h, mobility, bc=0):
     a, b = _f(phi_new), _f(phi_old); out = np.empty_like(a)
-    lib().or_mobility(C.byref(_grid(_shape(a), h)), int(mobility), _ptr(a), _ptr(b), _ptr(out))
+    lib().or_mobility(C.byref(_grid(_shape(a), h, bc)), int(mobility), _ptr(a), _ptr(b), _ptr(out))
     return out
 
 
 def residual_p(phi_new, phi_old, h, prm, dt):
     """Residual of Eq. NSOP with prm.mobility."""
     a, b = _f(phi_new), _f(phi_old); out = np.empty_like(a)
-    lib().or_residual_p(C.byref(_grid(_shape(a), h)), C.byref(prm), dt, _ptr(a), _ptr(b), _ptr(out))
+    lib().or_residual_p(C.byref(_grid(_shape(a), h, getattr(prm, 'bc', 0))), C.byref(prm), dt, _ptr(a), _ptr(b), _ptr(out))
     return out
 
 
 def jacobian_apply_p(phi_new, phi_old, v, h, prm, dt):
     a, b, v = _f(phi_new), _f(phi_old), _f(v); out = np.empty_like(a)
-    lib().or_jacobian_apply_p(C.byref(_grid(_shape(a), h)), C.byref(prm), dt, _ptr(a), _ptr(b),
+    lib().or_jacobian_apply_p(C.byref(_grid(_shape(a), h, getattr(prm, 'bc', 0))), C.byref(prm), dt, _ptr(a), _ptr(b),
                               _ptr(v), _ptr(out))
     return out
 
@@ -185,26 +190,26 @@ def ilu_dense(A, level):
     return LU
 
 
-def local_energy(phi, h, gamma):
+def local_energy(phi, h, gamma, bc=0):
     a = _f(phi); out = np.empty_like(a)
-    lib().or_local_energy(C.byref(_grid(_shape(a), h)), gamma, _ptr(a), _ptr(out))
+    lib().or_local_energy(C.byref(_grid(_shape(a), h, bc)), gamma, _ptr(a), _ptr(out))
     return out
 
 
-def free_energy(phi, h, gamma):
+def free_energy(phi, h, gamma, bc=0):
     a = _f(phi)
-    return lib().or_free_energy(C.byref(_grid(_shape(a), h)), gamma, _ptr(a))
+    return lib().or_free_energy(C.byref(_grid(_shape(a), h, bc)), gamma, _ptr(a))
 
 
-def mass(phi, h):
+def mass(phi, h, bc=0):
     a = _f(phi)
-    return lib().or_mass(C.byref(_grid(_shape(a), h)), _ptr(a))
+    return lib().or_mass(C.byref(_grid(_shape(a), h, bc)), _ptr(a))
 
 
 def local_jacobian_apply(shape, h, prm, dt, c_loc, v_loc):
     """A_k v on one ext box (modified BC); c_loc, v_loc on the ext box."""
     c, v = _f(c_loc), _f(v_loc); out = np.empty_like(v)
-    lib().or_local_jacobian_apply(C.byref(_grid(shape, h)), C.byref(prm), dt, _ptr(c), _ptr(v),
+    lib().or_local_jacobian_apply(C.byref(_grid(shape, h, getattr(prm, 'bc', 0))), C.byref(prm), dt, _ptr(c), _ptr(v),
                                   _ptr(out))
     return out
 
@@ -212,7 +217,7 @@ def local_jacobian_apply(shape, h, prm, dt, c_loc, v_loc):
 def ras_apply(phi_new, phi_old, v, h, prm, dt):
     """Schwarz preconditioner apply; prm.ras_variant selects left-RAS / AS / right-RAS."""
     a, b, v = _f(phi_new), _f(phi_old), _f(v); out = np.zeros_like(a)
-    lib().or_ras_apply(C.byref(_grid(_shape(a), h)), C.byref(prm), dt, _ptr(a), _ptr(b), _ptr(v),
+    lib().or_ras_apply(C.byref(_grid(_shape(a), h, getattr(prm, 'bc', 0))), C.byref(prm), dt, _ptr(a), _ptr(b), _ptr(v),
                        _ptr(out))
     return out
 
@@ -223,14 +228,14 @@ def ras_apply_box(phi_new, phi_old, v, h, prm, dt, box):
     nd = a.ndim
     shp = tuple(reversed([prm.ras_box[d] for d in range(nd)]))
     out = np.zeros(shp)
-    lib().or_ras_apply_box(C.byref(_grid(_shape(a), h)), C.byref(prm), dt, _ptr(a), _ptr(b),
+    lib().or_ras_apply_box(C.byref(_grid(_shape(a), h, getattr(prm, 'bc', 0))), C.byref(prm), dt, _ptr(a), _ptr(b),
                            _ptr(v), int(box), _ptr(out))
     return out
 
 
 def fgmres(phi_new, phi_old, b, h, prm, dt, precondition=True):
     a, o, b = _f(phi_new), _f(phi_old), _f(b); x = np.zeros_like(a); its = C.c_int(0)
-    ok = lib().or_fgmres(C.byref(_grid(_shape(a), h)), C.byref(prm), dt, _ptr(a), _ptr(o), _ptr(b),
+    ok = lib().or_fgmres(C.byref(_grid(_shape(a), h, getattr(prm, 'bc', 0))), C.byref(prm), dt, _ptr(a), _ptr(o), _ptr(b),
                          _ptr(x), int(precondition), C.byref(its))
     return x, bool(ok), its.value
 
@@ -238,7 +243,7 @@ def fgmres(phi_new, phi_old, b, h, prm, dt, precondition=True):
 def newton(phi_old, h, prm, dt, source=None):
     o = _f(phi_old); x = np.empty_like(o); info = NewtonInfo()
     src = _ptr(_f(source)) if source is not None else None
-    ok = lib().or_newton(C.byref(_grid(_shape(o), h)), C.byref(prm), dt, _ptr(o), src, _ptr(x),
+    ok = lib().or_newton(C.byref(_grid(_shape(o), h, getattr(prm, 'bc', 0))), C.byref(prm), dt, _ptr(o), src, _ptr(x),
                          C.byref(info))
     return x, bool(ok), info
 
@@ -250,9 +255,10 @@ def next_dt(dt_min, dt_max, eta, F_n, F_nm1, dt_nm1):
 def step(phi, h, prm, dt, gamma=None):
     """One time step n -> n+1 (Newton solve of Eq. NSOP) plus F_d before/after."""
     g = prm.gamma if gamma is None else gamma
-    F_n = free_energy(phi, h, g)
+    bc = getattr(prm, "bc", 0)
+    F_n = free_energy(phi, h, g, bc)
     new, ok, info = newton(phi, h, prm, dt)
-    return new, ok, info, F_n, free_energy(new, h, g)
+    return new, ok, info, F_n, free_energy(new, h, g, bc)
 
 
 def run(cfg, phi0, steps, prm=None, record=None):

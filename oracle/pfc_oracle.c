@@ -27,9 +27,26 @@ static int wrapi(int i, int n) {      /* periodic index, P:125 periodic BCs */
   return r < 0 ? r + n : r;
 }
 
+/* mirror index (reading R23): the cell-centred nodes x_i = (i+1/2)h (R2) reflected across the
+ * boundary faces x = 0 and x = L, i.e. the even extension; stencil offsets are <= 3 < n */
+static int mirrori(int i, int n) {
+  if (i < 0) return -1 - i;
+  if (i >= n) return 2 * n - 1 - i;
+  return i;
+}
+
+static int axisi(const or_grid* g, int i, int n) { return g->bc ? mirrori(i, n) : wrapi(i, n); }
+
 static size_t gidx(const or_grid* g, int i, int j, int k) {
-  return (size_t)wrapi(i, g->n[0]) +
-         (size_t)g->n[0] * ((size_t)wrapi(j, g->n[1]) + (size_t)g->n[1] * wrapi(k, g->n[2]));
+  return (size_t)axisi(g, i, g->n[0]) +
+         (size_t)g->n[0] * ((size_t)axisi(g, j, g->n[1]) + (size_t)g->n[1] * axisi(g, k, g->n[2]));
+}
+
+/* with mirror BCs the subdomains are clipped at the physical boundary (R23): an ext-box node
+ * outside the domain is no unknown of A_k */
+static int in_domain(const or_grid* g, int i, int j, int k) {
+  if (!g->bc) return 1;
+  return i >= 0 && i < g->n[0] && j >= 0 && j < g->n[1] && k >= 0 && k < g->n[2];
 }
 
 static double* alloc0(size_t n) { return (double*)calloc(n ? n : 1, sizeof(double)); }
@@ -57,7 +74,7 @@ double or_norm2(size_t n, const double* x) {          /* Euclidean norm, R6 */
 /* -------------------------------------------------- difference operators P:199-207 */
 
 /* Delta_d = sum over axes of D^<2>, D_x^<2> phi_i = (phi_{i+1} - 2 phi_i + phi_{i-1})/dx^2
- * (P:201), periodic. */
+ * (P:201), periodic or mirror ghosts (g->bc, R23). */
 void or_laplacian(const or_grid* g, const double* f, double* out) {
   const double ih2 = 1.0 / (g->h * g->h);
   for (int k = 0; k < g->n[2]; ++k)
@@ -406,17 +423,19 @@ static void givens(double a, double b, double* c, double* s) {
   *c = a / r; *s = b / r;
 }
 
-/* The subdomain operator of one box.  M = 1: or_local_jacobian_apply (zero ring on the
- * padded grid, R8).  Variable mobility: A_k = R_k^delta J (R_k^delta)^T, the "directly
- * generated" subdomain matrix of Eq. (Ak) P:422-428 (reading R8b): v_loc extended by zero to
- * the whole grid, the global J of or_jacobian_apply_p, restricted to the ext box. */
+/* The subdomain operator of one box.  M = 1, periodic: or_local_jacobian_apply (zero ring on
+ * the padded grid, R8).  Variable mobility or mirror BCs: A_k = R_k^delta J (R_k^delta)^T, the
+ * "directly generated" subdomain matrix of Eq. (Ak) P:422-428 (readings R8b, R23): v_loc
+ * extended by zero to the whole grid, the global J of or_jacobian_apply_p, restricted to the
+ * ext box; ext-box nodes outside the domain (mirror BCs) are no unknowns: never scattered, and
+ * their rows are zero. */
 typedef struct {
   const or_grid* g; const or_params* p; double dt; const double* c_loc;
   const double* pn; const double* po; int x0, y0, z0, E[3];
 } local_op;
 
 static void local_apply(const local_op* L, const double* v_loc, double* w_loc) {
-  if (!L->p->mobility) {
+  if (!L->p->mobility && !L->g->bc) {
     or_local_jacobian_apply(L->g, L->p, L->dt, L->c_loc, v_loc, w_loc);
     return;
   }
@@ -426,14 +445,16 @@ static void local_apply(const local_op* L, const double* v_loc, double* w_loc) {
   for (int k = 0; k < L->E[2]; ++k)                  /* (R_k^delta)^T v_loc */
     for (int j = 0; j < L->E[1]; ++j)
       for (int i = 0; i < L->E[0]; ++i)
-        vg[gidx(L->g, L->x0 + i, L->y0 + j, L->z0 + k)] =
-            v_loc[(size_t)i + (size_t)L->E[0] * ((size_t)j + (size_t)L->E[1] * k)];
+        if (in_domain(L->g, L->x0 + i, L->y0 + j, L->z0 + k))
+          vg[gidx(L->g, L->x0 + i, L->y0 + j, L->z0 + k)] =
+              v_loc[(size_t)i + (size_t)L->E[0] * ((size_t)j + (size_t)L->E[1] * k)];
   or_jacobian_apply_p(L->g, L->p, L->dt, L->pn, L->po, vg, wg);
   for (int k = 0; k < L->E[2]; ++k)                  /* R_k^delta */
     for (int j = 0; j < L->E[1]; ++j)
       for (int i = 0; i < L->E[0]; ++i)
         w_loc[(size_t)i + (size_t)L->E[0] * ((size_t)j + (size_t)L->E[1] * k)] =
-            wg[gidx(L->g, L->x0 + i, L->y0 + j, L->z0 + k)];
+            in_domain(L->g, L->x0 + i, L->y0 + j, L->z0 + k)
+                ? wg[gidx(L->g, L->x0 + i, L->y0 + j, L->z0 + k)] : 0.0;
   free(vg); free(wg);
 }
 
@@ -510,6 +531,10 @@ static void local_ilu(const local_op* L, const double* r, double* y, size_t n) {
     for (size_t i = 0; i < n; ++i) A[i * n + q] = col[i];
     e[q] = 0.0;
   }
+  for (size_t q = 0; q < n; ++q) {   /* ext-box nodes outside the domain (R23): identity rows */
+    const int i = (int)(q % L->E[0]), j = (int)((q / L->E[0]) % L->E[1]), k = (int)(q / ((size_t)L->E[0] * L->E[1]));
+    if (!in_domain(L->g, L->x0 + i, L->y0 + j, L->z0 + k)) A[q * n + q] = 1.0;
+  }
   double* LU = alloc0(n * n);
   or_ilu_dense((int)n, A, L->p->ras_local_solver == 2 ? (int)n : L->p->ras_ilu_level, LU);
   ilu_solve((int)n, LU, r, y);
@@ -526,7 +551,8 @@ static void local_solve(const local_op* L, const double* r, double* y, size_t n)
  *   1  classical AS  z = sum_k (R_k^delta)^T inv(A_k) R_k^delta v    Eq. (invM)
  *   2  right-RAS     z = sum_k (R_k^delta)^T inv(A_k) R_k^0 v        Eq. (eq:ash)
  * Boxes Omega_k of ras_box nodes in lexicographic (x-fastest) order; Omega_k^delta
- * extends each by ras_overlap mesh layers (R7) with periodic wrap; inv(A_k) is the
+ * extends each by ras_overlap mesh layers (R7) with periodic wrap (mirror BCs: clipped at the
+ * physical boundary, R23); inv(A_k) is the
  * fixed-work local GMRES (R9).  R_k^delta keeps the ext-box entries of v, R_k^0 only the
  * owned ones (zeros elsewhere on the ext box); (R_k^0)^T writes only the owned
  * nodes (disjoint), (R_k^delta)^T adds the whole ext-box solution into z,
@@ -558,7 +584,8 @@ void or_ras_apply(const or_grid* g, const or_params* p, double dt, const double*
               size_t l = (size_t)i + (size_t)E[0] * ((size_t)j + (size_t)E[1] * k);
               int owned = i >= o[0] && i < o[0] + b[0] && j >= o[1] && j < o[1] + b[1] &&
                           k >= o[2] && k < o[2] + b[2];
-              r[l] = (restrict_owned && !owned) ? 0.0 : v[q];
+              int act = in_domain(g, x0 + i, y0 + j, z0 + k);
+              r[l] = ((restrict_owned && !owned) || !act) ? 0.0 : v[q];
               c[l] = (3.0 * pn[q] * pn[q] + 2.0 * pn[q] * po[q] + po[q] * po[q]) / 4.0;
             }
         local_op L = {g, p, dt, c, pn, po, x0, y0, z0, {E[0], E[1], E[2]}};
@@ -575,7 +602,7 @@ void or_ras_apply(const or_grid* g, const or_params* p, double dt, const double*
             for (int j = 0; j < E[1]; ++j)
               for (int i = 0; i < E[0]; ++i) {
                 size_t l = (size_t)i + (size_t)E[0] * ((size_t)j + (size_t)E[1] * k);
-                z[gidx(g, x0 + i, y0 + j, z0 + k)] += y[l];
+                if (in_domain(g, x0 + i, y0 + j, z0 + k)) z[gidx(g, x0 + i, y0 + j, z0 + k)] += y[l];
               }
         }
       }
@@ -606,7 +633,7 @@ void or_ras_apply_box(const or_grid* g, const or_params* p, double dt, const dou
       for (int i = 0; i < E[0]; ++i) {
         size_t q = gidx(g, x0 + i, y0 + j, z0 + k);
         size_t l = (size_t)i + (size_t)E[0] * ((size_t)j + (size_t)E[1] * k);
-        r[l] = v[q];
+        r[l] = in_domain(g, x0 + i, y0 + j, z0 + k) ? v[q] : 0.0;
         c[l] = (3.0 * pn[q] * pn[q] + 2.0 * pn[q] * po[q] + po[q] * po[q]) / 4.0;
       }
   local_op L = {g, p, dt, c, pn, po, x0, y0, z0, {E[0], E[1], E[2]}};

@@ -18,6 +18,8 @@ typedef struct {
   int nd;      /* 2 or 3 */
   int n[3];    /* nodes per axis, n[2]=1 in 2D */
   double h;    /* uniform spacing dx=dy(=dz) */
+  int bc;      /* 0: periodic (the configurations); 1: Neumann-type mirror ghosts on every
+                * axis (row f3, reading R23): node -1-m mirrors node m, node n+m mirrors n-1-m */
 } or_grid;
 
 typedef struct {
