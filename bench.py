@@ -149,7 +149,7 @@ def fp64_peak():
 def variant_config(cfg, args):
     """The configuration with the NEXT-row options of the command line (mobility, Schwarz
     variant, ILU(k) / LU subdomain solves); unchanged without them."""
-    if not (args.mobility or args.ras_variant or args.ilu >= 0 or args.lu):
+    if not (args.mobility or args.ras_variant or args.ilu >= 0 or args.lu or args.bc):
         return cfg
     import dataclasses
     solver = 2 if args.lu else (1 if args.ilu >= 0 else 0)
@@ -158,8 +158,9 @@ def variant_config(cfg, args):
         tag += "reuse"
     return dataclasses.replace(cfg, mobility=args.mobility, ras_variant=args.ras_variant,
                                ras_local_solver=solver, ras_ilu_level=max(args.ilu, 0),
-                               ras_ilu_reuse=args.ilu_reuse,
+                               ras_ilu_reuse=args.ilu_reuse, bc=args.bc,
                                name=cfg.name + (f"_mobility{args.mobility}" if args.mobility else "")
+                               + ("_mirror" if args.bc else "")
                                + (f"_ras{args.ras_variant}" if args.ras_variant else "") + tag)
 
 
@@ -325,7 +326,8 @@ def bench_cuda(args):
                                  else "LU")
                               + (" factors reused per step" if cfg.ras_local_solver and
                                  cfg.ras_ilu_reuse else "")
-                              + (", mobility 1-phi^2" if cfg.mobility else "")),
+                              + (", mobility 1-phi^2" if cfg.mobility else "")
+                              + (", mirror walls" if getattr(cfg, "bc", 0) else "")),
                    "parallelism": f"{ws} independent replica(s)",
                    "l2": "step working set (61-field Krylov basis, 0.5 GB) > 126 MB L2; no flush"},
         "newton_its": newton, "gmres_its": gmres,
@@ -418,6 +420,7 @@ def main():
     ap.add_argument("--ilu", type=int, default=-1, help="k >= 0: ILU(k) subdomain solves (row f2)")
     ap.add_argument("--ilu-reuse", type=int, default=0, help="1: factors reused over a step")
     ap.add_argument("--lu", action="store_true", help="exact LU subdomain solves (row f2)")
+    ap.add_argument("--bc", type=int, default=0, help="1: Neumann-type mirror walls (row f3, 2D)")
     args = ap.parse_args()
     if args.warmup < 3:
         print("note: --warmup < 3 is below the timing contract", file=sys.stderr)

@@ -32,7 +32,7 @@
 extern "C" {
 #endif
 
-#define PFC_ABI_VERSION 4
+#define PFC_ABI_VERSION 5
 
 typedef struct pfc_ctx pfc_ctx;
 typedef int pfc_status;
@@ -72,6 +72,7 @@ typedef struct pfc_config {
   int ras_local_solver;   /* PFC_LOCAL_GMRES (default, reading R9), PFC_LOCAL_ILU, PFC_LOCAL_LU */
   int ras_ilu_level;      /* PFC_LOCAL_ILU: fill level k of ILU(k), 0..4 (Table 1) */
   int ras_ilu_reuse;      /* ILU / LU: 1 = factors of the step's first Newton iteration */
+  int bc;                 /* PFC_BC_PERIODIC (default) or PFC_BC_MIRROR (enum below) */
 } pfc_config;
 
 /* Subdomain solve inv(A_k) of the Schwarz preconditioner:
@@ -88,6 +89,19 @@ typedef struct pfc_config {
  *                    SURVEY App. A), reuse as above.  Band fill ~ 2 (3 E_x) per row: 2D ext
  *                    boxes up to the shared-memory plan (EINVAL beyond, e.g. every 3D box). */
 enum { PFC_LOCAL_GMRES = 0, PFC_LOCAL_ILU = 1, PFC_LOCAL_LU = 2 };
+
+/* Boundary conditions (row f3, reading R23):
+ *   PFC_BC_PERIODIC  the paper's periodic domain, all five configurations;
+ *   PFC_BC_MIRROR    Neumann-type mirror ghosts on every axis (the Test B variants' no-flux
+ *                    walls): with the cell-centred nodes x_i = (i+1/2)h, ghost node -1-m is node m
+ *                    and node n+m is node n-1-m, i.e. every operator acts on the even extension
+ *                    (so D+ / D- vanish across the walls, mass is conserved and the energy
+ *                    law of P:280-308 holds).  Subdomains are clipped at the walls: ext-box nodes
+ *                    outside the domain are no unknowns of A_k = R_k J R_k^T.  Built for
+ *                    ndim = 2, PFC_LOCAL_GMRES, ras_box >= 3; either mobility.  Runs the
+ *                    global-memory operator chain (mobility.cu) and the shared-memory-basis
+ *                    subdomain kernel; EINVAL otherwise. */
+enum { PFC_BC_PERIODIC = 0, PFC_BC_MIRROR = 1 };
 
 /* Mobility of Eq. (PFCeq) P:137-150 in the scheme's (grad . M_d grad)_d, P:208-212 (edge
  * midpoint value = average of the two end nodes), M_d = M((phi_new + phi_old)/2):

@@ -9,8 +9,10 @@
 //          u = (Phi+psi)/2, c = (3Phi^2 + 2Phi psi + psi^2)/4.
 // Each operator is a chain of three radius-1 kernels over global memory (neighbours through
 // L1/L2): Laplacian, Laplacian + pointwise combine, divergence form.  This is the
-// correctness-first path of the row (DESIGN.md §6 gives its measured rate); the M = 1
-// configurations run the fused single-pass stencils of stencil2d.cu / stencil3d.cu.
+// correctness-first path of the row (DESIGN.md §6 gives its measured rate); the periodic M = 1
+// configurations run the fused single-pass stencils of stencil2d.cu / stencil3d.cu.  The same
+// chain serves the Neumann-type mirror BCs (row f3, reading R23; with M = 1 too): every
+// radius-1 neighbour reflects across the boundary face, which composes to the even extension.
 #include "pfc_device.cuh"
 #include "pfc_internal.h"
 
@@ -20,18 +22,23 @@ namespace {
 
 constexpr int NT = 256;
 
-struct Grid { int nx, ny, nz, nd; };
+// bc: periodic or mirror ghosts (R23); mob: M = 1 - u^2 (else M = 1, the mirror-BC M = 1 path)
+struct Grid { int nx, ny, nz, nd, mirror, mob; };
 
-// the node q and its 2*nd periodic neighbours (x-, x+, y-, y+, z-, z+)
+// the node q and its 2*nd neighbours (x-, x+, y-, y+, z-, z+): periodic, or mirrored across
+// the boundary faces (node -1 is node 0, node n is node n-1)
 struct Nb {
   size_t c, m[3], p[3];
 };
 __device__ __forceinline__ Nb nbrs(size_t q, const Grid& G) {
   const size_t nxy = (size_t)G.nx * G.ny;
   const int i = (int)(q % G.nx), j = (int)((q / G.nx) % G.ny), k = (int)(q / nxy);
-  const int im = i == 0 ? G.nx - 1 : i - 1, ip = i + 1 == G.nx ? 0 : i + 1;
-  const int jm = j == 0 ? G.ny - 1 : j - 1, jp = j + 1 == G.ny ? 0 : j + 1;
-  const int km = k == 0 ? G.nz - 1 : k - 1, kp = k + 1 == G.nz ? 0 : k + 1;
+  const int im = i == 0 ? (G.mirror ? 0 : G.nx - 1) : i - 1;
+  const int ip = i + 1 == G.nx ? (G.mirror ? i : 0) : i + 1;
+  const int jm = j == 0 ? (G.mirror ? 0 : G.ny - 1) : j - 1;
+  const int jp = j + 1 == G.ny ? (G.mirror ? j : 0) : j + 1;
+  const int km = k == 0 ? (G.mirror ? 0 : G.nz - 1) : k - 1;
+  const int kp = k + 1 == G.nz ? (G.mirror ? k : 0) : k + 1;
   const size_t row = (size_t)G.nx * j + nxy * k;
   Nb n;
   n.c = q;
@@ -98,7 +105,10 @@ __global__ void k_resid_out(const double* __restrict__ phi, const double* __rest
                             double* __restrict__ partials, Grid G, double ih2, double idt) {
   __shared__ double red[64];
   const size_t N = (size_t)G.nx * G.ny * G.nz;
-  auto m = [&](size_t k) { const double u = 0.5 * (phi[k] + psi[k]); return 1.0 - u * u; };
+  auto m = [&](size_t k) {
+    const double u = 0.5 * (phi[k] + psi[k]);
+    return G.mob ? 1.0 - u * u : 1.0;
+  };
   double nrm = 0.0;
   for (size_t q = blockIdx.x * (size_t)blockDim.x + threadIdx.x; q < N;
        q += (size_t)gridDim.x * blockDim.x) {
@@ -120,12 +130,17 @@ __global__ void k_jv_out(const double* __restrict__ v, const double* __restrict_
                          double ih2, double idt, const int* gate) {
   if (gate && *gate) return;
   const size_t N = (size_t)G.nx * G.ny * G.nz;
-  auto m = [&](size_t k) { const double u = 0.5 * (phi[k] + psi[k]); return 1.0 - u * u; };
+  auto m = [&](size_t k) {
+    const double u = 0.5 * (phi[k] + psi[k]);
+    return G.mob ? 1.0 - u * u : 1.0;
+  };
   auto dm = [&](size_t k) { return -0.5 * (phi[k] + psi[k]) * v[k]; };
   for (size_t q = blockIdx.x * (size_t)blockDim.x + threadIdx.x; q < N;
        q += (size_t)gridDim.x * blockDim.x) {
     const Nb n = nbrs(q, G);
-    out[q] = v[q] * idt - div_mgrad(m, dA, n, G.nd, ih2) - div_mgrad(dm, A, n, G.nd, ih2);
+    double o = v[q] * idt - div_mgrad(m, dA, n, G.nd, ih2);
+    if (G.mob) o -= div_mgrad(dm, A, n, G.nd, ih2);   // M = 1: no mobility-derivative term
+    out[q] = o;
   }
 }
 
@@ -144,7 +159,8 @@ int grid_for(size_t N) {
 // A(Phi, psi) into `A` through the work field t0
 Grid grid_of(const pfc_ctx* ctx) {
   const pfc_config& c = ctx->cfg;
-  return Grid{c.n[0], c.n[1], c.ndim == 3 ? c.n[2] : 1, c.ndim};
+  return Grid{c.n[0], c.n[1], c.ndim == 3 ? c.n[2] : 1, c.ndim, c.bc == PFC_BC_MIRROR,
+              c.mobility == PFC_MOBILITY_QUADRATIC};
 }
 
 cudaError_t a_field(pfc_ctx* ctx, const double* phi, const double* psi, double* A, double* t0) {

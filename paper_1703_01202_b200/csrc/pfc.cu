@@ -121,19 +121,19 @@ bool tma_usable(const void* ptr) { return (reinterpret_cast<uintptr_t>(ptr) & 15
 
 cudaError_t launch_residual(pfc_ctx* ctx, const double* a, const double* b, double dt, double* F,
                             double* partials, int* nparts) {
-  if (ctx->cfg.mobility) return launch_residual_mob(ctx, a, b, dt, F, partials, nparts);
+  if (generic_path(ctx->cfg)) return launch_residual_mob(ctx, a, b, dt, F, partials, nparts);
   return ctx->cfg.ndim == 2 ? launch_residual_2d(ctx, a, b, dt, F, partials, nparts)
                             : launch_residual_3d(ctx, a, b, dt, F, partials, nparts);
 }
 
 cudaError_t launch_jv(pfc_ctx* ctx, const double* v, const double* c, double dt, double* out) {
-  if (ctx->cfg.mobility) return launch_jv_mob(ctx, v, c, dt, out);
+  if (generic_path(ctx->cfg)) return launch_jv_mob(ctx, v, c, dt, out);
   return ctx->cfg.ndim == 2 ? launch_jv_2d(ctx, v, c, dt, out) : launch_jv_3d(ctx, v, c, dt, out);
 }
 
 cudaError_t launch_jac_state(pfc_ctx* ctx, const double* phi_new, const double* phi_old) {
   cudaError_t e = launch_coef(ctx, phi_new, phi_old, ctx->c);
-  if (e != cudaSuccess || !ctx->cfg.mobility) return e;
+  if (e != cudaSuccess || !generic_path(ctx->cfg)) return e;
   return launch_mob_state(ctx, phi_new, phi_old);
 }
 
@@ -436,6 +436,7 @@ void pfc_config_default(pfc_config* c) {
   c->ras_local_solver = PFC_LOCAL_GMRES;
   c->ras_ilu_level = 0;
   c->ras_ilu_reuse = 0;
+  c->bc = PFC_BC_PERIODIC;
 }
 
 static pfc_status validate(const pfc_config& c, std::string* why) {
@@ -472,6 +473,14 @@ static pfc_status validate(const pfc_config& c, std::string* why) {
     return bad("ras_ilu_level in [0,4]");
   if (c.ras_local_solver != PFC_LOCAL_GMRES && c.mobility != PFC_MOBILITY_ONE)
     return bad("PFC_LOCAL_ILU / PFC_LOCAL_LU are built for PFC_MOBILITY_ONE");
+  if (c.bc != PFC_BC_PERIODIC && c.bc != PFC_BC_MIRROR)
+    return bad("bc must be PFC_BC_PERIODIC or PFC_BC_MIRROR");
+  if (c.bc == PFC_BC_MIRROR && c.ndim != 2)
+    return bad("PFC_BC_MIRROR is built for ndim = 2 (the 3D subdomain kernels are periodic)");
+  if (c.bc == PFC_BC_MIRROR && c.ras_local_solver != PFC_LOCAL_GMRES)
+    return bad("PFC_BC_MIRROR is built for PFC_LOCAL_GMRES subdomain solves");
+  if (c.bc == PFC_BC_MIRROR && (c.ras_box[0] < 3 || c.ras_box[1] < 3))
+    return bad("PFC_BC_MIRROR needs ras_box >= 3 (mirror partners inside the boundary box)");
   if (c.gmres_restart < 1 || c.gmres_restart > PFC_MAX_RESTART) return bad("gmres_restart in [1,32]");
   if (c.gmres_maxit < 1 || c.newton_maxit < 0) return bad("iteration limits must be positive");
   if (!(c.newton_rtol >= 0 && c.newton_atol >= 0 && c.gmres_rtol >= 0 && c.gmres_atol >= 0))
@@ -517,7 +526,7 @@ pfc_status pfc_create(const pfc_config* cfg, void* stream, pfc_ctx** out) {
                        &ctx->S,   &ctx->c,   &ctx->w, &ctx->stage};
   for (double** f : fields)
     if (pfc_check_cuda(ctx, cudaMalloc(f, bytes), "cudaMalloc field")) return fail(PFC_ENOMEM);
-  if (c.mobility) {
+  if (generic_path(c)) {
     double** mf[] = {&ctx->mob_A, &ctx->mob_t[0], &ctx->mob_t[1], &ctx->mob_t[2]};
     for (double** f : mf)
       if (pfc_check_cuda(ctx, cudaMalloc(f, bytes), "cudaMalloc mobility field")) return fail(PFC_ENOMEM);

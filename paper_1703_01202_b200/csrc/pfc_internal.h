@@ -116,6 +116,10 @@ cudaError_t launch_jac_state(pfc_ctx* ctx, const double* phi_new, const double* 
 cudaError_t launch_residual_mob(pfc_ctx*, const double* phi_new, const double* phi_old, double dt,
                                 double* F, double* partials, int* nparts);
 cudaError_t launch_jv_mob(pfc_ctx*, const double* v, const double* c, double dt, double* out);
+// the global-memory operator chain of mobility.cu serves variable mobility and mirror BCs
+inline bool generic_path(const pfc_config& c) {
+  return c.mobility != PFC_MOBILITY_ONE || c.bc != PFC_BC_PERIODIC;
+}
 cudaError_t launch_mob_state(pfc_ctx*, const double* phi_new, const double* phi_old);
 // ILU(k) subdomain solves (ilu.cu)
 pfc_status ilu_setup(pfc_ctx* ctx);

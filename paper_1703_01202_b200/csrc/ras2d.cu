@@ -54,7 +54,17 @@ struct RasArgs {
   const double* psi;
   const double* A;
   int mobility;
+  // Neumann-type mirror BCs (row f3, reading R23): subdomains clipped at the physical boundary
+  // (ext-box nodes outside the domain are no unknowns), and the padded plane carries the
+  // mirror ghosts of the Krylov vector (the even extension) so that the stencils act as J
+  int mirror;
 };
+
+// node index of global (x, y): periodic wrap, or the mirror partner (R23)
+__device__ __forceinline__ int axis2(int x, int n, int mirror) {
+  if (!mirror) return wrapi(x, n);
+  return x < 0 ? -1 - x : (x >= n ? 2 * n - 1 - x : x);
+}
 
 // Block sum of nv (runtime, <= NVP) values held by every thread in acc[]: the sums are left in
 // this warp's private copy hw[0..nv) (valid after return for every lane of the warp).  One
@@ -100,6 +110,8 @@ __global__ void __launch_bounds__(NT, 1) ras2d_kernel(RasArgs p) {
   double* pm = hwall + NW * 3 * NVP;     // mobility: M, A, u on the padded plane (np each)
   double* pa = pm + np;
   double* pu = pa + np;
+  double* pc = pm + (p.mobility ? 3 * np : 0);                          // mirror: c on the plane
+  int* gp = reinterpret_cast<int*>(pc + (p.mirror ? np : 0));           // mirror: ghost partners
   __shared__ double H[(K + 1) * K];
   __shared__ double gv[K + 1], cs[K], sn[K], yv[K];
 
@@ -125,12 +137,35 @@ __global__ void __launch_bounds__(NT, 1) ras2d_kernel(RasArgs p) {
 
   // zero the padded planes (ring stays zero), gather R_k^delta v and c with periodic wrap
   for (int q = tid; q < 3 * np; q += NT) pv[q] = 0.0;
+  auto gnode = [&](int x, int y) {
+    return (size_t)axis2(x, p.nx, p.mirror) + (size_t)p.nx * axis2(y, p.ny, p.mirror);
+  };
+  auto in_dom = [&](int x, int y) {
+    return !p.mirror || (x >= 0 && x < p.nx && y >= 0 && y < p.ny);
+  };
+  // mirror: does this box reach the boundary (its plane then has ghost positions)?
+  const bool ghosts = p.mirror && (gx0 - 3 < 0 || gy0 - 3 < 0 || gx0 + Px - 3 > p.nx ||
+                                   gy0 + Py - 3 > p.ny);
+  if (p.mirror) {   // c of the even extension on the plane; ghost -> partner map
+    for (int q = tid; q < np; q += NT) {
+      const int pi = q % Px, pj = q / Px, x = gx0 + pi - 3, y = gy0 + pj - 3;
+      const bool inext = pi >= 3 && pi < Px - 3 && pj >= 3 && pj < Py - 3;
+      const bool ghost = !in_dom(x, y);
+      pc[q] = (inext || ghost) ? p.c[gnode(x, y)] : 0.0;
+      int part = -1;
+      if (ghost) {
+        const int mi = axis2(x, p.nx, 1) - gx0 + 3, mj = axis2(y, p.ny, 1) - gy0 + 3;
+        part = (mi >= 3 && mi < Px - 3 && mj >= 3 && mj < Py - 3) ? mj * Px + mi : -2;
+      }
+      gp[q] = part;
+    }
+  }
   if (p.mobility) {   // M = 1 - u^2, A and u of the iterate on the ext box and its +1 ring
     for (int q = tid; q < np; q += NT) {
       const int pi = q % Px, pj = q / Px;
       double m = 0.0, a = 0.0, u = 0.0;
       if (pi >= 2 && pi < Px - 2 && pj >= 2 && pj < Py - 2) {
-        const size_t g = (size_t)wrapi(gx0 + pi - 3, p.nx) + (size_t)p.nx * wrapi(gy0 + pj - 3, p.ny);
+        const size_t g = gnode(gx0 + pi - 3, gy0 + pj - 3);
         u = 0.5 * (p.phi[g] + p.psi[g]);
         m = 1.0 - u * u;
         a = p.A[g];
@@ -140,17 +175,20 @@ __global__ void __launch_bounds__(NT, 1) ras2d_kernel(RasArgs p) {
   }
   double w[SLOTS];
   double acc[NVP];
+  bool act[SLOTS];   // unknowns of A_k: every ext-box node, except outside the domain (mirror)
 #pragma unroll
   for (int i = 0; i < NVP; ++i) acc[i] = 0.0;
 #pragma unroll
   for (int s = 0; s < SLOTS; ++s) {
     w[s] = 0.0;
+    act[s] = false;
     if (own[s]) {
       int l = tid + s * NT;
-      size_t g = (size_t)wrapi(gx0 + l % Ex, p.nx) + (size_t)p.nx * wrapi(gy0 + l / Ex, p.ny);
+      size_t g = gnode(gx0 + l % Ex, gy0 + l / Ex);
+      act[s] = in_dom(gx0 + l % Ex, gy0 + l / Ex);
       const int li = l % Ex - p.o, lj = l / Ex - p.o;
       const bool owned = li >= 0 && li < p.bx && lj >= 0 && lj < p.by;
-      w[s] = (p.restrict_owned && !owned) ? 0.0 : p.v[g];
+      w[s] = ((p.restrict_owned && !owned) || !act[s]) ? 0.0 : p.v[g];
       cl[l] = p.c[g];
       acc[0] += w[s] * w[s];
     }
@@ -189,6 +227,11 @@ __global__ void __launch_bounds__(NT, 1) ras2d_kernel(RasArgs p) {
 #pragma unroll 1
   for (int j = 0; j < K; ++j) {
     __syncthreads();                                   // pv holds V_j
+    if (ghosts) {   // mirror ghosts of V_j (the even extension; partners outside the box: 0)
+      for (int q = tid; q < np; q += NT)
+        if (gp[q] >= 0) pv[q] = pv[gp[q]];
+      __syncthreads();
+    }
     {   // L1 = Delta v on padded [1, P-1)
       int r = r0L, c = c0L;
       for (int q = tid; q < cntL; q += NT) {
@@ -208,7 +251,8 @@ __global__ void __launch_bounds__(NT, 1) ras2d_kernel(RasArgs p) {
         int f = pj * Px + pi;
         double vv = pv[f];
         int li = pi - 3, lj = pj - 3;
-        double cv = (li >= 0 && li < Ex && lj >= 0 && lj < Ey) ? cl[lj * Ex + li] * vv : 0.0;
+        double cv = p.mirror ? pc[f] * vv
+                             : (li >= 0 && li < Ex && lj >= 0 && lj < Ey) ? cl[lj * Ex + li] * vv : 0.0;
         double lapl = ih2 * ((pl[f - 1] + pl[f + 1]) + (pl[f - Px] + pl[f + Px]) - 4.0 * pl[f]);
         pb[f] = alpha * vv + cv + pl[f] + 0.5 * lapl;
       }
@@ -236,6 +280,7 @@ __global__ void __launch_bounds__(NT, 1) ras2d_kernel(RasArgs p) {
           double lapb = ih2 * ((pb[f - 1] + pb[f + 1]) + (pb[f - Px] + pb[f + Px]) - 4.0 * pb[f]);
           ww = pv[f] * idt - lapb;
         }
+        if (!act[s]) ww = 0.0;   // R_k: rows of the non-unknowns are dropped
         w[s] = ww;
 #pragma unroll
         for (int i = 0; i < K; ++i) {
@@ -803,9 +848,10 @@ size_t ras2d_col_smem_bytes(int R) {
 }
 
 typedef void (*ras2d_fn)(RasArgs);
-size_t ras2d_smem_bytes(int bx, int by, int o, int k, int mobility) {
+size_t ras2d_smem_bytes(int bx, int by, int o, int k, int mobility, int mirror) {
   const size_t Ex = bx + 2 * o, Ey = by + 2 * o, n = Ex * Ey, np = (Ex + 6) * (Ey + 6);
-  size_t d = (size_t)k * n + n + 3 * np + 2 * NW * 16 + NW * 3 * 16 + (mobility ? 3 * np : 0);
+  size_t d = (size_t)k * n + n + 3 * np + 2 * NW * 16 + NW * 3 * 16 + (mobility ? 3 * np : 0) +
+             (mirror ? np + (np + 1) / 2 : 0);   // c plane + ghost partner ints
   return d * sizeof(double) + 128;
 }
 
@@ -855,7 +901,7 @@ int ras2d_plan(pfc_ctx* ctx) {
   const pfc_config& c = ctx->cfg;
   const int Ex = c.ras_box[0] + 2 * c.ras_overlap, Ey = c.ras_box[1] + 2 * c.ras_overlap;
   if (Ex * Ey > MAXN) return 0;
-  if (getenv("PFC_RAS_SMEM_BASIS") == nullptr && !c.mobility) {
+  if (getenv("PFC_RAS_SMEM_BASIS") == nullptr && !c.mobility && c.bc == PFC_BC_PERIODIC) {
     const int r = col_rows(c.ras_local_k, Ex, Ey);
     if (r) {
       const int ns = (Ey + r - 1) / r;
@@ -866,7 +912,7 @@ int ras2d_plan(pfc_ctx* ctx) {
     }
   }
   size_t sm = ras2d_smem_bytes(c.ras_box[0], c.ras_box[1], c.ras_overlap, c.ras_local_k,
-                               c.mobility);
+                               c.mobility, c.bc == PFC_BC_MIRROR);
   if (sm + 2048 > 227 * 1024) return 0;   // + static shared memory (H, Givens, reductions)
   ctx->ras_smem = (int)sm;
   ctx->ras_threads = NT;        // shared-memory-basis kernel
@@ -919,7 +965,7 @@ cudaError_t launch_ras_2d(pfc_ctx* ctx, const double* v, const double* c, double
     RasArgs p{v, c, z, cf.n[0], cf.n[1], cf.ras_box[0], cf.ras_box[1], cf.ras_overlap,
               1.0 / dt, cf.gamma, ctx->ih2, cf.ras_variant == PFC_RAS_RIGHT,
               cf.ras_variant == PFC_RAS_LEFT ? nullptr : ctx->ras_y, ctx->gate,
-              ctx->mob_phi, ctx->mob_psi, ctx->mob_A, cf.mobility};
+              ctx->mob_phi, ctx->mob_psi, ctx->mob_A, cf.mobility, cf.bc == PFC_BC_MIRROR};
     fn<<<nb, NT, ctx->ras_smem, ctx->stream>>>(p);
   }
   ctx->launches++;

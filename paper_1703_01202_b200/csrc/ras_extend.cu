@@ -19,22 +19,24 @@ struct ExtArgs {
   double* z;
   int n[3], b[3], nb[3], E[3], o;
   int nd;
+  int mirror;        // mirror BCs (R23): boxes never wrap, ext-box nodes outside the domain
   const int* gate;   // device-resident FGMRES: skip the launch when *gate != 0 (f1)
 };
 
 // candidate boxes along one axis covering coordinate x: unique indices, local coordinates
 __device__ __forceinline__ int axis_candidates(int x, int n, int b, int nb, int E, int o,
-                                               int (&box)[3], int (&loc)[3]) {
+                                               int mirror, int (&box)[3], int (&loc)[3]) {
   const int own = x / b;
   int cnt = 0;
 #pragma unroll
   for (int d = -1; d <= 1; ++d) {
+    if (mirror && (own + d < 0 || own + d >= nb)) continue;   // clipped subdomains: no wrap
     const int c = wrapi(own + d, nb);
     bool dup = false;
     for (int i = 0; i < cnt; ++i) dup = dup || box[i] == c;
     if (dup) continue;
-    const int l = wrapi(x - (c * b - o), n);   // local coordinate in box c's ext range
-    if (l < E) {
+    const int l = mirror ? x - (c * b - o) : wrapi(x - (c * b - o), n);   // local coordinate
+    if (l >= 0 && l < E) {
       box[cnt] = c;
       loc[cnt] = l;
       ++cnt;
@@ -52,11 +54,12 @@ __global__ void __launch_bounds__(NT) k_ras_extend(const ExtArgs p) {
     const int y = (int)((q / p.n[0]) % p.n[1]);
     const int zz = (int)(q / ((size_t)p.n[0] * p.n[1]));
     int bx[3], lx[3], by[3], ly[3], bz[3], lz[3];
-    const int cx = axis_candidates(x, p.n[0], p.b[0], p.nb[0], p.E[0], p.o, bx, lx);
-    const int cy = axis_candidates(y, p.n[1], p.b[1], p.nb[1], p.E[1], p.o, by, ly);
+    const int cx = axis_candidates(x, p.n[0], p.b[0], p.nb[0], p.E[0], p.o, p.mirror, bx, lx);
+    const int cy = axis_candidates(y, p.n[1], p.b[1], p.nb[1], p.E[1], p.o, p.mirror, by, ly);
     int cz = 1;
     bz[0] = 0; lz[0] = 0;
-    if (p.nd == 3) cz = axis_candidates(zz, p.n[2], p.b[2], p.nb[2], p.E[2], p.o, bz, lz);
+    if (p.nd == 3)
+      cz = axis_candidates(zz, p.n[2], p.b[2], p.nb[2], p.E[2], p.o, p.mirror, bz, lz);
     double s = 0.0;
     for (int k = 0; k < cz; ++k)
       for (int j = 0; j < cy; ++j)
@@ -78,6 +81,7 @@ cudaError_t launch_ras_extend(pfc_ctx* ctx, double* z) {
   p.z = z;
   p.nd = c.ndim;
   p.o = c.ras_overlap;
+  p.mirror = c.bc == PFC_BC_MIRROR;
   p.gate = ctx->gate;
   for (int d = 0; d < 3; ++d) {
     const bool act = d < c.ndim;

@@ -133,6 +133,7 @@ class PFCConfig:
     ras_local_solver: int = 0       # 0 local GMRES(k) (R9); 1 ILU(k) (row f2)
     ras_ilu_level: int = 0
     ras_ilu_reuse: int = 0          # factors of the step's first Newton iteration
+    bc: int = 0                     # 0 periodic; 1 Neumann-type mirror walls (row f3, R23)
     ic: dict = field(default_factory=dict)
     seed: int = 1
 

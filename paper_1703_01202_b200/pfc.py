@@ -30,12 +30,13 @@ class PfcConfig(C.Structure):
                 ("gmres_rtol", C.c_double), ("gmres_atol", C.c_double),
                 ("ras_box", C.c_int * 3), ("ras_overlap", C.c_int), ("ras_local_k", C.c_int),
                 ("ras_variant", C.c_int), ("mobility", C.c_int), ("ras_local_solver", C.c_int),
-                ("ras_ilu_level", C.c_int), ("ras_ilu_reuse", C.c_int)]
+                ("ras_ilu_level", C.c_int), ("ras_ilu_reuse", C.c_int), ("bc", C.c_int)]
 
 
 PFC_RAS_LEFT, PFC_RAS_AS, PFC_RAS_RIGHT = 0, 1, 2   # include/pfc.h
 PFC_MOBILITY_ONE, PFC_MOBILITY_QUADRATIC = 0, 1     # include/pfc.h (M = 1; M = 1 - phi^2)
 PFC_LOCAL_GMRES, PFC_LOCAL_ILU, PFC_LOCAL_LU = 0, 1, 2   # include/pfc.h (R9; ILU(k); LU)
+PFC_BC_PERIODIC, PFC_BC_MIRROR = 0, 1                 # include/pfc.h (mirror walls, R23)
 
 
 class PfcStepInfo(C.Structure):
@@ -98,7 +99,8 @@ def make_config(cfg=None, **over) -> PfcConfig:
     Keyword overrides use the field names of include/pfc.h, e.g. ndim, n, h, gamma, adaptive,
     dt_min, dt_max, eta, newton_rtol, gmres_restart, ras_box, ras_overlap, ras_local_k,
     ras_variant (PFC_RAS_LEFT / _AS / _RIGHT), mobility (PFC_MOBILITY_ONE / _QUADRATIC),
-    ras_local_solver (PFC_LOCAL_GMRES / _ILU / _LU), ras_ilu_level, ras_ilu_reuse."""
+    ras_local_solver (PFC_LOCAL_GMRES / _ILU / _LU), ras_ilu_level, ras_ilu_reuse,
+    bc (PFC_BC_PERIODIC / PFC_BC_MIRROR)."""
     L = load()
     c = PfcConfig()
     L.pfc_config_default(C.byref(c))
@@ -114,7 +116,7 @@ def make_config(cfg=None, **over) -> PfcConfig:
                   mobility=getattr(cfg, "mobility", 0),
                   ras_local_solver=getattr(cfg, "ras_local_solver", 0),
                   ras_ilu_level=getattr(cfg, "ras_ilu_level", 0),
-                  ras_ilu_reuse=getattr(cfg, "ras_ilu_reuse", 0))
+                  ras_ilu_reuse=getattr(cfg, "ras_ilu_reuse", 0), bc=getattr(cfg, "bc", 0))
     kw.update(over)
     for k, v in kw.items():
         if k in ("n", "ras_box"):
