@@ -92,8 +92,8 @@ enum { PFC_LOCAL_GMRES = 0, PFC_LOCAL_ILU = 1, PFC_LOCAL_LU = 2 };
 
 /* Boundary conditions (row f3, reading R23):
  *   PFC_BC_PERIODIC  the paper's periodic domain, all five configurations;
- *   PFC_BC_MIRROR    Neumann-type mirror ghosts on every axis (the Test B variants' no-flux
- *                    walls): with the cell-centred nodes x_i = (i+1/2)h, ghost node -1-m is node m
+ *   PFC_BC_MIRROR    the paper's "Neumann-type boundary conditions" (Test B cases c, d
+ *                    P:620-621) as mirror ghosts on every axis: with the cell-centred nodes x_i = (i+1/2)h, ghost node -1-m is node m
  *                    and node n+m is node n-1-m, i.e. every operator acts on the even extension
  *                    (so D+ / D- vanish across the walls, mass is conserved and the energy
  *                    law of P:280-308 holds).  Subdomains are clipped at the walls: ext-box nodes
