@@ -6,8 +6,12 @@
 //
 // One CTA per extended box of E^3 nodes (E = b + 2o, e.g. 20^3 for the configs' 16^3 boxes with
 // overlap 2), persistent over the boxes.  Thread (x, y) owns the z-column of its E nodes:
-//  * the current Krylov vector v_j lives zero-padded in shared memory ((E+6)^3 doubles, 141 KB
-//    at E = 20) next to c on the box (E^3, 64 KB);
+//  * the current Krylov vector v_j lives zero-padded in x and y in shared memory (E planes of
+//    (E+6) rows at a row pitch PXR >= E+6 with PXR = E (mod 16), 146 KB at E = 20) next to c on
+//    the box (E^3, 64 KB).  A warp covers 32 consecutive (x, y) of rows of E nodes, so with
+//    PXR = E (mod 16) its 8-byte loads hit every bank pair exactly twice (conflict-free; the
+//    plain (E+6) pitch cost 3.1 wavefronts per load instead of 2).  The z-direction needs no
+//    zero planes: the unrolled z loop skips the out-of-box planes at compile time;
 //  * the local J v is ONE pass of the direct 63-point stencil of the linear part
 //      w = v/dt - alpha Delta v - Delta^2 v - Delta^3 v / 2 - Delta(c v),  alpha = (1-gamma)/2
 //    (class weights of h^2 Delta = L, L^2, L^3 summed on the host), read column by column with
@@ -50,10 +54,14 @@ constexpr int wclass3(int a, int b, int c) {
          : ((a == 3 || b == 3 || c == 3) ? 4 : ((a == 1 && b == 1 && c == 1) ? 6 : 5));
 }
 
-template <int K, int E>
+// row pitch of the padded plane: >= E + 6 and = E (mod 16) (conflict-free warp rows)
+constexpr int col3_pxr(int E) { return E + 6 + ((E - (E + 6)) % 16 + 16) % 16; }
+
+template <int E>
 struct Col3 {
-  static constexpr int PX = E + 6;           // padded edge
-  static constexpr int PP = PX * PX;         // padded plane
+  static constexpr int PXR = col3_pxr(E);    // row pitch (x)
+  static constexpr int PY = E + 6;           // padded rows (y)
+  static constexpr int PP = PXR * PY;        // plane pitch (z: E planes, no ring)
   static constexpr int NE = E * E * E;       // ext-box nodes
 };
 
@@ -62,15 +70,16 @@ struct Col3 {
 template <int E, int DX, int DY>
 __device__ __forceinline__ void col3_offset(const Ras3ColArgs& p, const double* pvb,
                                             const double* cl, int x, int y, double (&out)[E]) {
-  constexpr int PX = E + 6, PP = PX * PX;
+  constexpr int PXR = Col3<E>::PXR, PP = Col3<E>::PP;
   constexpr int R = iabs3(DX) + iabs3(DY);
   constexpr int A = 3 - R;
-  const double* col = pvb + DY * PX + DX;
+  const double* col = pvb + DY * PXR + DX;
   // c at this neighbour column (R == 1): c v enters Delta(c v); zero outside the extended box
   const bool cin = x + DX >= 0 && x + DX < E && y + DY >= 0 && y + DY < E;
   const double* ccol = cl + (y + DY) * E + (x + DX);
+  // planes zz < 0 and zz >= E are zero (the modified BC): skipped at compile time
 #pragma unroll
-  for (int zz = -A; zz < E + A; ++zz) {
+  for (int zz = 0; zz < E; ++zz) {
     const double val = col[zz * PP];
 #pragma unroll
     for (int z = (zz - A > 0 ? zz - A : 0); z <= (zz + A < E - 1 ? zz + A : E - 1); ++z) {
@@ -118,7 +127,7 @@ __device__ __forceinline__ bool col3_step(const Ras3ColArgs& p, double (&w)[E], 
                                           double* h1, double* h2, double* hx, double* H,
                                           double* cs, double* sn, double* gv, double* pvb,
                                           double* Vnext, double beta, int nwt) {
-  constexpr int PP = (E + 6) * (E + 6);
+  constexpr int PP = Col3<E>::PP;
   constexpr int NE = E * E * E;
   // pass 1: h1 = V^T w
   {
@@ -251,10 +260,10 @@ template <int K, int E>
 __global__ void __launch_bounds__((E * E + 31) / 32 * 32, 1)
     ras3d_col_kernel(const __grid_constant__ Ras3ColArgs p) {
   if (p.gate && *p.gate) return;
-  constexpr int PX = E + 6, PP = PX * PX, NE = E * E * E;
+  constexpr int PXR = Col3<E>::PXR, PP = Col3<E>::PP, NE = E * E * E;
   extern __shared__ __align__(128) double smem_dyn[];
-  double* pv = smem_dyn;                      // PX^3, zero ring
-  double* cl = pv + PX * PP;                  // E^3
+  double* pv = smem_dyn;                      // E planes of PY x PXR, zero x/y ring
+  double* cl = pv + E * PP;                   // E^3
   double* red = cl + NE;                      // 2 x NW3MAX x 16
   double* hwall = red + 2 * NW3MAX * 16;      // NW3MAX x 48
   __shared__ double H[(K + 1) * K];
@@ -266,7 +275,7 @@ __global__ void __launch_bounds__((E * E + 31) / 32 * 32, 1)
   double* hx = h2 + 16;
   const bool act = tid < E * E;
   const int x = act ? tid % E : 0, y = act ? tid / E : 0;
-  double* pvb = pv + 3 * PP + (y + 3) * PX + (x + 3);
+  double* pvb = pv + (y + 3) * PXR + (x + 3);
   double* V0 = p.basis + (size_t)blockIdx.x * K * NE;   // this CTA's basis scratch
   const double* Vb = V0 + y * E + x;                      // own column, stride E^2
   double* Vw = V0 + y * E + x;
@@ -274,7 +283,7 @@ __global__ void __launch_bounds__((E * E + 31) / 32 * 32, 1)
   const int nboxes = nbx * nby * nbz;
   const size_t NX = p.nx, NXY = (size_t)p.nx * p.ny;
 
-  for (int q = tid; q < PX * PP; q += blockDim.x) pv[q] = 0.0;
+  for (int q = tid; q < E * PP; q += blockDim.x) pv[q] = 0.0;
 
   for (int box = blockIdx.x; box < nboxes; box += gridDim.x) {
     const int ibx = box % nbx, iby = (box / nbx) % nby, ibz = box / (nbx * nby);
@@ -368,8 +377,7 @@ __global__ void __launch_bounds__((E * E + 31) / 32 * 32, 1)
 
 template <int K, int E>
 size_t col3_smem() {
-  constexpr int PX = E + 6;
-  return ((size_t)PX * PX * PX + (size_t)E * E * E + 2 * NW3MAX * 16 + NW3MAX * 48) *
+  return ((size_t)E * Col3<E>::PP + (size_t)E * E * E + 2 * NW3MAX * 16 + NW3MAX * 48) *
          sizeof(double);
 }
 
