@@ -428,7 +428,12 @@ __global__ void __launch_bounds__(NT, 1) ras2d_kernel(RasArgs p) {
 //    or 16), one barrier, and lane-parallel cross-warp sums: fixed order, deterministic.
 // Arithmetic: same algorithm as ras2d_kernel and the oracle (reading R9); the stencil sums the
 // 25 weighted terms instead of composing three 5-point Laplacians (rounding-level difference).
-constexpr int PP = 48;          // padded plane pitch (doubles): Ex + 6 <= 48
+constexpr int PP = 48;          // padded plane pitch (doubles) at most: Ex + 6 <= 48
+// Row pitch of the padded planes for R rows per thread: a warp covers consecutive x of strip s
+// and then strip s+1 (R rows further), so its 8-byte loads are conflict-free when
+// R * pitch = Ex (mod 16): 45 for R = 4 (Ex = 36, 20: cfg2/3), 50 for R = 2 (Ex = 20: cfg1);
+// other shapes are correct at any pitch, just not conflict-free.
+constexpr int col_pp(int R) { return R == 4 ? 45 : R == 2 ? 50 : PP; }
 constexpr int PPY = 56;         // padded plane rows: Ey + R + 5 <= 56
 constexpr int NTC = 384;        // threads per CTA at most (1 CTA per SM, <= 168 registers)
 constexpr int NWC = NTC / 32;
@@ -543,6 +548,7 @@ __device__ __forceinline__ bool col_step(double (&Vr)[K][R], double (&w)[R], dou
                                          double* hx, double* H, double* cs, double* sn,
                                          double* gv, double* rd, double* pvb, double* pcvb,
                                          double beta, int nwt, bool g0, double& hn_prev) {
+  constexpr int PP = col_pp(R);
   if constexpr (J > 0) {
     if (g0) col_givens<K, J - 1>(h1, h2, hn_prev, cs, sn, gv, H, rd);
   }
@@ -654,6 +660,7 @@ __device__ __forceinline__ bool col_dispatch(int j, double (&Vr)[K][R], double (
 
 template <int K, int R>
 __global__ void __launch_bounds__(NTC, 1) ras2d_col_kernel(const __grid_constant__ RasColArgs p) {
+  constexpr int PP = col_pp(R);
   extern __shared__ __align__(128) double smem_dyn[];
   double* pv = smem_dyn;                     // PP x PPY padded v (zero ring)
   double* pcv = pv + PP * PPY;               // PP x PPY padded c v
@@ -844,7 +851,7 @@ extern "C" void pfc_ras_prof_read(long long* out) {
 namespace {
 #endif
 size_t ras2d_col_smem_bytes(int R) {
-  return (size_t)(2 * PP * PPY + 2 * NWC * 16 + NWC * 48 + 2 * NTC * R) * sizeof(double);
+  return (size_t)(2 * col_pp(R) * PPY + 2 * NWC * 16 + NWC * 48 + 2 * NTC * R) * sizeof(double);
 }
 
 typedef void (*ras2d_fn)(RasArgs);
@@ -890,7 +897,7 @@ int col_rows(int k, int Ex, int Ey) {
   for (int i = 0; i < 4; ++i) {
     const int r = cand[i];
     const int ns = (Ey + r - 1) / r;
-    if ((Ex * ns + 31) / 32 * 32 + 32 <= NTC && pick_col(k, r)) return r;
+    if (Ex + 6 <= col_pp(r) && (Ex * ns + 31) / 32 * 32 + 32 <= NTC && pick_col(k, r)) return r;
   }
   return 0;
 }
