@@ -129,6 +129,11 @@ __device__ __forceinline__ bool col3_step(const Ras3ColArgs& p, double (&w)[E], 
                                           double* Vnext, double beta, int nwt) {
   constexpr int PP = Col3<E>::PP;
   constexpr int NE = E * E * E;
+  // basis value i at the thread's node z: v_J is also in the shared plane (bitwise the same
+  // value), which saves one of the J+1 L2 reads in each of the three passes below
+  auto vb = [&](int i, int z) -> double {
+    return i == J ? pvb[z * PP] : Vb[(size_t)i * NE + z * nodes_stride];
+  };
   // pass 1: h1 = V^T w
   {
     double acc[J + 1];
@@ -137,7 +142,7 @@ __device__ __forceinline__ bool col3_step(const Ras3ColArgs& p, double (&w)[E], 
       double t = 0.0;
       if (act) {
 #pragma unroll
-        for (int z = 0; z < E; ++z) t = fma(Vb[(size_t)i * NE + z * nodes_stride], w[z], t);
+        for (int z = 0; z < E; ++z) t = fma(vb(i, z), w[z], t);
       }
       acc[i] = t;
     }
@@ -159,7 +164,7 @@ __device__ __forceinline__ bool col3_step(const Ras3ColArgs& p, double (&w)[E], 
         double ww = w[z];
 #pragma unroll
         for (int i = 0; i <= J; ++i) {
-          vv[i] = Vb[(size_t)i * NE + z * nodes_stride];
+          vv[i] = vb(i, z);
           ww = fma(-hv[i], vv[i], ww);
         }
 #pragma unroll
@@ -184,7 +189,7 @@ __device__ __forceinline__ bool col3_step(const Ras3ColArgs& p, double (&w)[E], 
     for (int z = 0; z < E; ++z) {
       double ww = w[z];
 #pragma unroll
-      for (int i = 0; i <= J; ++i) ww = fma(-hv[i], Vb[(size_t)i * NE + z * nodes_stride], ww);
+      for (int i = 0; i <= J; ++i) ww = fma(-hv[i], vb(i, z), ww);
       w[z] = ww;
     }
   }
