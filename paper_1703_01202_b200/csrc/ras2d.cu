@@ -692,8 +692,8 @@ __global__ void __launch_bounds__(NTC, 1) ras2d_col_kernel(const __grid_constant
   double* pcvb = pcv + (y0 + 3) * PP + x + 3;
 
   for (int q = tid; q < 2 * PP * PPY; q += blockDim.x) pv[q] = 0.0;   // the ring stays zero
-  double* sv = stg + tid * R;
-  double* sc = stg + NTC * R + tid * R;
+  double* sv = stg + tid;              // [r][thread]: a warp's 8-byte accesses are contiguous
+  double* sc = stg + NTC * R + tid;
   // R_k^delta v and c of a box (periodic wrap) into this thread's staging slots, asynchronously
   auto prefetch = [&](int box) {
     if (box >= nboxes) return;
@@ -702,8 +702,8 @@ __global__ void __launch_bounds__(NTC, 1) ras2d_col_kernel(const __grid_constant
     for (int r = 0; r < R; ++r)
       if (own[r]) {
         const size_t g = (size_t)wrapi(gx0 + x, p.nx) + (size_t)p.nx * wrapi(gy0 + y0 + r, p.ny);
-        cp_async8(sv + r, p.v + g);
-        cp_async8(sc + r, p.c + g);
+        cp_async8(sv + r * NTC, p.v + g);
+        cp_async8(sc + r * NTC, p.c + g);
       }
     cp_async_commit();
   };
@@ -723,8 +723,8 @@ __global__ void __launch_bounds__(NTC, 1) ras2d_col_kernel(const __grid_constant
     if (own[r]) {
       const int li = x - p.o, lj = y0 + r - p.o;
       const bool owned = li >= 0 && li < p.bx && lj >= 0 && lj < p.by;
-      w[r] = (p.restrict_owned && !owned) ? 0.0 : sv[r];
-      cr[r] = sc[r];
+      w[r] = (p.restrict_owned && !owned) ? 0.0 : sv[r * NTC];
+      cr[r] = sc[r * NTC];
       acc0[0] = fma(w[r], w[r], acc0[0]);
     }
   }
