@@ -172,49 +172,89 @@ __global__ void __launch_bounds__(AWMAX * 32) k_ilu_apply(const IluArgs p, int n
     y[l] = (p.restrict_owned && !owned) ? 0.0 : p.v[gnode(p, l, gx0, gy0, gz0)];
   }
   __syncwarp();
-  for (int L = 0; L < p.nflev; ++L) {          // L y = r (unit lower)
-    for (int r = p.flev_ptr[L] + lane; r < p.flev_ptr[L + 1]; r += 32) {
-      const int i = p.flev_row[r];
-      const int q0 = __ldg(p.lptr + i), q1 = __ldg(p.lptr + i + 1);
-      double s = y[i];
-      for (int q = q0; q < q1; q += 8) {       // 8 independent loads in flight, then the
-        double av[8];                          // subtractions in ascending order
-        int cv[8];
+  // Both sweeps: rows of a level on the lanes.  The factor values and column indices of a row
+  // do not depend on the sweep, so the first NPRE entries of the lane's first row of level
+  // L+2 are loaded while level L computes: the factors of all boxes (e.g. 265 MB at cfg2) live
+  // in HBM, and each level would otherwise wait on a DRAM round trip.  Longer rows and further
+  // rows of a level load as before.  Same subtractions in the same order.
+  constexpr int NPRE = 16;
+  struct Pre { int i, q0, q1; double av[NPRE]; int cv[NPRE]; };
+  auto fetch = [&](const int* lev_ptr, const int* lev_row, int nlev, const int* ptr,
+                   const int* col, const double* val, int L, bool upper, Pre& P) {
+    P.i = -1;
+    if (L >= nlev) return;
+    const int r = __ldg(lev_ptr + L) + lane;
+    if (r >= __ldg(lev_ptr + L + 1)) return;
+    P.i = __ldg(lev_row + r);
+    P.q0 = __ldg(ptr + P.i) + (upper ? 1 : 0);   // U: the diagonal is read separately
+    P.q1 = __ldg(ptr + P.i + 1);
 #pragma unroll
-        for (int t = 0; t < 8; ++t) {
-          av[t] = q + t < q1 ? a[q + t] : 0.0;
-          cv[t] = q + t < q1 ? __ldg(p.lcol + q + t) : i;
-        }
-#pragma unroll
-        for (int t = 0; t < 8; ++t)
-          if (q + t < q1) s -= av[t] * y[cv[t]];
-      }
-      y[i] = s;
+    for (int t = 0; t < NPRE; ++t) {
+      P.av[t] = P.q0 + t < P.q1 ? val[P.q0 + t] : 0.0;
+      P.cv[t] = P.q0 + t < P.q1 ? __ldg(col + P.q0 + t) : P.i;
     }
-    __syncwarp();
+  };
+  auto row_sum = [&](const int* col, const double* val, int i, int q0, int q1, double s) {
+    for (int q = q0; q < q1; q += 8) {         // 8 independent loads in flight, then the
+      double av[8];                            // subtractions in ascending order
+      int cv[8];
+#pragma unroll
+      for (int t = 0; t < 8; ++t) {
+        av[t] = q + t < q1 ? val[q + t] : 0.0;
+        cv[t] = q + t < q1 ? __ldg(col + q + t) : i;
+      }
+#pragma unroll
+      for (int t = 0; t < 8; ++t)
+        if (q + t < q1) s -= av[t] * y[cv[t]];
+    }
+    return s;
+  };
+  {   // L y = r (unit lower)
+    Pre cur, nx1, nx2;
+    fetch(p.flev_ptr, p.flev_row, p.nflev, p.lptr, p.lcol, a, 0, false, cur);
+    fetch(p.flev_ptr, p.flev_row, p.nflev, p.lptr, p.lcol, a, 1, false, nx1);
+    for (int L = 0; L < p.nflev; ++L) {
+      fetch(p.flev_ptr, p.flev_row, p.nflev, p.lptr, p.lcol, a, L + 2, false, nx2);
+      if (cur.i >= 0) {
+        double s = y[cur.i];
+#pragma unroll
+        for (int t = 0; t < NPRE; ++t)
+          if (cur.q0 + t < cur.q1) s -= cur.av[t] * y[cur.cv[t]];
+        y[cur.i] = row_sum(p.lcol, a, cur.i, cur.q0 + NPRE, cur.q1, s);
+      }
+      for (int r = p.flev_ptr[L] + lane + 32; r < p.flev_ptr[L + 1]; r += 32) {
+        const int i = p.flev_row[r];
+        y[i] = row_sum(p.lcol, a, i, __ldg(p.lptr + i), __ldg(p.lptr + i + 1), y[i]);
+      }
+      __syncwarp();
+      cur = nx1;
+      nx1 = nx2;
+    }
   }
   const double* u = a + p.nL;
-  for (int L = 0; L < p.nblev; ++L) {          // U x = y
-    for (int r = p.blev_ptr[L] + lane; r < p.blev_ptr[L + 1]; r += 32) {
-      const int i = p.blev_row[r];
-      const int t0 = __ldg(p.uptr + i), t1 = __ldg(p.uptr + i + 1);
-      const double dii = u[t0];
-      double s = y[i];
-      for (int t = t0 + 1; t < t1; t += 8) {
-        double av[8];
-        int cv[8];
+  {   // U x = y
+    Pre cur, nx1, nx2;
+    fetch(p.blev_ptr, p.blev_row, p.nblev, p.uptr, p.ucol, u, 0, true, cur);
+    fetch(p.blev_ptr, p.blev_row, p.nblev, p.uptr, p.ucol, u, 1, true, nx1);
+    for (int L = 0; L < p.nblev; ++L) {
+      fetch(p.blev_ptr, p.blev_row, p.nblev, p.uptr, p.ucol, u, L + 2, true, nx2);
+      if (cur.i >= 0) {
+        const double dii = u[cur.q0 - 1];
+        double s = y[cur.i];
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          av[k] = t + k < t1 ? u[t + k] : 0.0;
-          cv[k] = t + k < t1 ? __ldg(p.ucol + t + k) : i;
-        }
-#pragma unroll
-        for (int k = 0; k < 8; ++k)
-          if (t + k < t1) s -= av[k] * y[cv[k]];
+        for (int t = 0; t < NPRE; ++t)
+          if (cur.q0 + t < cur.q1) s -= cur.av[t] * y[cur.cv[t]];
+        y[cur.i] = row_sum(p.ucol, u, cur.i, cur.q0 + NPRE, cur.q1, s) / dii;
       }
-      y[i] = s / dii;
+      for (int r = p.blev_ptr[L] + lane + 32; r < p.blev_ptr[L + 1]; r += 32) {
+        const int i = p.blev_row[r];
+        const int t0 = __ldg(p.uptr + i);
+        y[i] = row_sum(p.ucol, u, i, t0 + 1, __ldg(p.uptr + i + 1), y[i]) / u[t0];
+      }
+      __syncwarp();
+      cur = nx1;
+      nx1 = nx2;
     }
-    __syncwarp();
   }
   if (p.y_ext) {
     for (int l = lane; l < p.n; l += 32) p.y_ext[(size_t)box * p.n + l] = y[l];
