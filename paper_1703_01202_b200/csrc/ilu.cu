@@ -211,11 +211,35 @@ __global__ void __launch_bounds__(AWMAX * 32) k_ilu_apply(const IluArgs p, int n
     }
     return s;
   };
+  // A level holding ONE long row (every level of the complete-fill LU, whose rows chain
+  // i-1 -> i): the whole warp takes the row, lanes split its entries (coalesced loads), and a
+  // fixed-order warp sum closes it (a different summation order than the serial one: rounding
+  // only).  s = y[i] - sum_q val[q] y[col[q]].
+  auto row_warp = [&](const int* col, const double* val, int q0, int q1, double yi) {
+    double part = 0.0;
+    for (int q = q0 + lane; q < q1; q += 32) part = fma(val[q], y[__ldg(col + q)], part);
+    return yi - warp_sum(part);
+  };
+  constexpr int LONG = 24;   // entries from which a single-row level goes to the whole warp
   {   // L y = r (unit lower)
     Pre cur, nx1, nx2;
     fetch(p.flev_ptr, p.flev_row, p.nflev, p.lptr, p.lcol, a, 0, false, cur);
     fetch(p.flev_ptr, p.flev_row, p.nflev, p.lptr, p.lcol, a, 1, false, nx1);
     for (int L = 0; L < p.nflev; ++L) {
+      const int rs = __ldg(p.flev_ptr + L);
+      if (__ldg(p.flev_ptr + L + 1) - rs == 1) {
+        const int i = __ldg(p.flev_row + rs), q0 = __ldg(p.lptr + i), q1 = __ldg(p.lptr + i + 1);
+        if (q1 - q0 >= LONG) {
+          const double s = row_warp(p.lcol, a, q0, q1, y[i]);
+          __syncwarp();
+          if (lane == 0) y[i] = s;
+          __syncwarp();
+          fetch(p.flev_ptr, p.flev_row, p.nflev, p.lptr, p.lcol, a, L + 2, false, nx2);
+          cur = nx1;
+          nx1 = nx2;
+          continue;
+        }
+      }
       fetch(p.flev_ptr, p.flev_row, p.nflev, p.lptr, p.lcol, a, L + 2, false, nx2);
       if (cur.i >= 0) {
         double s = y[cur.i];
@@ -239,6 +263,20 @@ __global__ void __launch_bounds__(AWMAX * 32) k_ilu_apply(const IluArgs p, int n
     fetch(p.blev_ptr, p.blev_row, p.nblev, p.uptr, p.ucol, u, 0, true, cur);
     fetch(p.blev_ptr, p.blev_row, p.nblev, p.uptr, p.ucol, u, 1, true, nx1);
     for (int L = 0; L < p.nblev; ++L) {
+      const int rs = __ldg(p.blev_ptr + L);
+      if (__ldg(p.blev_ptr + L + 1) - rs == 1) {
+        const int i = __ldg(p.blev_row + rs), t0 = __ldg(p.uptr + i), t1 = __ldg(p.uptr + i + 1);
+        if (t1 - t0 - 1 >= LONG) {
+          const double s = row_warp(p.ucol, u, t0 + 1, t1, y[i]) / u[t0];
+          __syncwarp();
+          if (lane == 0) y[i] = s;
+          __syncwarp();
+          fetch(p.blev_ptr, p.blev_row, p.nblev, p.uptr, p.ucol, u, L + 2, true, nx2);
+          cur = nx1;
+          nx1 = nx2;
+          continue;
+        }
+      }
       fetch(p.blev_ptr, p.blev_row, p.nblev, p.uptr, p.ucol, u, L + 2, true, nx2);
       if (cur.i >= 0) {
         const double dii = u[cur.q0 - 1];
