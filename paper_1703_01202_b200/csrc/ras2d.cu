@@ -449,6 +449,10 @@ struct RasColArgs {
   const int* gate;   // device-resident FGMRES: skip the launch when *gate != 0 (f1)
   double W[6];                  // 25-point class weights: (0,0) (0,1) (0,2) (1,1) (0,3) (1,2)
   double ih2;
+  // Neumann-type mirror BCs (row f3, R23): ext-box nodes outside the domain are no unknowns
+  // (zero basis entries) and the padded planes carry the mirror ghosts of v and c v, refreshed
+  // after every basis write in boxes that touch a wall
+  int mirror;
 };
 
 constexpr int wclass(int ax, int ay) {
@@ -658,7 +662,7 @@ __device__ __forceinline__ bool col_dispatch(int j, double (&Vr)[K][R], double (
   }
 }
 
-template <int K, int R>
+template <int K, int R, bool MIR>
 __global__ void __launch_bounds__(NTC, 1) ras2d_col_kernel(const __grid_constant__ RasColArgs p) {
   constexpr int PP = col_pp(R);
   extern __shared__ __align__(128) double smem_dyn[];
@@ -667,6 +671,7 @@ __global__ void __launch_bounds__(NTC, 1) ras2d_col_kernel(const __grid_constant
   double* red = pcv + PP * PPY;              // 2 x NWC x 16
   double* hwall = red + 2 * NWC * 16;        // NWC x 3 x 16
   double* stg = hwall + NWC * 48;            // next box's v, c of each thread's nodes (2 x NTC x R)
+  int* gp = reinterpret_cast<int*>(stg + 2 * NTC * R);   // mirror: ghost -> partner (PP x PPY)
   __shared__ double H[(K + 1) * K];
   __shared__ double gv[K + 1], cs[K], sn[K], yv[K], rd[K];
 
@@ -710,20 +715,43 @@ __global__ void __launch_bounds__(NTC, 1) ras2d_col_kernel(const __grid_constant
   prefetch(blockIdx.x);
   // persistent CTA: boxes blockIdx.x, + gridDim.x, ...; the next box's inputs load while the
   // current box is solved
+  bool prev_ghosts = false;
   for (int box = blockIdx.x; box < nboxes; box += gridDim.x) {
   const int ibx = box % nbx, iby = box / nbx;
+  const int gx0 = ibx * p.bx - p.o, gy0 = iby * p.by - p.o;
+  // mirror: a box whose padded plane reaches past a wall has ghost positions
+  const bool ghosts = MIR && (gx0 - 3 < 0 || gy0 - 3 < 0 || gx0 + Ex + 3 > p.nx ||
+                                   gy0 + Ey + 3 > p.ny);
+  if (MIR && prev_ghosts)   // the previous box left ghost values on the ring: zero it again
+    for (int q = tid; q < 2 * PP * PPY; q += blockDim.x) pv[q] = 0.0;
+  if (MIR && ghosts)
+    for (int q = tid; q < PP * PPY; q += blockDim.x) {
+      const int pc = q % PP, pr = q / PP, gx = gx0 + pc - 3, gy = gy0 + pr - 3;
+      int part = -1;
+      if (pc < Ex + 6 && pr < Ey + 6 && (gx < 0 || gx >= p.nx || gy < 0 || gy >= p.ny)) {
+        const int mx = gx < 0 ? -1 - gx : (gx >= p.nx ? 2 * p.nx - 1 - gx : gx);
+        const int my = gy < 0 ? -1 - gy : (gy >= p.ny ? 2 * p.ny - 1 - gy : gy);
+        const int lx = mx - gx0, ly = my - gy0;   // partner in the ext box, else zero
+        part = (lx >= 0 && lx < Ex && ly >= 0 && ly < Ey) ? (ly + 3) * PP + lx + 3 : -2;
+      }
+      gp[q] = part;
+    }
+  prev_ghosts = ghosts;
   cp_async_wait_all();
   double Vr[K][R];
   double w[R], cr[R], cvv[R];
+  bool act[R];   // unknowns of A_k: the ext-box nodes inside the domain
   double acc0[1] = {0.0};
 #pragma unroll
   for (int r = 0; r < R; ++r) {
     w[r] = 0.0;
     cr[r] = 0.0;
+    act[r] = own[r] && (!MIR || (gx0 + x >= 0 && gx0 + x < p.nx && gy0 + y0 + r >= 0 &&
+                                      gy0 + y0 + r < p.ny));
     if (own[r]) {
       const int li = x - p.o, lj = y0 + r - p.o;
       const bool owned = li >= 0 && li < p.bx && lj >= 0 && lj < p.by;
-      w[r] = (p.restrict_owned && !owned) ? 0.0 : sv[r * NTC];
+      w[r] = ((p.restrict_owned && !owned) || !act[r]) ? 0.0 : sv[r * NTC];
       cr[r] = sc[r * NTC];
       acc0[0] = fma(w[r], w[r], acc0[0]);
     }
@@ -768,6 +796,13 @@ __global__ void __launch_bounds__(NTC, 1) ras2d_col_kernel(const __grid_constant
 #pragma unroll 1
   for (int j = 0; j < K; ++j) {
     __syncthreads();                                  // planes hold v_j and c v_j
+    if (MIR && ghosts) {   // mirror ghosts of v_j and c v_j (the even extension)
+      for (int q = tid; q < PP * PPY; q += blockDim.x) {
+        const int g = gp[q];
+        if (g >= 0) { pv[q] = pv[g]; pcv[q] = pcv[g]; }
+      }
+      __syncthreads();
+    }
     CPROF(0);
     // ---- w = A_k v_j: direct 25-point linear part, column by column (not in the Givens warp)
     if (!gwarp) {
@@ -788,11 +823,11 @@ __global__ void __launch_bounds__(NTC, 1) ras2d_col_kernel(const __grid_constant
     }
     // ---- minus Delta(c v): x-neighbours from the plane, y-neighbours from registers
 #pragma unroll
-    for (int r = 0; r < R; ++r) {
-      const double up = (r == 0) ? pcvb[-PP] : cvv[r - 1];
-      const double dn = (r == R - 1) ? pcvb[R * PP] : cvv[r + 1];
+    for (int r = 0; r < R; ++r) {   // (mirror: a y-neighbour in the strip may be a ghost)
+      const double up = (r == 0 || MIR) ? pcvb[(r - 1) * PP] : cvv[r - 1];
+      const double dn = (r == R - 1 || MIR) ? pcvb[(r + 1) * PP] : cvv[r + 1];
       const double lap = (pcvb[r * PP - 1] + pcvb[r * PP + 1]) + (up + dn) - 4.0 * cvv[r];
-      w[r] = own[r] ? fma(-p.ih2, lap, out[r]) : 0.0;
+      w[r] = act[r] ? fma(-p.ih2, lap, out[r]) : 0.0;
     }
     } else {
 #pragma unroll
@@ -851,7 +886,8 @@ extern "C" void pfc_ras_prof_read(long long* out) {
 namespace {
 #endif
 size_t ras2d_col_smem_bytes(int R) {
-  return (size_t)(2 * col_pp(R) * PPY + 2 * NWC * 16 + NWC * 48 + 2 * NTC * R) * sizeof(double);
+  return (size_t)(2 * col_pp(R) * PPY + 2 * NWC * 16 + NWC * 48 + 2 * NTC * R) * sizeof(double) +
+         (size_t)col_pp(R) * PPY * sizeof(int);
 }
 
 typedef void (*ras2d_fn)(RasArgs);
@@ -873,14 +909,15 @@ ras2d_fn pick(int k) {
 
 // column-strip instantiations: local GMRES steps K x rows per thread R
 typedef void (*ras2d_col_fn)(const RasColArgs);
-ras2d_col_fn pick_col(int k, int r) {
+template <bool MIR>
+ras2d_col_fn pick_col_t(int k, int r) {
 #define RC(K)                                              \
   case K:                                                  \
     switch (r) {                                           \
-      case 1: return ras2d_col_kernel<K, 1>;               \
-      case 2: return ras2d_col_kernel<K, 2>;               \
-      case 4: return ras2d_col_kernel<K, 4>;               \
-      case 5: return ras2d_col_kernel<K, 5>;               \
+      case 1: return ras2d_col_kernel<K, 1, MIR>;          \
+      case 2: return ras2d_col_kernel<K, 2, MIR>;          \
+      case 4: return ras2d_col_kernel<K, 4, MIR>;          \
+      case 5: return ras2d_col_kernel<K, 5, MIR>;          \
     }                                                      \
     return nullptr;
   switch (k) {
@@ -888,6 +925,9 @@ ras2d_col_fn pick_col(int k, int r) {
   }
 #undef RC
   return nullptr;
+}
+ras2d_col_fn pick_col(int k, int r, bool mirror = false) {
+  return mirror ? pick_col_t<true>(k, r) : pick_col_t<false>(k, r);
 }
 
 // rows per thread for the column kernel: the fewest that fit the extended box in NTC threads
@@ -908,7 +948,7 @@ int ras2d_plan(pfc_ctx* ctx) {
   const pfc_config& c = ctx->cfg;
   const int Ex = c.ras_box[0] + 2 * c.ras_overlap, Ey = c.ras_box[1] + 2 * c.ras_overlap;
   if (Ex * Ey > MAXN) return 0;
-  if (getenv("PFC_RAS_SMEM_BASIS") == nullptr && !c.mobility && c.bc == PFC_BC_PERIODIC) {
+  if (getenv("PFC_RAS_SMEM_BASIS") == nullptr && !c.mobility) {
     const int r = col_rows(c.ras_local_k, Ex, Ey);
     if (r) {
       const int ns = (Ey + r - 1) / r;
@@ -934,7 +974,7 @@ cudaError_t launch_ras_2d(pfc_ctx* ctx, const double* v, const double* c, double
   cudaError_t e;
   if (ctx->ras_rows > 0) {
     const int R = ctx->ras_rows;
-    ras2d_col_fn fn = pick_col(cf.ras_local_k, R);
+    ras2d_col_fn fn = pick_col(cf.ras_local_k, R, cf.bc == PFC_BC_MIRROR);
     if (!fn) return cudaErrorInvalidValue;
     e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, ctx->ras_smem);
     if (e != cudaSuccess) return e;
@@ -942,6 +982,7 @@ cudaError_t launch_ras_2d(pfc_ctx* ctx, const double* v, const double* c, double
     p.v = v; p.c = c; p.z = z;
     p.nx = cf.n[0]; p.ny = cf.n[1]; p.bx = cf.ras_box[0]; p.by = cf.ras_box[1];
     p.o = cf.ras_overlap; p.Ex = Ex; p.Ey = Ey; p.ns = (Ey + R - 1) / R;
+    p.mirror = cf.bc == PFC_BC_MIRROR;
     p.restrict_owned = cf.ras_variant == PFC_RAS_RIGHT;
     p.y_ext = cf.ras_variant == PFC_RAS_LEFT ? nullptr : ctx->ras_y;
     p.gate = ctx->gate;
