@@ -76,7 +76,8 @@ def test_mirror_residual_jacobian_energy_parity(shape, box, mob, omob):
 @pytest.mark.parametrize("variant", [P.PFC_RAS_LEFT, P.PFC_RAS_AS, P.PFC_RAS_RIGHT])
 @pytest.mark.parametrize("mob,omob", MOBS)
 @pytest.mark.parametrize("shape,box,o,k", [((64, 64), (16, 16), 2, 10), ((48, 36), (12, 12), 1, 5),
-                                           ((64, 48), (16, 16), 0, 10)])
+                                           ((64, 48), (16, 16), 0, 10),
+                                           ((128, 96), (32, 32), 2, 10)])   # cfg2's boxes
 def test_mirror_schwarz_parity(shape, box, o, k, variant, mob, omob):
     """clipped subdomains; o = 0 puts the walls on the zero ring of the boundary boxes"""
     phi = random_field(shape, 811, 0.07, 0.07)
@@ -98,6 +99,20 @@ def test_mirror_one_step_parity(mob, omob):
     phi = dev(phi0)
     _, info = ctx.step(phi, dt)
     ref, ok, oinfo = O.newton(phi0, H, prm_n((16, 16), mob=omob), dt)
+    assert ok and info["converged"]
+    assert info["newton_its"] == oinfo.newton_its and info["gmres_its"] == oinfo.gmres_its
+    assert rel(host(phi), ref) <= 1e-10
+
+
+def test_mirror_one_step_parity_cfg2_boxes():
+    """the production column kernel with 4 rows per thread (cfg2's 32^2 boxes, overlap 2)"""
+    shape = (128, 128)
+    phi0 = random_field(shape, 2, 0.07, 0.07)
+    dt = 0.5
+    ctx = ctx_n(shape, (32, 32))
+    phi = dev(phi0)
+    _, info = ctx.step(phi, dt)
+    ref, ok, oinfo = O.newton(phi0, H, prm_n((32, 32)), dt)
     assert ok and info["converged"]
     assert info["newton_its"] == oinfo.newton_its and info["gmres_its"] == oinfo.gmres_its
     assert rel(host(phi), ref) <= 1e-10
