@@ -449,10 +449,15 @@ struct RasColArgs {
   const int* gate;   // device-resident FGMRES: skip the launch when *gate != 0 (f1)
   double W[6];                  // 25-point class weights: (0,0) (0,1) (0,2) (1,1) (0,3) (1,2)
   double ih2;
+  double idt, alpha;            // MOB: 1/dt, (1 - gamma)/2
   // Neumann-type mirror BCs (row f3, R23): ext-box nodes outside the domain are no unknowns
   // (zero basis entries) and the padded planes carry the mirror ghosts of v and c v, refreshed
   // after every basis write in boxes that touch a wall
   int mirror;
+  // variable mobility (row f3, R8b): the Jacobian state of the iterate (Phi, psi, A)
+  const double* phi;
+  const double* psi;
+  const double* A;
 };
 
 constexpr int wclass(int ax, int ay) {
@@ -662,7 +667,10 @@ __device__ __forceinline__ bool col_dispatch(int j, double (&Vr)[K][R], double (
   }
 }
 
-template <int K, int R, bool MIR>
+// MOB: variable mobility M = 1 - u^2 (row f3, R8b): A_k v = R J R^T v staged on shared planes
+// like ras2d_kernel (L1 = Delta v; B = alpha v + L1 + Delta L1 / 2 + c v; then
+// v/dt - (grad . M grad) B - (grad . (-u v) grad) A at the own nodes), the basis in registers
+template <int K, int R, bool MIR, bool MOB = false>
 __global__ void __launch_bounds__(NTC, 1) ras2d_col_kernel(const __grid_constant__ RasColArgs p) {
   constexpr int PP = col_pp(R);
   extern __shared__ __align__(128) double smem_dyn[];
@@ -672,6 +680,11 @@ __global__ void __launch_bounds__(NTC, 1) ras2d_col_kernel(const __grid_constant
   double* hwall = red + 2 * NWC * 16;        // NWC x 3 x 16
   double* stg = hwall + NWC * 48;            // next box's v, c of each thread's nodes (2 x NTC x R)
   int* gp = reinterpret_cast<int*>(stg + 2 * NTC * R);   // mirror: ghost -> partner (PP x PPY)
+  double* pl = reinterpret_cast<double*>(gp + PP * PPY);  // MOB: L1, B, M, A, u planes
+  double* pb = pl + PP * PPY;
+  double* pm = pb + PP * PPY;
+  double* pa = pm + PP * PPY;
+  double* pu = pa + PP * PPY;
   __shared__ double H[(K + 1) * K];
   __shared__ double gv[K + 1], cs[K], sn[K], yv[K], rd[K];
 
@@ -697,6 +710,8 @@ __global__ void __launch_bounds__(NTC, 1) ras2d_col_kernel(const __grid_constant
   double* pcvb = pcv + (y0 + 3) * PP + x + 3;
 
   for (int q = tid; q < 2 * PP * PPY; q += blockDim.x) pv[q] = 0.0;   // the ring stays zero
+  if (MOB)
+    for (int q = tid; q < 2 * PP * PPY; q += blockDim.x) pl[q] = 0.0;  // L1, B outside their ranges
   double* sv = stg + tid;              // [r][thread]: a warp's 8-byte accesses are contiguous
   double* sc = stg + NTC * R + tid;
   // R_k^delta v and c of a box (periodic wrap) into this thread's staging slots, asynchronously
@@ -737,6 +752,18 @@ __global__ void __launch_bounds__(NTC, 1) ras2d_col_kernel(const __grid_constant
       gp[q] = part;
     }
   prev_ghosts = ghosts;
+  if (MOB)   // M = 1 - u^2, A and u of the iterate on the ext box and its +1 ring (else 0)
+    for (int q = tid; q < PP * PPY; q += blockDim.x) {
+      const int pc = q % PP, pr = q / PP;
+      double m = 0.0, a = 0.0, u = 0.0;
+      if (pc >= 2 && pc < Ex + 4 && pr >= 2 && pr < Ey + 4) {
+        const size_t g = (size_t)wrapi(gx0 + pc - 3, p.nx) + (size_t)p.nx * wrapi(gy0 + pr - 3, p.ny);
+        u = 0.5 * (p.phi[g] + p.psi[g]);
+        m = 1.0 - u * u;
+        a = p.A[g];
+      }
+      pm[q] = m; pa[q] = a; pu[q] = u;
+    }
   cp_async_wait_all();
   double Vr[K][R];
   double w[R], cr[R], cvv[R];
@@ -804,6 +831,37 @@ __global__ void __launch_bounds__(NTC, 1) ras2d_col_kernel(const __grid_constant
       __syncthreads();
     }
     CPROF(0);
+    if constexpr (MOB) {   // staged variable-coefficient operator (all threads share the stages)
+      const double ih2 = p.ih2, al = p.alpha;
+      const int wl = Ex + 4, wb = Ex + 2;
+      for (int q = tid; q < wl * (Ey + 4); q += blockDim.x) {   // L1 on padded [1, P-1)
+        const int f = (1 + q / wl) * PP + 1 + q % wl;
+        pl[f] = ih2 * ((pv[f - 1] + pv[f + 1]) + (pv[f - PP] + pv[f + PP]) - 4.0 * pv[f]);
+      }
+      __syncthreads();
+      for (int q = tid; q < wb * (Ey + 2); q += blockDim.x) {   // B on padded [2, P-2)
+        const int f = (2 + q / wb) * PP + 2 + q % wb;
+        const double lapl = ih2 * ((pl[f - 1] + pl[f + 1]) + (pl[f - PP] + pl[f + PP]) - 4.0 * pl[f]);
+        pb[f] = al * pv[f] + pcv[f] + pl[f] + 0.5 * lapl;
+      }
+      __syncthreads();
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        w[r] = 0.0;
+        if (!gwarp && act[r]) {
+          const int f = (y0 + r + 3) * PP + x + 3;
+          auto dmg = [&](const double* m, const double* g, bool uv) {
+            auto mm = [&](int k) { return uv ? -pu[k] * pv[k] : m[k]; };
+            const double mc = mm(f), gc = g[f];
+            return ih2 * (0.5 * (mc + mm(f + 1)) * (g[f + 1] - gc) -
+                          0.5 * (mc + mm(f - 1)) * (gc - g[f - 1]) +
+                          0.5 * (mc + mm(f + PP)) * (g[f + PP] - gc) -
+                          0.5 * (mc + mm(f - PP)) * (gc - g[f - PP]));
+          };
+          w[r] = pv[f] * p.idt - dmg(pm, pb, false) - dmg(nullptr, pa, true);
+        }
+      }
+    } else
     // ---- w = A_k v_j: direct 25-point linear part, column by column (not in the Givens warp)
     if (!gwarp) {
     double out[R];
@@ -885,9 +943,10 @@ extern "C" void pfc_ras_prof_read(long long* out) {
 }
 namespace {
 #endif
-size_t ras2d_col_smem_bytes(int R) {
+size_t ras2d_col_smem_bytes(int R, bool mob = false) {
   return (size_t)(2 * col_pp(R) * PPY + 2 * NWC * 16 + NWC * 48 + 2 * NTC * R) * sizeof(double) +
-         (size_t)col_pp(R) * PPY * sizeof(int);
+         (size_t)col_pp(R) * PPY * sizeof(int) +
+         (mob ? (size_t)5 * col_pp(R) * PPY * sizeof(double) : 0);
 }
 
 typedef void (*ras2d_fn)(RasArgs);
@@ -926,18 +985,32 @@ ras2d_col_fn pick_col_t(int k, int r) {
 #undef RC
   return nullptr;
 }
-ras2d_col_fn pick_col(int k, int r, bool mirror = false) {
+ras2d_col_fn pick_col_mob(int k, int r) {
+  switch (k) {
+    case 10:
+      switch (r) {
+        case 1: return ras2d_col_kernel<10, 1, false, true>;
+        case 2: return ras2d_col_kernel<10, 2, false, true>;
+        case 4: return ras2d_col_kernel<10, 4, false, true>;
+        case 5: return ras2d_col_kernel<10, 5, false, true>;
+      }
+  }
+  return nullptr;
+}
+ras2d_col_fn pick_col(int k, int r, bool mirror = false, bool mob = false) {
+  if (mob) return mirror ? nullptr : pick_col_mob(k, r);
   return mirror ? pick_col_t<true>(k, r) : pick_col_t<false>(k, r);
 }
 
 // rows per thread for the column kernel: the fewest that fit the extended box in NTC threads
-int col_rows(int k, int Ex, int Ey) {
+int col_rows(int k, int Ex, int Ey, bool mirror = false, bool mob = false) {
   if (Ex + 6 > PP || Ey > 42) return 0;
   const int cand[4] = {1, 2, 4, 5};
   for (int i = 0; i < 4; ++i) {
     const int r = cand[i];
     const int ns = (Ey + r - 1) / r;
-    if (Ex + 6 <= col_pp(r) && (Ex * ns + 31) / 32 * 32 + 32 <= NTC && pick_col(k, r)) return r;
+    if (Ex + 6 <= col_pp(r) && (Ex * ns + 31) / 32 * 32 + 32 <= NTC && pick_col(k, r, mirror, mob))
+      return r;
   }
   return 0;
 }
@@ -948,11 +1021,12 @@ int ras2d_plan(pfc_ctx* ctx) {
   const pfc_config& c = ctx->cfg;
   const int Ex = c.ras_box[0] + 2 * c.ras_overlap, Ey = c.ras_box[1] + 2 * c.ras_overlap;
   if (Ex * Ey > MAXN) return 0;
-  if (getenv("PFC_RAS_SMEM_BASIS") == nullptr && !c.mobility) {
-    const int r = col_rows(c.ras_local_k, Ex, Ey);
+  const bool mir = c.bc == PFC_BC_MIRROR, mob = c.mobility != PFC_MOBILITY_ONE;
+  if (getenv("PFC_RAS_SMEM_BASIS") == nullptr && !(mir && mob)) {
+    const int r = col_rows(c.ras_local_k, Ex, Ey, mir, mob);
     if (r) {
       const int ns = (Ey + r - 1) / r;
-      ctx->ras_smem = (int)ras2d_col_smem_bytes(r);
+      ctx->ras_smem = (int)ras2d_col_smem_bytes(r, mob);
       ctx->ras_threads = (Ex * ns + 31) / 32 * 32 + 32;   // node warps + the Givens warp
       ctx->ras_rows = r;                             // rows per thread
       return 1;
@@ -974,7 +1048,8 @@ cudaError_t launch_ras_2d(pfc_ctx* ctx, const double* v, const double* c, double
   cudaError_t e;
   if (ctx->ras_rows > 0) {
     const int R = ctx->ras_rows;
-    ras2d_col_fn fn = pick_col(cf.ras_local_k, R, cf.bc == PFC_BC_MIRROR);
+    const bool mob = cf.mobility != PFC_MOBILITY_ONE;
+    ras2d_col_fn fn = pick_col(cf.ras_local_k, R, cf.bc == PFC_BC_MIRROR, mob);
     if (!fn) return cudaErrorInvalidValue;
     e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, ctx->ras_smem);
     if (e != cudaSuccess) return e;
@@ -983,6 +1058,9 @@ cudaError_t launch_ras_2d(pfc_ctx* ctx, const double* v, const double* c, double
     p.nx = cf.n[0]; p.ny = cf.n[1]; p.bx = cf.ras_box[0]; p.by = cf.ras_box[1];
     p.o = cf.ras_overlap; p.Ex = Ex; p.Ey = Ey; p.ns = (Ey + R - 1) / R;
     p.mirror = cf.bc == PFC_BC_MIRROR;
+    p.phi = ctx->mob_phi; p.psi = ctx->mob_psi; p.A = ctx->mob_A;   // MOB: Jacobian state
+    p.idt = 1.0 / dt;
+    p.alpha = 0.5 * (1.0 - cf.gamma);
     p.restrict_owned = cf.ras_variant == PFC_RAS_RIGHT;
     p.y_ext = cf.ras_variant == PFC_RAS_LEFT ? nullptr : ctx->ras_y;
     p.gate = ctx->gate;
