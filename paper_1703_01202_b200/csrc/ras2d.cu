@@ -757,7 +757,8 @@ __global__ void __launch_bounds__(NTC, 1) ras2d_col_kernel(const __grid_constant
       const int pc = q % PP, pr = q / PP;
       double m = 0.0, a = 0.0, u = 0.0;
       if (pc >= 2 && pc < Ex + 4 && pr >= 2 && pr < Ey + 4) {
-        const size_t g = (size_t)wrapi(gx0 + pc - 3, p.nx) + (size_t)p.nx * wrapi(gy0 + pr - 3, p.ny);
+        const size_t g = (size_t)axis2(gx0 + pc - 3, p.nx, MIR) +
+                         (size_t)p.nx * axis2(gy0 + pr - 3, p.ny, MIR);   // MIR: even extension
         u = 0.5 * (p.phi[g] + p.psi[g]);
         m = 1.0 - u * u;
         a = p.A[g];
@@ -985,20 +986,21 @@ ras2d_col_fn pick_col_t(int k, int r) {
 #undef RC
   return nullptr;
 }
+template <bool MIR>
 ras2d_col_fn pick_col_mob(int k, int r) {
   switch (k) {
     case 10:
       switch (r) {
-        case 1: return ras2d_col_kernel<10, 1, false, true>;
-        case 2: return ras2d_col_kernel<10, 2, false, true>;
-        case 4: return ras2d_col_kernel<10, 4, false, true>;
-        case 5: return ras2d_col_kernel<10, 5, false, true>;
+        case 1: return ras2d_col_kernel<10, 1, MIR, true>;
+        case 2: return ras2d_col_kernel<10, 2, MIR, true>;
+        case 4: return ras2d_col_kernel<10, 4, MIR, true>;
+        case 5: return ras2d_col_kernel<10, 5, MIR, true>;
       }
   }
   return nullptr;
 }
 ras2d_col_fn pick_col(int k, int r, bool mirror = false, bool mob = false) {
-  if (mob) return mirror ? nullptr : pick_col_mob(k, r);
+  if (mob) return mirror ? pick_col_mob<true>(k, r) : pick_col_mob<false>(k, r);
   return mirror ? pick_col_t<true>(k, r) : pick_col_t<false>(k, r);
 }
 
@@ -1022,7 +1024,7 @@ int ras2d_plan(pfc_ctx* ctx) {
   const int Ex = c.ras_box[0] + 2 * c.ras_overlap, Ey = c.ras_box[1] + 2 * c.ras_overlap;
   if (Ex * Ey > MAXN) return 0;
   const bool mir = c.bc == PFC_BC_MIRROR, mob = c.mobility != PFC_MOBILITY_ONE;
-  if (getenv("PFC_RAS_SMEM_BASIS") == nullptr && !(mir && mob)) {
+  if (getenv("PFC_RAS_SMEM_BASIS") == nullptr) {
     const int r = col_rows(c.ras_local_k, Ex, Ey, mir, mob);
     if (r) {
       const int ns = (Ey + r - 1) / r;
