@@ -62,7 +62,6 @@ struct Col3 {
   static constexpr int PXR = col3_pxr(E);    // row pitch (x)
   static constexpr int PY = E + 6;           // padded rows (y)
   static constexpr int PP = PXR * PY;        // plane pitch (z: E planes, no ring)
-  static constexpr int NE = E * E * E;       // ext-box nodes
 };
 
 // Contribution of the xy offset (DX, DY) to the thread's E outputs: the z-segment of that
