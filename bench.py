@@ -413,7 +413,7 @@ def main():
     ap.add_argument("--impl", default="cuda", choices=["cuda", "reference"])
     ap.add_argument("--config", default="cfg2")
     ap.add_argument("--jv-size", type=int, default=512)
-    ap.add_argument("--cpu-steps", type=int, default=2)
+    ap.add_argument("--cpu-steps", type=int, default=4)   # ~13 s of oracle work on one core
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--mobility", type=int, default=0, help="1: M = 1 - phi^2 (row f3, 2D)")
     ap.add_argument("--ras-variant", type=int, default=0, help="0 left-RAS, 1 AS, 2 right-RAS")
