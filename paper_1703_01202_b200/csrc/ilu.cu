@@ -337,6 +337,21 @@ pfc_status ilu_setup(pfc_ctx* ctx) {
   int E[3] = {1, 1, 1};
   for (int d = 0; d < nd; ++d) E[d] = c.ras_box[d] + 2 * c.ras_overlap;
   const int n = E[0] * E[1] * E[2];
+  // cheap early rejection (before the symbolic factorisation, whose lists grow like band^2):
+  // the ext box must fit the factor kernel's shared-memory plan, and so must the complete fill
+  // of the natural-order LU, whose rows span the band b = 3 E0 (2D) / 3 E0 E1 (3D) on both
+  // sides of the diagonal (row length <= 2b+1) with up to b^2 IKJ updates per row
+  constexpr size_t kSmemPlan = 200 * 1024;
+  if ((size_t)n * sizeof(double) > kSmemPlan)
+    return pfc_fail(ctx, PFC_EINVAL, "ILU: ext box too large for the shared-memory plan");
+  if (c.ras_local_solver == PFC_LOCAL_LU) {
+    const size_t b = (size_t)3 * E[0] * (nd == 3 ? E[1] : 1);
+    const size_t mr = 2 * b + 1, mu = b * b;
+    if ((2 * mr + mu) * 8 + (mr + 1 + mu) * 4 > kSmemPlan)
+      return pfc_fail(ctx, PFC_EINVAL,
+                      "LU: complete fill of this ext box exceeds the shared-memory plan "
+                      "(every 3D box of the configs; use PFC_LOCAL_ILU or PFC_LOCAL_GMRES)");
+  }
   auto pos = [&](int i, int j, int k) { return i + E[0] * (j + E[1] * k); };
   // pattern of A: the radius-3 L1 stencil truncated at the box, per row a map col -> level
   std::vector<std::map<int, int>> rows(n);
@@ -455,12 +470,12 @@ pfc_status ilu_setup(pfc_ctx* ctx) {
       !up(ctx, &I->d_ecls, ecls) || !up(ctx, &I->d_ectype, ectype) ||
       !up(ctx, &I->d_ukptr, ukptr) || !up(ctx, &I->d_usrc, usrc) || !up(ctx, &I->d_udst, udst) ||
       !up(ctx, &I->d_flev_ptr, fptr) || !up(ctx, &I->d_flev_row, frow) ||
-      !up(ctx, &I->d_blev_ptr, bptr) || !up(ctx, &I->d_blev_row, brow) ||
-      cudaMalloc(&I->d_vals, I->nbox * nnz * sizeof(double)) != cudaSuccess)
+      !up(ctx, &I->d_blev_ptr, bptr) || !up(ctx, &I->d_blev_row, brow))
     return pfc_fail(ctx, PFC_ENOMEM, "ILU structures");
-  if ((size_t)n * sizeof(double) > 200 * 1024 ||
-      (size_t)(2 * I->maxrow + I->maxupd) * 8 + (I->maxrow + 1 + I->maxupd) * 4 > 200 * 1024)
-    return pfc_fail(ctx, PFC_EINVAL, "ILU: rows or ext box too large for the shared-memory plan");
+  if ((size_t)(2 * I->maxrow + I->maxupd) * 8 + (I->maxrow + 1 + I->maxupd) * 4 > kSmemPlan)
+    return pfc_fail(ctx, PFC_EINVAL, "ILU: rows too large for the shared-memory plan");
+  if (cudaMalloc(&I->d_vals, I->nbox * nnz * sizeof(double)) != cudaSuccess)   // after the checks
+    return pfc_fail(ctx, PFC_ENOMEM, "ILU factor values");
   return PFC_OK;
 }
 

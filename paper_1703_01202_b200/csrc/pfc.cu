@@ -546,7 +546,9 @@ pfc_status pfc_create(const pfc_config* cfg, void* stream, pfc_ctx** out) {
       pfc_check_cuda(ctx, cudaMalloc(&ctx->gm, sizeof(pfc_gmres_dev)), "gmres state") ||
       pfc_check_cuda(ctx, cudaMemset(ctx->gm, 0, sizeof(pfc_gmres_dev)), "gmres state") ||
       pfc_check_cuda(ctx, cudaMallocHost(&ctx->hflags, 4 * PFC_MAX_RESTART * sizeof(int)), "flags") ||
-      pfc_check_cuda(ctx, cudaMallocHost(&ctx->hscal, SC_TOTAL * sizeof(double)), "hscal"))
+      pfc_check_cuda(ctx, cudaMallocHost(&ctx->hscal, SC_TOTAL * sizeof(double)), "hscal") ||
+      pfc_check_cuda(ctx, cudaMalloc(&ctx->d_jcnt, 4 * sizeof(unsigned long long)), "jcnt") ||
+      pfc_check_cuda(ctx, cudaMemset(ctx->d_jcnt, 0, 4 * sizeof(unsigned long long)), "jcnt"))
     return fail(PFC_ENOMEM);
   if (c.ndim == 3) {
     int grid = 0;
@@ -582,6 +584,7 @@ void pfc_destroy(pfc_ctx* ctx) {
   for (double* f : fs)
     if (f) cudaFree(f);
   if (ctx->ticket) cudaFree(ctx->ticket);
+  if (ctx->d_jcnt) cudaFree(ctx->d_jcnt);
   if (ctx->gm) cudaFree(ctx->gm);
   if (ctx->hflags) cudaFreeHost(ctx->hflags);
   for (cudaEvent_t e : ctx->step_ev)
@@ -607,6 +610,9 @@ pfc_status pfc_profile_enable(pfc_ctx* ctx, int on) {
     ctx->prof_bytes[i] = 0.0;
     ctx->prof_flops[i] = 0.0;
   }
+  ctx->ras_model_next = ctx->ras_model_cs = ctx->ras_model_nout = 0.0;
+  CK(cudaMemsetAsync(ctx->d_jcnt, 0, 4 * sizeof(unsigned long long), ctx->stream), "jcnt reset");
+  CK(cudaStreamSynchronize(ctx->stream), "jcnt reset");
   return PFC_OK;
 }
 
@@ -617,7 +623,16 @@ pfc_status pfc_profile_query(pfc_ctx* ctx, int cls, long long* count, double* to
   if (count) *count = ctx->prof_count[cls];
   if (total_ms) *total_ms = ctx->prof_ms[cls];
   if (bytes) *bytes = ctx->prof_bytes[cls];
-  if (flops) *flops = ctx->prof_flops[cls];
+  if (flops) {
+    *flops = ctx->prof_flops[cls];
+    if (cls == PFC_K_RAS && ctx->ras_model_next > 0.0) {   // counted Arnoldi steps
+      unsigned long long j[3] = {0, 0, 0};
+      CK(cudaMemcpy(j, ctx->d_jcnt, sizeof j, cudaMemcpyDeviceToHost), "jcnt read");
+      const double s1 = (double)j[0], s2 = (double)j[1], nb = (double)j[2];
+      *flops += ctx->ras_model_next * (ctx->ras_model_cs * s1 + 4.0 * (s2 + s1) + 3.0 * s1 +
+                                       3.0 * nb) + 2.0 * s1 * ctx->ras_model_nout;
+    }
+  }
   return PFC_OK;
 }
 

@@ -90,7 +90,22 @@ struct pfc_ctx {
   double prof_ms[PFC_K_NCLASSES] = {0};
   double prof_bytes[PFC_K_NCLASSES] = {0};   // algorithmic bytes of the launched kernels
   double prof_flops[PFC_K_NCLASSES] = {0};   // algorithmic flops
+  // local-GMRES subdomain solves: flops come from the Arnoldi steps the boxes actually took
+  // (device counters d_jcnt = {sum jm, sum jm^2, boxes} over the profiled launches) and the
+  // per-box model of the launch (ext nodes, stencil flops per node and step, output nodes)
+  unsigned long long* d_jcnt = nullptr;
+  double ras_model_next = 0.0, ras_model_cs = 0.0, ras_model_nout = 0.0;
 };
+
+// record the per-box flop model of a local-GMRES subdomain-solve launch (profiling only):
+// flops of a box = next (Cs jm + 4 jm (jm+1) + 3 jm + 3) + 2 jm nout
+inline void ras_flop_model(pfc_ctx* ctx, double next_box, double cs, double nout_box) {
+  if (ctx->prof) {
+    ctx->ras_model_next = next_box;
+    ctx->ras_model_cs = cs;
+    ctx->ras_model_nout = nout_box;
+  }
+}
 
 // algorithmic bytes/flops of a launch (counted only while profiling)
 inline void pfc_account(pfc_ctx* ctx, int cls, double bytes, double flops) {

@@ -58,6 +58,7 @@ struct RasArgs {
   // (ext-box nodes outside the domain are no unknowns), and the padded plane carries the
   // mirror ghosts of the Krylov vector (the even extension) so that the stencils act as J
   int mirror;
+  unsigned long long* jcnt;   // profiling: Arnoldi steps taken (ras_count)
 };
 
 // node index of global (x, y): periodic wrap, or the mirror partner (R23)
@@ -198,6 +199,7 @@ __global__ void __launch_bounds__(NT, 1) ras2d_kernel(RasArgs p) {
   rb ^= 1;
   const double beta = sqrt(hx[0]);
   if (beta == 0.0) {
+    if (tid == 0) ras_count(p.jcnt, 0);
     if (p.y_ext) {
       for (int l = tid; l < n; l += NT) p.y_ext[(size_t)blockIdx.x * n + l] = 0.0;
     } else {
@@ -391,6 +393,7 @@ __global__ void __launch_bounds__(NT, 1) ras2d_kernel(RasArgs p) {
       for (int l = i + 1; l < jm; ++l) s -= H[i + ld * l] * yv[l];
       yv[i] = s / H[i + ld * i];
     }
+    ras_count(p.jcnt, jm);
   }
   __syncthreads();
   // (R_k^0)^T: owned nodes only, y = V yv
@@ -458,6 +461,7 @@ struct RasColArgs {
   const double* phi;
   const double* psi;
   const double* A;
+  unsigned long long* jcnt;     // profiling: Arnoldi steps taken (ras_count)
 };
 
 constexpr int wclass(int ax, int ay) {
@@ -791,6 +795,7 @@ __global__ void __launch_bounds__(NTC, 1) ras2d_col_kernel(const __grid_constant
   rb ^= 1;
   const double beta = sqrt(hx[0]);
   if (beta == 0.0) {
+    if (tid == 0) ras_count(p.jcnt, 0);
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       const int li = x - p.o, lj = y0 + r - p.o;
@@ -800,6 +805,9 @@ __global__ void __launch_bounds__(NTC, 1) ras2d_col_kernel(const __grid_constant
         p.z[(size_t)(ibx * p.bx + li) + (size_t)p.nx * (iby * p.by + lj)] = 0.0;
       }
     }
+    // every warp must be done reading this box's beta from red[0] before the next box's
+    // first col_allreduce writes its partials there (rb restarts at 0)
+    __syncthreads();
     continue;   // uniform: every thread saw beta = 0
   }
   {
@@ -914,6 +922,7 @@ __global__ void __launch_bounds__(NTC, 1) ras2d_col_kernel(const __grid_constant
       y[i] = sacc * rd[i];
       yv[i] = y[i];
     }
+    ras_count(p.jcnt, jm);
   }
   __syncthreads();
   // (R_k^0)^T: the owner thread of each owned node writes y = V yv; (R_k^delta)^T (AS,
@@ -1066,6 +1075,7 @@ cudaError_t launch_ras_2d(pfc_ctx* ctx, const double* v, const double* c, double
     p.restrict_owned = cf.ras_variant == PFC_RAS_RIGHT;
     p.y_ext = cf.ras_variant == PFC_RAS_LEFT ? nullptr : ctx->ras_y;
     p.gate = ctx->gate;
+    p.jcnt = ctx->prof ? ctx->d_jcnt : nullptr;
     // class weights of the linear part v/dt - alpha Delta v - Delta^2 v - Delta^3 v / 2 with
     // h^2 Delta = L:  L (0,0) -4, (0,1) 1;  L^2 (0,0) 20, (0,1) -8, (0,2) 1, (1,1) 2;
     // L^3 (0,0) -112, (0,1) 57, (0,2) -12, (1,1) -24, (0,3) 1, (1,2) 3
@@ -1093,17 +1103,17 @@ cudaError_t launch_ras_2d(pfc_ctx* ctx, const double* v, const double* c, double
     RasArgs p{v, c, z, cf.n[0], cf.n[1], cf.ras_box[0], cf.ras_box[1], cf.ras_overlap,
               1.0 / dt, cf.gamma, ctx->ih2, cf.ras_variant == PFC_RAS_RIGHT,
               cf.ras_variant == PFC_RAS_LEFT ? nullptr : ctx->ras_y, ctx->gate,
-              ctx->mob_phi, ctx->mob_psi, ctx->mob_A, cf.mobility, cf.bc == PFC_BC_MIRROR};
+              ctx->mob_phi, ctx->mob_psi, ctx->mob_A, cf.mobility, cf.bc == PFC_BC_MIRROR,
+              ctx->prof ? ctx->d_jcnt : nullptr};
     fn<<<nb, NT, ctx->ras_smem, ctx->stream>>>(p);
   }
   ctx->launches++;
   {  // algorithmic: v, c gathered on the extended boxes, z written on owned nodes; flops of
      // k local J v (25/pt) + CGS2 vector work 4k(k+1) + 3k + 3 per ext node + V y
-    const double k = cf.ras_local_k;
     const double next = (double)nb * Ex * Ey;
     const double nout = cf.ras_variant == PFC_RAS_LEFT ? (double)ctx->N : next;
-    pfc_account(ctx, PFC_K_RAS, 8.0 * (2.0 * next + nout),
-                next * (25.0 * k + 4.0 * k * (k + 1) + 3.0 * k + 3.0) + 2.0 * k * nout);
+    pfc_account(ctx, PFC_K_RAS, 8.0 * (2.0 * next + nout), 0.0);
+    ras_flop_model(ctx, (double)Ex * Ey, 25.0, nout / nb);   // flops from the step counters
   }
   cudaError_t e2 = cudaGetLastError();
   if (e2 != cudaSuccess || cf.ras_variant == PFC_RAS_LEFT) return e2;

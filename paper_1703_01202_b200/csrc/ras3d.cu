@@ -8,6 +8,7 @@
 // b, b + G, b + 2G, ...  Reductions are block-level and deterministic.
 #include "pfc_device.cuh"
 #include "pfc_internal.h"
+#include "ras_common.cuh"
 
 namespace {
 
@@ -32,6 +33,7 @@ struct Ras3Args {
   const double* psi;
   const double* A;
   int mobility;
+  unsigned long long* jcnt;   // profiling: Arnoldi steps taken (ras_count)
 };
 
 __global__ void __launch_bounds__(NT, 1) ras3d_kernel(Ras3Args p) {
@@ -106,6 +108,7 @@ __global__ void __launch_bounds__(NT, 1) ras3d_kernel(Ras3Args p) {
     }
     const double beta = sqrt(scal[0]);
     if (beta == 0.0) {
+      if (tid == 0) ras_count(p.jcnt, 0);
       if (p.y_ext) {
         for (int l = tid; l < n; l += NT) p.y_ext[(size_t)box * n + l] = 0.0;
         continue;
@@ -241,6 +244,7 @@ __global__ void __launch_bounds__(NT, 1) ras3d_kernel(Ras3Args p) {
         for (int l = i + 1; l < jm; ++l) s -= H[i + ld * l] * yv[l];
         yv[i] = s / H[i + ld * i];
       }
+      ras_count(p.jcnt, jm);
     }
     __syncthreads();
     if (p.y_ext) {   // (R_k^delta)^T: the whole ext-box solution, summed by ras_extend
@@ -296,18 +300,19 @@ cudaError_t launch_ras_3d(pfc_ctx* ctx, const double* v, const double* c, double
              cf.ras_box[0], cf.ras_box[1], cf.ras_box[2], cf.ras_overlap, cf.ras_local_k,
              1.0 / dt, cf.gamma, ctx->ih2, cf.ras_variant == PFC_RAS_RIGHT,
              cf.ras_variant == PFC_RAS_LEFT ? nullptr : ctx->ras_y, ctx->gate,
-             ctx->mob_phi, ctx->mob_psi, ctx->mob_A, cf.mobility};
+             ctx->mob_phi, ctx->mob_psi, ctx->mob_A, cf.mobility,
+             ctx->prof ? ctx->d_jcnt : nullptr};
   ras3d_kernel<<<grid, NT, 0, ctx->stream>>>(p);
   ctx->launches++;
   {
-    const double k = cf.ras_local_k;
     const double nb = (double)(cf.n[0] / cf.ras_box[0]) * (cf.n[1] / cf.ras_box[1]) *
                       (cf.n[2] / cf.ras_box[2]);
-    const double next = nb * (cf.ras_box[0] + 2 * cf.ras_overlap) *
+    const double ebox = (double)(cf.ras_box[0] + 2 * cf.ras_overlap) *
                         (cf.ras_box[1] + 2 * cf.ras_overlap) * (cf.ras_box[2] + 2 * cf.ras_overlap);
+    const double next = nb * ebox;
     const double nout = cf.ras_variant == PFC_RAS_LEFT ? (double)ctx->N : next;
-    pfc_account(ctx, PFC_K_RAS, 8.0 * (2.0 * next + nout),
-                next * (31.0 * k + 4.0 * k * (k + 1) + 3.0 * k + 3.0) + 2.0 * k * nout);
+    pfc_account(ctx, PFC_K_RAS, 8.0 * (2.0 * next + nout), 0.0);
+    ras_flop_model(ctx, ebox, 31.0, nout / nb);   // flops from the step counters
   }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess || cf.ras_variant == PFC_RAS_LEFT) return e;

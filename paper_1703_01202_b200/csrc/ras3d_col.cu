@@ -43,6 +43,7 @@ struct Ras3ColArgs {
   const int* gate;       // device-resident FGMRES: skip when *gate != 0
   double W[7];           // classes (0,0,0) (0,0,1) (0,0,2) (0,1,1) (0,0,3) (0,1,2) (1,1,1)
   double ih2;
+  unsigned long long* jcnt;   // profiling: Arnoldi steps taken (ras_count)
 };
 
 constexpr int iabs3(int a) { return a < 0 ? -a : a; }
@@ -315,6 +316,7 @@ __global__ void __launch_bounds__((E * E + 31) / 32 * 32, 1)
     rb ^= 1;
     const double beta = sqrt(hx[0]);
     if (beta == 0.0) {
+      if (tid == 0) ras_count(p.jcnt, 0);
       if (act) {
 #pragma unroll
         for (int z = 0; z < E; ++z) {
@@ -360,6 +362,7 @@ __global__ void __launch_bounds__((E * E + 31) / 32 * 32, 1)
         for (int l = i + 1; l < jm; ++l) s -= H[i + ld * l] * yv[l];
         yv[i] = s / H[i + ld * i];
       }
+      ras_count(p.jcnt, jm);
     }
     __syncthreads();
     if (act) {
@@ -435,6 +438,7 @@ cudaError_t launch_ras_3d_col(pfc_ctx* ctx, const double* v, const double* c, do
   p.restrict_owned = cf.ras_variant == PFC_RAS_RIGHT;
   p.y_ext = cf.ras_variant == PFC_RAS_LEFT ? nullptr : ctx->ras_y;
   p.gate = ctx->gate;
+  p.jcnt = ctx->prof ? ctx->d_jcnt : nullptr;
   // class weights of v/dt - alpha Delta v - Delta^2 v - Delta^3 v / 2 with h^2 Delta = L:
   // L (000) -6, (001) 1;  L^2 (000) 42, (001) -12, (002) 1, (011) 2;
   // L^3 (000) -324, (001) 123, (002) -18, (011) -36, (003) 1, (012) 3, (111) 6
@@ -452,13 +456,12 @@ cudaError_t launch_ras_3d_col(pfc_ctx* ctx, const double* v, const double* c, do
   fn<<<grid, threads, smem, ctx->stream>>>(p);
   ctx->launches++;
   {
-    const double k = cf.ras_local_k;
     const double nb = (double)(cf.n[0] / cf.ras_box[0]) * (cf.n[1] / cf.ras_box[1]) *
                       (cf.n[2] / cf.ras_box[2]);
     const double next = nb * e * e * e;
     const double nout = cf.ras_variant == PFC_RAS_LEFT ? (double)ctx->N : next;
-    pfc_account(ctx, PFC_K_RAS, 8.0 * (2.0 * next + nout),
-                next * (31.0 * k + 4.0 * k * (k + 1) + 3.0 * k + 3.0) + 2.0 * k * nout);
+    pfc_account(ctx, PFC_K_RAS, 8.0 * (2.0 * next + nout), 0.0);
+    ras_flop_model(ctx, (double)e * e * e, 31.0, nout / nb);   // flops from the step counters
   }
   cudaError_t e2 = cudaGetLastError();
   if (e2 != cudaSuccess || cf.ras_variant == PFC_RAS_LEFT) return e2;

@@ -70,3 +70,15 @@ __device__ __forceinline__ void sized_allreduce(const double (&acc)[NV], double*
 }
 
 }  // namespace
+
+// Arnoldi steps actually taken by the subdomain solves of a launch (bench roofline): one thread
+// per box adds jm, jm^2 and 1 (boxes that exit at beta = 0 or break down early do less than
+// k steps, so the algorithmic flops are counted from these sums, not from k).  Null unless the
+// library is profiling.
+__device__ __forceinline__ void ras_count(unsigned long long* cnt, int jm) {
+  if (cnt) {
+    atomicAdd(cnt, (unsigned long long)jm);
+    atomicAdd(cnt + 1, (unsigned long long)jm * (unsigned long long)jm);
+    atomicAdd(cnt + 2, 1ull);
+  }
+}

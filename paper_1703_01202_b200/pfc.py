@@ -131,6 +131,24 @@ def _ptr(t):
     return C.c_void_p(t.data_ptr())
 
 
+def _field(t, N, device=None, name="field"):
+    """Pointer of a field argument after the checks the C ABI cannot make itself (it reads and
+    writes exactly N contiguous fp64 values): dtype float64, contiguous, numel == N and, for
+    the operator calls, a CUDA tensor on the context's device.  Raises PfcError(PFC_EINVAL)."""
+    import torch
+    if not isinstance(t, torch.Tensor):
+        raise PfcError(PFC_EINVAL, f"{name}: expected a torch.Tensor, got {type(t).__name__}")
+    if t.dtype != torch.float64:
+        raise PfcError(PFC_EINVAL, f"{name}: dtype must be torch.float64, got {t.dtype}")
+    if not t.is_contiguous():
+        raise PfcError(PFC_EINVAL, f"{name}: must be contiguous (x-fastest)")
+    if t.numel() != N:
+        raise PfcError(PFC_EINVAL, f"{name}: numel {t.numel()} != grid size {N}")
+    if device is not None and (t.device.type != "cuda" or t.device.index != device):
+        raise PfcError(PFC_EINVAL, f"{name}: must be a CUDA tensor on cuda:{device}, got {t.device}")
+    return _ptr(t)
+
+
 class Context:
     """One pfc_ctx on the current CUDA device and torch's current stream."""
 
@@ -141,6 +159,10 @@ class Context:
         if stream is None:
             stream = torch.cuda.current_stream()
         self.stream = stream
+        self.N = int(self.config.n[0]) * int(self.config.n[1]) * (
+            int(self.config.n[2]) if self.config.ndim == 3 else 1)
+        self.device = stream.device.index if stream.device.index is not None else \
+            torch.cuda.current_device()
         h = C.c_void_p()
         st = self.L.pfc_create(C.byref(self.config), C.c_void_p(stream.cuda_stream), C.byref(h))
         self._h = h
@@ -183,48 +205,58 @@ class Context:
             out[name] = dict(launches=n.value, ms=ms.value, bytes=b.value, flops=f.value)
         return out
 
+    def _dev(self, t, name):
+        return _field(t, self.N, self.device, name)
+
+    def _any(self, t, name):
+        """CUDA tensor on the context's device, or a CPU tensor (host path of the ABI)."""
+        return _field(t, self.N, None if t.device.type == "cpu" else self.device, name)
+
     def residual(self, phi_new, phi_old, dt, out=None):
         import torch
         out = torch.empty_like(phi_new) if out is None else out
-        self._check(self.L.pfc_residual(self._h, _ptr(phi_new), _ptr(phi_old), dt, _ptr(out)))
+        self._check(self.L.pfc_residual(self._h, self._dev(phi_new, "phi_new"),
+                                        self._dev(phi_old, "phi_old"), dt, self._dev(out, "out")))
         return out
 
     def jacobian_apply(self, phi_new, phi_old, dt, v, out=None):
         import torch
         out = torch.empty_like(v) if out is None else out
-        self._check(self.L.pfc_jacobian_apply(self._h, _ptr(phi_new), _ptr(phi_old), dt, _ptr(v),
-                                              _ptr(out)))
+        self._check(self.L.pfc_jacobian_apply(self._h, self._dev(phi_new, "phi_new"),
+                                              self._dev(phi_old, "phi_old"), dt,
+                                              self._dev(v, "v"), self._dev(out, "out")))
         return out
 
     def ras_apply(self, phi_new, phi_old, dt, v, out=None):
         import torch
         out = torch.empty_like(v) if out is None else out
-        self._check(self.L.pfc_ras_apply(self._h, _ptr(phi_new), _ptr(phi_old), dt, _ptr(v),
-                                         _ptr(out)))
+        self._check(self.L.pfc_ras_apply(self._h, self._dev(phi_new, "phi_new"),
+                                         self._dev(phi_old, "phi_old"), dt,
+                                         self._dev(v, "v"), self._dev(out, "out")))
         return out
 
     def step(self, phi, dt):
         """In-place phi^n -> phi^{n+1}; returns (dt_next, info dict).  phi: CUDA or CPU tensor."""
         d = C.c_double(dt)
         info = PfcStepInfo()
-        self._check(self.L.pfc_step(self._h, _ptr(phi), C.byref(d), C.byref(info)))
+        self._check(self.L.pfc_step(self._h, self._any(phi, "phi"), C.byref(d), C.byref(info)))
         return d.value, info.as_dict()
 
     def try_step(self, phi, dt):
         """Like step() but returns (status, dt_next, info) instead of raising on ENOCONV."""
         d = C.c_double(dt)
         info = PfcStepInfo()
-        st = self.L.pfc_step(self._h, _ptr(phi), C.byref(d), C.byref(info))
+        st = self.L.pfc_step(self._h, self._any(phi, "phi"), C.byref(d), C.byref(info))
         if st not in (PFC_OK, PFC_ENOCONV, PFC_EBREAKDOWN):
             self._check(st)
         return st, d.value, info.as_dict()
 
     def energy(self, phi) -> float:
         out = C.c_double()
-        self._check(self.L.pfc_energy(self._h, _ptr(phi), C.byref(out)))
+        self._check(self.L.pfc_energy(self._h, self._any(phi, "phi"), C.byref(out)))
         return out.value
 
     def mass(self, phi) -> float:
         out = C.c_double()
-        self._check(self.L.pfc_mass(self._h, _ptr(phi), C.byref(out)))
+        self._check(self.L.pfc_mass(self._h, self._any(phi, "phi"), C.byref(out)))
         return out.value

@@ -120,3 +120,21 @@ def test_product_package_does_not_reference_the_oracle():
                 text = open(os.path.join(dirpath, f)).read()
                 assert not re.search(r"^\s*(from|import)\s+oracle|#include\s*[<\"].*oracle|"
                                      r"liboracle|pfc_oracle", text, flags=re.M), f
+
+
+def test_binding_rejects_fields_the_abi_would_overrun():
+    """The C ABI reads and writes exactly N contiguous fp64 values per field; the binding must
+    refuse anything else before the pointer reaches the library (PFC_EINVAL), since a float32,
+    strided or short tensor would be overrun on the device or, for host pointers, on the heap."""
+    import torch
+    N = 8 * 6
+    ok = torch.zeros(6, 8, dtype=torch.float64)
+    assert P._field(ok, N).value == ok.data_ptr()
+    bad = [ok.float(), ok.t(), torch.zeros(5, 8, dtype=torch.float64), [0.0] * N]
+    for t in bad:
+        with pytest.raises(P.PfcError) as e:
+            P._field(t, N)
+        assert e.value.status == P.PFC_EINVAL
+    with pytest.raises(P.PfcError) as e:           # operator calls need a CUDA tensor
+        P._field(ok, N, device=0)
+    assert e.value.status == P.PFC_EINVAL

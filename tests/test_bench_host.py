@@ -54,3 +54,28 @@ def test_replica_value_is_whole_job_rate():
     # 4 replicas of 50 steps, slowest rank 100 ms -> 4 * 50 / 0.1 s
     assert bench.replica_value(100.0, 50, 4) == pytest.approx(2000.0)
     assert bench.max_over_ranks(12.5, 1, device="cpu") == 12.5
+
+
+def test_reference_arm_line_is_consistent(capsys):
+    """--impl reference: `steps` and `ms_per_step` describe the oracle steps that actually ran
+    (the time budget may stop the sample early) and `config` is the CUDA arm's config dict."""
+    import json
+    args = argparse.Namespace(config="cfg1", steps=3, warmup=0, ref_budget_s=0.0, mobility=0,
+                              ras_variant=0, ilu=-1, ilu_reuse=0, lu=False, bc=0)
+    bench.bench_reference(args)
+    line = json.loads(capsys.readouterr().out.strip().splitlines()[-1])
+    assert line["impl"] == "reference" and line["steps"] == 1      # budget 0: one step ran
+    assert line["value"] == pytest.approx(1e3 / line["ms_per_step"], rel=1e-2)
+    assert line["config"] == bench.config_dict(CONFIGS["cfg1"], 0, 3, 1)
+    assert line["cpu_baseline"]["value"] == line["value"]
+
+
+def test_oracle_operator_estimate_scales_counts():
+    """The 3D oracle estimate multiplies per-operator times by the per-step operator counts."""
+    cfg = CONFIGS["cfg4"]
+    counts = {"steps": 2, "newton_its": 6, "gmres_its": 40, "ls_backtracks": 0, "residuals": 8,
+              "jv": 46, "ras": 40, "energy": 4}
+    s, t, how = bench.oracle_estimate(cfg, counts, sample_n=32, ras_boxes=2)
+    assert s == pytest.approx((8 * t["residual"] + 46 * t["jv"] + 40 * t["ras"]
+                               + 4 * t["energy"]) / 2)
+    assert all(v > 0 for v in t.values()) and "32^3" in how

@@ -341,6 +341,66 @@ def test_schwarz_with_exact_local_solve(shape, box, o, variant):
     assert rel(z, zref) < 1e-9
 
 
+def _owned_block(z, shape, box, bidx):
+    """the owned block R_k^0 z of box bidx (numpy shape reversed(box))"""
+    nd = len(shape)
+    nb = [shape[d] // box[d] for d in range(nd)]
+    b, r = [], bidx
+    for d in range(nd):
+        b.append(r % nb[d]); r //= nb[d]
+    sl = tuple(slice(b[d] * box[d], (b[d] + 1) * box[d]) for d in reversed(range(nd)))
+    return z[sl]
+
+
+@pytest.mark.parametrize("shape,box,o,k", [((24, 24), (8, 8), 2, 10), ((36, 30), (12, 10), 3, 7),
+                                           ((12, 12, 12), (4, 4, 4), 1, 10),
+                                           ((15, 12, 12), (5, 4, 4), 1, 6)])
+def test_ras_apply_box_equals_owned_block_of_full_apply(shape, box, o, k):
+    """or_ras_apply_box (the per-box oracle of the full-size 3D GPU tests) re-decodes the box
+    index, restricts R_k^delta v and c with periodic wrap and returns the owned entries
+    (R_k^0)^T of ONE box of Eq. (eq:ras) P:398-409.  For every box of a grid with 3 boxes per
+    axis (so each box has distinct -x/+x, -y/+y(, -z/+z) neighbours, wrapped edges included)
+    it must equal the owned block of the full left-RAS apply or_ras_apply, bitwise."""
+    phi = random_field(shape, 81, 0.07, 0.3)
+    psi = random_field(shape, 82, 0.07, 0.3)
+    v = random_field(shape, 83)
+    prm = O.params(gamma=GAMMA, ras_box=box, ras_overlap=o, ras_local_k=k)
+    z = O.ras_apply(phi, psi, v, H, prm, 0.5)
+    nb = int(np.prod([s // b for s, b in zip(shape, box)]))
+    assert nb == 3 ** len(shape)
+    for bidx in range(nb):
+        zb = O.ras_apply_box(phi, psi, v, H, prm, 0.5, bidx)
+        assert np.array_equal(zb, _owned_block(z, shape, box, bidx)), bidx
+
+
+@pytest.mark.parametrize("shape,box,o", [((12, 12), (4, 4), 1), ((12, 12, 12), (4, 4, 4), 1)])
+def test_ras_apply_box_exact_local_solve_dense(shape, box, o):
+    """Independent of or_ras_apply: with k_loc = #ext-box unknowns the per-box oracle's output
+    is the owned part of the dense numpy solve A_k^{-1} R_k^delta v, A_k = R J R^T assembled
+    column by column from the global J (Eq. Ak, reading R8), for every box."""
+    rs = tuple(reversed(shape))
+    phi = random_field(shape, 84, 0.07, 0.3)
+    psi = random_field(shape, 85, 0.07, 0.3)
+    v = random_field(shape, 86)
+    dt = 0.5
+    N = int(np.prod(shape))
+    J = np.zeros((N, N))
+    for q in range(N):
+        e = np.zeros(N); e[q] = 1.0
+        J[:, q] = O.jacobian_apply(phi, psi, e.reshape(rs), H, GAMMA, dt).ravel()
+    E = [b + 2 * o for b in box]
+    n = int(np.prod(E))
+    nd = len(shape)
+    prm = O.params(gamma=GAMMA, ras_box=box, ras_overlap=o, ras_local_k=n)
+    loc = np.arange(n).reshape(tuple(reversed(E)))
+    own = loc[tuple(slice(o, o + box[d]) for d in reversed(range(nd)))].ravel()
+    for bidx in range(3 ** nd):
+        idx, _ = _ext_indices(shape, box, o, bidx)
+        y = np.linalg.solve(J[np.ix_(idx, idx)], v.ravel()[idx])
+        zb = O.ras_apply_box(phi, psi, v, H, prm, dt, bidx)
+        assert rel(zb.ravel(), y[own]) < 1e-9, bidx
+
+
 @pytest.mark.parametrize("shape,box", [((16, 16), (4, 4)), ((8, 8, 8), (4, 4, 2))])
 def test_schwarz_variants_coincide_without_overlap(shape, box):
     """With no overlap (delta = 0) R_k^delta = R_k^0, so AS, left-RAS
