@@ -11,7 +11,7 @@ CSRC = os.path.join(HERE, "csrc")
 LIBDIR = os.path.join(HERE, "lib")
 LIB = os.path.join(LIBDIR, os.environ.get("PFC_LIB_NAME", "libpfc.so"))
 SOURCES = ["pfc.cu", "stencil2d.cu", "stencil3d.cu", "krylov.cu", "energy.cu", "ras2d.cu",
-           "ras3d.cu", "ras3d_col.cu", "ras_extend.cu", "mobility.cu",
+           "ras3d.cu", "ras3d_col.cu", "ras3d_cl2.cu", "ras_extend.cu", "mobility.cu",
            "ilu.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
@@ -40,12 +40,20 @@ def build(force: bool = False, verbose: bool = False) -> str:
     only = [f for f in os.environ.get("PFC_VARIANT_SOURCES", "").split(",") if f]
     basedir = os.path.join(HERE, "..", "build", "obj")
 
+    headers = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if not f.endswith(".cu")]
+    headers.append(os.path.join(HERE, "..", "include", "pfc.h"))
+    hdr_t = max(os.path.getmtime(h) for h in headers)
+
     def compile_one(src):
         obj = os.path.join(objdir, src.replace(".cu", ".o"))
         if only and src not in only:
             base = os.path.join(basedir, src.replace(".cu", ".o"))
             if os.path.exists(base):
                 return base, ""
+        # incremental: an object newer than its source and every header is reused
+        if not force and os.path.exists(obj) and os.path.getmtime(obj) > max(
+                os.path.getmtime(os.path.join(CSRC, src)), hdr_t):
+            return obj, ""
         cmd = [NVCC, *FLAGS, "-c", os.path.join(CSRC, src), "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:

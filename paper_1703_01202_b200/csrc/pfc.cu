@@ -142,6 +142,7 @@ int ras_plan(pfc_ctx* ctx) { return ctx->cfg.ndim == 2 ? ras2d_plan(ctx) : ras3d
 cudaError_t launch_ras(pfc_ctx* ctx, const double* v, const double* c, double dt, double* z) {
   if (ctx->cfg.ras_local_solver != PFC_LOCAL_GMRES) return launch_ras_ilu(ctx, v, z);
   if (ctx->cfg.ndim == 2) return launch_ras_2d(ctx, v, c, dt, z);
+  if (ctx->ras3_col == 2) return launch_ras_3d_cl2(ctx, v, c, dt, z, ctx->ras_scratch);
   return ctx->ras3_col ? launch_ras_3d_col(ctx, v, c, dt, z, ctx->ras_scratch)
                        : launch_ras_3d(ctx, v, c, dt, z, ctx->ras_scratch);
 }
@@ -551,11 +552,19 @@ pfc_status pfc_create(const pfc_config* cfg, void* stream, pfc_ctx** out) {
       pfc_check_cuda(ctx, cudaMemset(ctx->d_jcnt, 0, 4 * sizeof(unsigned long long)), "jcnt"))
     return fail(PFC_ENOMEM);
   if (c.ndim == 3) {
+    // subdomain kernel: the 2-CTA cluster kernel (basis on chip) where instantiated, else the
+    // single-CTA column kernel, else the global-scratch kernel; PFC_RAS3D=col|v1 forces one
     int grid = 0;
     size_t d = 0;
-    ctx->ras3_col = getenv("PFC_RAS3D_V1") == nullptr && !c.mobility &&
-                    ras3d_col_plan(ctx, &d, &grid);
-    if (!ctx->ras3_col) d = ras3d_scratch_doubles(ctx, &grid);
+    const char* force = getenv("PFC_RAS3D");
+    const bool v1 = getenv("PFC_RAS3D_V1") != nullptr || (force && !strcmp(force, "v1"));
+    ctx->ras3_col = 0;
+    if (!v1 && !c.mobility && !(force && !strcmp(force, "col")) && ras3d_cl2_plan(ctx, &grid, &d))
+      ctx->ras3_col = 2;
+    else if (!v1 && !c.mobility && ras3d_col_plan(ctx, &d, &grid))
+      ctx->ras3_col = 1;
+    else
+      d = ras3d_scratch_doubles(ctx, &grid);
     if (pfc_check_cuda(ctx, cudaMalloc(&ctx->ras_scratch, d * sizeof(double)), "ras scratch"))
       return fail(PFC_ENOMEM);
   }

@@ -75,7 +75,8 @@ struct pfc_ctx {
   int ras_threads = 0;
   int ras_cluster = 1;
   int ras_rows = 0;
-  int ras3_col = 0;        // 3D: on-chip column kernel (ras3d_col.cu) instead of ras3d.cu
+  int ras3_col = 0;        // 3D: 2 = 2-CTA cluster kernel (ras3d_cl2.cu), 1 = column kernel
+                           // (ras3d_col.cu), 0 = global-scratch kernel (ras3d.cu)
 
   long long launches = 0;
   std::string err;
@@ -162,6 +163,9 @@ cudaError_t launch_ras_2d(pfc_ctx*, const double* v, const double* c, double dt,
 cudaError_t launch_ras_3d(pfc_ctx*, const double* v, const double* c, double dt, double* z,
                           double* scratch);
 int ras3d_col_plan(pfc_ctx* ctx, size_t* scratch_doubles, int* grid);
+int ras3d_cl2_plan(pfc_ctx* ctx, int* clusters, size_t* scratch_doubles);
+cudaError_t launch_ras_3d_cl2(pfc_ctx*, const double* v, const double* c, double dt, double* z,
+                              double* scratch);
 cudaError_t launch_ras_3d_col(pfc_ctx*, const double* v, const double* c, double dt, double* z,
                               double* scratch);
 

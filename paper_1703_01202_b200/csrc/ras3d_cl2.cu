@@ -15,11 +15,14 @@
 //    sub-partitions cap a thread at 128 registers), NR..NR+NS-1 in shared memory (NS = 4),
 //    the last NG = 2 in a small per-CTA global scratch (64 KB per CTA, 9.5 MB in all: L2-
 //    resident, read only by Arnoldi steps >= 8), and v_{K-1} in the stencil planes;
-//  * the current vector v_j sits in ZL + 3 unpadded 20x20 planes (the own ZL planes plus the 3
-//    halo planes on the partner's side, written by the partner through DSMEM; beyond the box
-//    the planes are zero by the modified BC and are never read); the x/y zero ring is a
-//    bounds mask on the 24 neighbour columns;
-//  * c' = -c/h^2 on the own planes plus the one plane on the partner's side (static per box);
+//  * the current vector v_j sits in ZL + 3 planes (the own ZL planes plus the 3 halo planes on
+//    the partner's side, written by the partner through DSMEM; beyond the box the planes are
+//    zero by the modified BC and are never read), padded by the 3-node zero ring in x and y
+//    (row pitch 28 = 12 mod 16): a half-warp owns a 4x4 tile of columns, so every 8-byte
+//    neighbour load of a half-warp hits 16 distinct bank pairs, with no bounds masks;
+//  * c' = -c/h^2 on the own planes plus the one plane on the partner's side (static per box),
+//    unpadded (pitch E, also conflict-free for 4x4 tiles): an xy-neighbour c' outside the box
+//    is read from a finite neighbouring cell or guard row and multiplies a zero v;
 //  * w = A_k v_j is the direct 63-point stencil of the linear part plus -Delta(c v) (class
 //    weights of h^2 Delta = L, L^2, L^3 summed on the host), evaluated column by column with
 //    the symmetric neighbour columns summed first (4 / 4+4 / 4+8 columns per ring R = 1, 2, 3
@@ -34,6 +37,8 @@
 #include "pfc_device.cuh"
 #include "pfc_internal.h"
 #include "ras_common.cuh"
+
+#include <type_traits>
 
 namespace {
 
@@ -76,28 +81,52 @@ __device__ __forceinline__ void cl_sync() {
   cl_arrive();
   cl_wait();
 }
+// asynchronous 8-byte store into the partner CTA's shared memory that completes 8 bytes of
+// transaction count on the partner's mbarrier (no cluster barrier, no memory fence)
+__device__ __forceinline__ void st_async(uint32_t addr, double v, uint32_t mbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];" ::"r"(addr),
+               "l"(__double_as_longlong(v)), "r"(mbar)
+               : "memory");
+}
+// wait for phase `parity` of a local mbarrier, acquiring at cluster scope (the data came from
+// the partner CTA through st.async)
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
 
 template <int E>
 struct Cl2 {
   static constexpr int ZL = E / 2;                 // own z-planes per CTA
-  static constexpr int PL = E * E;                 // plane size (unpadded)
-  static constexpr int NT = (PL + 31) / 32 * 32;   // threads
-  static constexpr int NW = NT / 32;
+  static constexpr int PL = E * E;                 // nodes per plane (= columns)
+  static constexpr int NWN = (PL + 31) / 32;      // node warps (E % 4 == 0: 4x4 column tiles)
+  static constexpr int NW = NWN + 1;               // + the Givens warp
+  static constexpr int NT = NW * 32;
+  static constexpr int PX = E + 6 + ((12 - (E + 6)) % 16 + 16) % 16;   // >= E+6, = 12 mod 16
+  static constexpr int PP = PX * (E + 6);          // padded v plane
   static constexpr int NVB = ZL + 3;   // v_j planes: own + 3 on the partner's side
   static constexpr int NCB = ZL + 1;   // c' planes: own + 1 on the partner's side
+  static constexpr int CG = 2 * E;     // c' guard before and after the planes
 };
 
-template <int K>
+template <int K, int NRX>
 struct Cl2K {
-  static constexpr int NR = (K - 1) < 3 ? (K - 1) : 3;                     // registers
-  static constexpr int NS = (K - 1 - NR) < 4 ? (K - 1 - NR) : 4;          // shared memory
+  static constexpr int NR = (K - 1) < NRX ? (K - 1) : NRX;                 // registers
+  static constexpr int NS = (K - 1 - NR) < 3 ? (K - 1 - NR) : 3;          // shared memory
   static constexpr int NG = K - 1 - NR - NS;                               // global scratch
 };
 
-template <int K, int E>
+template <int K, int E, int NRX>
 constexpr size_t cl2_smem_doubles() {
-  return (size_t)Cl2<E>::NVB * Cl2<E>::PL + (size_t)Cl2<E>::NCB * Cl2<E>::PL +
-         (size_t)Cl2K<K>::NS * Cl2<E>::ZL * Cl2<E>::PL + 2 * 2 * Cl2<E>::NW * RS +
+  return (size_t)Cl2<E>::NVB * Cl2<E>::PP + (size_t)Cl2<E>::NCB * Cl2<E>::PL + 2 * Cl2<E>::CG +
+         (size_t)Cl2K<K, NRX>::NS * Cl2<E>::ZL * Cl2<E>::PL + 2 * 2 * Cl2<E>::NW * RS +
          Cl2<E>::NW * 3 * RS;
 }
 
@@ -105,49 +134,106 @@ constexpr size_t cl2_smem_doubles() {
 // [rank][warp][i] of the reduction buffer in BOTH CTAs (local store + DSMEM store).
 template <int NW>
 __device__ __forceinline__ void cl2_put(double s, int i, double* redb, uint32_t redb_rem,
-                                        int rank, int wid, int lane) {
+                                        uint32_t mbar_rem, int rank, int wid, int lane) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
   if (lane == 0) {
     const int off = (rank * NW + wid) * RS + i;
     redb[off] = s;
-    st_cluster(redb_rem + off * 8u, s);
+    st_async(redb_rem + off * 8u, s, mbar_rem);
   }
+}
+
+// Warp partials of nv values at once (acc[0..nv), nv <= 16): a sized reduce-scatter over the
+// lanes (fewer shuffles than nv butterflies); the lane holding value i stores it in both CTAs.
+template <int NW, int NVP>
+__device__ __forceinline__ void cl2_rs_put(const double (&acc)[16], int nv, double* redb,
+                                           uint32_t redb_rem, uint32_t mbar_rem, int rank,
+                                           int wid, int lane) {
+  constexpr int SH = 5 - (NVP == 1 ? 0 : NVP == 2 ? 1 : NVP == 4 ? 2 : NVP == 8 ? 3 : 4);
+  double a[NVP];
+#pragma unroll
+  for (int i = 0; i < NVP; ++i) a[i] = acc[i];
+  const double s = warp_reduce_scatter<NVP>(a);
+  const int vi = lane >> SH;
+  if ((lane & ((1 << SH) - 1)) == 0 && vi < nv) {
+    const int off = (rank * NW + wid) * RS + vi;
+    redb[off] = s;
+    st_async(redb_rem + off * 8u, s, mbar_rem);
+  }
+}
+template <int NW>
+__device__ __forceinline__ void cl2_put_multi(const double (&acc)[16], int nv, double* redb,
+                                              uint32_t redb_rem, uint32_t mbar_rem, int rank,
+                                              int wid, int lane) {
+  if (nv <= 2) cl2_rs_put<NW, 2>(acc, nv, redb, redb_rem, mbar_rem, rank, wid, lane);
+  else if (nv <= 4) cl2_rs_put<NW, 4>(acc, nv, redb, redb_rem, mbar_rem, rank, wid, lane);
+  else if (nv <= 8) cl2_rs_put<NW, 8>(acc, nv, redb, redb_rem, mbar_rem, rank, wid, lane);
+  else cl2_rs_put<NW, 16>(acc, nv, redb, redb_rem, mbar_rem, rank, wid, lane);
+}
+
+// call f(std::integral_constant<int, j>) for the runtime j in [0, K)
+template <int K, int J = 0, typename F>
+__device__ __forceinline__ void dispatch_j(int j, F& f) {
+  if constexpr (J < K) {
+    if (j == J) f(std::integral_constant<int, J>{});
+    else dispatch_j<K, J + 1>(j, f);
+  }
+}
+
+// Givens update of Hessenberg column j (previous rotations, then a new one) in the oracle's
+// order, on shared-memory arrays (runtime indices): run by one lane of the Givens warp
+__device__ __forceinline__ void givens_col(int j, const double* h1, const double* h2, double hn,
+                                           double* H, double* cs, double* sn, double* gv, int ld) {
+  for (int i = 0; i <= j; ++i) H[i + ld * j] = h1[i] + h2[i];
+  H[j + 1 + ld * j] = hn;
+  for (int i = 0; i < j; ++i) {
+    const double a = H[i + ld * j], b = H[i + 1 + ld * j];
+    H[i + ld * j] = cs[i] * a + sn[i] * b;
+    H[i + 1 + ld * j] = -sn[i] * a + cs[i] * b;
+  }
+  const double a = H[j + ld * j], b = H[j + 1 + ld * j];
+  const double rr = sqrt(a * a + b * b);
+  double cc = 1.0, ss = 0.0;
+  if (rr != 0.0) { cc = a / rr; ss = b / rr; }
+  cs[j] = cc; sn[j] = ss;
+  H[j + ld * j] = cc * a + ss * b;
+  H[j + 1 + ld * j] = 0.0;
+  gv[j + 1] = -ss * gv[j];
+  gv[j] = cc * gv[j];
 }
 
 // After the cluster barrier: lanes < nv sum the 2 x NW warp partials of value `lane` in a fixed
 // order (rank 0's warps, then rank 1's) into this warp's copy hwv[lane].
 template <int NW>
 __device__ __forceinline__ void cl2_get(int nv, const double* redb, double* hwv, int lane) {
-  if (lane < nv) {
-    double t = 0.0;
+  if (lane < nv) {   // two independent chains (rank 0's warps, rank 1's), then their sum
+    double t0 = 0.0, t1 = 0.0;
 #pragma unroll
-    for (int q = 0; q < 2 * NW; ++q) t += redb[q * RS + lane];
-    hwv[lane] = t;
+    for (int q = 0; q < NW; ++q) {
+      t0 += redb[q * RS + lane];
+      t1 += redb[(NW + q) * RS + lane];
+    }
+    hwv[lane] = t0 + t1;
   }
   __syncwarp();
 }
 
 // Contributions of the v_j planes zz in [LO, HI) to the thread's ZL outputs (all bounds
-// compile-time: out[] stays in registers).  pv -> own column at zl = 0 of the v_j planes,
-// pc -> own column at zl = 0 of the c' planes.  Neighbour columns outside the extended box
-// are zero (the modified BC), hence the x/y masks.
+// compile-time: out[] stays in registers).  pv -> own column at zl = 0 of the padded v_j planes
+// (the zero ring outside the extended box is the modified BC), pc -> own column at zl = 0 of
+// the unpadded c' planes.
 template <int E, int LO, int HI>
 __device__ __forceinline__ void cl2_stencil(const Ras3Cl2Args& p, const double* pv,
-                                            const double* pc, int x, int y, double (&out)[E / 2]) {
-  constexpr int ZL = E / 2, PL = E * E;
+                                            const double* pc, double (&out)[E / 2]) {
+  constexpr int ZL = E / 2, PL = E * E, PX = Cl2<E>::PX, PP = Cl2<E>::PP;
   const double W0 = p.W[0], W1 = p.W[1], W2 = p.W[2], W3 = p.W[3], W4 = p.W[4], W5 = p.W[5],
                W6 = p.W[6];
-  auto ok = [&](int dx, int dy) {
-    return (unsigned)(x + dx) < (unsigned)E && (unsigned)(y + dy) < (unsigned)E;
-  };
-  auto ld = [&](int dx, int dy, int zz) -> double {
-    return ok(dx, dy) ? pv[zz * PL + dx + E * dy] : 0.0;
-  };
+  auto ld = [&](int dx, int dy, int zz) -> double { return pv[zz * PP + dx + PX * dy]; };
   // R = 0: own column, z-reach 3; with the z-neighbour and centre terms of -Delta(c v)
 #pragma unroll
   for (int zz = (LO > -3 ? LO : -3); zz < (HI < ZL + 3 ? HI : ZL + 3); ++zz) {
-    const double val = pv[zz * PL];
+    const double val = pv[zz * PP];
 #pragma unroll
     for (int z = (zz - 3 > 0 ? zz - 3 : 0); z <= (zz + 3 < ZL - 1 ? zz + 3 : ZL - 1); ++z) {
       const int dz = zz > z ? zz - z : z - zz;
@@ -171,12 +257,12 @@ __device__ __forceinline__ void cl2_stencil(const Ras3Cl2Args& p, const double* 
       const int dz = zz > z ? zz - z : z - zz;
       out[z] = fma(dz == 0 ? W1 : dz == 1 ? W3 : W5, s, out[z]);
     }
-    if (zz >= 0 && zz < ZL) {
+    if (zz >= 0 && zz < ZL) {   // v = 0 outside the box: the c' read there is inert
       double t = out[zz];
-      if (ok(-1, 0)) t = fma(pc[zz * PL - 1], a, t);
-      if (ok(1, 0)) t = fma(pc[zz * PL + 1], b, t);
-      if (ok(0, -1)) t = fma(pc[zz * PL - E], cc, t);
-      if (ok(0, 1)) t = fma(pc[zz * PL + E], d, t);
+      t = fma(pc[zz * PL - 1], a, t);
+      t = fma(pc[zz * PL + 1], b, t);
+      t = fma(pc[zz * PL - E], cc, t);
+      t = fma(pc[zz * PL + E], d, t);
       out[zz] = t;
     }
   }
@@ -203,31 +289,43 @@ __device__ __forceinline__ void cl2_stencil(const Ras3Cl2Args& p, const double* 
   }
 }
 
-template <int K, int E>
+template <int K, int E, int NRX>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cl2<E>::NT, 1)
     ras3d_cl2_kernel(const __grid_constant__ Ras3Cl2Args p) {
   if (p.gate && *p.gate) return;     // uniform over the cluster: both CTAs leave at once
   constexpr int ZL = Cl2<E>::ZL, PL = Cl2<E>::PL, NW = Cl2<E>::NW;
-  constexpr int NVB = Cl2<E>::NVB, NCB = Cl2<E>::NCB;
-  constexpr int NR = Cl2K<K>::NR, NS = Cl2K<K>::NS, NG = Cl2K<K>::NG;
+  constexpr int NVB = Cl2<E>::NVB, NCB = Cl2<E>::NCB, PX = Cl2<E>::PX, PP = Cl2<E>::PP;
+  constexpr int CG = Cl2<E>::CG;
+  constexpr int NR = Cl2K<K, NRX>::NR, NS = Cl2K<K, NRX>::NS, NG = Cl2K<K, NRX>::NG;
   constexpr int NE = E * E * E;
   extern __shared__ __align__(128) double smem_dyn[];
-  double* vb = smem_dyn;                 // NVB planes: v_j (rank 0: zl in [0, ZL+3), rank 1: [-3, ZL))
-  double* cb = vb + NVB * PL;            // NCB planes: c' = -c/h^2 (rank 0: [0, ZL], rank 1: [-1, ZL))
-  double* vs = cb + NCB * PL;            // NS x ZL x PL: basis vectors NR..K-2
+  double* vb = smem_dyn;                 // NVB padded planes: v_j (rank 0: zl in [0, ZL+3),
+                                         // rank 1: [-3, ZL))
+  double* cb = vb + NVB * PP + CG;       // NCB planes: c' = -c/h^2 (rank 0: [0, ZL], rank 1:
+                                         // [-1, ZL)), guard rows before and after
+  double* vs = cb + NCB * PL + CG;       // NS x ZL x PL: basis vectors NR..K-2
   double* red = vs + NS * ZL * PL;       // 2 buffers x [rank][warp][RS]
   double* hw = red + 2 * 2 * NW * RS;    // per warp: h1, h2, scratch
   __shared__ double H[(K + 1) * K];
   __shared__ double gv[K + 1], cs[K], sn[K], yv[K];
+  // mbarriers: [0], [1] the two reduction buffers, [2] the halo planes; each completes when the
+  // local thread 0 has armed it (arrive + expected bytes) and the partner's bytes have landed
+  __shared__ __align__(8) uint64_t mbar[3];
 
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const bool g0 = wid == NW - 1 && lane == 0;   // Givens lane: Hessenberg columns, back-subst.
   const int rank = (int)cluster_rank(), partner = rank ^ 1;
   const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
-  const bool act = tid < PL;
-  const int x = act ? tid % E : 0, y = act ? tid / E : 0;
+  // half-warp h owns the 4x4 column tile h of the E/4 x E/4 tiling of the xy plane
+  const int tile = tid >> 4, l16 = tid & 15;
+  const bool act = tile < (E / 4) * (E / 4);
+  const int x = act ? 4 * (tile % (E / 4)) + (l16 & 3) : 0;
+  const int y = act ? 4 * (tile / (E / 4)) + (l16 >> 2) : 0;
+  const int col = y * E + x;                       // unpadded column index
+  const int colp = (y + 3) * PX + (x + 3);         // padded column index
   const int pv0 = rank == 0 ? 0 : 3, pc0 = rank == 0 ? 0 : 1;   // plane of zl = 0
-  const double* pv = vb + pv0 * PL + tid;          // own column, zl = 0
-  const double* pc = cb + pc0 * PL + tid;
+  const double* pv = vb + pv0 * PP + colp;         // own column, zl = 0
+  const double* pc = cb + pc0 * PL + col;
   double* gs = p.gscr + (size_t)blockIdx.x * (NG > 0 ? NG : 1) * ZL * PL + tid;
   double* h1 = hw + wid * 3 * RS;
   double* h2 = h1 + RS;
@@ -238,10 +336,32 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cl2<E>::NT, 1)
   const int nboxes = nbx * nby * nbz;
   const size_t NX = p.nx, NXY = (size_t)p.nx * p.ny;
 
-  cl_sync();   // the partner is running before any DSMEM store
+  int rb = 0;
+  const uint32_t mbar_rem0 = mapa_rank(smem_u32(&mbar[0]), (uint32_t)partner);
+  // zero v planes (the ring stays zero: only interior columns are ever written) and finite c'
+  for (int q = tid; q < NVB * PP + NCB * PL + 2 * CG; q += blockDim.x) vb[q] = 0.0;
+  if (tid == 0) {
+    for (int q = 0; q < 3; ++q) mbar_init(&mbar[q], 1);
+    fence_mbar_init();
+  }
+  cl_sync();   // the partner is running, zeroed and its mbarriers initialised before any DSMEM store
+  uint32_t ph = 0;   // phase parity bits: bit q for mbar[q]
+  constexpr uint32_t HALO_BYTES = (uint32_t)PL * 3u * 8u;
+  // one cluster reduction: warp partials are in both CTAs (cl2_put); arm, sync, wait, sum
+  auto reduce = [&](int nsent, int nget, double* hwv) {
+    if (tid == 0) mbar_expect_tx(&mbar[rb], (uint32_t)(NW * nsent * 8));
+    __syncthreads();
+    mbar_wait_cluster(&mbar[rb], (ph >> rb) & 1u);
+    ph ^= 1u << rb;
+    cl2_get<NW>(nget, red + rb * 2 * NW * RS, hwv, lane);
+    rb ^= 1;
+  };
 
   double vr[NR > 0 ? NR : 1][ZL];
-  int rb = 0;
+#pragma unroll
+  for (int s = 0; s < (NR > 0 ? NR : 1); ++s)
+#pragma unroll
+    for (int zl = 0; zl < ZL; ++zl) vr[s][zl] = 0.0;
   for (int box = cid; box < nboxes; box += ncl) {
     const int ibx = box % nbx, iby = (box / nbx) % nby, ibz = box / (nbx * nby);
     const int gx0 = ibx * p.bx - p.o, gy0 = iby * p.by - p.o, gz0 = ibz * p.bz - p.o;
@@ -257,22 +377,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cl2<E>::NT, 1)
         const int ez = ez0 + zl;
         const bool owned = oxy && ez >= p.o && ez < p.o + p.bz;
         w[zl] = (p.restrict_owned && !owned) ? 0.0 : p.v[g];
-        cb[(zl + pc0) * PL + tid] = -p.ih2 * p.c[g];
+        cb[(zl + pc0) * PL + col] = -p.ih2 * p.c[g];
         acc = fma(w[zl], w[zl], acc);
       }
       // the c' plane on the partner's side (inside the box): zl = ZL (rank 0) / -1 (rank 1)
       const int zh = rank == 0 ? ZL : -1;
-      cb[(zh + pc0) * PL + tid] = -p.ih2 * p.c[gxy + NXY * wrapi(gz0 + ez0 + zh, p.nz)];
+      cb[(zh + pc0) * PL + col] = -p.ih2 * p.c[gxy + NXY * wrapi(gz0 + ez0 + zh, p.nz)];
     } else {
 #pragma unroll
       for (int zl = 0; zl < ZL; ++zl) w[zl] = 0.0;
     }
     double* redb = red + rb * 2 * NW * RS;
     uint32_t redr = red_rem + (uint32_t)(rb * 2 * NW * RS) * 8u;
-    cl2_put<NW>(acc, 0, redb, redr, rank, wid, lane);
-    cl_sync();
-    cl2_get<NW>(1, redb, hx, lane);
-    rb ^= 1;
+    uint32_t mbr = mbar_rem0 + 8u * rb;
+    cl2_put<NW>(acc, 0, redb, redr, mbr, rank, wid, lane);
+    reduce(1, 1, hx);
     const double beta = sqrt(hx[0]);
     if (beta == 0.0) {
       if (act) {
@@ -304,15 +423,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cl2<E>::NT, 1)
         for (int zl = 0; zl < ZL; ++zl) gs[((slot - NR - NS) * ZL + zl) * PL] = w[zl];
       }
 #pragma unroll
-      for (int zl = 0; zl < ZL; ++zl) vb[(zl + pv0) * PL + tid] = w[zl];
+      for (int zl = 0; zl < ZL; ++zl) vb[(zl + pv0) * PP + colp] = w[zl];
+      const uint32_t hm = mbar_rem0 + 16u;   // the partner's halo mbarrier
       if (rank == 0) {   // own planes ZL-3..ZL-1 -> partner's zl' = -3..-1 (its planes 0..2)
 #pragma unroll
         for (int q = 0; q < 3; ++q)
-          st_cluster(vb_rem + (uint32_t)(q * PL + tid) * 8u, w[ZL - 3 + q]);
+          st_async(vb_rem + (uint32_t)(q * PP + colp) * 8u, w[ZL - 3 + q], hm);
       } else {           // own planes 0..2 -> partner's zl' = ZL..ZL+2 (its planes ZL..ZL+2)
 #pragma unroll
         for (int q = 0; q < 3; ++q)
-          st_cluster(vb_rem + (uint32_t)((ZL + q) * PL + tid) * 8u, w[q]);
+          st_async(vb_rem + (uint32_t)((ZL + q) * PP + colp) * 8u, w[q], hm);
       }
     };
     // basis value i of the thread's node zl (i compile-time after unrolling)
@@ -320,7 +440,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cl2<E>::NT, 1)
       if (i < NR) return vr[i < NR ? i : 0][zl];
       if (i < NR + NS) return vs[((i - NR) * ZL + zl) * PL + tid];
       if (i < K - 1) return gs[((i - NR - NS) * ZL + zl) * PL];
-      return pv[zl * PL];                            // v_{K-1}: only in the v_j planes
+      return pv[zl * PP];                            // v_{K-1}: only in the v_j planes
     };
     {
       const double ib = 1.0 / beta;
@@ -328,111 +448,116 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cl2<E>::NT, 1)
       for (int zl = 0; zl < ZL; ++zl) w[zl] *= ib;
       put_v(0);
     }
-    if (tid == 0) gv[0] = beta;
+    if (g0) gv[0] = beta;
     int jm = 0;
+    double hn_prev = 0.0;
 #pragma unroll 1
     for (int j = 0; j < K; ++j) {
       // ---- w = A_k v_j: own planes while the partner's halo planes are in flight
-      cl_arrive();
+      if (tid == 0) mbar_expect_tx(&mbar[2], HALO_BYTES);
       __syncthreads();
+      // the Givens lane turns column j-1 while the node warps run the stencil (its h1, h2
+      // copies of step j-1 are overwritten only by this step's reductions)
+      if (g0 && j > 0) givens_col(j - 1, h1, h2, hn_prev, H, cs, sn, gv, K + 1);
 #pragma unroll
       for (int zl = 0; zl < ZL; ++zl) w[zl] = 0.0;
-      if (act) cl2_stencil<E, 0, ZL>(p, pv, pc, x, y, w);
-      cl_wait();
+      if (act) cl2_stencil<E, 0, ZL>(p, pv, pc, w);
+      mbar_wait_cluster(&mbar[2], (ph >> 2) & 1u);
+      ph ^= 4u;
       if (act) {
-        if (rank == 0) cl2_stencil<E, ZL, ZL + 3>(p, pv, pc, x, y, w);
-        else cl2_stencil<E, -3, 0>(p, pv, pc, x, y, w);
+        if (rank == 0) cl2_stencil<E, ZL, ZL + 3>(p, pv, pc, w);
+        else cl2_stencil<E, -3, 0>(p, pv, pc, w);
       }
-      // ---- CGS2 pass 1: h1 = V^T w
-      redb = red + rb * 2 * NW * RS;
-      redr = red_rem + (uint32_t)(rb * 2 * NW * RS) * 8u;
-#pragma unroll
-      for (int i = 0; i < K; ++i)
-        if (i <= j) {
-          double s = 0.0;
-#pragma unroll
-          for (int zl = 0; zl < ZL; ++zl) s = fma(V(i, zl), w[zl], s);
-          cl2_put<NW>(s, i, redb, redr, rank, wid, lane);
-        }
-      cl_sync();
-      cl2_get<NW>(j + 1, redb, h1, lane);
-      rb ^= 1;
-      // ---- pass 2: w' = w - V h1, h2 = V^T w', |w'|^2
-#pragma unroll
-      for (int i = 0; i < K; ++i)
-        if (i <= j) {
-          const double hi = h1[i];
-#pragma unroll
-          for (int zl = 0; zl < ZL; ++zl) w[zl] = fma(-hi, V(i, zl), w[zl]);
-        }
-      redb = red + rb * 2 * NW * RS;
-      redr = red_rem + (uint32_t)(rb * 2 * NW * RS) * 8u;
-#pragma unroll
-      for (int i = 0; i < K; ++i)
-        if (i <= j) {
-          double s = 0.0;
-#pragma unroll
-          for (int zl = 0; zl < ZL; ++zl) s = fma(V(i, zl), w[zl], s);
-          cl2_put<NW>(s, i, redb, redr, rank, wid, lane);
-        }
-      {
-        double s = 0.0;
-#pragma unroll
-        for (int zl = 0; zl < ZL; ++zl) s = fma(w[zl], w[zl], s);
-        cl2_put<NW>(s, j + 1, redb, redr, rank, wid, lane);
-      }
-      cl_sync();
-      cl2_get<NW>(j + 2, redb, h2, lane);
-      rb ^= 1;
-      double h2n = 0.0;
-      for (int i = 0; i <= j; ++i) h2n += h2[i] * h2[i];
-      const double wn2 = h2[j + 1];
-      // ---- pass 3: w'' = w' - V h2
-#pragma unroll
-      for (int i = 0; i < K; ++i)
-        if (i <= j) {
-          const double hi = h2[i];
-#pragma unroll
-          for (int zl = 0; zl < ZL; ++zl) w[zl] = fma(-hi, V(i, zl), w[zl]);
-        }
-      double hn2;
-      if (h2n <= 1e-8 * wn2) {
-        hn2 = wn2 - h2n;                             // |w''|^2 = |w'|^2 - |h2|^2
-      } else {
+      // ---- CGS2 on w (Arnoldi step j dispatched to code specialised for J = j: every basis
+      // index compile-time, no per-node guards)
+      double hn2 = 0.0;
+      auto cgs2 = [&](auto Jc) {
+        constexpr int J = decltype(Jc)::value;
+        // pass 1: h1 = V^T w (node-outer loops: J+1 independent accumulation chains)
         redb = red + rb * 2 * NW * RS;
         redr = red_rem + (uint32_t)(rb * 2 * NW * RS) * 8u;
-        double s = 0.0;
+        mbr = mbar_rem0 + 8u * rb;
+        {
+          double acc[16];
 #pragma unroll
-        for (int zl = 0; zl < ZL; ++zl) s = fma(w[zl], w[zl], s);
-        cl2_put<NW>(s, 0, redb, redr, rank, wid, lane);
-        cl_sync();
-        cl2_get<NW>(1, redb, hx, lane);
-        rb ^= 1;
-        hn2 = hx[0];
-      }
-      const double hn = sqrt(hn2 > 0.0 ? hn2 : 0.0);
-      if (tid == 0) {   // Hessenberg column j: previous rotations, a new one (oracle order)
-        double col[K + 1];
+          for (int i = 0; i < 16; ++i) acc[i] = 0.0;
+          if (act) {   // threads without a node contribute exactly 0
 #pragma unroll
-        for (int i = 0; i <= K; ++i) col[i] = 0.0;
-        for (int i = 0; i <= j; ++i) col[i] = h1[i] + h2[i];
-        col[j + 1] = hn;
-        for (int i = 0; i < j; ++i) {
-          const double a = col[i], b = col[i + 1];
-          col[i] = cs[i] * a + sn[i] * b;
-          col[i + 1] = -sn[i] * a + cs[i] * b;
+            for (int zl = 0; zl < ZL; ++zl) {
+              const double wz = w[zl];
+#pragma unroll
+              for (int i = 0; i <= J; ++i)
+                acc[i] = fma(V(i, zl), wz, acc[i]);
+            }
+          }
+          cl2_put_multi<NW>(acc, J + 1, redb, redr, mbr, rank, wid, lane);
         }
-        const double a = col[j], b = col[j + 1];
-        const double rr = sqrt(a * a + b * b);
-        double cc = 1.0, ss = 0.0;
-        if (rr != 0.0) { cc = a / rr; ss = b / rr; }
-        cs[j] = cc; sn[j] = ss;
-        col[j] = cc * a + ss * b;
-        const double g = gv[j];
-        gv[j + 1] = -ss * g;
-        gv[j] = cc * g;
-        for (int i = 0; i <= j; ++i) H[i + (K + 1) * j] = col[i];
-      }
+        reduce(J + 1, J + 1, h1);
+        // pass 2: w' = w - V h1, h2 = V^T w', |w'|^2
+        redb = red + rb * 2 * NW * RS;
+        redr = red_rem + (uint32_t)(rb * 2 * NW * RS) * 8u;
+        mbr = mbar_rem0 + 8u * rb;
+        {
+          double hv[J + 1], acc[16], nrm = 0.0;
+#pragma unroll
+          for (int i = 0; i <= J; ++i) hv[i] = h1[i];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) acc[i] = 0.0;
+          if (act) {
+#pragma unroll
+            for (int zl = 0; zl < ZL; ++zl) {
+              double ww = w[zl];
+#pragma unroll
+              for (int i = 0; i <= J; ++i)
+                ww = fma(-hv[i], V(i, zl), ww);
+#pragma unroll
+              for (int i = 0; i <= J; ++i)
+                acc[i] = fma(V(i, zl), ww, acc[i]);
+              nrm = fma(ww, ww, nrm);
+              w[zl] = ww;
+            }
+          }
+          cl2_put_multi<NW>(acc, J + 1, redb, redr, mbr, rank, wid, lane);
+          cl2_put<NW>(nrm, J + 1, redb, redr, mbr, rank, wid, lane);   // |w'|^2 in slot j+1
+        }
+        reduce(J + 2, J + 2, h2);
+        double h2n = 0.0;
+        for (int i = 0; i <= J; ++i) h2n += h2[i] * h2[i];
+        const double wn2 = h2[J + 1];
+        // pass 3: w'' = w' - V h2
+        if (act) {
+          double hv[J + 1];
+#pragma unroll
+          for (int i = 0; i <= J; ++i) hv[i] = h2[i];
+#pragma unroll
+          for (int zl = 0; zl < ZL; ++zl) {
+            double ww = w[zl];
+#pragma unroll
+            for (int i = 0; i <= J; ++i)
+              ww = fma(-hv[i], V(i, zl), ww);
+            w[zl] = ww;
+          }
+        }
+        if (h2n <= 1e-8 * wn2) {
+          hn2 = wn2 - h2n;                             // |w''|^2 = |w'|^2 - |h2|^2
+        } else {
+          redb = red + rb * 2 * NW * RS;
+          redr = red_rem + (uint32_t)(rb * 2 * NW * RS) * 8u;
+          mbr = mbar_rem0 + 8u * rb;
+          double s = 0.0;
+          if (act) {
+#pragma unroll
+            for (int zl = 0; zl < ZL; ++zl) s = fma(w[zl], w[zl], s);
+          }
+          cl2_put<NW>(s, 0, redb, redr, mbr, rank, wid, lane);
+          reduce(1, 1, hx);
+          hn2 = hx[0];
+        }
+        return hn2;
+      };
+      dispatch_j<K>(j, cgs2);
+      const double hn = sqrt(hn2 > 0.0 ? hn2 : 0.0);
+      hn_prev = hn;
       jm = j + 1;
       if (hn <= 1e-14 * beta) break;                 // exact breakdown (identical on both CTAs)
       if (j + 1 < K) {
@@ -442,9 +567,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cl2<E>::NT, 1)
         put_v(j + 1);
       }
     }
-    __syncthreads();
-    if (tid == 0) {   // back substitution R yv = g (R reduced column by column)
+    if (g0) {   // last Hessenberg column, then back substitution R yv = g
       const int ld = K + 1;
+      givens_col(jm - 1, h1, h2, hn_prev, H, cs, sn, gv, ld);
       for (int i = jm - 1; i >= 0; --i) {
         double s = gv[i];
         for (int l = i + 1; l < jm; ++l) s -= H[i + ld * l] * yv[l];
@@ -481,14 +606,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cl2<E>::NT, 1)
 
 typedef void (*ras3cl2_fn)(const Ras3Cl2Args);
 
-ras3cl2_fn pick_cl2(int k, int e, size_t* smem, int* threads) {
-#define C2(K, E)                                                \
-  if (k == K && e == E) {                                       \
-    *smem = cl2_smem_doubles<K, E>() * sizeof(double);          \
-    *threads = Cl2<E>::NT;                                      \
-    return ras3d_cl2_kernel<K, E>;                              \
+// NR = basis vectors in registers (1, 2 or 3; PFC_CL2_NR selects, default 1: measured fastest)
+int cl2_nr() {
+  const int nr = getenv("PFC_CL2_NR") ? atoi(getenv("PFC_CL2_NR")) : 1;
+  return nr == 3 ? 3 : nr == 2 ? 2 : 1;
+}
+
+ras3cl2_fn pick_cl2(int k, int e, size_t* smem, int* threads, int* ng) {
+  const int nr = cl2_nr();
+#define C2(K, E, NR)                                                \
+  if (k == K && e == E && nr == NR) {                               \
+    *smem = cl2_smem_doubles<K, E, NR>() * sizeof(double);          \
+    *threads = Cl2<E>::NT;                                          \
+    *ng = Cl2K<K, NR>::NG;                                          \
+    return ras3d_cl2_kernel<K, E, NR>;                              \
   }
-  C2(10, 20) C2(4, 20) C2(10, 12) C2(4, 12)
+  C2(10, 20, 1) C2(4, 20, 1) C2(10, 12, 1) C2(4, 12, 1) C2(10, 20, 2) C2(10, 20, 3)
 #undef C2
   return nullptr;
 }
@@ -500,16 +633,15 @@ ras3cl2_fn pick_cl2(int k, int e, size_t* smem, int* threads) {
 int ras3d_cl2_plan(pfc_ctx* ctx, int* clusters, size_t* scratch_doubles) {
   const pfc_config& c = ctx->cfg;
   const int e = c.ras_box[0] + 2 * c.ras_overlap;
-  if (c.ras_box[1] != c.ras_box[0] || c.ras_box[2] != c.ras_box[0] || (e & 1)) return 0;
+  if (c.ras_box[1] != c.ras_box[0] || c.ras_box[2] != c.ras_box[0] || (e & 3)) return 0;
   size_t smem = 0;
-  int threads = 0;
-  if (!pick_cl2(c.ras_local_k, e, &smem, &threads)) return 0;
+  int threads = 0, ng = 0;
+  if (!pick_cl2(c.ras_local_k, e, &smem, &threads, &ng)) return 0;
   if (smem + 2048 > 227 * 1024) return 0;
   const int nboxes = (c.n[0] / c.ras_box[0]) * (c.n[1] / c.ras_box[1]) * (c.n[2] / c.ras_box[2]);
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
   *clusters = nboxes < sms / 2 ? nboxes : sms / 2;
-  const int ng = c.ras_local_k - 1 - 3 - 4;   // Cl2K<K>::NG
   *scratch_doubles = (size_t)2 * (*clusters) * (ng > 0 ? ng : 1) * (e / 2) * e * e;
   return 1;
 }
@@ -519,8 +651,8 @@ cudaError_t launch_ras_3d_cl2(pfc_ctx* ctx, const double* v, const double* c, do
   const pfc_config& cf = ctx->cfg;
   const int e = cf.ras_box[0] + 2 * cf.ras_overlap;
   size_t smem = 0;
-  int threads = 0;
-  ras3cl2_fn fn = pick_cl2(cf.ras_local_k, e, &smem, &threads);
+  int threads = 0, ng = 0;
+  ras3cl2_fn fn = pick_cl2(cf.ras_local_k, e, &smem, &threads, &ng);
   if (!fn) return cudaErrorInvalidValue;
   cudaError_t err = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem);
