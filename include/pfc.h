@@ -7,7 +7,9 @@
  * Conventions (all entry points)
  *  - Fields are fp64, contiguous, x-fastest: idx = i + n[0]*(j + n[1]*k), N = n[0]*n[1]*n[2]
  *    (n[2] = 1 in 2D).  Nodes are cell-centred x_i = (i + 1/2) h; the grid is
- *    periodic in every axis.  Mobility M = 1, so grad_d.M_d grad_d = Delta_d.
+ *    periodic in every axis unless pfc_config.bc selects the mirror walls (ABI 5), and the
+ *    mobility is M = 1 (grad_d.M_d grad_d = Delta_d) unless pfc_config.mobility
+ *    selects M(phi) = 1 - phi^2 (ABI 3); the enums below define both.
  *  - Field arguments of the operator calls (pfc_residual, pfc_jacobian_apply, pfc_ras_apply)
  *    are DEVICE pointers on the context's device.  pfc_step, pfc_energy and pfc_mass accept
  *    device OR host pointers (host buffers are staged through context-owned device memory;
@@ -99,7 +101,9 @@ enum { PFC_LOCAL_GMRES = 0, PFC_LOCAL_ILU = 1, PFC_LOCAL_LU = 2 };
  *                    law of P:280-308 holds).  Subdomains are clipped at the walls: ext-box nodes
  *                    outside the domain are no unknowns of A_k = R_k J R_k^T.  Built for
  *                    ndim = 2, PFC_LOCAL_GMRES, ras_box >= 3; either mobility.  Runs the
- *                    global-memory operator chain (mobility.cu) and the shared-memory-basis
+ *                    global-memory operator chain (mobility.cu) and, for ras_local_k = 10
+ *                    (any k with M = 1), the column subdomain kernel with the basis in
+ *                    registers (ras2d.cu, MIR instantiation), else the shared-memory-basis
  *                    subdomain kernel; EINVAL otherwise. */
 enum { PFC_BC_PERIODIC = 0, PFC_BC_MIRROR = 1 };
 

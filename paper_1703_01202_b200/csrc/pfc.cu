@@ -186,7 +186,7 @@ static pfc_status energy_mass(pfc_ctx* ctx, const double* phi, double* F_d, doub
 
 // Solve J S = -F approximately: right-preconditioned flexible GMRES(m), CGS2 Arnoldi, Givens,
 // x0 = 0, stop at ||r|| <= max(xi_r ||F||, xi_a) or gmres_maxit iterations.  Host-driven
-// reference loop (one D2H round trip per Arnoldi step); fgmres_device is the default.
+// loop (one D2H round trip per Arnoldi step): the default (see fgmres() below for why).
 static pfc_status fgmres_host(pfc_ctx* ctx, double dt, double Fnorm, int* its_out) {
   const pfc_config& c = ctx->cfg;
   const int m = c.gmres_restart;

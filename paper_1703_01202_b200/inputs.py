@@ -104,6 +104,44 @@ def hexagonal_crystallites(n: int, h: float, seed: int, phibar: float = 0.285,
     return phi
 
 
+def bcc_density(X, Y, Z, L, phibar=-0.35, A=1.0, q=1.0 / math.sqrt(2.0), d0=5.0 * math.pi,
+                centres=((0.5, 0.75, 0.5), (0.25, 0.25, 0.5), (0.75, 0.25, 0.5)),
+                angles=(0.0, -math.pi / 8.0, math.pi / 8.0)):
+    """Test D initial density at coordinates (X, Y, Z) of a periodic cube of edge L
+    (§5.1D): phi = phibar + A rho(x) phi_BCC(x~) with
+    phi_BCC(x) = cos(qx)cos(qy) + cos(qx)cos(qz) + cos(qy)cos(qz) (the paper's Eq. "BBC"),
+    the quartic bump rho = (1 - (|x - x0|/d0)^2)^2 inside the sphere |x - x0| <= d0 and 0
+    outside, and x~ the rotation by omega about the z-axis of x - x0.  Centres are
+    given as fractions of L: (L/2, 3L/4, L/2), (L/4, L/4, L/2), (3L/4, L/4, L/2), angles
+    0, -pi/8, pi/8, d0 = 5 pi, phibar = -0.35, q = 1/sqrt(2), A = 1.  The spheres
+    are disjoint for L = 80 pi (distance >= L/2 > 2 d0), so their bumps are summed (reading
+    R24: with disjoint supports sum = the paper's per-sphere definition).  Displacements are
+    taken minimum-image (periodic domain)."""
+    phi = np.full(np.broadcast(X, Y, Z).shape, phibar, dtype=np.float64)
+    for (fx, fy, fz), w in zip(centres, angles):
+        dx = (X - fx * L + L / 2) % L - L / 2
+        dy = (Y - fy * L + L / 2) % L - L / 2
+        dz = (Z - fz * L + L / 2) % L - L / 2
+        r2 = dx * dx + dy * dy + dz * dz
+        inside = r2 <= d0 * d0
+        rho = np.where(inside, (1.0 - r2 / (d0 * d0)) ** 2, 0.0)
+        xt = math.cos(w) * dx - math.sin(w) * dy
+        yt = math.sin(w) * dx + math.cos(w) * dy
+        zt = dz
+        bcc = (np.cos(q * xt) * np.cos(q * yt) + np.cos(q * xt) * np.cos(q * zt)
+               + np.cos(q * yt) * np.cos(q * zt))
+        phi = phi + A * rho * bcc
+    return phi
+
+
+def bcc_crystallites(n: int, h: float, **kw) -> np.ndarray:
+    """Test D IC on an n^3 grid of spacing h (cell-centred nodes, R2), numpy shape (z, y, x)."""
+    L = n * h
+    x = node_coords(n, h)
+    Z, Y, X = np.meshgrid(x, x, x, indexing="ij")
+    return bcc_density(X, Y, Z, L, **kw)
+
+
 @dataclass
 class PFCConfig:
     """One BASELINE.json config plus the solver settings DESIGN.md fixes for it."""
@@ -147,6 +185,8 @@ class PFCConfig:
             return random_field(self.n, self.seed, self.ic["mean"], self.ic["amp"])
         if kind == "hexagonal":
             return hexagonal_crystallites(self.n[0], self.h, self.seed)
+        if kind == "bcc":
+            return bcc_crystallites(self.n[0], self.h)
         raise ValueError(kind)
 
 
@@ -166,6 +206,13 @@ CONFIGS = {
     "cfg4": PFCConfig("cfg4_3d_128", 3, (128, 128, 128), adaptive=True, dt0=0.5, dt_min=0.5,
                       dt_max=10.0, eta=500.0, steps=100, ras_box=(16, 16, 16),
                       ic={"kind": "random", "mean": -0.35, "amp": 0.05}, seed=4),
+    # the paper's Test D (row f4's second workload): 3D polycrystalline growth on
+    # [0, 80 pi]^3 with a 256^3 mesh (h = 80 pi / 256), gamma = 0.35, three rotated BCC
+    # crystallite spheres in the liquid phibar = -0.35, adaptive dt in [0.5, 10], eta = 500;
+    # RAS as config 4 (16^3 boxes, overlap 2)
+    "testD": PFCConfig("testD_3d_256", 3, (256, 256, 256), h=80.0 * math.pi / 256.0, gamma=0.35,
+                       adaptive=True, dt0=0.5, dt_min=0.5, dt_max=10.0, eta=500.0, steps=20,
+                       ras_box=(16, 16, 16), ic={"kind": "bcc"}, seed=0),
     # configs[4]: 512^3, fixed dt=1.0, 10 steps
     "cfg5": PFCConfig("cfg5_3d_512", 3, (512, 512, 512), dt0=1.0, steps=10,
                       ras_box=(16, 16, 16), ic={"kind": "random", "mean": -0.35, "amp": 0.05}, seed=5),

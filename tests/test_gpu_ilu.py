@@ -130,3 +130,53 @@ def test_lu_3d_box_beyond_the_plan_is_einval():
     with pytest.raises(P.PfcError):
         P.Context(None, ndim=3, n=(24, 24, 24), h=H, gamma=G, ras_box=[8, 8, 8], ras_overlap=1,
                   ras_local_solver=P.PFC_LOCAL_LU)
+
+
+# ---- the bench's geometry: cfg2's 32^2 boxes with overlap 2 (E = 36, 1296-row subdomain
+# matrices; 141-level ILU schedules, 1296-row LU chains; the factor kernel's widest launch
+# plan), on a 128^2 grid of 16 boxes so the oracle stays fast
+@pytest.mark.parametrize("variant", [P.PFC_RAS_LEFT, P.PFC_RAS_AS, P.PFC_RAS_RIGHT])
+@pytest.mark.parametrize("level", [0, 1])
+def test_ilu_schwarz_parity_cfg2_geometry(level, variant):
+    shape, box, o = (128, 128), (32, 32), 2
+    phi = random_field(shape, 621, 0.07, 0.07)
+    psi = random_field(shape, 622, 0.07, 0.07)
+    v = random_field(shape, 623, 0.0, 1.0)
+    dt = 0.02
+    ctx = ctx_ilu(shape, box, o, level, ras_variant=variant)
+    z = host(ctx.ras_apply(dev(phi), dev(psi), dt, dev(v)))
+    zo = O.ras_apply(phi, psi, v, H, prm_ilu(box, o, level, ras_variant=variant), dt)
+    assert rel(z, zo) <= 1e-12
+
+
+@pytest.mark.parametrize("variant", [P.PFC_RAS_LEFT, P.PFC_RAS_AS, P.PFC_RAS_RIGHT])
+def test_lu_schwarz_parity_cfg2_geometry(variant):
+    shape, box, o = (128, 128), (32, 32), 2
+    phi = random_field(shape, 631, 0.07, 0.07)
+    psi = random_field(shape, 632, 0.07, 0.07)
+    v = random_field(shape, 633, 0.0, 1.0)
+    dt = 0.5
+    ctx = P.Context(None, ndim=2, n=shape, h=H, gamma=G, ras_box=[32, 32, 1], ras_overlap=o,
+                    ras_local_solver=P.PFC_LOCAL_LU, ras_variant=variant)
+    z = host(ctx.ras_apply(dev(phi), dev(psi), dt, dev(v)))
+    zo = O.ras_apply(phi, psi, v, H, O.params(gamma=G, ras_box=box, ras_overlap=o,
+                                              ras_local_solver=O.LOCAL_LU, ras_variant=variant), dt)
+    assert rel(z, zo) <= 1e-12
+
+
+@pytest.mark.parametrize("solver,level,dt", [(P.PFC_LOCAL_ILU, 0, 0.02), (P.PFC_LOCAL_LU, 0, 0.5)])
+def test_factor_one_step_parity_cfg2_geometry(solver, level, dt):
+    """One Newton step with factor reuse at E = 36: same Newton / FGMRES counts as the oracle."""
+    shape = (128, 128)
+    phi0 = random_field(shape, 2, 0.07, 0.07)
+    ctx = P.Context(None, ndim=2, n=shape, h=H, gamma=G, ras_box=[32, 32, 1], ras_overlap=2,
+                    ras_local_solver=solver, ras_ilu_level=level, ras_ilu_reuse=1)
+    phi = dev(phi0)
+    _, info = ctx.step(phi, dt)
+    osolver = O.LOCAL_ILU if solver == P.PFC_LOCAL_ILU else O.LOCAL_LU
+    ref, ok, oinfo = O.newton(phi0, H, O.params(gamma=G, ras_box=(32, 32), ras_overlap=2,
+                                                ras_local_solver=osolver, ras_ilu_level=level,
+                                                ras_ilu_reuse=1), dt)
+    assert ok and info["converged"]
+    assert info["newton_its"] == oinfo.newton_its and info["gmres_its"] == oinfo.gmres_its
+    assert rel(host(phi), ref) <= 1e-10

@@ -361,3 +361,116 @@ def test_cfg3_one_step_parity():
     ctx.step(phi, cfg.dt0)
     ref, _ = O.run(cfg, phi0, 1)
     assert rel(host(phi), ref) <= 1e-10
+
+
+def test_cfg4_full_size_two_steps():
+    """Config 4 at its full size (128^3, 512 boxes of 16^3, 8 per axis: every box has distinct
+    periodic neighbours) in the bench's launch configuration: two adaptive steps from the IC
+    against the oracle's (tests/golden/cfg4_128_two_steps.npz, written by
+    tools/make_golden_cfg4.py from oracle/ only, since an oracle step takes ~2 min here):
+    65536 seeded sample nodes (rel L2 <= 1e-10 after one step, <= 1e-8 after two), the
+    full-field norm, F_d, mass, the dt law (Eq. sencondt) and the Newton / FGMRES
+    counts of both steps."""
+    import os
+    g = np.load(os.path.join(os.path.dirname(__file__), "golden", "cfg4_128_two_steps.npz"))
+    idx, hist = g["idx"], g["hist"]
+    cfg = CONFIGS["cfg4"]
+    phi0 = cfg.initial_condition()
+    ctx = P.Context(cfg)
+    phi = dev(phi0)
+    dt1, i1 = ctx.step(phi, cfg.dt0)
+    a1 = host(phi).ravel()
+    dt2, i2 = ctx.step(phi, dt1)
+    a2 = host(phi).ravel()
+    assert rel(a1[idx], g["phi1"]) <= 1e-10
+    assert rel(a2[idx], g["phi2"]) <= 1e-8
+    assert abs(np.linalg.norm(a1) - g["norm1"]) <= 1e-12 * g["norm1"]
+    assert abs(np.linalg.norm(a2) - g["norm2"]) <= 1e-10 * g["norm2"]
+    for info, row, dt in ((i1, hist[0], cfg.dt0), (i2, hist[1], dt1)):
+        assert info["converged"] == 1
+        assert info["newton_its"] == int(row[5]) and info["gmres_its"] == int(row[6])
+        assert abs(info["dt_used"] - row[2]) <= 1e-12 * row[2] and abs(dt - row[2]) <= 1e-12 * dt
+        assert abs(info["energy"] - row[3]) <= 1e-10 * abs(row[3])
+        assert abs(info["mass"] - row[4]) <= 1e-9 * abs(row[4])
+
+
+def test_cfg5_full_size_step_solves_the_scheme():
+    """Config 5 at its full size (512^3, 32768 boxes, 1 GiB per field), one fixed-dt step in
+    the bench's launch configuration.  An oracle step is out of reach (hours, ~69 GiB), so the
+    step is checked by properties that hold at any size, evaluated with the ORACLE's operators
+    on the GPU's result: the DVD residual F(phi^1; phi^0) of Eq. NSOP is below the
+    Newton stopping threshold (the oracle's own ||F_0||); mass is conserved to the
+    Newton tolerance (h^3 sum(phi^1 - phi^0) = dt h^3 sum F); the discrete energy
+    decreases (Proposition) and equals the library's F_d."""
+    cfg = CONFIGS["cfg5"]
+    phi0 = cfg.initial_condition()
+    ctx = P.Context(cfg)
+    phi = dev(phi0)
+    _, info = ctx.step(phi, cfg.dt0)
+    phi1 = host(phi)
+    del phi
+    ctx.close()
+    torch.cuda.empty_cache()
+    assert info["converged"] == 1
+    F0 = O.residual(phi0, phi0, H, G, cfg.dt0)
+    stop = max(cfg.newton_rtol * np.linalg.norm(F0), cfg.newton_atol)
+    del F0
+    F1 = O.residual(phi1, phi0, H, G, cfg.dt0)
+    assert np.linalg.norm(F1) <= 1.01 * stop
+    sF = math.fsum(F1.ravel())
+    del F1
+    m0, m1 = O.mass(phi0, H), O.mass(phi1, H)
+    h3 = H ** 3
+    # the mass identity h^3 sum(phi^1 - phi^0) = dt h^3 sum F, and its Newton-tolerance bound
+    assert abs((m1 - m0) - cfg.dt0 * h3 * sF) <= 1e-12 * abs(m0)
+    assert abs(m1 - m0) <= cfg.dt0 * h3 * math.sqrt(cfg.N) * stop + 1e-12 * abs(m0)
+    E0, E1 = O.free_energy(phi0, H, G), O.free_energy(phi1, H, G)
+    assert E1 < E0
+    assert abs(info["energy"] - E1) <= 1e-11 * abs(E1)
+    assert abs(info["energy_old"] - E0) <= 1e-11 * abs(E0)
+
+
+def _testd_cfg(n):
+    """The paper's Test D IC law and settings on an n^3 grid of the paper's
+    spacing h = 80 pi / 256 (domain n h; crystallite centres at the same fractions of it)."""
+    base = CONFIGS["testD"]
+    return PFCConfig(f"testD_{n}", 3, (n, n, n), h=base.h, gamma=base.gamma, adaptive=True,
+                     dt0=base.dt0, dt_min=base.dt_min, dt_max=base.dt_max, eta=base.eta,
+                     ras_box=(16, 16, 16), ic={"kind": "bcc"})
+
+
+def test_testD_ic_law_one_step_parity():
+    """Row f4's second workload (Test D, gamma = 0.35, BCC crystallites with amplitude
+    up to 2.3 in the phibar = -0.35 liquid) at 64^3: one adaptive step and the next dt vs the
+    oracle, same Newton / FGMRES counts."""
+    cfg = _testd_cfg(64)
+    phi0 = cfg.initial_condition()
+    out, infos = _run_gpu(cfg, phi0, 1)
+    ref, hist = O.run(cfg, phi0, 1)
+    assert rel(out, ref) <= 1e-10
+    assert infos[0]["newton_its"] == hist[0][5] and infos[0]["gmres_its"] == hist[0][6]
+    assert abs(infos[0]["energy"] - hist[0][3]) <= 1e-10 * abs(hist[0][3])
+
+
+def test_testD_full_size_step_solves_the_scheme():
+    """Test D at the paper's 256^3 (4096 boxes): one adaptive step, checked with the ORACLE's
+    operators on the GPU's result (as for config 5): the DVD residual is below the Newton
+    threshold, mass is conserved per the identity of P:276-277, the energy decreases."""
+    cfg = CONFIGS["testD"]
+    phi0 = cfg.initial_condition()
+    ctx = P.Context(cfg)
+    phi = dev(phi0)
+    _, info = ctx.step(phi, cfg.dt0)
+    phi1 = host(phi)
+    del phi
+    ctx.close()
+    assert info["converged"] == 1
+    F0 = O.residual(phi0, phi0, cfg.h, cfg.gamma, cfg.dt0)
+    stop = max(cfg.newton_rtol * np.linalg.norm(F0), cfg.newton_atol)
+    F1 = O.residual(phi1, phi0, cfg.h, cfg.gamma, cfg.dt0)
+    assert np.linalg.norm(F1) <= 1.01 * stop
+    h3 = cfg.h ** 3
+    m0, m1 = O.mass(phi0, cfg.h), O.mass(phi1, cfg.h)
+    assert abs((m1 - m0) - cfg.dt0 * h3 * math.fsum(F1.ravel())) <= 1e-12 * abs(m0)
+    E0, E1 = O.free_energy(phi0, cfg.h, cfg.gamma), O.free_energy(phi1, cfg.h, cfg.gamma)
+    assert E1 < E0 and abs(info["energy"] - E1) <= 1e-11 * abs(E1)

@@ -1,7 +1,10 @@
 // fp64_peak.cu -- measured FP64 (DFMA) throughput of this GPU, the ALU roofline denominator for
 // the RAS subdomain solves.  8 independent DFMA chains per thread, full occupancy.
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 tools/fp64_peak.cu -o tools/fp64_peak
+#include <algorithm>
 #include <cstdio>
+#include <cstdlib>
+#include <vector>
 #include <cuda_runtime.h>
 
 __global__ void dfma_kernel(double* out, int iters, double a, double b) {
@@ -17,8 +20,9 @@ __global__ void dfma_kernel(double* out, int iters, double a, double b) {
   out[blockIdx.x * blockDim.x + threadIdx.x] = x0 + x1 + x2 + x3 + x4 + x5 + x6 + x7;
 }
 
-int main() {
+int main(int argc, char** argv) {
   int dev = 0, sms = 0, clk = 0;
+  const int reps = argc > 1 ? atoi(argv[1]) : 1;   // timed launches (best and median reported)
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, dev);
   const int threads = 256, blocks = sms * 8, iters = 4096;
@@ -28,14 +32,21 @@ int main() {
   cudaDeviceSynchronize();
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0); cudaEventCreate(&e1);
-  cudaEventRecord(e0);
-  dfma_kernel<<<blocks, threads>>>(out, iters, 0.999999, 1e-7);
-  cudaEventRecord(e1);
-  cudaEventSynchronize(e1);
-  float ms = 0; cudaEventElapsedTime(&ms, e0, e1);
+  std::vector<float> t(reps);
+  for (int r = 0; r < reps; ++r) {
+    cudaEventRecord(e0);
+    dfma_kernel<<<blocks, threads>>>(out, iters, 0.999999, 1e-7);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    cudaEventElapsedTime(&t[r], e0, e1);
+  }
+  std::sort(t.begin(), t.end());
   const double flops = 2.0 * 8 * 16 * (double)iters * threads * blocks;
-  printf("{\"fp64_dfma_tflops\": %.3f, \"sms\": %d, \"clock_mhz_attr\": %.0f, \"ms\": %.3f, "
+  const float best = t[0], med = t[reps / 2];
+  printf("{\"fp64_dfma_tflops\": %.3f, \"fp64_dfma_tflops_median\": %.3f, \"reps\": %d, "
+         "\"sms\": %d, \"clock_mhz_attr\": %.0f, \"ms_best\": %.3f, "
          "\"dfma_per_clk_per_sm_at_attr_clock\": %.1f}\n",
-         flops / ms / 1e9, sms, clk / 1e3, ms, flops / 2 / (ms * 1e-3) / sms / (clk * 1e3));
+         flops / best / 1e9, flops / med / 1e9, reps, sms, clk / 1e3, best,
+         flops / 2 / (best * 1e-3) / sms / (clk * 1e3));
   return 0;
 }
