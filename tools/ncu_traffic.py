@@ -2,8 +2,11 @@
 """Write the DRAM traffic per launch of the ncu --set full captures into a committed JSON file
 that bench.py reads for the roofline `traffic` fields.
 
-usage: python tools/ncu_traffic.py profiles/ncu_traffic.json gpurun_out/prof_*.ncu-rep
+usage: python tools/ncu_traffic.py profiles/ncu_traffic.json [workload=]gpurun_out/prof_*.ncu-rep
+Entries of captures given again are replaced; the others are kept.  A `workload=` prefix tags
+the capture's kernels with the bench workload they were taken on (bench.ncu_traffic matches it).
 """
+import os
 import csv
 import json
 import subprocess
@@ -33,9 +36,18 @@ def kernels(path):
 
 
 if __name__ == "__main__":
-    out = []
-    for p in sys.argv[2:]:
-        out.extend(kernels(p))
-    json.dump(out, open(sys.argv[1], "w"), indent=1)
-    for k in out:
+    path = sys.argv[1]
+    old = json.load(open(path)) if os.path.exists(path) else []
+    new = []
+    for arg in sys.argv[2:]:
+        wl, _, p = arg.rpartition("=")
+        ks = kernels(p)
+        for k in ks:
+            if wl:
+                k["workload"] = wl
+        new.extend(ks)
+    caps = {k["capture"] for k in new}
+    out = [k for k in old if k["capture"] not in caps] + new
+    json.dump(out, open(path, "w"), indent=1)
+    for k in new:
         print(f"{k['kernel'][:60]:60s} {k['traffic_bytes']/1e6:10.1f} MB {k['duration_s']*1e6:9.1f} us")

@@ -2,7 +2,7 @@
 per-apply time of the left-RAS apply on the cfg4 (128^3) and cfg5 (512^3) shapes, and the
 max relative difference of each variant's output against the column kernel's.
 
-usage: python tools/ras3_probe.py [128|512] [reps]
+usage: [RAS3_VARIANTS=col:2,cl2:1] python tools/ras3_probe.py [128|512] [reps]
 """
 import os
 import sys
@@ -21,7 +21,9 @@ shape = (n, n, n)
 a = -0.35 + 0.05 * (2 * torch.rand(shape, dtype=torch.float64, device="cuda", generator=g) - 1)
 v = torch.rand(shape, dtype=torch.float64, device="cuda", generator=g)
 ref = None
-for variant, nr in (("col", "2"), ("cl2", "1"), ("cl2", "2"), ("cl2", "3")):
+variants = [tuple(v.split(":")) for v in
+            os.environ.get("RAS3_VARIANTS", "col:2,cl2:1,cl2:2,cl2:3").split(",")]
+for variant, nr in variants:
     os.environ["PFC_RAS3D"] = variant
     os.environ["PFC_CL2_NR"] = nr
     ctx = P.Context(cfg, n=shape)
