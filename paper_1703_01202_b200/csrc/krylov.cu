@@ -10,6 +10,7 @@
 // Results are bitwise reproducible run to run.
 #include "pfc_device.cuh"
 #include "pfc_internal.h"
+#include "gmres_close.cuh"
 
 namespace {
 
@@ -41,49 +42,6 @@ __device__ __forceinline__ bool finalize_last_block(const double* partials, doub
   if (threadIdx.x < NV) out[threadIdx.x] = outv[threadIdx.x];
   if (threadIdx.x == 0) *ticket = 0u;    // ready for the next reduction on this stream
   return true;
-}
-
-// End of Arnoldi step j on the device (f1): Hessenberg column j = h1 + h2 (CGS2) and
-// h_{j+1,j} = ||w||, reduced by the previous Givens rotations and a new one, residual estimate
-// |g_{j+1}|, and the stopping decision of the host loop it replaces: non-finite,
-// happy breakdown h_{j+1,j} <= 1e-14 beta, ||r|| <= tol, its >= maxit, end of the cycle.
-__device__ void arnoldi_close(pfc_gmres_dev* gm, int j, const double* h1, const double* h2,
-                              double nrm2) {
-  const int m = gm->m, ld = m + 1;
-  double* H = gm->H;
-  const double hn = sqrt(nrm2);
-  for (int i = 0; i <= j; ++i) H[i + ld * j] = h1[i] + h2[i];
-  H[j + 1 + ld * j] = hn;
-  for (int i = 0; i < j; ++i) {
-    const double a = H[i + ld * j], b = H[i + 1 + ld * j];
-    H[i + ld * j] = gm->cs[i] * a + gm->sn[i] * b;
-    H[i + 1 + ld * j] = -gm->sn[i] * a + gm->cs[i] * b;
-  }
-  const double a = H[j + ld * j], b = H[j + 1 + ld * j];
-  const double r = sqrt(a * a + b * b);
-  const double c = r == 0.0 ? 1.0 : a / r, s = r == 0.0 ? 0.0 : b / r;
-  gm->cs[j] = c;
-  gm->sn[j] = s;
-  H[j + ld * j] = c * a + s * b;
-  H[j + 1 + ld * j] = 0.0;
-  gm->g[j + 1] = -s * gm->g[j];
-  gm->g[j] = c * gm->g[j];
-  gm->its += 1;
-  gm->jm = j + 1;
-  const double res = fabs(gm->g[j + 1]);
-  gm->res = res;
-  int reason = PFC_GM_RUNNING;
-  if (!isfinite(res)) reason = PFC_GM_NONFINITE;
-  else if (hn <= 1e-14 * gm->beta) reason = PFC_GM_HAPPY;
-  else {
-    gm->ihn = 1.0 / hn;
-    if (res <= gm->tol) reason = PFC_GM_CONVERGED;
-    else if (gm->its >= gm->maxit) reason = PFC_GM_MAXIT;
-    else if (j + 1 == m) reason = PFC_GM_RESTART;
-  }
-  gm->reason = reason;
-  __threadfence();
-  gm->stop = reason != PFC_GM_RUNNING;
 }
 
 struct Coef {

@@ -209,10 +209,14 @@ static pfc_status fgmres_host(pfc_ctx* ctx, double dt, double Fnorm, int* its_ou
       double* Vj = ctx->V + (size_t)j * N;
       double* Zj = ctx->Z + (size_t)j * N;
       KL(PFC_K_RAS, launch_ras(ctx, Vj, ctx->c, dt, Zj), "ras");
-      KL(PFC_K_JV, launch_jv(ctx, Zj, ctx->c, dt, ctx->w), "jv");
-      KL(PFC_K_ORTH, launch_multidot(ctx, ctx->V, j + 1, ctx->w, ctx->partials, ctx->dscal + SC_H1), "multidot");
-      KL(PFC_K_ORTH, launch_axpy_dot(ctx, ctx->V, j + 1, ctx->dscal + SC_H1, ctx->w, ctx->partials, ctx->dscal + SC_H2), "cgs2");
-      KL(PFC_K_ORTH, launch_axpy_norm(ctx, ctx->V, j + 1, ctx->dscal + SC_H2, ctx->w, ctx->partials, ctx->dscal + SC_NRM), "cgs2");
+      if (ctx->tail) {   // w = J z_j, CGS2 and v_{j+1} = w/|w| in one cooperative kernel
+        KL(PFC_K_ORTH, launch_arnoldi_tail(ctx, ctx->V, Zj, ctx->c, dt, j, ctx->V + (size_t)(j + 1) * N, ctx->dscal), "arnoldi tail");
+      } else {
+        KL(PFC_K_JV, launch_jv(ctx, Zj, ctx->c, dt, ctx->w), "jv");
+        KL(PFC_K_ORTH, launch_multidot(ctx, ctx->V, j + 1, ctx->w, ctx->partials, ctx->dscal + SC_H1), "multidot");
+        KL(PFC_K_ORTH, launch_axpy_dot(ctx, ctx->V, j + 1, ctx->dscal + SC_H1, ctx->w, ctx->partials, ctx->dscal + SC_H2), "cgs2");
+        KL(PFC_K_ORTH, launch_axpy_norm(ctx, ctx->V, j + 1, ctx->dscal + SC_H2, ctx->w, ctx->partials, ctx->dscal + SC_NRM), "cgs2");
+      }
       pfc_status s = fetch(ctx, 0, SC_NRM + 1);
       if (s) return s;
       const double* h1 = ctx->hscal + SC_H1;
@@ -238,7 +242,8 @@ static pfc_status fgmres_host(pfc_ctx* ctx, double dt, double Fnorm, int* its_ou
       const double res = fabs(g[j + 1]);
       if (!isfinite(res)) return pfc_fail(ctx, PFC_EBREAKDOWN, "FGMRES: non-finite residual");
       if (hn <= 1e-14 * beta) { stop = true; break; }           // happy breakdown
-      KL(PFC_K_VECTOR, launch_axpby(ctx, 1.0 / hn, ctx->w, 0.0, nullptr, ctx->V + (size_t)(j + 1) * N), "scale");
+      if (!ctx->tail)   // (the fused tail has written v_{j+1} already)
+        KL(PFC_K_VECTOR, launch_axpby(ctx, 1.0 / hn, ctx->w, 0.0, nullptr, ctx->V + (size_t)(j + 1) * N), "scale");
       if (res <= tol || its >= c.gmres_maxit) { stop = true; break; }
     }
     for (int i = jm - 1; i >= 0; --i) {
@@ -288,12 +293,16 @@ static pfc_status fgmres_device(pfc_ctx* ctx, double dt, double Fnorm, int* its_
       double* Vj = ctx->V + (size_t)j * N;
       double* Zj = ctx->Z + (size_t)j * N;
       KL(PFC_K_RAS, launch_ras(ctx, Vj, ctx->c, dt, Zj), "ras");
-      KL(PFC_K_JV, launch_jv(ctx, Zj, ctx->c, dt, ctx->w), "jv");
-      KL(PFC_K_ORTH, launch_multidot(ctx, ctx->V, j + 1, ctx->w, ctx->partials, ctx->dscal + SC_H1), "multidot");
-      KL(PFC_K_ORTH, launch_axpy_dot(ctx, ctx->V, j + 1, ctx->dscal + SC_H1, ctx->w, ctx->partials, ctx->dscal + SC_H2), "cgs2");
-      KL(PFC_K_ORTH, launch_axpy_norm_close(ctx, ctx->V, j + 1, ctx->dscal + SC_H1, ctx->dscal + SC_H2, ctx->w, ctx->partials, ctx->dscal + SC_NRM), "cgs2");
-      if (j + 1 < m)
-        KL(PFC_K_VECTOR, launch_scale_next(ctx, ctx->w, ctx->V + (size_t)(j + 1) * N), "scale");
+      if (ctx->tail) {   // J z, CGS2, v_{j+1} and the device Givens / stop test in one kernel
+        KL(PFC_K_ORTH, launch_arnoldi_tail(ctx, ctx->V, Zj, ctx->c, dt, j, ctx->V + (size_t)(j + 1) * N, ctx->dscal, ctx->gm), "arnoldi tail");
+      } else {
+        KL(PFC_K_JV, launch_jv(ctx, Zj, ctx->c, dt, ctx->w), "jv");
+        KL(PFC_K_ORTH, launch_multidot(ctx, ctx->V, j + 1, ctx->w, ctx->partials, ctx->dscal + SC_H1), "multidot");
+        KL(PFC_K_ORTH, launch_axpy_dot(ctx, ctx->V, j + 1, ctx->dscal + SC_H1, ctx->w, ctx->partials, ctx->dscal + SC_H2), "cgs2");
+        KL(PFC_K_ORTH, launch_axpy_norm_close(ctx, ctx->V, j + 1, ctx->dscal + SC_H1, ctx->dscal + SC_H2, ctx->w, ctx->partials, ctx->dscal + SC_NRM), "cgs2");
+        if (j + 1 < m)
+          KL(PFC_K_VECTOR, launch_scale_next(ctx, ctx->w, ctx->V + (size_t)(j + 1) * N), "scale");
+      }
       CK(cudaMemcpyAsync(ctx->hflags + 4 * j, &ctx->gm->stop, 4 * sizeof(int),
                          cudaMemcpyDeviceToHost, ctx->stream), "D2H flags");
       CK(cudaEventRecord(ctx->step_ev[j], ctx->stream), "event");
@@ -333,8 +342,13 @@ static pfc_status fgmres_device(pfc_ctx* ctx, double dt, double Fnorm, int* its_
 // (2-3 Arnoldi steps per Newton iteration at the configs' dt), so the early-exit kernels of the
 // one speculative step per cycle cost more than the ~5 us host round trips they remove.
 // PFC_DEVICE_ARNOLDI=1 selects fgmres_device (same results to rounding; parity-tested).
+// With the fused Arnoldi tail (2D grids of configs 1-3) an Arnoldi step is two kernels; the
+// device-resident cycle then measured 479 vs 473 steps/s on cfg1 and 418 vs 430 on cfg2
+// (round 2, bench.py): still not worth its speculative launches, so it stays opt-in
+// (PFC_DEVICE_ARNOLDI=1; it uses the fused tail where the host loop does).
 static pfc_status fgmres(pfc_ctx* ctx, double dt, double Fnorm, int* its_out) {
-  static const bool dev = getenv("PFC_DEVICE_ARNOLDI") != nullptr;
+  const char* e = getenv("PFC_DEVICE_ARNOLDI");
+  const bool dev = e && e[0] != '0';
   return dev ? fgmres_device(ctx, dt, Fnorm, its_out) : fgmres_host(ctx, dt, Fnorm, its_out);
 }
 
@@ -539,7 +553,8 @@ pfc_status pfc_create(const pfc_config* cfg, void* stream, pfc_ctx** out) {
   size_t tiles = 0;
   if (c.ndim == 2) tiles = (size_t)((c.n[0] + 31) / 32) * ((c.n[1] + 15) / 16);
   else tiles = (size_t)((c.n[0] + 31) / 32) * ((c.n[1] + 15) / 16) * (size_t)c.n[2];
-  ctx->npartials = std::max<size_t>(tiles, (size_t)blas_nblocks(ctx->N) * 32) + 64;
+  ctx->npartials = std::max<size_t>(std::max<size_t>(tiles, (size_t)blas_nblocks(ctx->N) * 32),
+                                    (size_t)4096 * 40) + 64;   // (fused tail: blocks x 40)
   if (pfc_check_cuda(ctx, cudaMalloc(&ctx->partials, ctx->npartials * sizeof(double)), "partials") ||
       pfc_check_cuda(ctx, cudaMalloc(&ctx->dscal, SC_TOTAL * sizeof(double)), "dscal") ||
       pfc_check_cuda(ctx, cudaMalloc(&ctx->ticket, sizeof(unsigned int)), "ticket") ||
@@ -568,6 +583,7 @@ pfc_status pfc_create(const pfc_config* cfg, void* stream, pfc_ctx** out) {
     if (pfc_check_cuda(ctx, cudaMalloc(&ctx->ras_scratch, d * sizeof(double)), "ras scratch"))
       return fail(PFC_ENOMEM);
   }
+  ctx->tail = tail_enabled(ctx);
   ctx->step_ev.resize(PFC_MAX_RESTART);
   for (auto& e : ctx->step_ev)
     if (pfc_check_cuda(ctx, cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "events"))

@@ -75,6 +75,7 @@ struct pfc_ctx {
   int ras_threads = 0;
   int ras_cluster = 1;
   int ras_rows = 0;
+  int tail = 0;            // 2D small grids: fused J v + CGS2 + next vector (tail2d.cu)
   int ras3_col = 0;        // 3D: 2 = 2-CTA cluster kernel (ras3d_cl2.cu), 1 = column kernel
                            // (ras3d_col.cu), 0 = global-scratch kernel (ras3d.cu)
 
@@ -168,6 +169,12 @@ cudaError_t launch_ras_3d_cl2(pfc_ctx*, const double* v, const double* c, double
                               double* scratch);
 cudaError_t launch_ras_3d_col(pfc_ctx*, const double* v, const double* c, double dt, double* z,
                               double* scratch);
+
+// fused Arnoldi tail (tail2d.cu): w = J z, CGS2, v_{j+1} = w/|w| in one cooperative kernel
+int tail_enabled(pfc_ctx* ctx);
+cudaError_t launch_arnoldi_tail(pfc_ctx* ctx, const double* V, const double* z, const double* c,
+                                double dt, int j, double* vnext, double* out,
+                                pfc_gmres_dev* gm = nullptr);
 
 // Krylov / pointwise (krylov.cu)
 int blas_nblocks(size_t N);
