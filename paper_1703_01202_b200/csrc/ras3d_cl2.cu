@@ -40,6 +40,21 @@
 
 #include <type_traits>
 
+// diagnostic builds only (tools: PFC_EXTRA_NVCC_FLAGS=-DCL2_DIAG=n, results WRONG): bit 0 skips
+// the stencil, bit 1 skips the CGS2 vector arithmetic (the reductions still run)
+#ifndef CL2_DIAG
+#define CL2_DIAG 0
+#endif
+// phase timing of CTA 0's thread 0 (diagnostic builds with -DCL2_PROF; tools/ras3_probe.py)
+#ifdef CL2_PROF
+__device__ long long cl2_prof[16];
+__device__ long long cl2_prof_last;
+#define C2P(i) do { if (blockIdx.x == 0 && threadIdx.x == 0) { long long t_ = clock64(); \
+    cl2_prof[i] += t_ - cl2_prof_last; cl2_prof_last = t_; } } while (0)
+#else
+#define C2P(i) do {} while (0)
+#endif
+
 namespace {
 
 constexpr int RS = 12;   // reduction slot stride (>= K + 1 values)
@@ -137,7 +152,7 @@ __device__ __forceinline__ void cl2_put(double s, int i, double* redb, uint32_t 
   if (lane == 0) {
     const int off = (rank * NW + wid) * RS + i;
     redb[off] = s;
-    st_async(redb_rem + off * 8u, s, mbar_rem);
+    if (!(CL2_DIAG & 4)) st_async(redb_rem + off * 8u, s, mbar_rem);
   }
 }
 
@@ -156,7 +171,7 @@ __device__ __forceinline__ void cl2_rs_put(const double (&acc)[16], int nv, doub
   if ((lane & ((1 << SH) - 1)) == 0 && vi < nv) {
     const int off = (rank * NW + wid) * RS + vi;
     redb[off] = s;
-    st_async(redb_rem + off * 8u, s, mbar_rem);
+    if (!(CL2_DIAG & 4)) st_async(redb_rem + off * 8u, s, mbar_rem);
   }
 }
 template <int NW>
@@ -342,13 +357,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cl2<E>::NT, 1)
     fence_mbar_init();
   }
   cl_sync();   // the partner is running, zeroed and its mbarriers initialised before any DSMEM store
+#ifdef CL2_PROF
+  if (blockIdx.x == 0 && tid == 0) cl2_prof_last = clock64();
+#endif
   uint32_t ph = 0;   // phase parity bits: bit q for mbar[q]
   constexpr uint32_t HALO_BYTES = (uint32_t)PL * 3u * 8u;
   // one cluster reduction: warp partials are in both CTAs (cl2_put); arm, sync, wait, sum
   auto reduce = [&](int nsent, int nget, double* hwv) {
-    if (tid == 0) mbar_expect_tx(&mbar[rb], (uint32_t)(NW * nsent * 8));
+    if (!(CL2_DIAG & 4) && tid == 0) mbar_expect_tx(&mbar[rb], (uint32_t)(NW * nsent * 8));
     __syncthreads();
-    mbar_wait_cluster(&mbar[rb], (ph >> rb) & 1u);
+    if (!(CL2_DIAG & 4)) mbar_wait_cluster(&mbar[rb], (ph >> rb) & 1u);
     ph ^= 1u << rb;
     cl2_get<NW>(nget, red + rb * 2 * NW * RS, hwv, lane);
     rb ^= 1;
@@ -387,8 +405,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cl2<E>::NT, 1)
     double* redb = red + rb * 2 * NW * RS;
     uint32_t redr = red_rem + (uint32_t)(rb * 2 * NW * RS) * 8u;
     uint32_t mbr = mbar_rem0 + 8u * rb;
+    C2P(0);   // gather v, c of the box
     cl2_put<NW>(acc, 0, redb, redr, mbr, rank, wid, lane);
     reduce(1, 1, hx);
+    C2P(1);   // beta reduction
     const double beta = sqrt(hx[0]);
     if (beta == 0.0) {
       if (act) {
@@ -451,20 +471,30 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cl2<E>::NT, 1)
 #pragma unroll 1
     for (int j = 0; j < K; ++j) {
       // ---- w = A_k v_j: own planes while the partner's halo planes are in flight
+      C2P(10);  // put_v / loop top
       if (tid == 0) mbar_expect_tx(&mbar[2], HALO_BYTES);
       __syncthreads();
+      C2P(2);   // step barrier
       // the Givens lane turns column j-1 while the node warps run the stencil (its h1, h2
       // copies of step j-1 are overwritten only by this step's reductions)
       if (g0 && j > 0) givens_col(j - 1, h1, h2, hn_prev, H, cs, sn, gv, K + 1);
 #pragma unroll
       for (int zl = 0; zl < ZL; ++zl) w[zl] = 0.0;
-      if (act) cl2_stencil<E, 0, ZL>(p, pv, pc, w);
+      if (act && !(CL2_DIAG & 1)) cl2_stencil<E, 0, ZL>(p, pv, pc, w);
+      if (CL2_DIAG & 1) {
+#pragma unroll
+        for (int zl = 0; zl < ZL; ++zl) w[zl] = pv[zl * PP] * (1.0 + 0.01 * zl);
+      }
+      C2P(3);   // stencil, own planes
       mbar_wait_cluster(&mbar[2], (ph >> 2) & 1u);
       ph ^= 4u;
+      C2P(4);   // halo wait
       if (act) {
-        if (rank == 0) cl2_stencil<E, ZL, ZL + 3>(p, pv, pc, w);
+        if (CL2_DIAG & 1) {
+        } else if (rank == 0) cl2_stencil<E, ZL, ZL + 3>(p, pv, pc, w);
         else cl2_stencil<E, -3, 0>(p, pv, pc, w);
       }
+      C2P(5);   // stencil, halo planes
       // ---- CGS2 on w (Arnoldi step j dispatched to code specialised for J = j: every basis
       // index compile-time, no per-node guards)
       double hn2 = 0.0;
@@ -484,7 +514,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cl2<E>::NT, 1)
               const double wz = w[zl];
 #pragma unroll
               for (int i = 0; i <= J; ++i)
-                acc[i] = fma(V(i, zl), wz, acc[i]);
+                acc[i] = (CL2_DIAG & 2) ? wz : fma(V(i, zl), wz, acc[i]);
             }
           }
           cl2_put_multi<NW>(acc, J + 1, redb, redr, mbr, rank, wid, lane);
@@ -506,10 +536,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cl2<E>::NT, 1)
               double ww = w[zl];
 #pragma unroll
               for (int i = 0; i <= J; ++i)
-                ww = fma(-hv[i], V(i, zl), ww);
+                ww = (CL2_DIAG & 2) ? ww : fma(-hv[i], V(i, zl), ww);
 #pragma unroll
               for (int i = 0; i <= J; ++i)
-                acc[i] = fma(V(i, zl), ww, acc[i]);
+                acc[i] = (CL2_DIAG & 2) ? ww : fma(V(i, zl), ww, acc[i]);
               nrm = fma(ww, ww, nrm);
               w[zl] = ww;
             }
@@ -531,7 +561,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cl2<E>::NT, 1)
             double ww = w[zl];
 #pragma unroll
             for (int i = 0; i <= J; ++i)
-              ww = fma(-hv[i], V(i, zl), ww);
+              ww = (CL2_DIAG & 2) ? ww : fma(-hv[i], V(i, zl), ww);
             w[zl] = ww;
           }
         }
@@ -553,7 +583,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cl2<E>::NT, 1)
         return hn2;
       };
       dispatch_j<K>(j, cgs2);
-      const double hn = sqrt(hn2 > 0.0 ? hn2 : 0.0);
+      C2P(6);   // CGS2 (three passes, two or three reductions)
+      const double hn = CL2_DIAG ? 1.0 : sqrt(hn2 > 0.0 ? hn2 : 0.0);
       hn_prev = hn;
       jm = j + 1;
       if (hn <= 1e-14 * beta) break;                 // exact breakdown (identical on both CTAs)
@@ -564,6 +595,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cl2<E>::NT, 1)
         put_v(j + 1);
       }
     }
+    C2P(10);
     if (g0) {   // last Hessenberg column, then back substitution R yv = g
       const int ld = K + 1;
       givens_col(jm - 1, h1, h2, hn_prev, H, cs, sn, gv, ld);
@@ -575,6 +607,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cl2<E>::NT, 1)
       if (rank == 0) ras_count(p.jcnt, jm);
     }
     __syncthreads();
+    C2P(7);   // Givens / back substitution (waiting for the Givens warp)
     if (act) {
       double yl[ZL];
 #pragma unroll
@@ -597,6 +630,464 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cl2<E>::NT, 1)
         }
       }
     }
+    C2P(9);   // final V y and the output stores
+  }
+  C2P(8);
+  cl_sync();   // no CTA leaves while its partner may still address its shared memory
+}
+
+// ============================================================================================
+// Two columns per thread (CP = 2): thread t < E^2/2 owns the z-columns (x, y0) and (x, y0+1),
+// x = t % E, y0 = 2 (t / E), of its CTA's z-half.  The 63-point stencils of the two columns
+// read the union of their radius-3 diamonds, 32 neighbour columns instead of 2 x 25, so the
+// shared-memory traffic of the stencil (the bound of the one-column kernel: ~90% of the
+// shared-memory bandwidth while the stencil runs) falls by ~35%; 7 node warps + the Givens
+// warp, up to 255 registers per thread, which holds NR basis vectors of both columns.
+// Layouts (linear thread order, conflict-free because a half-warp spans at most two row pairs
+// and 2 PX = E (mod 16)): v_j planes padded to PX x (E+6), c' planes padded to CX x (E+2).
+template <int E>
+struct Cl2p {
+  static constexpr int ZL = E / 2, PL = E * E;
+  static constexpr int NTN = PL / 2;                 // node threads
+  static constexpr int NWN = (NTN + 31) / 32;        // node warps
+  static constexpr int NW = NWN + 1;                 // + the Givens warp
+  static constexpr int NT = NW * 32;
+  // smallest pitch >= w with 2 pitch = E (mod 16)
+  static constexpr int pitch(int w) {
+    int q = w;
+    while (((2 * q - E) % 16 + 16) % 16 != 0) ++q;
+    return q;
+  }
+  static constexpr int PX = pitch(E + 6), PP = PX * (E + 6);   // v_j plane
+  static constexpr int CX = pitch(E + 2), CP = CX * (E + 2);   // c' plane
+  static constexpr int NVB = ZL + 3, NCB = ZL + 1;
+};
+
+template <int K, int NRX>
+struct Cl2pK {
+  static constexpr int NR = (K - 1) < NRX ? (K - 1) : NRX;
+  static constexpr int NS = (K - 1 - NR) < 3 ? (K - 1 - NR) : 3;
+  static constexpr int NG = K - 1 - NR - NS;
+};
+
+template <int K, int E, int NRX>
+constexpr size_t cl2p_smem_doubles() {
+  using C = Cl2p<E>;
+  return (size_t)C::NVB * C::PP + (size_t)C::NCB * C::CP +
+         (size_t)Cl2pK<K, NRX>::NS * 2 * C::ZL * C::NTN + 2 * 2 * C::NW * RS + C::NW * 3 * RS;
+}
+
+// group of union column (dx, du) for output o (dy = du - o): 0 own, 1 R1, 2 R2 axis,
+// 3 R2 diagonal, 4 R3 axis, 5 R3 off-axis, -1 none
+__host__ __device__ constexpr int cl2p_group(int o, int dx, int du) {
+  const int dy = du - o;
+  const int ax = dx < 0 ? -dx : dx, ay = dy < 0 ? -dy : dy, r = ax + ay;
+  return r == 0 ? 0 : r == 1 ? 1 : r == 2 ? ((ax == 0 || ay == 0) ? 2 : 3)
+         : r == 3 ? ((ax == 0 || ay == 0) ? 4 : 5) : -1;
+}
+__host__ __device__ constexpr int cl2p_reach(int g) {
+  return g == 0 ? 3 : g == 1 ? 2 : (g == 2 || g == 3) ? 1 : 0;
+}
+
+template <int E, int LO, int HI>
+__device__ __forceinline__ void cl2p_stencil(const Ras3Cl2Args& p, const double* pv,
+                                             const double* pc, double (&out)[2][E / 2]) {
+  using C = Cl2p<E>;
+  constexpr int ZL = C::ZL, PX = C::PX, PP = C::PP, CX = C::CX, CP = C::CP;
+  const double W0 = p.W[0], W1 = p.W[1], W2 = p.W[2], W3 = p.W[3], W4 = p.W[4], W5 = p.W[5],
+               W6 = p.W[6];
+#pragma unroll
+  for (int zz = (LO > -3 ? LO : -3); zz < (HI < ZL + 3 ? HI : ZL + 3); ++zz) {
+    double g[2][6], cvn[2], cvo[2];
+#pragma unroll
+    for (int o = 0; o < 2; ++o) {
+      cvn[o] = 0.0;
+      cvo[o] = 0.0;
+#pragma unroll
+      for (int k = 0; k < 6; ++k) g[o][k] = 0.0;
+    }
+#pragma unroll
+    for (int dx = -3; dx <= 3; ++dx) {
+#pragma unroll
+      for (int du = -3; du <= 4; ++du) {
+        bool need = false;
+#pragma unroll
+        for (int o = 0; o < 2; ++o) {
+          const int k = cl2p_group(o, dx, du);
+          if (k >= 0 && zz >= -cl2p_reach(k) && zz < ZL + cl2p_reach(k)) need = true;
+        }
+        if (!need) continue;
+        const double val = pv[zz * PP + dx + PX * du];
+#pragma unroll
+        for (int o = 0; o < 2; ++o) {
+          const int k = cl2p_group(o, dx, du);
+          if (k < 0 || zz < -cl2p_reach(k) || zz >= ZL + cl2p_reach(k)) continue;
+          g[o][k] += val;
+          // -Delta(c v): the xy neighbours at dz = 0 and the own column (c' = -c/h^2; v = 0
+          // outside the box, so the finite c' read there is inert)
+          if (k == 1 && zz >= 0 && zz < ZL) cvn[o] = fma(pc[zz * CP + dx + CX * du], val, cvn[o]);
+          if (k == 0 && zz >= -1 && zz <= ZL) cvo[o] = pc[zz * CP + CX * o] * val;
+        }
+      }
+    }
+#pragma unroll
+    for (int o = 0; o < 2; ++o) {
+#pragma unroll
+      for (int z = (zz - 3 > 0 ? zz - 3 : 0); z <= (zz + 3 < ZL - 1 ? zz + 3 : ZL - 1); ++z) {
+        const int dz = zz > z ? zz - z : z - zz;
+        out[o][z] = fma(dz == 0 ? W0 : dz == 1 ? W1 : dz == 2 ? W2 : W4, g[o][0], out[o][z]);
+        if (dz <= 2) out[o][z] = fma(dz == 0 ? W1 : dz == 1 ? W3 : W5, g[o][1], out[o][z]);
+        if (dz <= 1) {
+          out[o][z] = fma(dz == 0 ? W2 : W5, g[o][2], out[o][z]);
+          out[o][z] = fma(dz == 0 ? W3 : W6, g[o][3], out[o][z]);
+        }
+        if (dz == 0) {
+          out[o][z] = fma(W4, g[o][4], out[o][z]);
+          out[o][z] = fma(W5, g[o][5], out[o][z]);
+        }
+      }
+      if (zz >= 0 && zz < ZL) out[o][zz] += cvn[o];
+      if (zz >= -1 && zz <= ZL) {
+        if (zz - 1 >= 0 && zz - 1 < ZL) out[o][zz - 1] += cvo[o];
+        if (zz + 1 >= 0 && zz + 1 < ZL) out[o][zz + 1] += cvo[o];
+        if (zz >= 0 && zz < ZL) out[o][zz] = fma(-6.0, cvo[o], out[o][zz]);
+      }
+    }
+  }
+}
+
+template <int K, int E, int NRX>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cl2p<E>::NT, 1)
+    ras3d_cl2p_kernel(const __grid_constant__ Ras3Cl2Args p) {
+  if (p.gate && *p.gate) return;     // uniform over the cluster: both CTAs leave at once
+  using C = Cl2p<E>;
+  constexpr int ZL = C::ZL, PL = C::PL, NW = C::NW, NTN = C::NTN;
+  constexpr int PX = C::PX, PP = C::PP, CX = C::CX, CP = C::CP, NVB = C::NVB, NCB = C::NCB;
+  constexpr int NR = Cl2pK<K, NRX>::NR, NS = Cl2pK<K, NRX>::NS, NG = Cl2pK<K, NRX>::NG;
+  constexpr int NE = E * E * E;
+  extern __shared__ __align__(128) double smem_dyn[];
+  double* vb = smem_dyn;                 // NVB padded planes of v_j (rank 0: zl in [0, ZL+3),
+                                         // rank 1: [-3, ZL))
+  double* cb = vb + NVB * PP;            // NCB padded planes of c' (rank 0: [0, ZL], rank 1:
+                                         // [-1, ZL))
+  double* vs = cb + NCB * CP;            // NS x [col][zl][thread]: basis vectors NR..NR+NS-1
+  double* red = vs + NS * 2 * ZL * NTN;  // 2 buffers x [rank][warp][RS]
+  double* hw = red + 2 * 2 * NW * RS;    // per warp: h1, h2, scratch
+  __shared__ double H[(K + 1) * K];
+  __shared__ double gv[K + 1], cs[K], sn[K], yv[K];
+  __shared__ __align__(8) uint64_t mbar[3];
+
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const bool g0 = wid == NW - 1 && lane == 0;
+  const int rank = (int)cluster_rank(), partner = rank ^ 1;
+  const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+  const bool act = tid < NTN;
+  const int x = act ? tid % E : 0, y0 = act ? 2 * (tid / E) : 0;
+  const int colp = (y0 + 3) * PX + (x + 3);        // padded v column of (x, y0)
+  const int colc = (y0 + 1) * CX + (x + 1);        // padded c' column of (x, y0)
+  const int pv0 = rank == 0 ? 0 : 3, pc0 = rank == 0 ? 0 : 1;   // plane of zl = 0
+  const double* pv = vb + pv0 * PP + colp;
+  const double* pc = cb + pc0 * CP + colc;
+  double* gs = p.gscr + (size_t)blockIdx.x * (NG > 0 ? NG : 1) * 2 * ZL * NTN + tid;
+  double* h1 = hw + wid * 3 * RS;
+  double* h2 = h1 + RS;
+  double* hx = h2 + RS;
+  const uint32_t red_rem = mapa_rank(smem_u32(red), (uint32_t)partner);
+  const uint32_t vb_rem = mapa_rank(smem_u32(vb), (uint32_t)partner);
+  const int nbx = p.nx / p.bx, nby = p.ny / p.by, nbz = p.nz / p.bz;
+  const int nboxes = nbx * nby * nbz;
+  const size_t NX = p.nx, NXY = (size_t)p.nx * p.ny;
+
+  int rb = 0;
+  const uint32_t mbar_rem0 = mapa_rank(smem_u32(&mbar[0]), (uint32_t)partner);
+  for (int q = tid; q < NVB * PP + NCB * CP; q += blockDim.x) vb[q] = 0.0;
+  if (tid == 0) {
+    for (int q = 0; q < 3; ++q) mbar_init(&mbar[q], 1);
+    fence_mbar_init();
+  }
+  cl_sync();   // the partner is running, zeroed and its mbarriers initialised before any DSMEM store
+  uint32_t ph = 0;
+  constexpr uint32_t HALO_BYTES = (uint32_t)PL * 3u * 8u;
+  auto reduce = [&](int nsent, int nget, double* hwv) {
+    if (tid == 0) mbar_expect_tx(&mbar[rb], (uint32_t)(NW * nsent * 8));
+    __syncthreads();
+    mbar_wait_cluster(&mbar[rb], (ph >> rb) & 1u);
+    ph ^= 1u << rb;
+    cl2_get<NW>(nget, red + rb * 2 * NW * RS, hwv, lane);
+    rb ^= 1;
+  };
+
+  double vr[NR > 0 ? NR : 1][2][ZL];
+#pragma unroll
+  for (int s = 0; s < (NR > 0 ? NR : 1); ++s)
+#pragma unroll
+    for (int c = 0; c < 2; ++c)
+#pragma unroll
+      for (int zl = 0; zl < ZL; ++zl) vr[s][c][zl] = 0.0;
+  for (int box = cid; box < nboxes; box += ncl) {
+    const int ibx = box % nbx, iby = (box / nbx) % nby, ibz = box / (nbx * nby);
+    const int gx0 = ibx * p.bx - p.o, gy0 = iby * p.by - p.o, gz0 = ibz * p.bz - p.o;
+    const int ez0 = rank * ZL;
+    double w[2][ZL];
+    double acc = 0.0;
+    if (act) {
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        const int y = y0 + c;
+        const size_t gxy = (size_t)wrapi(gx0 + x, p.nx) + NX * wrapi(gy0 + y, p.ny);
+        const bool oxy = x >= p.o && x < p.o + p.bx && y >= p.o && y < p.o + p.by;
+#pragma unroll
+        for (int zl = 0; zl < ZL; ++zl) {
+          const size_t g = gxy + NXY * wrapi(gz0 + ez0 + zl, p.nz);
+          const int ez = ez0 + zl;
+          const bool owned = oxy && ez >= p.o && ez < p.o + p.bz;
+          w[c][zl] = (p.restrict_owned && !owned) ? 0.0 : p.v[g];
+          cb[(zl + pc0) * CP + colc + c * CX] = -p.ih2 * p.c[g];
+          acc = fma(w[c][zl], w[c][zl], acc);
+        }
+        const int zh = rank == 0 ? ZL : -1;
+        cb[(zh + pc0) * CP + colc + c * CX] =
+            -p.ih2 * p.c[gxy + NXY * wrapi(gz0 + ez0 + zh, p.nz)];
+      }
+    } else {
+#pragma unroll
+      for (int c = 0; c < 2; ++c)
+#pragma unroll
+        for (int zl = 0; zl < ZL; ++zl) w[c][zl] = 0.0;
+    }
+    double* redb = red + rb * 2 * NW * RS;
+    uint32_t redr = red_rem + (uint32_t)(rb * 2 * NW * RS) * 8u;
+    uint32_t mbr = mbar_rem0 + 8u * rb;
+    cl2_put<NW>(acc, 0, redb, redr, mbr, rank, wid, lane);
+    reduce(1, 1, hx);
+    const double beta = sqrt(hx[0]);
+    if (beta == 0.0) {
+      if (act) {
+#pragma unroll
+        for (int c = 0; c < 2; ++c)
+#pragma unroll
+          for (int zl = 0; zl < ZL; ++zl) {
+            const int y = y0 + c;
+            const int ez = ez0 + zl, li = x - p.o, lj = y - p.o, lk = ez - p.o;
+            if (p.y_ext) p.y_ext[(size_t)box * NE + (ez * E + y) * E + x] = 0.0;
+            else if (li >= 0 && li < p.bx && lj >= 0 && lj < p.by && lk >= 0 && lk < p.bz)
+              p.z[(size_t)(ibx * p.bx + li) + NX * (iby * p.by + lj) + NXY * (ibz * p.bz + lk)] = 0.0;
+          }
+      }
+      if (tid == 0 && rank == 0) ras_count(p.jcnt, 0);
+      continue;
+    }
+    auto put_v = [&](int slot) {
+      if (!act) return;
+#pragma unroll
+      for (int s = 0; s < NR; ++s)
+        if (s == slot) {
+#pragma unroll
+          for (int c = 0; c < 2; ++c)
+#pragma unroll
+            for (int zl = 0; zl < ZL; ++zl) vr[s][c][zl] = w[c][zl];
+        }
+      if (slot >= NR && slot < NR + NS) {
+#pragma unroll
+        for (int c = 0; c < 2; ++c)
+#pragma unroll
+          for (int zl = 0; zl < ZL; ++zl)
+            vs[(((slot - NR) * 2 + c) * ZL + zl) * NTN + tid] = w[c][zl];
+      } else if (slot >= NR + NS && slot < K - 1) {
+#pragma unroll
+        for (int c = 0; c < 2; ++c)
+#pragma unroll
+          for (int zl = 0; zl < ZL; ++zl)
+            gs[(((slot - NR - NS) * 2 + c) * ZL + zl) * NTN] = w[c][zl];
+      }
+#pragma unroll
+      for (int c = 0; c < 2; ++c)
+#pragma unroll
+        for (int zl = 0; zl < ZL; ++zl) vb[(zl + pv0) * PP + colp + c * PX] = w[c][zl];
+      const uint32_t hm = mbar_rem0 + 16u;
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        if (rank == 0) {
+#pragma unroll
+          for (int q = 0; q < 3; ++q)
+            st_async(vb_rem + (uint32_t)(q * PP + colp + c * PX) * 8u, w[c][ZL - 3 + q], hm);
+        } else {
+#pragma unroll
+          for (int q = 0; q < 3; ++q)
+            st_async(vb_rem + (uint32_t)((ZL + q) * PP + colp + c * PX) * 8u, w[c][q], hm);
+        }
+      }
+    };
+    auto V = [&](int i, int c, int zl) -> double {
+      if (i < NR) return vr[i < NR ? i : 0][c][zl];
+      if (i < NR + NS) return vs[(((i - NR) * 2 + c) * ZL + zl) * NTN + tid];
+      if (i < K - 1) return gs[(((i - NR - NS) * 2 + c) * ZL + zl) * NTN];
+      return pv[zl * PP + c * PX];
+    };
+    {
+      const double ib = 1.0 / beta;
+#pragma unroll
+      for (int c = 0; c < 2; ++c)
+#pragma unroll
+        for (int zl = 0; zl < ZL; ++zl) w[c][zl] *= ib;
+      put_v(0);
+    }
+    if (g0) gv[0] = beta;
+    int jm = 0;
+    double hn_prev = 0.0;
+#pragma unroll 1
+    for (int j = 0; j < K; ++j) {
+      if (tid == 0) mbar_expect_tx(&mbar[2], HALO_BYTES);
+      __syncthreads();
+      if (g0 && j > 0) givens_col(j - 1, h1, h2, hn_prev, H, cs, sn, gv, K + 1);
+#pragma unroll
+      for (int c = 0; c < 2; ++c)
+#pragma unroll
+        for (int zl = 0; zl < ZL; ++zl) w[c][zl] = 0.0;
+      if (act) cl2p_stencil<E, 0, ZL>(p, pv, pc, w);
+      mbar_wait_cluster(&mbar[2], (ph >> 2) & 1u);
+      ph ^= 4u;
+      if (act) {
+        if (rank == 0) cl2p_stencil<E, ZL, ZL + 3>(p, pv, pc, w);
+        else cl2p_stencil<E, -3, 0>(p, pv, pc, w);
+      }
+      double hn2 = 0.0;
+      auto cgs2 = [&](auto Jc) {
+        constexpr int J = decltype(Jc)::value;
+        redb = red + rb * 2 * NW * RS;
+        redr = red_rem + (uint32_t)(rb * 2 * NW * RS) * 8u;
+        mbr = mbar_rem0 + 8u * rb;
+        {
+          double acc[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) acc[i] = 0.0;
+          if (act) {
+#pragma unroll
+            for (int c = 0; c < 2; ++c)
+#pragma unroll
+              for (int zl = 0; zl < ZL; ++zl) {
+                const double wz = w[c][zl];
+#pragma unroll
+                for (int i = 0; i <= J; ++i) acc[i] = fma(V(i, c, zl), wz, acc[i]);
+              }
+          }
+          cl2_put_multi<NW>(acc, J + 1, redb, redr, mbr, rank, wid, lane);
+        }
+        reduce(J + 1, J + 1, h1);
+        redb = red + rb * 2 * NW * RS;
+        redr = red_rem + (uint32_t)(rb * 2 * NW * RS) * 8u;
+        mbr = mbar_rem0 + 8u * rb;
+        {
+          double hv[J + 1], acc[16], nrm = 0.0;
+#pragma unroll
+          for (int i = 0; i <= J; ++i) hv[i] = h1[i];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) acc[i] = 0.0;
+          if (act) {
+#pragma unroll
+            for (int c = 0; c < 2; ++c)
+#pragma unroll
+              for (int zl = 0; zl < ZL; ++zl) {
+                double ww = w[c][zl];
+#pragma unroll
+                for (int i = 0; i <= J; ++i) ww = fma(-hv[i], V(i, c, zl), ww);
+#pragma unroll
+                for (int i = 0; i <= J; ++i) acc[i] = fma(V(i, c, zl), ww, acc[i]);
+                nrm = fma(ww, ww, nrm);
+                w[c][zl] = ww;
+              }
+          }
+          cl2_put_multi<NW>(acc, J + 1, redb, redr, mbr, rank, wid, lane);
+          cl2_put<NW>(nrm, J + 1, redb, redr, mbr, rank, wid, lane);
+        }
+        reduce(J + 2, J + 2, h2);
+        double h2n = 0.0;
+        for (int i = 0; i <= J; ++i) h2n += h2[i] * h2[i];
+        const double wn2 = h2[J + 1];
+        if (act) {
+          double hv[J + 1];
+#pragma unroll
+          for (int i = 0; i <= J; ++i) hv[i] = h2[i];
+#pragma unroll
+          for (int c = 0; c < 2; ++c)
+#pragma unroll
+            for (int zl = 0; zl < ZL; ++zl) {
+              double ww = w[c][zl];
+#pragma unroll
+              for (int i = 0; i <= J; ++i) ww = fma(-hv[i], V(i, c, zl), ww);
+              w[c][zl] = ww;
+            }
+        }
+        if (h2n <= 1e-8 * wn2) {
+          hn2 = wn2 - h2n;
+        } else {
+          redb = red + rb * 2 * NW * RS;
+          redr = red_rem + (uint32_t)(rb * 2 * NW * RS) * 8u;
+          mbr = mbar_rem0 + 8u * rb;
+          double s = 0.0;
+          if (act) {
+#pragma unroll
+            for (int c = 0; c < 2; ++c)
+#pragma unroll
+              for (int zl = 0; zl < ZL; ++zl) s = fma(w[c][zl], w[c][zl], s);
+          }
+          cl2_put<NW>(s, 0, redb, redr, mbr, rank, wid, lane);
+          reduce(1, 1, hx);
+          hn2 = hx[0];
+        }
+        return hn2;
+      };
+      dispatch_j<K>(j, cgs2);
+      const double hn = sqrt(hn2 > 0.0 ? hn2 : 0.0);
+      hn_prev = hn;
+      jm = j + 1;
+      if (hn <= 1e-14 * beta) break;
+      if (j + 1 < K) {
+        const double ihn = 1.0 / hn;
+#pragma unroll
+        for (int c = 0; c < 2; ++c)
+#pragma unroll
+          for (int zl = 0; zl < ZL; ++zl) w[c][zl] *= ihn;
+        put_v(j + 1);
+      }
+    }
+    if (g0) {
+      const int ld = K + 1;
+      givens_col(jm - 1, h1, h2, hn_prev, H, cs, sn, gv, ld);
+      for (int i = jm - 1; i >= 0; --i) {
+        double s = gv[i];
+        for (int l = i + 1; l < jm; ++l) s -= H[i + ld * l] * yv[l];
+        yv[i] = s / H[i + ld * i];
+      }
+      if (rank == 0) ras_count(p.jcnt, jm);
+    }
+    __syncthreads();
+    if (act) {
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        double yl[ZL];
+#pragma unroll
+        for (int zl = 0; zl < ZL; ++zl) yl[zl] = 0.0;
+#pragma unroll
+        for (int i = 0; i < K; ++i)
+          if (i < jm) {
+            const double yi = yv[i];
+#pragma unroll
+            for (int zl = 0; zl < ZL; ++zl) yl[zl] = fma(yi, V(i, c, zl), yl[zl]);
+          }
+        const int y = y0 + c;
+#pragma unroll
+        for (int zl = 0; zl < ZL; ++zl) {
+          const int ez = ez0 + zl, li = x - p.o, lj = y - p.o, lk = ez - p.o;
+          if (p.y_ext) {
+            p.y_ext[(size_t)box * NE + (ez * E + y) * E + x] = yl[zl];
+          } else if (li >= 0 && li < p.bx && lj >= 0 && lj < p.by && lk >= 0 && lk < p.bz) {
+            p.z[(size_t)(ibx * p.bx + li) + NX * (iby * p.by + lj) + NXY * (ibz * p.bz + lk)] =
+                yl[zl];
+          }
+        }
+      }
+    }
   }
   cl_sync();   // no CTA leaves while its partner may still address its shared memory
 }
@@ -609,8 +1100,29 @@ int cl2_nr() {
   return nr == 3 ? 3 : nr == 2 ? 2 : 1;
 }
 
+// columns per thread: 1 (ras3d_cl2_kernel) or 2 (ras3d_cl2p_kernel); PFC_CL2_CP selects
+int cl2_cp() {   // default 2: measured 39.3 vs 50.1 ms per 512^3 apply (round 2)
+  const char* e = getenv("PFC_CL2_CP");
+  return e && e[0] == '1' ? 1 : 2;
+}
+
 ras3cl2_fn pick_cl2(int k, int e, size_t* smem, int* threads, int* ng) {
   const int nr = cl2_nr();
+  if (cl2_cp() == 2) {
+    const char* en = getenv("PFC_CL2_NR");
+    const int nr2 = en ? atoi(en) : 3;   // measured fastest (NR = 4 spills at 255 registers)
+#define C2P2(K, E, NR)                                              \
+    if (k == K && e == E && nr2 == NR) {                            \
+      *smem = cl2p_smem_doubles<K, E, NR>() * sizeof(double);       \
+      *threads = Cl2p<E>::NT;                                       \
+      *ng = Cl2pK<K, NR>::NG;                                       \
+      return ras3d_cl2p_kernel<K, E, NR>;                           \
+    }
+    C2P2(10, 20, 3) C2P2(4, 20, 3) C2P2(10, 12, 3) C2P2(4, 12, 3)
+    C2P2(10, 20, 1) C2P2(10, 20, 2) C2P2(10, 20, 4)
+#undef C2P2
+    return nullptr;
+  }
 #define C2(K, E, NR)                                                \
   if (k == K && e == E && nr == NR) {                               \
     *smem = cl2_smem_doubles<K, E, NR>() * sizeof(double);          \
@@ -692,3 +1204,11 @@ cudaError_t launch_ras_3d_cl2(pfc_ctx* ctx, const double* v, const double* c, do
   if (e2 != cudaSuccess || cf.ras_variant == PFC_RAS_LEFT) return e2;
   return launch_ras_extend(ctx, z);
 }
+
+#ifdef CL2_PROF
+extern "C" void pfc_cl2_prof_read(long long* out) {
+  cudaMemcpyFromSymbol(out, cl2_prof, sizeof(long long) * 16);
+  long long z[16] = {0};
+  cudaMemcpyToSymbol(cl2_prof, z, sizeof(z));
+}
+#endif
