@@ -806,6 +806,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cl2p<E>::NT, 1)
     fence_mbar_init();
   }
   cl_sync();   // the partner is running, zeroed and its mbarriers initialised before any DSMEM store
+#ifdef CL2_PROF
+  if (blockIdx.x == 0 && tid == 0) cl2_prof_last = clock64();
+#endif
   uint32_t ph = 0;
   constexpr uint32_t HALO_BYTES = (uint32_t)PL * 3u * 8u;
   auto reduce = [&](int nsent, int nget, double* hwv) {
@@ -858,8 +861,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cl2p<E>::NT, 1)
     double* redb = red + rb * 2 * NW * RS;
     uint32_t redr = red_rem + (uint32_t)(rb * 2 * NW * RS) * 8u;
     uint32_t mbr = mbar_rem0 + 8u * rb;
+    C2P(0);
     cl2_put<NW>(acc, 0, redb, redr, mbr, rank, wid, lane);
     reduce(1, 1, hx);
+    C2P(1);
     const double beta = sqrt(hx[0]);
     if (beta == 0.0) {
       if (act) {
@@ -937,20 +942,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cl2p<E>::NT, 1)
     double hn_prev = 0.0;
 #pragma unroll 1
     for (int j = 0; j < K; ++j) {
+      C2P(10);
       if (tid == 0) mbar_expect_tx(&mbar[2], HALO_BYTES);
       __syncthreads();
+      C2P(2);
       if (g0 && j > 0) givens_col(j - 1, h1, h2, hn_prev, H, cs, sn, gv, K + 1);
 #pragma unroll
       for (int c = 0; c < 2; ++c)
 #pragma unroll
         for (int zl = 0; zl < ZL; ++zl) w[c][zl] = 0.0;
       if (act) cl2p_stencil<E, 0, ZL>(p, pv, pc, w);
+      C2P(3);
       mbar_wait_cluster(&mbar[2], (ph >> 2) & 1u);
       ph ^= 4u;
+      C2P(4);
       if (act) {
         if (rank == 0) cl2p_stencil<E, ZL, ZL + 3>(p, pv, pc, w);
         else cl2p_stencil<E, -3, 0>(p, pv, pc, w);
       }
+      C2P(5);
       double hn2 = 0.0;
       auto cgs2 = [&](auto Jc) {
         constexpr int J = decltype(Jc)::value;
@@ -1038,6 +1048,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cl2p<E>::NT, 1)
         return hn2;
       };
       dispatch_j<K>(j, cgs2);
+      C2P(6);
       const double hn = sqrt(hn2 > 0.0 ? hn2 : 0.0);
       hn_prev = hn;
       jm = j + 1;
@@ -1051,6 +1062,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cl2p<E>::NT, 1)
         put_v(j + 1);
       }
     }
+    C2P(10);
     if (g0) {
       const int ld = K + 1;
       givens_col(jm - 1, h1, h2, hn_prev, H, cs, sn, gv, ld);
@@ -1062,6 +1074,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cl2p<E>::NT, 1)
       if (rank == 0) ras_count(p.jcnt, jm);
     }
     __syncthreads();
+    C2P(7);
     if (act) {
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
@@ -1088,7 +1101,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cl2p<E>::NT, 1)
         }
       }
     }
+    C2P(9);
   }
+  C2P(8);
   cl_sync();   // no CTA leaves while its partner may still address its shared memory
 }
 
