@@ -1017,8 +1017,11 @@ ras2d_col_fn pick_col(int k, int r, bool mirror = false, bool mob = false) {
 int col_rows(int k, int Ex, int Ey, bool mirror = false, bool mob = false) {
   if (Ex + 6 > PP || Ey > 42) return 0;
   const int cand[4] = {1, 2, 4, 5};
+  const char* force = getenv("PFC_RAS2_ROWS");   // A/B probes only: rows per thread
+  const int rmin = force ? atoi(force) : 1;
   for (int i = 0; i < 4; ++i) {
     const int r = cand[i];
+    if (r < rmin) continue;
     const int ns = (Ey + r - 1) / r;
     if (Ex + 6 <= col_pp(r) && (Ex * ns + 31) / 32 * 32 + 32 <= NTC && pick_col(k, r, mirror, mob))
       return r;

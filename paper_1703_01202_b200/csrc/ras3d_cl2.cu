@@ -47,10 +47,12 @@
 #endif
 // phase timing of CTA 0's thread 0 (diagnostic builds with -DCL2_PROF; tools/ras3_probe.py)
 #ifdef CL2_PROF
+// thread 0 of CTA 0 accumulates in registers-backed locals (no global traffic inside the timed
+// region), flushed to cl2_prof at the end of the kernel
 __device__ long long cl2_prof[16];
 __device__ long long cl2_prof_last;
 #define C2P(i) do { if (blockIdx.x == 0 && threadIdx.x == 0) { long long t_ = clock64(); \
-    cl2_prof[i] += t_ - cl2_prof_last; cl2_prof_last = t_; } } while (0)
+    c2p_acc[i] += t_ - c2p_last; c2p_last = t_; } } while (0)
 #else
 #define C2P(i) do {} while (0)
 #endif
@@ -358,7 +360,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cl2<E>::NT, 1)
   }
   cl_sync();   // the partner is running, zeroed and its mbarriers initialised before any DSMEM store
 #ifdef CL2_PROF
-  if (blockIdx.x == 0 && tid == 0) cl2_prof_last = clock64();
+  long long c2p_acc[16] = {0}, c2p_last = clock64();
 #endif
   uint32_t ph = 0;   // phase parity bits: bit q for mbar[q]
   constexpr uint32_t HALO_BYTES = (uint32_t)PL * 3u * 8u;
@@ -633,6 +635,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cl2<E>::NT, 1)
     C2P(9);   // final V y and the output stores
   }
   C2P(8);
+#ifdef CL2_PROF
+  if (blockIdx.x == 0 && tid == 0)
+    for (int i = 0; i < 16; ++i) cl2_prof[i] += c2p_acc[i];
+#endif
   cl_sync();   // no CTA leaves while its partner may still address its shared memory
 }
 
@@ -807,7 +813,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cl2p<E>::NT, 1)
   }
   cl_sync();   // the partner is running, zeroed and its mbarriers initialised before any DSMEM store
 #ifdef CL2_PROF
-  if (blockIdx.x == 0 && tid == 0) cl2_prof_last = clock64();
+  long long c2p_acc[16] = {0}, c2p_last = clock64();
 #endif
   uint32_t ph = 0;
   constexpr uint32_t HALO_BYTES = (uint32_t)PL * 3u * 8u;
@@ -981,9 +987,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cl2p<E>::NT, 1)
                 for (int i = 0; i <= J; ++i) acc[i] = fma(V(i, c, zl), wz, acc[i]);
               }
           }
+          C2P(11);
           cl2_put_multi<NW>(acc, J + 1, redb, redr, mbr, rank, wid, lane);
         }
         reduce(J + 1, J + 1, h1);
+        C2P(12);
         redb = red + rb * 2 * NW * RS;
         redr = red_rem + (uint32_t)(rb * 2 * NW * RS) * 8u;
         mbr = mbar_rem0 + 8u * rb;
@@ -1007,10 +1015,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cl2p<E>::NT, 1)
                 w[c][zl] = ww;
               }
           }
+          C2P(13);
           cl2_put_multi<NW>(acc, J + 1, redb, redr, mbr, rank, wid, lane);
           cl2_put<NW>(nrm, J + 1, redb, redr, mbr, rank, wid, lane);
         }
         reduce(J + 2, J + 2, h2);
+        C2P(14);
         double h2n = 0.0;
         for (int i = 0; i <= J; ++i) h2n += h2[i] * h2[i];
         const double wn2 = h2[J + 1];
@@ -1104,6 +1114,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cl2p<E>::NT, 1)
     C2P(9);
   }
   C2P(8);
+#ifdef CL2_PROF
+  if (blockIdx.x == 0 && tid == 0)
+    for (int i = 0; i < 16; ++i) cl2_prof[i] += c2p_acc[i];
+#endif
   cl_sync();   // no CTA leaves while its partner may still address its shared memory
 }
 

@@ -29,7 +29,9 @@ torch.cuda.synchronize()
 L.pfc_cl2_prof_read(buf)
 names = {0: "gather v, c", 1: "beta reduction", 2: "step barrier (+Givens lag)", 3: "stencil own",
          4: "halo wait", 5: "stencil halo", 6: "CGS2 passes+reductions", 7: "post-loop Givens/backsub",
-         8: "tail", 9: "V y + stores", 10: "put_v / next step"}
+         8: "tail", 9: "V y + stores", 10: "put_v / next step", 11: "pass 1 (dots)",
+         12: "reduction 1", 13: "pass 2 (axpy + dots)", 14: "reduction 2",
+         6: "pass 3 (+3rd reduction)"}
 tot = sum(buf[i] for i in range(16))
 for i in range(16):
     if buf[i]:
