@@ -580,7 +580,8 @@ pfc_status pfc_create(const pfc_config* cfg, void* stream, pfc_ctx** out) {
       ctx->ras3_col = 1;
     else
       d = ras3d_scratch_doubles(ctx, &grid);
-    if (pfc_check_cuda(ctx, cudaMalloc(&ctx->ras_scratch, d * sizeof(double)), "ras scratch"))
+    if (pfc_check_cuda(ctx, cudaMalloc(&ctx->ras_scratch, d * sizeof(double)), "ras scratch") ||
+        pfc_check_cuda(ctx, cudaMemset(ctx->ras_scratch, 0, d * sizeof(double)), "ras scratch"))
       return fail(PFC_ENOMEM);
   }
   ctx->tail = tail_enabled(ctx);

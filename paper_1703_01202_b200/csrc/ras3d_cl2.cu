@@ -806,7 +806,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cl2p<E>::NT, 1)
 
   int rb = 0;
   const uint32_t mbar_rem0 = mapa_rank(smem_u32(&mbar[0]), (uint32_t)partner);
-  for (int q = tid; q < NVB * PP + NCB * CP; q += blockDim.x) vb[q] = 0.0;
+  // zero v planes (ring stays zero), finite c' and finite basis slots (the final V y reads
+  // every slot with a zero coefficient beyond the steps taken; the L2 scratch is zeroed at
+  // context creation)
+  for (int q = tid; q < NVB * PP + NCB * CP + NS * 2 * ZL * NTN; q += blockDim.x) vb[q] = 0.0;
   if (tid == 0) {
     for (int q = 0; q < 3; ++q) mbar_init(&mbar[q], 1);
     fence_mbar_init();
@@ -845,9 +848,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cl2p<E>::NT, 1)
         const int y = y0 + c;
         const size_t gxy = (size_t)wrapi(gx0 + x, p.nx) + NX * wrapi(gy0 + y, p.ny);
         const bool oxy = x >= p.o && x < p.o + p.bx && y >= p.o && y < p.o + p.by;
+        int gz = wrapi(gz0 + ez0, p.nz);   // wrapped z of own plane 0, advanced without '%'
 #pragma unroll
-        for (int zl = 0; zl < ZL; ++zl) {
-          const size_t g = gxy + NXY * wrapi(gz0 + ez0 + zl, p.nz);
+        for (int zl = 0; zl < ZL; ++zl, gz = gz + 1 == p.nz ? 0 : gz + 1) {
+          const size_t g = gxy + NXY * (size_t)gz;
           const int ez = ez0 + zl;
           const bool owned = oxy && ez >= p.o && ez < p.o + p.bz;
           w[c][zl] = (p.restrict_owned && !owned) ? 0.0 : p.v[g];
@@ -1081,32 +1085,38 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cl2p<E>::NT, 1)
         for (int l = i + 1; l < jm; ++l) s -= H[i + ld * l] * yv[l];
         yv[i] = s / H[i + ld * i];
       }
+      for (int i = jm; i < K; ++i) yv[i] = 0.0;   // steps not taken: zero coefficients
       if (rank == 0) ras_count(p.jcnt, jm);
     }
     __syncthreads();
     C2P(7);
     if (act) {
+      // y = V yv with no data-dependent branch, so every basis load (three vectors from the L2
+      // scratch) is issued up front; fma(0, v, s) = s exactly for the finite unused slots
+      double yl[2][ZL];
+#pragma unroll
+      for (int c = 0; c < 2; ++c)
+#pragma unroll
+        for (int zl = 0; zl < ZL; ++zl) yl[c][zl] = 0.0;
+#pragma unroll
+      for (int i = 0; i < K; ++i) {
+        const double yi = yv[i];
+#pragma unroll
+        for (int c = 0; c < 2; ++c)
+#pragma unroll
+          for (int zl = 0; zl < ZL; ++zl) yl[c][zl] = fma(yi, V(i, c, zl), yl[c][zl]);
+      }
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
-        double yl[ZL];
-#pragma unroll
-        for (int zl = 0; zl < ZL; ++zl) yl[zl] = 0.0;
-#pragma unroll
-        for (int i = 0; i < K; ++i)
-          if (i < jm) {
-            const double yi = yv[i];
-#pragma unroll
-            for (int zl = 0; zl < ZL; ++zl) yl[zl] = fma(yi, V(i, c, zl), yl[zl]);
-          }
         const int y = y0 + c;
 #pragma unroll
         for (int zl = 0; zl < ZL; ++zl) {
           const int ez = ez0 + zl, li = x - p.o, lj = y - p.o, lk = ez - p.o;
           if (p.y_ext) {
-            p.y_ext[(size_t)box * NE + (ez * E + y) * E + x] = yl[zl];
+            p.y_ext[(size_t)box * NE + (ez * E + y) * E + x] = yl[c][zl];
           } else if (li >= 0 && li < p.bx && lj >= 0 && lj < p.by && lk >= 0 && lk < p.bz) {
             p.z[(size_t)(ibx * p.bx + li) + NX * (iby * p.by + lj) + NXY * (ibz * p.bz + lk)] =
-                yl[zl];
+                yl[c][zl];
           }
         }
       }
