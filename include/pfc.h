@@ -100,11 +100,12 @@ enum { PFC_LOCAL_GMRES = 0, PFC_LOCAL_ILU = 1, PFC_LOCAL_LU = 2 };
  *                    (so D+ / D- vanish across the walls, mass is conserved and the energy
  *                    law of P:280-308 holds).  Subdomains are clipped at the walls: ext-box nodes
  *                    outside the domain are no unknowns of A_k = R_k J R_k^T.  Built for
- *                    ndim = 2, PFC_LOCAL_GMRES, ras_box >= 3; either mobility.  Runs the
- *                    global-memory operator chain (mobility.cu) and, for ras_local_k = 10
- *                    (any k with M = 1), the column subdomain kernel with the basis in
- *                    registers (ras2d.cu, MIR instantiation), else the shared-memory-basis
- *                    subdomain kernel; EINVAL otherwise. */
+ *                    ndim = 2 and 3 (3D since round 2), PFC_LOCAL_GMRES, ras_box >= 3; either
+ *                    mobility.  Runs the global-memory operator chain (mobility.cu); the
+ *                    subdomain solves run, in 2D for ras_local_k = 10 (any k with M = 1), the
+ *                    column kernel with the basis in registers (ras2d.cu, MIR instantiation),
+ *                    else the shared-memory-basis kernel, and in 3D the global-scratch kernel
+ *                    (ras3d.cu) with per-box mirror ghosts; EINVAL otherwise. */
 enum { PFC_BC_PERIODIC = 0, PFC_BC_MIRROR = 1 };
 
 /* Mobility of Eq. (PFCeq) P:137-150 in the scheme's (grad . M_d grad)_d, P:208-212 (edge

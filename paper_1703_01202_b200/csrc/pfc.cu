@@ -490,11 +490,10 @@ static pfc_status validate(const pfc_config& c, std::string* why) {
     return bad("PFC_LOCAL_ILU / PFC_LOCAL_LU are built for PFC_MOBILITY_ONE");
   if (c.bc != PFC_BC_PERIODIC && c.bc != PFC_BC_MIRROR)
     return bad("bc must be PFC_BC_PERIODIC or PFC_BC_MIRROR");
-  if (c.bc == PFC_BC_MIRROR && c.ndim != 2)
-    return bad("PFC_BC_MIRROR is built for ndim = 2 (the 3D subdomain kernels are periodic)");
   if (c.bc == PFC_BC_MIRROR && c.ras_local_solver != PFC_LOCAL_GMRES)
     return bad("PFC_BC_MIRROR is built for PFC_LOCAL_GMRES subdomain solves");
-  if (c.bc == PFC_BC_MIRROR && (c.ras_box[0] < 3 || c.ras_box[1] < 3))
+  if (c.bc == PFC_BC_MIRROR &&
+      (c.ras_box[0] < 3 || c.ras_box[1] < 3 || (c.ndim == 3 && c.ras_box[2] < 3)))
     return bad("PFC_BC_MIRROR needs ras_box >= 3 (mirror partners inside the boundary box)");
   if (c.gmres_restart < 1 || c.gmres_restart > PFC_MAX_RESTART) return bad("gmres_restart in [1,32]");
   if (c.gmres_maxit < 1 || c.newton_maxit < 0) return bad("iteration limits must be positive");
@@ -574,9 +573,11 @@ pfc_status pfc_create(const pfc_config* cfg, void* stream, pfc_ctx** out) {
     const char* force = getenv("PFC_RAS3D");
     const bool v1 = getenv("PFC_RAS3D_V1") != nullptr || (force && !strcmp(force, "v1"));
     ctx->ras3_col = 0;
-    if (!v1 && !c.mobility && !(force && !strcmp(force, "col")) && ras3d_cl2_plan(ctx, &grid, &d))
+    // (variable mobility and mirror walls run the global-scratch kernel)
+    const bool plain = !c.mobility && c.bc == PFC_BC_PERIODIC;
+    if (!v1 && plain && !(force && !strcmp(force, "col")) && ras3d_cl2_plan(ctx, &grid, &d))
       ctx->ras3_col = 2;
-    else if (!v1 && !c.mobility && ras3d_col_plan(ctx, &d, &grid))
+    else if (!v1 && plain && ras3d_col_plan(ctx, &d, &grid))
       ctx->ras3_col = 1;
     else
       d = ras3d_scratch_doubles(ctx, &grid);

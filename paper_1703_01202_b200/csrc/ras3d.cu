@@ -34,7 +34,17 @@ struct Ras3Args {
   const double* A;
   int mobility;
   unsigned long long* jcnt;   // profiling: Arnoldi steps taken (ras_count)
+  // Neumann-type mirror BCs (row f3, reading R23; round 2 in 3D): subdomains clipped at the
+  // walls (ext-box nodes outside the domain are no unknowns), the padded grid carries the
+  // mirror ghosts of v (the even extension) and c of the even extension, as in ras2d_kernel
+  int mirror;
 };
+
+// index along an axis: periodic wrap, or the mirror partner (R23: node -1 is node 0)
+__device__ __forceinline__ int axis3(int x, int n, int mirror) {
+  if (!mirror) return wrapi(x, n);
+  return x < 0 ? -1 - x : (x >= n ? 2 * n - 1 - x : x);
+}
 
 __global__ void __launch_bounds__(NT, 1) ras3d_kernel(Ras3Args p) {
   __shared__ double H[(KMAX + 1) * KMAX];
@@ -58,6 +68,8 @@ __global__ void __launch_bounds__(NT, 1) ras3d_kernel(Ras3Args p) {
   double* pm = pb + np;      // mobility: M, A, u on the padded grid (scratch sized for them)
   double* pa = pm + np;
   double* pu = pa + np;
+  double* pc = pm + (p.mobility ? 3 * np : 0);                   // mirror: c of the even ext.
+  int* gp = reinterpret_cast<int*>(pc + (p.mirror ? np : 0));    // mirror: ghost -> partner
 
   if (p.gate && *p.gate) return;
   const int tid = threadIdx.x;
@@ -75,24 +87,55 @@ __global__ void __launch_bounds__(NT, 1) ras3d_kernel(Ras3Args p) {
     double acc[KMAX + 1];
     acc[0] = 0.0;
     __syncthreads();
+    if (p.mirror)   // the previous box may have left mirror ghosts on the ring
+      for (int q = tid; q < np; q += NT) pv[q] = 0.0;
+    auto in_dom = [&](int x, int y, int z) {
+      return !p.mirror || (x >= 0 && x < p.nx && y >= 0 && y < p.ny && z >= 0 && z < p.nz);
+    };
     for (int l = tid; l < n; l += NT) {
       int li = l % Ex, lj = (l / Ex) % Ey, lk = l / (Ex * Ey);
-      size_t g = (size_t)wrapi(gx0 + li, p.nx) + NX * wrapi(gy0 + lj, p.ny) +
-                 NXY * wrapi(gz0 + lk, p.nz);
+      const bool act = in_dom(gx0 + li, gy0 + lj, gz0 + lk);   // an unknown of A_k
+      size_t g = (size_t)axis3(gx0 + li, p.nx, p.mirror) + NX * axis3(gy0 + lj, p.ny, p.mirror) +
+                 NXY * axis3(gz0 + lk, p.nz, p.mirror);
       const bool owned = li >= p.o && li < p.o + p.bx && lj >= p.o && lj < p.o + p.by &&
                          lk >= p.o && lk < p.o + p.bz;
-      double vv = (p.restrict_owned && !owned) ? 0.0 : p.v[g];
+      double vv = ((p.restrict_owned && !owned) || !act) ? 0.0 : p.v[g];
       V[l] = vv;
       cl[l] = p.c[g];
       acc[0] += vv * vv;
+    }
+    // mirror: does this box's padded grid reach past a wall (then it has ghost positions)?
+    const bool ghosts = p.mirror && (gx0 - 3 < 0 || gy0 - 3 < 0 || gz0 - 3 < 0 ||
+                                     gx0 + Px - 3 > p.nx || gy0 + Py - 3 > p.ny ||
+                                     gz0 + Pz - 3 > p.nz);
+    if (p.mirror) {   // c of the even extension on the padded grid; ghost -> partner map
+      for (int q = tid; q < np; q += NT) {
+        const int pi = q % Px, pj = (q / Px) % Py, pk = q / PP;
+        const int x = gx0 + pi - 3, y = gy0 + pj - 3, z = gz0 + pk - 3;
+        const bool inext = pi >= 3 && pi < Px - 3 && pj >= 3 && pj < Py - 3 && pk >= 3 &&
+                           pk < Pz - 3;
+        const bool ghost = !in_dom(x, y, z);
+        const size_t g = (size_t)axis3(x, p.nx, 1) + NX * axis3(y, p.ny, 1) +
+                         NXY * axis3(z, p.nz, 1);
+        pc[q] = (inext || ghost) ? p.c[g] : 0.0;
+        int part = -1;
+        if (ghost) {   // the mirror image inside the ext box, else the zero of the modified BC
+          const int mi = axis3(x, p.nx, 1) - gx0 + 3, mj = axis3(y, p.ny, 1) - gy0 + 3,
+                    mk = axis3(z, p.nz, 1) - gz0 + 3;
+          part = (mi >= 3 && mi < Px - 3 && mj >= 3 && mj < Py - 3 && mk >= 3 && mk < Pz - 3)
+                     ? mk * PP + mj * Px + mi : -2;
+        }
+        gp[q] = part;
+      }
     }
     if (p.mobility) {   // M = 1 - u^2, A, u of the iterate on the ext box and its +1 ring
       for (int q = tid; q < np; q += NT) {
         const int pi = q % Px, pj = (q / Px) % Py, pk = q / PP;
         double m = 0.0, a = 0.0, u = 0.0;
         if (pi >= 2 && pi < Px - 2 && pj >= 2 && pj < Py - 2 && pk >= 2 && pk < Pz - 2) {
-          const size_t g = (size_t)wrapi(gx0 + pi - 3, p.nx) + NX * wrapi(gy0 + pj - 3, p.ny) +
-                           NXY * wrapi(gz0 + pk - 3, p.nz);
+          const size_t g = (size_t)axis3(gx0 + pi - 3, p.nx, p.mirror) +
+                           NX * axis3(gy0 + pj - 3, p.ny, p.mirror) +
+                           NXY * axis3(gz0 + pk - 3, p.nz, p.mirror);   // mirror: even ext.
           u = 0.5 * (p.phi[g] + p.psi[g]);
           m = 1.0 - u * u;
           a = p.A[g];
@@ -131,6 +174,14 @@ __global__ void __launch_bounds__(NT, 1) ras3d_kernel(Ras3Args p) {
         pv[(lk + 3) * PP + (lj + 3) * Px + li + 3] = Vj[l];
       }
       __syncthreads();
+      if (ghosts) {   // mirror ghosts of V_j (the even extension; partners outside the box: 0)
+        for (int q = tid; q < np; q += NT) {
+          const int g = gp[q];
+          if (g >= 0) pv[q] = pv[g];
+          else if (g == -2) pv[q] = 0.0;
+        }
+        __syncthreads();
+      }
       {
         const int wx = Px - 2, wy = Py - 2, cnt = wx * wy * (Pz - 2);
         for (int q = tid; q < cnt; q += NT) {
@@ -147,7 +198,8 @@ __global__ void __launch_bounds__(NT, 1) ras3d_kernel(Ras3Args p) {
           int f = pk * PP + pj * Px + pi;
           double vv = pv[f];
           int li = pi - 3, lj = pj - 3, lk = pk - 3;
-          double cv = (li >= 0 && li < Ex && lj >= 0 && lj < Ey && lk >= 0 && lk < Ez)
+          double cv = p.mirror ? pc[f] * vv
+                      : (li >= 0 && li < Ex && lj >= 0 && lj < Ey && lk >= 0 && lk < Ez)
                           ? cl[(lk * Ey + lj) * Ex + li] * vv
                           : 0.0;
           double lapl = ih2 * ((pl[f - 1] + pl[f + 1]) + (pl[f - Px] + pl[f + Px]) +
@@ -179,6 +231,7 @@ __global__ void __launch_bounds__(NT, 1) ras3d_kernel(Ras3Args p) {
                                (pb[f - PP] + pb[f + PP]) - 6.0 * pb[f]);
           ww = pv[f] * idt - lapb;
         }
+        if (p.mirror && !in_dom(gx0 + li, gy0 + lj, gz0 + lk)) ww = 0.0;   // not an unknown
         w[l] = ww;
 #pragma unroll
         for (int i = 0; i <= KMAX; ++i)
@@ -269,7 +322,8 @@ size_t ras3d_scratch_per_cta(const pfc_config& c) {
   const size_t Ex = c.ras_box[0] + 2 * c.ras_overlap, Ey = c.ras_box[1] + 2 * c.ras_overlap,
                Ez = c.ras_box[2] + 2 * c.ras_overlap;
   const size_t n = Ex * Ey * Ez, np = (Ex + 6) * (Ey + 6) * (Ez + 6);
-  size_t d = (size_t)(c.ras_local_k + 1) * n + 2 * n + (c.mobility ? 6 : 3) * np;
+  size_t d = (size_t)(c.ras_local_k + 1) * n + 2 * n + (c.mobility ? 6 : 3) * np +
+             (c.bc == PFC_BC_MIRROR ? np + (np + 1) / 2 : 0);   // mirror: pc, gp
   return (d + 31) & ~size_t(31);
 }
 
@@ -301,7 +355,7 @@ cudaError_t launch_ras_3d(pfc_ctx* ctx, const double* v, const double* c, double
              1.0 / dt, cf.gamma, ctx->ih2, cf.ras_variant == PFC_RAS_RIGHT,
              cf.ras_variant == PFC_RAS_LEFT ? nullptr : ctx->ras_y, ctx->gate,
              ctx->mob_phi, ctx->mob_psi, ctx->mob_A, cf.mobility,
-             ctx->prof ? ctx->d_jcnt : nullptr};
+             ctx->prof ? ctx->d_jcnt : nullptr, cf.bc == PFC_BC_MIRROR};
   ras3d_kernel<<<grid, NT, 0, ctx->stream>>>(p);
   ctx->launches++;
   {
