@@ -44,6 +44,10 @@ __device__ __forceinline__ bool finalize_last_block(const double* partials, doub
   return true;
 }
 
+__device__ __forceinline__ double2 ld2g(const double* p) {
+  return *reinterpret_cast<const double2*>(p);
+}
+
 struct Coef {
   double c[PFC_MAX_RESTART];
 };
@@ -80,10 +84,22 @@ __global__ void __launch_bounds__(NT) k_multidot(const double* __restrict__ V, s
   double acc[NV];
 #pragma unroll
   for (int k = 0; k < NV; ++k) acc[k] = 0.0;
-  for (size_t i = blockIdx.x * (size_t)NT + threadIdx.x; i < N; i += (size_t)gridDim.x * NT) {
-    double wi = w[i];
+  if ((N & 1) == 0) {   // 16-byte pairs (N even: every column of V starts 16-byte aligned)
+    const size_t N2 = N >> 1;
+    for (size_t q = blockIdx.x * (size_t)NT + threadIdx.x; q < N2; q += (size_t)gridDim.x * NT) {
+      const double2 wi = ld2g(w + 2 * q);
 #pragma unroll
-    for (int k = 0; k < NV; ++k) acc[k] += V[k * ldv + i] * wi;
+      for (int k = 0; k < NV; ++k) {
+        const double2 v = ld2g(V + k * ldv + 2 * q);
+        acc[k] = fma(v.y, wi.y, fma(v.x, wi.x, acc[k]));
+      }
+    }
+  } else {
+    for (size_t i = blockIdx.x * (size_t)NT + threadIdx.x; i < N; i += (size_t)gridDim.x * NT) {
+      double wi = w[i];
+#pragma unroll
+      for (int k = 0; k < NV; ++k) acc[k] += V[k * ldv + i] * wi;
+    }
   }
   block_sum_multi<NV>(acc, red, outv);
   if (threadIdx.x < NV) partials[blockIdx.x * NV + threadIdx.x] = outv[threadIdx.x];
@@ -104,14 +120,31 @@ __global__ void __launch_bounds__(NT) k_axpy_dot(const double* __restrict__ V, s
   double hk[NV], acc[NV];
 #pragma unroll
   for (int k = 0; k < NV; ++k) { hk[k] = h[k]; acc[k] = 0.0; }
-  for (size_t i = blockIdx.x * (size_t)NT + threadIdx.x; i < N; i += (size_t)gridDim.x * NT) {
-    double v[NV];
-    double wi = w[i];
+  if ((N & 1) == 0) {
+    const size_t N2 = N >> 1;
+    for (size_t q = blockIdx.x * (size_t)NT + threadIdx.x; q < N2; q += (size_t)gridDim.x * NT) {
+      double2 v[NV];
+      double2 wi = ld2g(w + 2 * q);
 #pragma unroll
-    for (int k = 0; k < NV; ++k) { v[k] = V[k * ldv + i]; wi -= hk[k] * v[k]; }
-    w[i] = wi;
+      for (int k = 0; k < NV; ++k) {
+        v[k] = ld2g(V + k * ldv + 2 * q);
+        wi.x -= hk[k] * v[k].x;
+        wi.y -= hk[k] * v[k].y;
+      }
+      *reinterpret_cast<double2*>(w + 2 * q) = wi;
 #pragma unroll
-    for (int k = 0; k < NV; ++k) acc[k] += v[k] * wi;
+      for (int k = 0; k < NV; ++k) acc[k] = fma(v[k].y, wi.y, fma(v[k].x, wi.x, acc[k]));
+    }
+  } else {
+    for (size_t i = blockIdx.x * (size_t)NT + threadIdx.x; i < N; i += (size_t)gridDim.x * NT) {
+      double v[NV];
+      double wi = w[i];
+#pragma unroll
+      for (int k = 0; k < NV; ++k) { v[k] = V[k * ldv + i]; wi -= hk[k] * v[k]; }
+      w[i] = wi;
+#pragma unroll
+      for (int k = 0; k < NV; ++k) acc[k] += v[k] * wi;
+    }
   }
   block_sum_multi<NV>(acc, red, outv);
   if (threadIdx.x < NV) partials[blockIdx.x * NV + threadIdx.x] = outv[threadIdx.x];
@@ -134,12 +167,27 @@ __global__ void __launch_bounds__(NT) k_axpy_norm(const double* __restrict__ V, 
 #pragma unroll
   for (int k = 0; k < NV; ++k) hk[k] = h[k];
   double acc[1] = {0.0};
-  for (size_t i = blockIdx.x * (size_t)NT + threadIdx.x; i < N; i += (size_t)gridDim.x * NT) {
-    double wi = w[i];
+  if ((N & 1) == 0) {
+    const size_t N2 = N >> 1;
+    for (size_t q = blockIdx.x * (size_t)NT + threadIdx.x; q < N2; q += (size_t)gridDim.x * NT) {
+      double2 wi = ld2g(w + 2 * q);
 #pragma unroll
-    for (int k = 0; k < NV; ++k) wi -= hk[k] * V[k * ldv + i];
-    w[i] = wi;
-    acc[0] += wi * wi;
+      for (int k = 0; k < NV; ++k) {
+        const double2 v = ld2g(V + k * ldv + 2 * q);
+        wi.x -= hk[k] * v.x;
+        wi.y -= hk[k] * v.y;
+      }
+      *reinterpret_cast<double2*>(w + 2 * q) = wi;
+      acc[0] = fma(wi.y, wi.y, fma(wi.x, wi.x, acc[0]));
+    }
+  } else {
+    for (size_t i = blockIdx.x * (size_t)NT + threadIdx.x; i < N; i += (size_t)gridDim.x * NT) {
+      double wi = w[i];
+#pragma unroll
+      for (int k = 0; k < NV; ++k) wi -= hk[k] * V[k * ldv + i];
+      w[i] = wi;
+      acc[0] += wi * wi;
+    }
   }
   block_sum_multi<1>(acc, red, outv);
   if (threadIdx.x == 0) partials[blockIdx.x] = outv[0];
