@@ -11,8 +11,8 @@ Metric (BASELINE.json): "PFC time steps/sec and Jacobian-apply HBM GB/s (fp64, 1
   roofline = the dominant kernel class of the step (library-side CUDA-event profile pass).
   jacobian_apply / sweep = isolated J v, residual and RAS applies on 64^3..512^3 and
            1024^2..16384^2 grids, L2 flushed before each repetition.
-  other_configs = step rates of configs 1, 2, 4 and the paper's Test D (256^3 BCC crystallites)
-           beside the headline (short runs).
+  other_configs = step rates of configs 1, 2, 4 and the paper's Tests C (4096x1024 crack) and D
+           (256^3 BCC crystallites) beside the headline (short runs).
   cpu_baseline = the oracle on this host (rank 0, N=1 only): per-operator times of a bounded
            sample x the operator counts of the timed steps (3D), or timed oracle steps (2D).
   --impl reference: the oracle arm (rank 0 only) on the same config/metric/unit.
@@ -404,7 +404,8 @@ def bench_cuda(args):
     others = {}
     for name in [x for x in args.extra.split(",") if x and x != args.config]:
         oc = CONFIGS[name]
-        kk = min(oc.steps - 3, 197 if oc.ndim == 2 else 20 if oc.n[0] <= 128 else 7)
+        kk = min(oc.steps - 3, (197 if oc.N <= 4 << 20 else 17) if oc.ndim == 2
+                 else 20 if oc.n[0] <= 128 else 7)
         o = timed_workload(oc, 3, kk, ws, local, with_e2e=False, with_profile=True)
         odom = max(o["prof"], key=lambda k: o["prof"][k]["ms"])
         others[name] = {"workload": oc.name, "value": round(replica_value(o["ms"], kk, ws), 3),
@@ -620,7 +621,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="cuda", choices=["cuda", "reference"])
     ap.add_argument("--config", default="cfg5")
-    ap.add_argument("--extra", default="cfg1,cfg2,cfg4,testD",
+    ap.add_argument("--extra", default="cfg1,cfg2,cfg4,testC,testD",
                     help="other configs whose step rate is reported beside the headline")
     ap.add_argument("--sweep", type=int, default=1,
                     help="1: isolated J v / residual / RAS sweep 64^3..512^3, 1024^2..16384^2")

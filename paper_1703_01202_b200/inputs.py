@@ -104,6 +104,27 @@ def hexagonal_crystallites(n: int, h: float, seed: int, phibar: float = 0.285,
     return phi
 
 
+def crack_density(X, Y, qx=math.sqrt(3.0) / 2.0, stretch=0.9):
+    """Test C lattice (§5.1C): phi = 0.49 + cos(q_y y / sqrt3) cos(q_x x)
+    - 0.5 cos(2 q_y y / sqrt3) with q_x = sqrt3/2 and q_y = 0.9 q_x (a 1/9 stretch in y)."""
+    qy = stretch * qx
+    s3 = math.sqrt(3.0)
+    return 0.49 + np.cos(qy * Y / s3) * np.cos(qx * X) - 0.5 * np.cos(2.0 * qy * Y / s3)
+
+
+def crack_ic(nx: int, ny: int, h: float, notch=(40, 20), liquid=0.79) -> np.ndarray:
+    """Test C initial condition: the stretched lattice on the cell-centred nodes
+    (R2), with a centred notch of notch[0] x notch[1] nodes replaced by the coexisting liquid
+    phi = 0.79 (reading R26).  numpy shape (ny, nx)."""
+    x = node_coords(nx, h)
+    y = node_coords(ny, h)
+    X, Y = np.meshgrid(x, y, indexing="xy")
+    phi = crack_density(X, Y)
+    i0, j0 = nx // 2 - notch[0] // 2, ny // 2 - notch[1] // 2
+    phi[j0:j0 + notch[1], i0:i0 + notch[0]] = liquid
+    return phi
+
+
 def bcc_density(X, Y, Z, L, phibar=-0.35, A=1.0, q=1.0 / math.sqrt(2.0), d0=5.0 * math.pi,
                 centres=((0.5, 0.75, 0.5), (0.25, 0.25, 0.5), (0.75, 0.25, 0.5)),
                 angles=(0.0, -math.pi / 8.0, math.pi / 8.0)):
@@ -187,6 +208,8 @@ class PFCConfig:
             return hexagonal_crystallites(self.n[0], self.h, self.seed)
         if kind == "bcc":
             return bcc_crystallites(self.n[0], self.h)
+        if kind == "crack":
+            return crack_ic(self.n[0], self.n[1], self.h)
         raise ValueError(kind)
 
 
@@ -206,6 +229,13 @@ CONFIGS = {
     "cfg4": PFCConfig("cfg4_3d_128", 3, (128, 128, 128), adaptive=True, dt0=0.5, dt_min=0.5,
                       dt_max=10.0, eta=500.0, steps=100, ras_box=(16, 16, 16),
                       ic={"kind": "random", "mean": -0.35, "amp": 0.05}, seed=4),
+    # the paper's Test C (row f4): crack propagation in a stretched hexagonal lattice
+    # on a 4096 x 1024 mesh of the domain 4096 pi/3 x 1024 pi/3 (h = pi/3), a centred 40 x 20
+    # notch of liquid phi = 0.79, gamma = 1, M = 1, adaptive dt in [1, 5], eta = 100;
+    # RAS as config 2 (32^2 boxes, overlap 2)
+    "testC": PFCConfig("testC_2d_4096x1024", 2, (4096, 1024), h=math.pi / 3.0, gamma=1.0,
+                       adaptive=True, dt0=1.0, dt_min=1.0, dt_max=5.0, eta=100.0, steps=20,
+                       ras_box=(32, 32, 1), ic={"kind": "crack"}, seed=0),
     # the paper's Test D (row f4's second workload): 3D polycrystalline growth on
     # [0, 80 pi]^3 with a 256^3 mesh (h = 80 pi / 256), gamma = 0.35, three rotated BCC
     # crystallite spheres in the liquid phibar = -0.35, adaptive dt in [0.5, 10], eta = 500;

@@ -474,3 +474,20 @@ def test_testD_full_size_step_solves_the_scheme():
     assert abs((m1 - m0) - cfg.dt0 * h3 * math.fsum(F1.ravel())) <= 1e-12 * abs(m0)
     E0, E1 = O.free_energy(phi0, cfg.h, cfg.gamma), O.free_energy(phi1, cfg.h, cfg.gamma)
     assert E1 < E0 and abs(info["energy"] - E1) <= 1e-11 * abs(E1)
+
+
+def test_testC_full_size_one_step_parity():
+    """The paper's Test C at its full 4096 x 1024 (row f4 workload): one adaptive
+    step from the notched stretched lattice against the oracle (rel L2 <= 1e-10), the same
+    Newton / FGMRES counts, F_d, and the next dt of Eq. sencondt."""
+    cfg = CONFIGS["testC"]
+    phi0 = cfg.initial_condition()
+    ctx = P.Context(cfg)
+    phi = dev(phi0)
+    dt1, info = ctx.step(phi, cfg.dt0)
+    ref, hist = O.run(cfg, phi0, 1)
+    assert rel(host(phi), ref) <= 1e-10
+    assert info["newton_its"] == hist[0][5] and info["gmres_its"] == hist[0][6]
+    assert abs(info["energy"] - hist[0][3]) <= 1e-10 * abs(hist[0][3])
+    Fn = O.free_energy(phi0, cfg.h, cfg.gamma)
+    assert abs(dt1 - O.next_dt(cfg.dt_min, cfg.dt_max, cfg.eta, hist[0][3], Fn, cfg.dt0)) <= 1e-9 * dt1
