@@ -12,7 +12,7 @@ LIBDIR = os.path.join(HERE, "lib")
 LIB = os.path.join(LIBDIR, os.environ.get("PFC_LIB_NAME", "libpfc.so"))
 SOURCES = ["pfc.cu", "stencil2d.cu", "stencil3d.cu", "krylov.cu", "energy.cu", "ras2d.cu",
            "ras3d.cu", "ras3d_col.cu", "ras3d_cl2.cu", "ras_extend.cu", "mobility.cu",
-           "ilu.cu", "tail2d.cu"]
+           "ilu.cu", "tail2d.cu", "newton_graph.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
          "-Xcompiler", "-fPIC", "-Xptxas", "-v", "--expt-relaxed-constexpr"]

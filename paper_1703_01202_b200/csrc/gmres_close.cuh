@@ -17,17 +17,19 @@ __device__ __noinline__ void arnoldi_close(pfc_gmres_dev* gm, int j, const doubl
   const double hn = sqrt(nrm2);
   for (int i = 0; i <= j; ++i) H[i + ld * j] = h1[i] + h2[i];
   H[j + 1 + ld * j] = hn;
+  // products rounded before the sums (__dmul_rn / __dadd_rn: no FMA contraction), as the host
+  // loop of pfc.cu rounds them, so the device-resident paths are bitwise equal to it
   for (int i = 0; i < j; ++i) {
     const double a = H[i + ld * j], b = H[i + 1 + ld * j];
-    H[i + ld * j] = gm->cs[i] * a + gm->sn[i] * b;
-    H[i + 1 + ld * j] = -gm->sn[i] * a + gm->cs[i] * b;
+    H[i + ld * j] = __dadd_rn(__dmul_rn(gm->cs[i], a), __dmul_rn(gm->sn[i], b));
+    H[i + 1 + ld * j] = __dadd_rn(__dmul_rn(-gm->sn[i], a), __dmul_rn(gm->cs[i], b));
   }
   const double a = H[j + ld * j], b = H[j + 1 + ld * j];
-  const double r = sqrt(a * a + b * b);
+  const double r = sqrt(__dadd_rn(__dmul_rn(a, a), __dmul_rn(b, b)));
   const double c = r == 0.0 ? 1.0 : a / r, s = r == 0.0 ? 0.0 : b / r;
   gm->cs[j] = c;
   gm->sn[j] = s;
-  H[j + ld * j] = c * a + s * b;
+  H[j + ld * j] = __dadd_rn(__dmul_rn(c, a), __dmul_rn(s, b));
   H[j + 1 + ld * j] = 0.0;
   gm->g[j + 1] = -s * gm->g[j];
   gm->g[j] = c * gm->g[j];
@@ -47,6 +49,11 @@ __device__ __noinline__ void arnoldi_close(pfc_gmres_dev* gm, int j, const doubl
   gm->reason = reason;
   __threadfence();
   gm->stop = reason != PFC_GM_RUNNING;
+  if (gm->graph) {   // the device-resident graph step (newton_graph.cu): next SWITCH body
+    gm->klaunch += gm->kstep[j];
+    cudaGraphSetConditional(gm->hSW, (unsigned)(j + 1));
+    cudaGraphSetConditional(gm->hA, reason == PFC_GM_RUNNING ? 1u : 0u);
+  }
 }
 
 }  // namespace

@@ -253,16 +253,17 @@ __global__ void k_cycle_init(pfc_gmres_dev* gm, double beta, double tol, int m, 
   gm->jm = 0;
   gm->reason = PFC_GM_RUNNING;
   gm->stop = 0;
+  gm->graph = 0;
   for (int i = 0; i <= m; ++i) gm->g[i] = 0.0;
   gm->g[0] = beta;
 }
 
-// y = R^{-1} g (back substitution, the host loop's order) by one thread ...
+// y = R^{-1} g (back substitution, the host loop's order and roundings) by one thread ...
 __global__ void k_backsolve(pfc_gmres_dev* gm) {
   const int jm = gm->jm, ld = gm->m + 1;
   for (int i = jm - 1; i >= 0; --i) {
     double s = gm->g[i];
-    for (int l = i + 1; l < jm; ++l) s -= gm->H[i + ld * l] * gm->y[l];
+    for (int l = i + 1; l < jm; ++l) s = __dsub_rn(s, __dmul_rn(gm->H[i + ld * l], gm->y[l]));
     gm->y[i] = s / gm->H[i + ld * i];
   }
 }
@@ -402,6 +403,12 @@ cudaError_t launch_backsolve_lincomb(pfc_ctx* ctx, double* x, const double* Z, i
   k_lincomb_dev<<<blas_nblocks(ctx->N), NT, 0, ctx->stream>>>(x, Z, ctx->N, ctx->gm, ctx->N);
   ctx->launches++;
   pfc_account(ctx, PFC_K_VECTOR, 8.0 * (jm + 2) * ctx->N, 2.0 * jm * ctx->N);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_lincomb_dev(pfc_ctx* ctx, double* x, const double* Z) {
+  k_lincomb_dev<<<blas_nblocks(ctx->N), NT, 0, ctx->stream>>>(x, Z, ctx->N, ctx->gm, ctx->N);
+  ctx->launches++;
   return cudaGetLastError();
 }
 

@@ -21,12 +21,37 @@ struct pfc_gmres_dev {
   double cs[PFC_MAX_RESTART], sn[PFC_MAX_RESTART];
   double g[PFC_MAX_RESTART + 1], y[PFC_MAX_RESTART];
   double beta, tol, ihn, res;
+  double scal;   // graph path (f1): the scale of the next V_0 (-1/beta, then 1/|r| at a restart)
+  // graph path (f1): arnoldi_close also sets the WHILE (continue the cycle) and SWITCH (next j)
+  // handles and counts the kernels of step j (kstep[j]) into klaunch
+  cudaGraphConditionalHandle hA, hSW;
+  long long klaunch;
+  int kstep[PFC_MAX_RESTART];
+  int graph;
   int m, maxit;
   // read back by the host after every step (contiguous): stop flag, columns, total its, why
   int stop, jm, its, reason;
 };
 enum { PFC_GM_RUNNING = 0, PFC_GM_CONVERGED = 1, PFC_GM_HAPPY = 2, PFC_GM_MAXIT = 3,
        PFC_GM_RESTART = 4, PFC_GM_NONFINITE = 5 };
+
+// Device-resident Newton state of the graph path (NEXT row f1, newton_graph.cu): the scalars
+// of the inexact Newton loop with its line search, read back once per time step.
+struct pfc_newton_dev {
+  double nrm, n0, stop, lambda;
+  double e_old[2], e_new[2];   // raw sums of G_d and phi before / after the step (x h^d on host)
+  long long launches;          // kernels of this library executed by the graph
+  int newton_its, gmres_its, ls_backtracks, ls_t, accepted, status, why;
+  // conditional-node handles (Newton, FGMRES cycle, restart section, line search) and the
+  // kernel counts of the graph's sections, written by the host after the capture
+  cudaGraphConditionalHandle hN, hR, hRS, hLS;
+  int kc[8];
+};
+enum { PFC_GW_NONE = 0, PFC_GW_NEWTON_NONFINITE = 1, PFC_GW_NEWTON_MAXIT = 2,
+       PFC_GW_LINESEARCH = 3, PFC_GW_FGMRES_NONFINITE = 4 };
+
+// device-scalar slots of ctx->dscal
+enum { SC_H1 = 0, SC_H2 = 32, SC_NRM = 64, SC_EN = 66, SC_TOTAL = 128 };
 
 struct pfc_ilu;   // ILU(k) subdomain-solve structures (ilu.cu, row f2)
 
@@ -69,6 +94,16 @@ struct pfc_ctx {
   int* hflags = nullptr;           // pinned: per-step snapshots of gm->{stop, jm, its, reason}
   std::vector<cudaEvent_t> step_ev;   // one event per Arnoldi step of a cycle
   const int* gate = nullptr;       // &gm->stop while a device-resident cycle is being launched
+
+  // device-resident time step as one CUDA graph with conditional nodes (f1, newton_graph.cu):
+  // the executable graph, the dt and field pointers it was captured with, and its state
+  pfc_newton_dev* nd = nullptr;
+  pfc_newton_dev* hnd = nullptr;   // pinned host mirror
+  cudaGraphExec_t gexec = nullptr;
+  double g_dt = 0.0;
+  const double* g_ptrs[4] = {nullptr, nullptr, nullptr, nullptr};
+  long long g_post_launches = 0;   // kernels after the Newton loop (counted on the host)
+  int use_graph = 0;
 
   // RAS launch plan
   int ras_smem = 0;
@@ -195,10 +230,18 @@ cudaError_t launch_axpy_norm_close(pfc_ctx* ctx, const double* V, int nv, const 
 cudaError_t launch_scale_next(pfc_ctx* ctx, const double* w, double* vnext);
 cudaError_t launch_cycle_init(pfc_ctx* ctx, double beta, double tol, int its_done);
 cudaError_t launch_backsolve_lincomb(pfc_ctx* ctx, double* x, const double* Z, int jm);
+// x += Z y with y, jm from the device FGMRES state (graph path)
+cudaError_t launch_lincomb_dev(pfc_ctx* ctx, double* x, const double* Z);
 cudaError_t launch_norm2(pfc_ctx* ctx, const double* x, double* partials, double* out);
 cudaError_t launch_finalize(pfc_ctx* ctx, const double* partials, int nblk, int nval,
                             double* out);
 cudaError_t launch_lincomb(pfc_ctx* ctx, double* x, const double* Z, int nv, const double* coef);
+
+// device-resident time step (newton_graph.cu, row f1)
+int graph_enabled(pfc_ctx* ctx);
+pfc_status newton_graph(pfc_ctx* ctx, double dt, pfc_step_info* inf);
+void graph_free(pfc_ctx* ctx);
+cudaError_t launch_energy_mass_into(pfc_ctx* ctx, const double* phi, double* out2);
 
 // TMA descriptor encoding through the driver entry point (no libcuda link dependency)
 bool tma_encode(CUtensorMap* map, const double* ptr, int ndim, const int* n, const int* box);
