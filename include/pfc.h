@@ -192,7 +192,13 @@ pfc_status pfc_ras_apply(pfc_ctx* ctx, const double* phi_new, const double* phi_
  *         F' = (F_d^{n+1} - F_d^n)/Delta t_n (Eq. sencondt) when adaptive, else unchanged.
  *   info: may be NULL.
  * On PFC_ENOCONV / PFC_EBREAKDOWN phi is left unchanged (phi^n) so the caller may retry with
- * a smaller dt; info still reports the failed attempt. */
+ * a smaller dt; info still reports the failed attempt.
+ * Execution: either the host-driven loop (one small D2H read per Arnoldi step and per residual
+ * norm) or, with the default local GMRES solves, the whole step (both energies, Newton, line
+ * search, FGMRES with restarts) as ONE CUDA graph with conditional nodes whose decisions run on
+ * the device (captured once per context, dt passed as a device scalar; one D2H read per step).
+ * Both give bitwise identical results and counts.  The graph is the default; environment
+ * PFC_GRAPH=0 selects the host loop (so does the profiling mode, which times every launch). */
 pfc_status pfc_step(pfc_ctx* ctx, double* phi, double* dt, pfc_step_info* info);
 
 /* Discrete free energy F_d = h^d sum G_d, Eq. (relations)-(freeenergy) P:218-233:

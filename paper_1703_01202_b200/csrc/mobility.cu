@@ -102,8 +102,10 @@ __device__ __forceinline__ double div_mgrad(const MF& m, const double* __restric
 // residual: F = (Phi - psi)/dt - (grad . M grad) A, M = 1 - u^2; fixed-grid per-block ||F||^2
 __global__ void k_resid_out(const double* __restrict__ phi, const double* __restrict__ psi,
                             const double* __restrict__ A, double* __restrict__ F,
-                            double* __restrict__ partials, Grid G, double ih2, double idt) {
+                            double* __restrict__ partials, Grid G, double ih2, double idt_h,
+                            const double* dtp) {
   __shared__ double red[64];
+  const double idt = dt_inv(dtp, idt_h);
   const size_t N = (size_t)G.nx * G.ny * G.nz;
   auto m = [&](size_t k) {
     const double u = 0.5 * (phi[k] + psi[k]);
@@ -127,8 +129,9 @@ __global__ void k_resid_out(const double* __restrict__ phi, const double* __rest
 __global__ void k_jv_out(const double* __restrict__ v, const double* __restrict__ dA,
                          const double* __restrict__ phi, const double* __restrict__ psi,
                          const double* __restrict__ A, double* __restrict__ out, Grid G,
-                         double ih2, double idt, const int* gate) {
+                         double ih2, double idt_h, const int* gate, const double* dtp) {
   if (gate && *gate) return;
+  const double idt = dt_inv(dtp, idt_h);
   const size_t N = (size_t)G.nx * G.ny * G.nz;
   auto m = [&](size_t k) {
     const double u = 0.5 * (phi[k] + psi[k]);
@@ -189,7 +192,7 @@ cudaError_t launch_residual_mob(pfc_ctx* ctx, const double* phi, const double* p
   if (e != cudaSuccess) return e;
   const int g = grid_for(ctx->N);
   k_resid_out<<<g, NT, 0, ctx->stream>>>(phi, psi, ctx->mob_t[1], F, partials, G, ctx->ih2,
-                                          1.0 / dt);
+                                          1.0 / dt, ctx->dtdev);
   ctx->launches++;
   if (nparts) *nparts = g;
   // algorithmic: Phi, psi in, F out (the two intermediate fields are work of this path)
@@ -207,7 +210,7 @@ cudaError_t launch_jv_mob(pfc_ctx* ctx, const double* v, const double* c, double
   k_combine<true><<<g, NT, 0, ctx->stream>>>(v, c, ctx->mob_t[0], ctx->mob_t[1], G, ctx->ih2,
                                              ctx->cfg.gamma);
   k_jv_out<<<g, NT, 0, ctx->stream>>>(v, ctx->mob_t[1], ctx->mob_phi, ctx->mob_psi, ctx->mob_A,
-                                       out, G, ctx->ih2, 1.0 / dt, ctx->gate);
+                                       out, G, ctx->ih2, 1.0 / dt, ctx->gate, ctx->dtdev);
   ctx->launches += 3;
   pfc_account(ctx, PFC_K_JV, 24.0 * ctx->N, 45.0 * ctx->N);
   return cudaGetLastError();

@@ -1,8 +1,9 @@
 // newton_graph.cu -- the device-resident time step (NEXT row f1): the inexact Newton loop with
 // its line search, the restarted FGMRES(m) inside it and the energy
-// before and after, captured ONCE per dt as a CUDA graph with conditional nodes and replayed by
-// every pfc_step with that dt.  The host launches one graph per step and reads one small state
-// block back; no host round trip happens inside the step.
+// before and after, captured ONCE per context as a CUDA graph with conditional nodes and
+// replayed by every pfc_step (dt is a device scalar that every dt-dependent kernel reads).  The
+// host writes dt, launches one graph per step and reads one small state block back; no host
+// round trip happens inside the step.
 //
 // Structure (WHILE / IF / SWITCH are conditional nodes; their handles are set by the host
 // loop's decisions -- pfc.cu newton() / fgmres_host(), statement for statement, in the same
@@ -305,20 +306,18 @@ struct Cap {
 
 }  // namespace
 
-// Default: the graph on fixed-dt runs of grids of <= 2^18 nodes.  A conditional body costs
-// ~3 us on the device (tools/graph_cond_test.cu: a WHILE iteration of a 1-kernel body 4.2 us,
-// a kernel node 1.0 us), about what a host-loop round trip costs, so the graph pays where the
-// kernels are short and launch-bound (cfg1 64^2: 476 -> 567 steps/s) and is even where they
-// are long (cfg4 128^3 25.0 -> 25.4, Test C 47.6 -> 48.2).  dt is captured into the kernel
-// arguments, so every new dt costs a capture (~0.9 ms) and an instantiation (~1.7 ms): with
-// adaptive dt on small grids (cfg2: 493 host vs 465 graph) the host loop is the default.
-// PFC_GRAPH=1 / 0 forces the graph on / off.
+// Default: the graph for the local-GMRES subdomain solves (all configurations).  A conditional
+// body costs ~3 us on the device (tools/graph_cond_test.cu: a WHILE iteration of a 1-kernel
+// body 4.2 us, a kernel node 1.0 us), about what a host-loop round trip costs, so the graph
+// pays most where the kernels are short (cfg1 64^2: 476 -> 567 steps/s).  dt is read from the
+// device state by every dt-dependent kernel, so one capture serves every dt of an adaptive run.
+// PFC_GRAPH=1 / 0 forces it on / off.
 int graph_enabled(pfc_ctx* ctx) {
   // the factor-based local solves decide per Newton iteration on the host (reuse)
   if (ctx->cfg.ras_local_solver != PFC_LOCAL_GMRES) return 0;
   const char* e = getenv("PFC_GRAPH");
   if (e && e[0]) return e[0] != '0';
-  return (ctx->N <= ((size_t)1 << 18) && !ctx->cfg.adaptive) ? 1 : 0;
+  return 1;
 }
 
 void graph_free(pfc_ctx* ctx) {
@@ -330,7 +329,8 @@ void graph_free(pfc_ctx* ctx) {
   ctx->hnd = nullptr;
 }
 
-// record the whole step for this dt (every pointer and scalar of the launches is fixed)
+// record the whole step (every pointer of the launches is fixed; dt is read from nd->dt, the
+// launchers' host dt only fills the unused host-value fields)
 static cudaError_t capture(pfc_ctx* ctx, double dt, cudaGraph_t* out) {
   const pfc_config& c = ctx->cfg;
   const size_t N = ctx->N;
@@ -358,6 +358,7 @@ static cudaError_t capture(pfc_ctx* ctx, double dt, cudaGraph_t* out) {
   cudaGraphConditionalHandle hA = 0, hSW = 0;
   const bool prof = ctx->prof;
   ctx->prof = false;   // no per-launch event bracketing or accounting inside a capture
+  ctx->dtdev = nd->dt;   // every dt-dependent kernel reads its dt scalars from the device state
   if (cp.err == cudaSuccess) {
     ctx->stream = cp.s[0];
     cp.ok(cudaStreamBeginCapture(cp.s[0], cudaStreamCaptureModeThreadLocal));
@@ -471,6 +472,7 @@ static cudaError_t capture(pfc_ctx* ctx, double dt, cudaGraph_t* out) {
   cp.ok(cudaGetLastError());
   ctx->stream = user;
   ctx->prof = prof;
+  ctx->dtdev = nullptr;
   ctx->launches = l_start;   // captured, not executed
   for (int i = 0; i < 8; ++i)
     if (cp.s[i]) cudaStreamDestroy(cp.s[i]);
@@ -488,11 +490,11 @@ static cudaError_t capture(pfc_ctx* ctx, double dt, cudaGraph_t* out) {
 pfc_status newton_graph(pfc_ctx* ctx, double dt, pfc_step_info* inf) {
   if (!ctx->nd) {
     if (pfc_check_cuda(ctx, cudaMalloc(&ctx->nd, sizeof(pfc_newton_dev)), "newton state") ||
-        pfc_check_cuda(ctx, cudaMallocHost(&ctx->hnd, sizeof(pfc_newton_dev)), "newton state"))
+        pfc_check_cuda(ctx, cudaMallocHost(&ctx->hnd, 2 * sizeof(pfc_newton_dev)), "newton state"))
       return PFC_ENOMEM;
   }
   const double* ptrs[4] = {ctx->phi, ctx->F, ctx->trial, ctx->Ft};
-  bool same = ctx->gexec && ctx->g_dt == dt;
+  bool same = ctx->gexec != nullptr;
   for (int i = 0; i < 4; ++i) same = same && ctx->g_ptrs[i] == ptrs[i];
   if (!same) {
     if (ctx->gexec) cudaGraphExecDestroy(ctx->gexec);
@@ -504,18 +506,31 @@ pfc_status newton_graph(pfc_ctx* ctx, double dt, pfc_step_info* inf) {
     if (e == cudaSuccess) e = cudaGraphInstantiate(&ctx->gexec, g, 0);
     const auto t2 = std::chrono::steady_clock::now();
     if (getenv("PFC_GRAPH_VERBOSE"))
-      fprintf(stderr, "pfc graph: capture %.1f us, instantiate %.1f us (dt %.17g)\n",
+      fprintf(stderr, "pfc graph: capture %.1f us, instantiate %.1f us\n",
               std::chrono::duration<double, std::micro>(t1 - t0).count(),
-              std::chrono::duration<double, std::micro>(t2 - t1).count(), dt);
+              std::chrono::duration<double, std::micro>(t2 - t1).count());
     if (g) cudaGraphDestroy(g);
     if (e != cudaSuccess) {
       ctx->gexec = nullptr;
       return pfc_check_cuda(ctx, e, "newton graph capture");
     }
-    ctx->g_dt = dt;
     for (int i = 0; i < 4; ++i) ctx->g_ptrs[i] = ptrs[i];
   }
-  pfc_status s = pfc_check_cuda(ctx, cudaGraphLaunch(ctx->gexec, ctx->stream), "graph launch");
+  // dt of this step into the device state (hnd[1] is the pinned H2D source: hnd[0] receives the
+  // state at the end of the previous step's launch)
+  {  // the launchers' expressions (stencil2d/3d, tail2d, ras2d, ras3d*: 1/dt and W0)
+    const double ih2 = ctx->ih2, ih4 = ih2 * ih2, ih6 = ih4 * ih2;
+    const double al = 0.5 * (1.0 - ctx->cfg.gamma);
+    double* t = ctx->hnd[1].dt;
+    t[0] = dt;
+    t[1] = 1.0 / dt;
+    t[2] = 1.0 / dt + 4.0 * al * ih2 - 20.0 * ih4 + 56.0 * ih6;
+    t[3] = 1.0 / dt + 6.0 * al * ih2 - 42.0 * ih4 + 162.0 * ih6;
+  }
+  pfc_status s = pfc_check_cuda(ctx, cudaMemcpyAsync(ctx->nd->dt, ctx->hnd[1].dt, 4 * sizeof(double),
+                                                     cudaMemcpyHostToDevice, ctx->stream), "H2D dt");
+  if (s) return s;
+  s = pfc_check_cuda(ctx, cudaGraphLaunch(ctx->gexec, ctx->stream), "graph launch");
   if (s) return s;
   s = pfc_check_cuda(ctx, cudaMemcpyAsync(ctx->hnd, ctx->nd, sizeof(pfc_newton_dev),
                                           cudaMemcpyDeviceToHost, ctx->stream), "D2H state");

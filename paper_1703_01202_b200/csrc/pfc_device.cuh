@@ -126,6 +126,17 @@ __device__ __forceinline__ void block_sum_multi(double (&acc)[NV], double* red, 
   __syncthreads();
 }
 
+// dt-dependent scalars held on the device (the graph path of row f1 replays one capture for
+// every dt): dtp -> {dt, 1/dt, W0 (2D), W0 (3D)}, computed by the host with the launchers'
+// expressions; without dtp, the launch's own value
+__device__ __forceinline__ double dt_inv(const double* dtp, double idt) {
+  return dtp ? dtp[1] : idt;
+}
+template <int D>
+__device__ __forceinline__ double dt_w0(const double* dtp, double w0) {
+  return dtp ? dtp[D == 2 ? 2 : 3] : w0;
+}
+
 __device__ __forceinline__ double block_sum(double v, double* red) {
   double a[1] = {v};
   block_sum_multi<1>(a, red, red + 32);

@@ -42,6 +42,7 @@ struct pfc_newton_dev {
   double e_old[2], e_new[2];   // raw sums of G_d and phi before / after the step (x h^d on host)
   long long launches;          // kernels of this library executed by the graph
   int newton_its, gmres_its, ls_backtracks, ls_t, accepted, status, why;
+  double dt[4];                // {dt, 1/dt, W0 2D, W0 3D} of the step (host-written per launch)
   // conditional-node handles (Newton, FGMRES cycle, restart section, line search) and the
   // kernel counts of the graph's sections, written by the host after the capture
   cudaGraphConditionalHandle hN, hR, hRS, hLS;
@@ -98,11 +99,12 @@ struct pfc_ctx {
   // device-resident time step as one CUDA graph with conditional nodes (f1, newton_graph.cu):
   // the executable graph, the dt and field pointers it was captured with, and its state
   pfc_newton_dev* nd = nullptr;
-  pfc_newton_dev* hnd = nullptr;   // pinned host mirror
+  pfc_newton_dev* hnd = nullptr;   // pinned: [0] host mirror of *nd, [1].dt the H2D dt source
   cudaGraphExec_t gexec = nullptr;
-  double g_dt = 0.0;
   const double* g_ptrs[4] = {nullptr, nullptr, nullptr, nullptr};
   long long g_post_launches = 0;   // kernels after the Newton loop (counted on the host)
+  // while capturing the graph: the device copy of dt every dt-dependent kernel reads
+  const double* dtdev = nullptr;
   int use_graph = 0;
 
   // RAS launch plan

@@ -59,6 +59,7 @@ struct RasArgs {
   // mirror ghosts of the Krylov vector (the even extension) so that the stencils act as J
   int mirror;
   unsigned long long* jcnt;   // profiling: Arnoldi steps taken (ras_count)
+  const double* dtp;   // graph path (f1): dt on the device
 };
 
 // node index of global (x, y): periodic wrap, or the mirror partner (R23)
@@ -124,7 +125,7 @@ __global__ void __launch_bounds__(NT, 1) ras2d_kernel(RasArgs p) {
   const int nbx = p.nx / p.bx;
   const int ibx = blockIdx.x % nbx, iby = blockIdx.x / nbx;
   const int gx0 = ibx * p.bx - p.o, gy0 = iby * p.by - p.o;
-  const double ih2 = p.ih2, idt = p.idt, alpha = 0.5 * (1.0 - p.gamma);
+  const double ih2 = p.ih2, idt = dt_inv(p.dtp, p.idt), alpha = 0.5 * (1.0 - p.gamma);
 
   // own box nodes: l = tid + s*NT; padded index of node l
   int pidx[SLOTS];
@@ -462,6 +463,7 @@ struct RasColArgs {
   const double* psi;
   const double* A;
   unsigned long long* jcnt;     // profiling: Arnoldi steps taken (ras_count)
+  const double* dtp;             // graph path (f1): dt-dependent scalars on the device
 };
 
 constexpr int wclass(int ax, int ay) {
@@ -693,6 +695,7 @@ __global__ void __launch_bounds__(NTC, 1) ras2d_col_kernel(const __grid_constant
   __shared__ double gv[K + 1], cs[K], sn[K], yv[K], rd[K];
 
   if (p.gate && *p.gate) return;
+  const double W0 = dt_w0<2>(p.dtp, p.W[0]), idt = dt_inv(p.dtp, p.idt);
   const int tid = threadIdx.x, nwt = blockDim.x >> 5;
   const bool gwarp = (tid >> 5) == nwt - 1;     // the Givens warp: no nodes, reduces H
   const bool g0 = gwarp && (tid & 31) == 0;
@@ -867,7 +870,7 @@ __global__ void __launch_bounds__(NTC, 1) ras2d_col_kernel(const __grid_constant
                           0.5 * (mc + mm(f + PP)) * (g[f + PP] - gc) -
                           0.5 * (mc + mm(f - PP)) * (gc - g[f - PP]));
           };
-          w[r] = pv[f] * p.idt - dmg(pm, pb, false) - dmg(nullptr, pa, true);
+          w[r] = pv[f] * idt - dmg(pm, pb, false) - dmg(nullptr, pa, true);
         }
       }
     } else
@@ -886,7 +889,8 @@ __global__ void __launch_bounds__(NTC, 1) ras2d_col_kernel(const __grid_constant
       for (int r = 0; r < R; ++r)
 #pragma unroll
         for (int dy = -a; dy <= a; ++dy)
-          out[r] = fma(p.W[wclass(iabs(dx), iabs(dy))], col[r + dy + a], out[r]);
+          out[r] = fma(wclass(iabs(dx), iabs(dy)) == 0 ? W0 : p.W[wclass(iabs(dx), iabs(dy))],
+                       col[r + dy + a], out[r]);
     }
     // ---- minus Delta(c v): x-neighbours from the plane, y-neighbours from registers
 #pragma unroll
@@ -1085,6 +1089,7 @@ cudaError_t launch_ras_2d(pfc_ctx* ctx, const double* v, const double* c, double
     const double ih2 = ctx->ih2, ih4 = ih2 * ih2, ih6 = ih4 * ih2;
     const double al = 0.5 * (1.0 - cf.gamma);
     p.W[0] = 1.0 / dt + 4.0 * al * ih2 - 20.0 * ih4 + 56.0 * ih6;
+    p.dtp = ctx->dtdev;
     p.W[1] = -al * ih2 + 8.0 * ih4 - 28.5 * ih6;
     p.W[2] = -ih4 + 6.0 * ih6;
     p.W[3] = -2.0 * ih4 + 12.0 * ih6;
@@ -1108,6 +1113,7 @@ cudaError_t launch_ras_2d(pfc_ctx* ctx, const double* v, const double* c, double
               cf.ras_variant == PFC_RAS_LEFT ? nullptr : ctx->ras_y, ctx->gate,
               ctx->mob_phi, ctx->mob_psi, ctx->mob_A, cf.mobility, cf.bc == PFC_BC_MIRROR,
               ctx->prof ? ctx->d_jcnt : nullptr};
+    p.dtp = ctx->dtdev;
     fn<<<nb, NT, ctx->ras_smem, ctx->stream>>>(p);
   }
   ctx->launches++;

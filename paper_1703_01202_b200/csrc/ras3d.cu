@@ -38,6 +38,7 @@ struct Ras3Args {
   // walls (ext-box nodes outside the domain are no unknowns), the padded grid carries the
   // mirror ghosts of v (the even extension) and c of the even extension, as in ras2d_kernel
   int mirror;
+  const double* dtp;   // graph path (f1): dt on the device
 };
 
 // index along an axis: periodic wrap, or the mirror partner (R23: node -1 is node 0)
@@ -75,7 +76,7 @@ __global__ void __launch_bounds__(NT, 1) ras3d_kernel(Ras3Args p) {
   const int tid = threadIdx.x;
   const int nbx = p.nx / p.bx, nby = p.ny / p.by, nbz = p.nz / p.bz;
   const int nboxes = nbx * nby * nbz;
-  const double ih2 = p.ih2, idt = p.idt, alpha = 0.5 * (1.0 - p.gamma);
+  const double ih2 = p.ih2, idt = dt_inv(p.dtp, p.idt), alpha = 0.5 * (1.0 - p.gamma);
   const size_t NX = p.nx, NXY = (size_t)p.nx * p.ny;
 
   // zero padded arrays once (the ring is never written)
@@ -356,6 +357,7 @@ cudaError_t launch_ras_3d(pfc_ctx* ctx, const double* v, const double* c, double
              cf.ras_variant == PFC_RAS_LEFT ? nullptr : ctx->ras_y, ctx->gate,
              ctx->mob_phi, ctx->mob_psi, ctx->mob_A, cf.mobility,
              ctx->prof ? ctx->d_jcnt : nullptr, cf.bc == PFC_BC_MIRROR};
+  p.dtp = ctx->dtdev;
   ras3d_kernel<<<grid, NT, 0, ctx->stream>>>(p);
   ctx->launches++;
   {

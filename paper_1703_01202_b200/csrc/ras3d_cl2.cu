@@ -73,6 +73,7 @@ struct Ras3Cl2Args {
   double W[7];           // classes (0,0,0) (0,0,1) (0,0,2) (0,1,1) (0,0,3) (0,1,2) (1,1,1)
   double ih2;
   unsigned long long* jcnt;
+  const double* dtp;     // graph path (f1): dt-dependent scalars on the device
 };
 
 __device__ __forceinline__ uint32_t cluster_rank() {
@@ -241,7 +242,7 @@ template <int E, int LO, int HI>
 __device__ __forceinline__ void cl2_stencil(const Ras3Cl2Args& p, const double* pv,
                                             const double* pc, double (&out)[E / 2]) {
   constexpr int ZL = E / 2, PL = E * E, PX = Cl2<E>::PX, PP = Cl2<E>::PP;
-  const double W0 = p.W[0], W1 = p.W[1], W2 = p.W[2], W3 = p.W[3], W4 = p.W[4], W5 = p.W[5],
+  const double W0 = dt_w0<3>(p.dtp, p.W[0]), W1 = p.W[1], W2 = p.W[2], W3 = p.W[3], W4 = p.W[4], W5 = p.W[5],
                W6 = p.W[6];
   auto ld = [&](int dx, int dy, int zz) -> double { return pv[zz * PP + dx + PX * dy]; };
   // R = 0: own column, z-reach 3; with the z-neighbour and centre terms of -Delta(c v)
@@ -700,7 +701,7 @@ __device__ __forceinline__ void cl2p_stencil(const Ras3Cl2Args& p, const double*
                                              const double* pc, double (&out)[2][E / 2]) {
   using C = Cl2p<E>;
   constexpr int ZL = C::ZL, PX = C::PX, PP = C::PP, CX = C::CX, CP = C::CP;
-  const double W0 = p.W[0], W1 = p.W[1], W2 = p.W[2], W3 = p.W[3], W4 = p.W[4], W5 = p.W[5],
+  const double W0 = dt_w0<3>(p.dtp, p.W[0]), W1 = p.W[1], W2 = p.W[2], W3 = p.W[3], W4 = p.W[4], W5 = p.W[5],
                W6 = p.W[6];
 #pragma unroll
   for (int zz = (LO > -3 ? LO : -3); zz < (HI < ZL + 3 ? HI : ZL + 3); ++zz) {
@@ -1222,6 +1223,7 @@ cudaError_t launch_ras_3d_cl2(pfc_ctx* ctx, const double* v, const double* c, do
   const double ih2 = ctx->ih2, ih4 = ih2 * ih2, ih6 = ih4 * ih2;
   const double al = 0.5 * (1.0 - cf.gamma);
   p.W[0] = 1.0 / dt + 6.0 * al * ih2 - 42.0 * ih4 + 162.0 * ih6;
+  p.dtp = ctx->dtdev;
   p.W[1] = -al * ih2 + 12.0 * ih4 - 61.5 * ih6;
   p.W[2] = -ih4 + 9.0 * ih6;
   p.W[3] = -2.0 * ih4 + 18.0 * ih6;

@@ -44,6 +44,7 @@ struct Ras3ColArgs {
   double W[7];           // classes (0,0,0) (0,0,1) (0,0,2) (0,1,1) (0,0,3) (0,1,2) (1,1,1)
   double ih2;
   unsigned long long* jcnt;   // profiling: Arnoldi steps taken (ras_count)
+  const double* dtp;     // graph path (f1): dt-dependent scalars on the device
 };
 
 constexpr int iabs3(int a) { return a < 0 ? -a : a; }
@@ -84,7 +85,8 @@ __device__ __forceinline__ void col3_offset(const Ras3ColArgs& p, const double* 
 #pragma unroll
     for (int z = (zz - A > 0 ? zz - A : 0); z <= (zz + A < E - 1 ? zz + A : E - 1); ++z) {
       const int dz = zz - z;
-      out[z] = fma(p.W[wclass3(iabs3(DX), iabs3(DY), iabs3(dz))], val, out[z]);
+      const int cls = wclass3(iabs3(DX), iabs3(DY), iabs3(dz));   // (unrolled: a constant)
+      out[z] = fma(cls == 0 ? dt_w0<3>(p.dtp, p.W[0]) : p.W[cls], val, out[z]);
     }
     if constexpr (R == 1) {
       if (zz >= 0 && zz < E) {
@@ -445,6 +447,7 @@ cudaError_t launch_ras_3d_col(pfc_ctx* ctx, const double* v, const double* c, do
   const double ih2 = ctx->ih2, ih4 = ih2 * ih2, ih6 = ih4 * ih2;
   const double al = 0.5 * (1.0 - cf.gamma);
   p.W[0] = 1.0 / dt + 6.0 * al * ih2 - 42.0 * ih4 + 162.0 * ih6;
+  p.dtp = ctx->dtdev;
   p.W[1] = -al * ih2 + 12.0 * ih4 - 61.5 * ih6;
   p.W[2] = -ih4 + 9.0 * ih6;
   p.W[3] = -2.0 * ih4 + 18.0 * ih6;

@@ -50,6 +50,7 @@ struct S2Args {
   double idt, k0, k1, k2, kout;   // (1-gamma)/2, ih2, ih2^2/2, -ih2
   int vec;           // 16-byte pair loads / stores (n_x even, aligned bases)
   const int* gate;   // device-resident FGMRES: skip the launch when *gate != 0 (f1)
+  const double* dtp; // graph path (f1): dt on the device
 };
 
 struct p2 { double x, y; };   // the lane's two columns
@@ -67,6 +68,7 @@ __device__ __forceinline__ p2 lap_pair(p2 f, p2 m, p2 p) {
 template <int OP>
 __global__ void __launch_bounds__(NT, 2) stencil2d_kernel(const __grid_constant__ S2Args p) {
   if (p.gate && *p.gate) return;
+  const double idt = dt_inv(p.dtp, p.idt);
   const int lane = threadIdx.x & 31;
   const int item = blockIdx.x * (NT / 32) + (threadIdx.x >> 5);
   if (item >= p.nstrips * p.nchunks) return;   // whole warps only
@@ -109,10 +111,10 @@ __global__ void __launch_bounds__(NT, 2) stencil2d_kernel(const __grid_constant_
     p2 Lnew, Pnew;
     if (OP == OP_RESID) {
       Lnew = lap_pair(add2(A1, B1), add2(A2, B2), add2(A0, B0));
-      Pnew = {(A1.x - B1.x) * p.idt, (A1.y - B1.y) * p.idt};
+      Pnew = {(A1.x - B1.x) * idt, (A1.y - B1.y) * idt};
     } else {
       Lnew = lap_pair(A1, A2, A0);
-      Pnew = {A1.x * p.idt, A1.y * p.idt};
+      Pnew = {A1.x * idt, A1.y * idt};
     }
     // ---- stage 2: A | B at row t-2
     p2 Mnew;
@@ -181,6 +183,7 @@ struct S2TArgs {
   double idt, gamma, ih2;
   int use_tma;
   const int* gate;   // device-resident FGMRES: skip the launch when *gate != 0 (f1)
+  const double* dtp; // graph path (f1): dt on the device
 };
 
 __device__ __forceinline__ double lap5(const double* f, int q, double ih2) {
@@ -281,8 +284,8 @@ __global__ void __launch_bounds__(NT) stencil2d_tile_kernel(const __grid_constan
     int f = (HY + r) * WX + HX + cc;
     int gx = x0 + cc, gy = y0 + r;
     double o;
-    if (OP == OP_RESID) o = (A0[f] - B0[f]) * p.idt - lap5(AA, f, ih2);
-    else o = A0[f] * p.idt - lap5(AA, f, ih2);
+    if (OP == OP_RESID) o = (A0[f] - B0[f]) * dt_inv(p.dtp, p.idt) - lap5(AA, f, ih2);
+    else o = A0[f] * dt_inv(p.dtp, p.idt) - lap5(AA, f, ih2);
     if (gx < nx && gy < ny) {
       p.out[(size_t)gx + (size_t)nx * gy] = o;
       nrm += o * o;
@@ -309,6 +312,7 @@ cudaError_t launch2d_tile(pfc_ctx* ctx, const double* a, const double* b, double
   const int nx = ctx->cfg.n[0], ny = ctx->cfg.n[1];
   S2TArgs p{a, b, out, partials, nx, ny, 1.0 / dt, ctx->cfg.gamma, ctx->ih2, 0,
            OP == OP_JV ? ctx->gate : nullptr};
+  p.dtp = ctx->dtdev;
   CUtensorMap ma, mb;
   memset(&ma, 0, sizeof(ma));
   memset(&mb, 0, sizeof(mb));
@@ -356,6 +360,7 @@ cudaError_t launch2d(pfc_ctx* ctx, const double* a, const double* b, double dt, 
   S2Args p{a, b, out, partials, nx, ny, nstrips, nchunks, chunk, 1.0 / dt,
            0.5 * (1.0 - ctx->cfg.gamma), ih2, 0.5 * ih2 * ih2, -ih2, vec ? 1 : 0,
            OP == OP_JV ? ctx->gate : nullptr};
+  p.dtp = ctx->dtdev;
   const int items = nstrips * nchunks;
   if (nparts) *nparts = items;
   stencil2d_kernel<OP><<<(items + NT / 32 - 1) / (NT / 32), NT, 0, ctx->stream>>>(p);

@@ -86,6 +86,7 @@ struct S3Args {
   double idt, k0, k1, k2, kout;   // (1-gamma)/2, ih2, ih2^2/2, -ih2
   int mode;          // 0: plain loads; 1: TMA + wrapped re-reads; 2: seam-aligned TMA tiles
   const int* gate;   // device-resident FGMRES: skip the launch when *gate != 0 (f1)
+  const double* dtp; // graph path (f1): dt on the device
 };
 
 struct q4 { double a, b, c, d; };   // (row0,col0) (row0,col1) (row1,col0) (row1,col1)
@@ -163,6 +164,7 @@ __global__ void __launch_bounds__(NT, 1) stencil3d_kernel(const __grid_constant_
   __shared__ double red[64];
 
   if (p.gate && *p.gate) return;
+  const double idt = dt_inv(p.dtp, p.idt);
   const int tid = threadIdx.x, lane = tid & 31;
   const int nx = p.nx, ny = p.ny, nz = p.nz;
   const int ntx = (nx + TX - 1) / TX;
@@ -323,10 +325,10 @@ __global__ void __launch_bounds__(NT, 1) stencil3d_kernel(const __grid_constant_
       }
       q4 Pnew;     // pointwise part of the output at plane t-1
       if (OP == OP_RESID)
-        Pnew = {(A1.a - B1.a) * p.idt, (A1.b - B1.b) * p.idt, (A1.c - B1.c) * p.idt,
-                (A1.d - B1.d) * p.idt};
+        Pnew = {(A1.a - B1.a) * idt, (A1.b - B1.b) * idt, (A1.c - B1.c) * idt,
+                (A1.d - B1.d) * idt};
       else
-        Pnew = {A1.a * p.idt, A1.b * p.idt, A1.c * p.idt, A1.d * p.idt};
+        Pnew = {A1.a * idt, A1.b * idt, A1.c * idt, A1.d * idt};
       // everything that needs no outside neighbour, while other warps finish iteration t-1:
       // the centre and z parts of the three Laplacians and the pointwise part of A|B
       const q4 c1 = (OP == OP_RESID) ? lap_own(add4(A1, B1), add4(A2, B2), add4(A0, B0))
@@ -449,6 +451,7 @@ cudaError_t launch3d(pfc_ctx* ctx, const double* a, const double* b, double dt, 
   const double ih2 = ctx->ih2;
   S3Args p{a, b, out, partials, nx, ny, nz, zc, 1.0 / dt, 0.5 * (1.0 - ctx->cfg.gamma), ih2,
            0.5 * ih2 * ih2, -ih2, 0, OP == OP_JV ? ctx->gate : nullptr};
+  p.dtp = ctx->dtdev;
   S3Maps m;
   memset(&m, 0, sizeof(m));
   const int box[3] = {NW, BH, 1}, box22[3] = {BW, BH, 1};

@@ -47,10 +47,11 @@ struct TailArgs {
   // stopped); gm != null: block 0 closes the Arnoldi step on the device (Givens, stop flag)
   const int* gate;
   pfc_gmres_dev* gm;
+  const double* dtp;   // graph path (f1): dt-dependent scalars on the device (dt_w0)
 };
 
 // J z at node (x, y): sum over the radius-3 diamond of W_class z + the 5-point -Delta(c z)
-__device__ __forceinline__ double jz_point(const TailArgs& p, int x, int y) {
+__device__ __forceinline__ double jz_point(const TailArgs& p, double W0, int x, int y) {
   const int nx = p.nx, ny = p.ny;
   int xs[7], ys[7];
 #pragma unroll
@@ -72,7 +73,7 @@ __device__ __forceinline__ double jz_point(const TailArgs& p, int x, int y) {
   const double s03 = (Z(-3, 0) + Z(3, 0)) + (Z(0, -3) + Z(0, 3));
   const double s12 = ((Z(-1, -2) + Z(1, -2)) + (Z(-2, -1) + Z(2, -1))) +
                      ((Z(-2, 1) + Z(2, 1)) + (Z(-1, 2) + Z(1, 2)));
-  double r = p.W[0] * z0;
+  double r = W0 * z0;
   r = fma(p.W[1], s01, r);
   r = fma(p.W[2], s02, r);
   r = fma(p.W[3], s11, r);
@@ -126,13 +127,14 @@ __global__ void __launch_bounds__(TT) k_arnoldi_tail(const __grid_constant__ Tai
   const size_t G = (size_t)gridDim.x * TT;
   const size_t g = (size_t)blockIdx.x * TT + threadIdx.x;
   const int j = p.j;
+  const double W0 = dt_w0<2>(p.dtp, p.W[0]);
   double w[MAXP];
   // ---- w = J z_j
 #pragma unroll
   for (int k = 0; k < MAXP; ++k) {
     const size_t q = g + k * G;
     w[k] = 0.0;
-    if (q < N) w[k] = jz_point(p, (int)(q % p.nx), (int)(q / p.nx));
+    if (q < N) w[k] = jz_point(p, W0, (int)(q % p.nx), (int)(q / p.nx));
   }
   // ---- pass 1: h1 = V^T w
   for (int i = 0; i <= j; ++i) {
@@ -287,6 +289,7 @@ cudaError_t launch_arnoldi_tail(pfc_ctx* ctx, const double* V, const double* z, 
   const double al = 0.5 * (1.0 - cf.gamma);
   // class weights of v/dt - alpha Delta v - Delta^2 v - Delta^3 v / 2
   p.W[0] = 1.0 / dt + 4.0 * al * ih2 - 20.0 * ih4 + 56.0 * ih6;
+  p.dtp = ctx->dtdev;
   p.W[1] = -al * ih2 + 8.0 * ih4 - 28.5 * ih6;
   p.W[2] = -ih4 + 6.0 * ih6;
   p.W[3] = -2.0 * ih4 + 12.0 * ih6;

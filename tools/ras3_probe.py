@@ -2,7 +2,7 @@
 per-apply time of the left-RAS apply on the cfg4 (128^3) and cfg5 (512^3) shapes, and the
 max relative difference of each variant's output against the column kernel's.
 
-usage: [RAS3_VARIANTS=col:2,cl2:1,cl2p:2] python tools/ras3_probe.py [128|512] [reps]
+usage: [RAS3_VARIANTS=col:2,cl2:1,cl2p:3,cq:3] python tools/ras3_probe.py [128|512] [reps]
 """
 import os
 import sys
@@ -24,8 +24,8 @@ ref = None
 variants = [tuple(v.split(":")) for v in
             os.environ.get("RAS3_VARIANTS", "col:2,cl2:1,cl2p:3").split(",")]
 for variant, nr in variants:
-    os.environ["PFC_RAS3D"] = "cl2" if variant == "cl2p" else variant
-    os.environ["PFC_CL2_CP"] = "2" if variant == "cl2p" else "1"
+    os.environ["PFC_RAS3D"] = "cl2" if variant in ("cl2p", "cq") else variant
+    os.environ["PFC_CL2_CP"] = {"cl2p": "2", "cq": "4"}.get(variant, "1")
     os.environ["PFC_CL2_NR"] = nr
     ctx = P.Context(cfg, n=shape)
     z = torch.empty_like(v)
