@@ -113,6 +113,8 @@ struct pfc_ctx {
   int ras_cluster = 1;
   int ras_rows = 0;
   int tail = 0;            // 2D small grids: fused J v + CGS2 + next vector (tail2d.cu)
+  int tail_rs = 0;         //   its tiled form: rows per thread (0: the gather form)
+  int tail_blocks = 0;     //   and co-resident tiles
   int ras3_col = 0;        // 3D: 2 = 2-CTA cluster kernel (ras3d_cl2.cu), 1 = column kernel
                            // (ras3d_col.cu), 0 = global-scratch kernel (ras3d.cu)
 

@@ -223,6 +223,200 @@ __global__ void __launch_bounds__(TT) k_arnoldi_tail(const __grid_constant__ Tai
   }
 }
 
+// Tiled variant (grids with n_x % 64 == 0): block b owns the 64 x 4RS tile (x0, y0) of the
+// grid, thread t the column x0 + t % 64, rows y0 + RS (t / 64) .. + RS - 1.  z (halo 3) and c
+// (halo 1) of the tile are staged in shared memory once, so J z is evaluated column by column
+// (the direct 25-point class weights + the 5-point -Delta(c z)) from shared memory with the
+// column's y-neighbours in registers, instead of 30 gathers per node through L1 with 64-bit
+// index arithmetic; the CGS2 passes then read V row-coalesced at the thread's own nodes.
+constexpr int TXT = 64;
+template <int RS>
+struct TileGeom {
+  static constexpr int TYT = 4 * RS, ZW = TXT + 6, ZH = TYT + 6, CW = TXT + 2, CH = TYT + 2;
+  static constexpr int SMEM = (ZW * ZH + CW * CH) * (int)sizeof(double);
+};
+
+template <int RS>
+__global__ void __launch_bounds__(TT, 2) k_arnoldi_tail_tile(const __grid_constant__ TailArgs p) {
+  if (p.gate && *p.gate) return;   // uniform: every block reads the same flag
+  using TG = TileGeom<RS>;
+  constexpr int TYT = TG::TYT, ZW = TG::ZW, ZH = TG::ZH, CW = TG::CW, CH = TG::CH;
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ __align__(16) double tile_sm[];
+  double* zt = tile_sm;             // z on the tile + halo 3
+  double* ct = tile_sm + ZW * ZH;   // c on the tile + halo 1
+  __shared__ double red[NWT * HS];
+  __shared__ double h1[HS], h2[HS], hx[2];
+  const int nx = p.nx, ny = p.ny;
+  const size_t N = p.N;
+  const int ntx = nx / TXT;
+  const int x0 = (blockIdx.x % ntx) * TXT, y0 = (blockIdx.x / ntx) * TYT;
+  for (int q = threadIdx.x; q < ZW * ZH; q += TT) {
+    const int r = q / ZW, cc = q - r * ZW;
+    const int gx = wrapi(x0 + cc - 3, nx), gy = wrapi(y0 + r - 3, ny);
+    zt[q] = __ldcg(p.z + (size_t)gx + (size_t)nx * gy);
+  }
+  for (int q = threadIdx.x; q < CW * CH; q += TT) {
+    const int r = q / CW, cc = q - r * CW;
+    const int gx = wrapi(x0 + cc - 1, nx), gy = wrapi(y0 + r - 1, ny);
+    ct[q] = __ldcg(p.c + (size_t)gx + (size_t)nx * gy);
+  }
+  const int j = p.j;
+  const double W0 = dt_w0<2>(p.dtp, p.W[0]);
+  const int tx = threadIdx.x % TXT, yr = (threadIdx.x / TXT) * RS;
+  const size_t g0 = (size_t)(x0 + tx) + (size_t)nx * (size_t)(y0 + yr);
+  __syncthreads();
+  double w[RS];
+  // ---- w = J z_j: linear part, column by column (rows yr - a .. yr + RS - 1 + a of column
+  // dx in registers), then -Delta(c z) from the 5-point neighbours
+  {
+#pragma unroll
+    for (int r = 0; r < RS; ++r) w[r] = 0.0;
+    const double* zc = zt + (yr + 3) * ZW + tx + 3;   // (row yr, column tx) of the z tile
+#pragma unroll
+    for (int dx = -3; dx <= 3; ++dx) {
+      const int a = 3 - (dx < 0 ? -dx : dx);
+      double col[RS + 6];
+#pragma unroll
+      for (int rr = -a; rr < RS + a; ++rr) col[rr + a] = zc[rr * ZW + dx];
+#pragma unroll
+      for (int r = 0; r < RS; ++r)
+#pragma unroll
+        for (int dy = -a; dy <= a; ++dy) {
+          const int ax = dx < 0 ? -dx : dx, ay = dy < 0 ? -dy : dy;
+          const int cls = (ax + ay == 0) ? 0 : (ax + ay == 1) ? 1 : (ax == 1 && ay == 1) ? 3
+                          : (ax + ay == 2) ? 2 : (ax + ay == 3 && (ax == 0 || ay == 0)) ? 4 : 5;
+          w[r] = fma(cls == 0 ? W0 : p.W[cls], col[r + dy + a], w[r]);
+        }
+    }
+    const double* cc = ct + (yr + 1) * CW + tx + 1;
+    double czo[RS + 2];   // c z of the own column, rows -1 .. RS
+#pragma unroll
+    for (int rr = -1; rr <= RS; ++rr) czo[rr + 1] = cc[rr * CW] * zc[rr * ZW];
+#pragma unroll
+    for (int r = 0; r < RS; ++r) {
+      const double lap = (cc[r * CW - 1] * zc[r * ZW - 1] + cc[r * CW + 1] * zc[r * ZW + 1]) +
+                         (czo[r] + czo[r + 2]) - 4.0 * czo[r + 1];
+      w[r] = fma(-p.ih2, lap, w[r]);
+    }
+  }
+  // ---- pass 1: h1 = V^T w
+  for (int i = 0; i <= j; ++i) {
+    const double* Vi = p.V + (size_t)i * N + g0;
+    double s = 0.0;
+#pragma unroll
+    for (int r = 0; r < RS; ++r) s = fma(__ldcg(Vi + (size_t)r * nx), w[r], s);
+    block_put(s, i, red);
+  }
+  __syncthreads();
+  block_flush(j + 1, red, p.partials);
+  grid.sync();
+  grid_total(j + 1, p.partials, h1);
+  // ---- pass 2: w <- w - V h1, h2 = V^T w, |w|^2
+  for (int i = 0; i <= j; ++i) {
+    const double* Vi = p.V + (size_t)i * N + g0;
+    const double hi = h1[i];
+#pragma unroll
+    for (int r = 0; r < RS; ++r) w[r] = fma(-hi, __ldcg(Vi + (size_t)r * nx), w[r]);
+  }
+  for (int i = 0; i <= j; ++i) {
+    const double* Vi = p.V + (size_t)i * N + g0;
+    double s = 0.0;
+#pragma unroll
+    for (int r = 0; r < RS; ++r) s = fma(__ldcg(Vi + (size_t)r * nx), w[r], s);
+    block_put(s, i, red);
+  }
+  {
+    double s = 0.0;
+#pragma unroll
+    for (int r = 0; r < RS; ++r) s = fma(w[r], w[r], s);
+    block_put(s, j + 1, red);
+  }
+  __syncthreads();
+  block_flush(j + 2, red, p.partials);
+  grid.sync();
+  grid_total(j + 2, p.partials, h2);
+  // ---- pass 3: w <- w - V h2, |w|^2
+  for (int i = 0; i <= j; ++i) {
+    const double* Vi = p.V + (size_t)i * N + g0;
+    const double hi = h2[i];
+#pragma unroll
+    for (int r = 0; r < RS; ++r) w[r] = fma(-hi, __ldcg(Vi + (size_t)r * nx), w[r]);
+  }
+  {
+    double s = 0.0;
+#pragma unroll
+    for (int r = 0; r < RS; ++r) s = fma(w[r], w[r], s);
+    block_put(s, 0, red);
+  }
+  __syncthreads();
+  block_flush(1, red, p.partials);
+  grid.sync();
+  grid_total(1, p.partials, hx);
+  // ---- v_{j+1} = w / |w| (written unless |w| = 0; the host checks breakdown)
+  const double nrm2 = hx[0];
+  if (nrm2 > 0.0) {
+    const double ihn = 1.0 / sqrt(nrm2);
+#pragma unroll
+    for (int r = 0; r < RS; ++r) p.vnext[g0 + (size_t)r * nx] = ihn * w[r];
+  }
+  if (blockIdx.x == 0) {
+    for (int i = threadIdx.x; i <= j; i += TT) {
+      p.out[i] = h1[i];
+      p.out[32 + i] = h2[i];
+    }
+    if (threadIdx.x == 0) {
+      p.out[64] = nrm2;
+      if (p.gm) arnoldi_close(p.gm, j, h1, h2, nrm2);
+    }
+  }
+}
+
+typedef void (*tail_tile_fn)(const TailArgs);
+
+tail_tile_fn pick_tail_tile(int rs, int* smem) {
+  switch (rs) {
+#define TTC(R) case R: *smem = TileGeom<R>::SMEM; return k_arnoldi_tail_tile<R>;
+    TTC(1) TTC(2) TTC(4) TTC(8) TTC(16)
+#undef TTC
+  }
+  return nullptr;
+}
+
+// tiled plan: the smallest rows-per-thread RS whose tiles are all co-resident; 0 if none
+int tail_tile_plan(pfc_ctx* ctx, int* blocks, int* rs_out, int* smem_out) {
+  const int nx = ctx->cfg.n[0], ny = ctx->cfg.n[1];
+  const char* e = getenv("PFC_TAIL_TILE");
+  if ((e && e[0] == '0') || nx % TXT != 0) return 0;
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
+  for (int rs = 1; rs <= 16; rs *= 2) {
+    if (ny % (4 * rs) != 0) continue;
+    int smem = 0;
+    tail_tile_fn fn = pick_tail_tile(rs, &smem);
+    if (!fn) continue;
+    if (cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
+        cudaSuccess) {
+      cudaGetLastError();
+      continue;
+    }
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, TT, smem) != cudaSuccess ||
+        per_sm < 1) {
+      cudaGetLastError();
+      continue;
+    }
+    const long need = (long)(nx / TXT) * (ny / (4 * rs));
+    if (need <= (long)sms * per_sm) {
+      *blocks = (int)need;
+      *rs_out = rs;
+      *smem_out = smem;
+      return 1;
+    }
+  }
+  return 0;
+}
+
 typedef void (*tail_fn)(const TailArgs);
 
 tail_fn pick_tail(int maxp) {
@@ -270,7 +464,13 @@ int tail_enabled(pfc_ctx* ctx) {
   const char* e = getenv("PFC_TAIL");
   if (e && e[0] == '0') return 0;
   if (c.ndim != 2 || generic_path(c) || c.gmres_restart + 1 > HS) return 0;
-  int b = 0, mp = 0;
+  int b = 0, mp = 0, sm = 0;
+  ctx->tail_rs = 0;
+  if (tail_tile_plan(ctx, &b, &mp, &sm)) {
+    ctx->tail_rs = mp;
+    ctx->tail_blocks = b;
+    return 1;
+  }
   return tail_plan(ctx, &b, &mp) ? 1 : 0;
 }
 
@@ -281,7 +481,7 @@ cudaError_t launch_arnoldi_tail(pfc_ctx* ctx, const double* V, const double* z, 
                                 pfc_gmres_dev* gm) {
   const pfc_config& cf = ctx->cfg;
   int blocks = 0, maxp = 0;
-  if (!tail_plan(ctx, &blocks, &maxp)) return cudaErrorInvalidValue;
+  if (!ctx->tail_rs && !tail_plan(ctx, &blocks, &maxp)) return cudaErrorInvalidValue;
   TailArgs p{};
   p.V = V; p.z = z; p.c = c; p.vnext = vnext; p.partials = ctx->partials; p.out = out;
   p.N = ctx->N; p.nx = cf.n[0]; p.ny = cf.n[1]; p.j = j;
@@ -299,8 +499,16 @@ cudaError_t launch_arnoldi_tail(pfc_ctx* ctx, const double* V, const double* z, 
   p.gate = ctx->gate;
   p.gm = gm;
   void* args[] = {&p};
-  cudaError_t e = cudaLaunchCooperativeKernel((const void*)pick_tail(maxp), dim3(blocks),
-                                              dim3(TT), args, 0, ctx->stream);
+  cudaError_t e;
+  if (ctx->tail_rs) {   // tiled J z (shared memory; plan made once by tail_enabled)
+    int tsm = 0;
+    tail_tile_fn fn = pick_tail_tile(ctx->tail_rs, &tsm);
+    e = cudaLaunchCooperativeKernel((const void*)fn, dim3(ctx->tail_blocks), dim3(TT), args,
+                                    (size_t)tsm, ctx->stream);
+  }
+  else
+    e = cudaLaunchCooperativeKernel((const void*)pick_tail(maxp), dim3(blocks), dim3(TT), args, 0,
+                                    ctx->stream);
   ctx->launches++;
   {  // algorithmic: z (25-pt) + c read once, V read 3 (j+1) times, v_{j+1} written
     const double n = (double)ctx->N, jj = j + 1;
