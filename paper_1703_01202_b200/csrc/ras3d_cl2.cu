@@ -1132,6 +1132,508 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cl2p<E>::NT, 1)
   cl_sync();   // no CTA leaves while its partner may still address its shared memory
 }
 
+
+// ---- tensor memory as basis storage (ras3d_cl2t_kernel): tcgen05.st / tcgen05.ld of the
+// 32x32b shape move each thread's own TMEM lane row (32-bit columns); a double is two columns.
+// Measured on this pool (tools/tmem_probe.cu, 8 warps): tcgen05.ld 427 B/clk/SM with a wait
+// after every x16, tcgen05.st 977 B/clk/SM -- 3x and 7x the 128 B/clk of shared memory.
+__device__ __forceinline__ void tm_alloc512(uint32_t* dst) {   // one warp
+  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                   smem_u32(dst))
+               : "memory");
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tm_dealloc512(uint32_t base) {   // the allocating warp
+  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(base) : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tm_st16(uint32_t ta, const uint32_t* r) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+      "%14,%15,%16};" ::"r"(ta),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),
+      "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+      : "memory");
+}
+__device__ __forceinline__ void tm_st8(uint32_t ta, const uint32_t* r) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(ta),
+               "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]),
+               "r"(r[7])
+               : "memory");
+}
+// load + wait in one statement: the registers are valid when the statement ends
+__device__ __forceinline__ void tm_ld16(uint32_t ta, uint32_t* v) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
+      "%15}, [%16];\n\ttcgen05.wait::ld.sync.aligned;"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+        "=r"(v[14]), "=r"(v[15])
+      : "r"(ta)
+      : "memory");
+}
+__device__ __forceinline__ void tm_ld8(uint32_t ta, uint32_t* v) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n\t"
+      "tcgen05.wait::ld.sync.aligned;"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+        "=r"(v[7])
+      : "r"(ta)
+      : "memory");
+}
+// a thread's 2 x ZL doubles <-> 4 ZL columns at ta (chunks of 16 columns, then 8)
+template <int ZL>
+__device__ __forceinline__ void tm_st_vec(uint32_t ta, const double (&w)[2][ZL]) {
+  constexpr int NC = 4 * ZL;
+  static_assert(NC % 8 == 0, "columns in chunks of 8");
+  uint32_t r[NC];
+#pragma unroll
+  for (int k = 0; k < 2 * ZL; ++k) {
+    const double d = w[k / ZL][k % ZL];
+    r[2 * k] = (uint32_t)__double2loint(d);
+    r[2 * k + 1] = (uint32_t)__double2hiint(d);
+  }
+#pragma unroll
+  for (int c = 0; c + 16 <= NC; c += 16) tm_st16(ta + c, r + c);
+  if constexpr (NC % 16 == 8) tm_st8(ta + (NC - 8), r + (NC - 8));
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
+template <int ZL>
+__device__ __forceinline__ void tm_ld_vec(uint32_t ta, double (&v)[2][ZL]) {
+  constexpr int NC = 4 * ZL;
+  uint32_t r[NC];
+#pragma unroll
+  for (int c = 0; c + 16 <= NC; c += 16) tm_ld16(ta + c, r + c);
+  if constexpr (NC % 16 == 8) tm_ld8(ta + (NC - 8), r + (NC - 8));
+#pragma unroll
+  for (int k = 0; k < 2 * ZL; ++k)
+    v[k / ZL][k % ZL] = __hiloint2double((int)r[2 * k + 1], (int)r[2 * k]);
+}
+
+// Cl2p with the basis vectors NR..K-2 in tensor memory instead of shared memory (NS) and the
+// L2 scratch (NG): the whole Krylov basis on chip.  Same layouts, same arithmetic in the same
+// order (bitwise identical to ras3d_cl2p_kernel), the CGS2 passes vector by vector.
+template <int K, int E, int NRX>
+constexpr size_t cl2t_smem_doubles() {
+  using C = Cl2p<E>;
+  return (size_t)C::NVB * C::PP + (size_t)C::NCB * C::CP + 2 * 2 * C::NW * RS + C::NW * 3 * RS;
+}
+
+template <int K, int E, int NRX>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cl2p<E>::NT, 1)
+    ras3d_cl2t_kernel(const __grid_constant__ Ras3Cl2Args p) {
+  if (p.gate && *p.gate) return;     // uniform over the cluster: both CTAs leave at once
+  using C = Cl2p<E>;
+  constexpr int ZL = C::ZL, PL = C::PL, NW = C::NW, NTN = C::NTN;
+  constexpr int PX = C::PX, PP = C::PP, CX = C::CX, CP = C::CP, NVB = C::NVB, NCB = C::NCB;
+  constexpr int NR = Cl2pK<K, NRX>::NR, NS = 0, NG = 0;
+  constexpr int NTM = K - 1 - NR;              // basis vectors NR..K-2 in tensor memory
+  constexpr int TMC = 4 * ZL;                  // TMEM columns per vector (2 x ZL doubles)
+  static_assert(NTM * TMC <= 256, "two warps share a TMEM lane quarter: 256 columns each");
+  constexpr int NE = E * E * E;
+  extern __shared__ __align__(128) double smem_dyn[];
+  double* vb = smem_dyn;                 // NVB padded planes of v_j (rank 0: zl in [0, ZL+3),
+                                         // rank 1: [-3, ZL))
+  double* cb = vb + NVB * PP;            // NCB padded planes of c' (rank 0: [0, ZL], rank 1:
+                                         // [-1, ZL))
+  double* vs = cb + NCB * CP;            // NS x [col][zl][thread]: basis vectors NR..NR+NS-1
+  double* red = vs + NS * 2 * ZL * NTN;  // 2 buffers x [rank][warp][RS]
+  double* hw = red + 2 * 2 * NW * RS;    // per warp: h1, h2, scratch
+  __shared__ double H[(K + 1) * K];
+  __shared__ double gv[K + 1], cs[K], sn[K], yv[K];
+  __shared__ __align__(8) uint64_t mbar[3];
+  __shared__ uint32_t tm_base;
+
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const bool g0 = wid == NW - 1 && lane == 0;
+  const int rank = (int)cluster_rank(), partner = rank ^ 1;
+  const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+  const bool act = tid < NTN;
+  const int x = act ? tid % E : 0, y0 = act ? 2 * (tid / E) : 0;
+  const int colp = (y0 + 3) * PX + (x + 3);        // padded v column of (x, y0)
+  const int colc = (y0 + 1) * CX + (x + 1);        // padded c' column of (x, y0)
+  const int pv0 = rank == 0 ? 0 : 3, pc0 = rank == 0 ? 0 : 1;   // plane of zl = 0
+  const double* pv = vb + pv0 * PP + colp;
+  const double* pc = cb + pc0 * CP + colc;
+  double* gs = p.gscr + (size_t)blockIdx.x * (NG > 0 ? NG : 1) * 2 * ZL * NTN + tid;
+  double* h1 = hw + wid * 3 * RS;
+  double* h2 = h1 + RS;
+  double* hx = h2 + RS;
+  const uint32_t red_rem = mapa_rank(smem_u32(red), (uint32_t)partner);
+  const uint32_t vb_rem = mapa_rank(smem_u32(vb), (uint32_t)partner);
+  const int nbx = p.nx / p.bx, nby = p.ny / p.by, nbz = p.nz / p.bz;
+  const int nboxes = nbx * nby * nbz;
+  const size_t NX = p.nx, NXY = (size_t)p.nx * p.ny;
+
+  int rb = 0;
+  const uint32_t mbar_rem0 = mapa_rank(smem_u32(&mbar[0]), (uint32_t)partner);
+  // zero v planes (ring stays zero) and finite c'
+  for (int q = tid; q < NVB * PP + NCB * CP; q += blockDim.x) vb[q] = 0.0;
+  if (tid == 0) {
+    for (int q = 0; q < 3; ++q) mbar_init(&mbar[q], 1);
+    fence_mbar_init();
+  }
+  if (wid == 0) tm_alloc512(&tm_base);   // all 512 columns (one CTA per SM: registers)
+  tc_fence_before();
+  cl_sync();   // the partner is running, zeroed and its mbarriers initialised before any DSMEM store
+  tc_fence_after();
+  // this thread's TMEM row: lane quarter of its warp, column half by warp pair (w, w + 4)
+  const uint32_t tma = tm_base + ((uint32_t)(32 * (wid & 3)) << 16) + (uint32_t)(256 * (wid >> 2));
+  {  // finite basis slots: the final V y reads every slot, with a zero coefficient beyond the
+     // steps taken
+    double zr[2][ZL];
+#pragma unroll
+    for (int c = 0; c < 2; ++c)
+#pragma unroll
+      for (int zl = 0; zl < ZL; ++zl) zr[c][zl] = 0.0;
+#pragma unroll
+    for (int s = 0; s < NTM; ++s) tm_st_vec<ZL>(tma + (uint32_t)(s * TMC), zr);
+  }
+#ifdef CL2_PROF
+  long long c2p_acc[16] = {0}, c2p_last = clock64();
+#endif
+  uint32_t ph = 0;
+  constexpr uint32_t HALO_BYTES = (uint32_t)PL * 3u * 8u;
+  auto reduce = [&](int nsent, int nget, double* hwv) {
+    if (tid == 0) mbar_expect_tx(&mbar[rb], (uint32_t)(NW * nsent * 8));
+    __syncthreads();
+    mbar_wait_cluster(&mbar[rb], (ph >> rb) & 1u);
+    ph ^= 1u << rb;
+    cl2_get<NW>(nget, red + rb * 2 * NW * RS, hwv, lane);
+    rb ^= 1;
+  };
+
+  double vr[NR > 0 ? NR : 1][2][ZL];
+#pragma unroll
+  for (int s = 0; s < (NR > 0 ? NR : 1); ++s)
+#pragma unroll
+    for (int c = 0; c < 2; ++c)
+#pragma unroll
+      for (int zl = 0; zl < ZL; ++zl) vr[s][c][zl] = 0.0;
+  for (int box = cid; box < nboxes; box += ncl) {
+    const int ibx = box % nbx, iby = (box / nbx) % nby, ibz = box / (nbx * nby);
+    const int gx0 = ibx * p.bx - p.o, gy0 = iby * p.by - p.o, gz0 = ibz * p.bz - p.o;
+    const int ez0 = rank * ZL;
+    double w[2][ZL];
+    double acc = 0.0;
+    if (act) {
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        const int y = y0 + c;
+        const size_t gxy = (size_t)wrapi(gx0 + x, p.nx) + NX * wrapi(gy0 + y, p.ny);
+        const bool oxy = x >= p.o && x < p.o + p.bx && y >= p.o && y < p.o + p.by;
+        int gz = wrapi(gz0 + ez0, p.nz);   // wrapped z of own plane 0, advanced without '%'
+#pragma unroll
+        for (int zl = 0; zl < ZL; ++zl, gz = gz + 1 == p.nz ? 0 : gz + 1) {
+          const size_t g = gxy + NXY * (size_t)gz;
+          const int ez = ez0 + zl;
+          const bool owned = oxy && ez >= p.o && ez < p.o + p.bz;
+          w[c][zl] = (p.restrict_owned && !owned) ? 0.0 : p.v[g];
+          cb[(zl + pc0) * CP + colc + c * CX] = -p.ih2 * p.c[g];
+          acc = fma(w[c][zl], w[c][zl], acc);
+        }
+        const int zh = rank == 0 ? ZL : -1;
+        cb[(zh + pc0) * CP + colc + c * CX] =
+            -p.ih2 * p.c[gxy + NXY * wrapi(gz0 + ez0 + zh, p.nz)];
+      }
+    } else {
+#pragma unroll
+      for (int c = 0; c < 2; ++c)
+#pragma unroll
+        for (int zl = 0; zl < ZL; ++zl) w[c][zl] = 0.0;
+    }
+    double* redb = red + rb * 2 * NW * RS;
+    uint32_t redr = red_rem + (uint32_t)(rb * 2 * NW * RS) * 8u;
+    uint32_t mbr = mbar_rem0 + 8u * rb;
+    C2P(0);
+    cl2_put<NW>(acc, 0, redb, redr, mbr, rank, wid, lane);
+    reduce(1, 1, hx);
+    C2P(1);
+    const double beta = sqrt(hx[0]);
+    if (beta == 0.0) {
+      if (act) {
+#pragma unroll
+        for (int c = 0; c < 2; ++c)
+#pragma unroll
+          for (int zl = 0; zl < ZL; ++zl) {
+            const int y = y0 + c;
+            const int ez = ez0 + zl, li = x - p.o, lj = y - p.o, lk = ez - p.o;
+            if (p.y_ext) p.y_ext[(size_t)box * NE + (ez * E + y) * E + x] = 0.0;
+            else if (li >= 0 && li < p.bx && lj >= 0 && lj < p.by && lk >= 0 && lk < p.bz)
+              p.z[(size_t)(ibx * p.bx + li) + NX * (iby * p.by + lj) + NXY * (ibz * p.bz + lk)] = 0.0;
+          }
+      }
+      if (tid == 0 && rank == 0) ras_count(p.jcnt, 0);
+      continue;
+    }
+    auto put_v = [&](int slot) {
+      // tensor memory: warp-collective, every lane (inactive lanes store their zero w)
+      if (slot >= NR && slot < K - 1) tm_st_vec<ZL>(tma + (uint32_t)((slot - NR) * TMC), w);
+      if (!act) return;
+#pragma unroll
+      for (int s = 0; s < NR; ++s)
+        if (s == slot) {
+#pragma unroll
+          for (int c = 0; c < 2; ++c)
+#pragma unroll
+            for (int zl = 0; zl < ZL; ++zl) vr[s][c][zl] = w[c][zl];
+        }
+#pragma unroll
+      for (int c = 0; c < 2; ++c)
+#pragma unroll
+        for (int zl = 0; zl < ZL; ++zl) vb[(zl + pv0) * PP + colp + c * PX] = w[c][zl];
+      const uint32_t hm = mbar_rem0 + 16u;
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        if (rank == 0) {
+#pragma unroll
+          for (int q = 0; q < 3; ++q)
+            st_async(vb_rem + (uint32_t)(q * PP + colp + c * PX) * 8u, w[c][ZL - 3 + q], hm);
+        } else {
+#pragma unroll
+          for (int q = 0; q < 3; ++q)
+            st_async(vb_rem + (uint32_t)((ZL + q) * PP + colp + c * PX) * 8u, w[c][q], hm);
+        }
+      }
+    };
+    // basis vector i of the thread's 2 x ZL nodes: registers (i < NR), tensor memory (NR <= i <
+    // K-1, warp-collective load: called by every lane) or the stencil planes (i = K-1)
+    auto getv = [&](int i, double (&vt)[2][ZL]) {   // (i a constant after unrolling)
+      if (i < NR) {
+#pragma unroll
+        for (int c = 0; c < 2; ++c)
+#pragma unroll
+          for (int zl = 0; zl < ZL; ++zl) vt[c][zl] = vr[i < NR ? i : 0][c][zl];
+      } else if (i < K - 1) {
+        tm_ld_vec<ZL>(tma + (uint32_t)((i - NR) * TMC), vt);
+      } else {
+#pragma unroll
+        for (int c = 0; c < 2; ++c)
+#pragma unroll
+          for (int zl = 0; zl < ZL; ++zl) vt[c][zl] = pv[zl * PP + c * PX];
+      }
+    };
+    {
+      const double ib = 1.0 / beta;
+#pragma unroll
+      for (int c = 0; c < 2; ++c)
+#pragma unroll
+        for (int zl = 0; zl < ZL; ++zl) w[c][zl] *= ib;
+      put_v(0);
+    }
+    if (g0) gv[0] = beta;
+    int jm = 0;
+    double hn_prev = 0.0;
+#pragma unroll 1
+    for (int j = 0; j < K; ++j) {
+      C2P(10);
+      if (tid == 0) mbar_expect_tx(&mbar[2], HALO_BYTES);
+      __syncthreads();
+      C2P(2);
+      if (g0 && j > 0) givens_col(j - 1, h1, h2, hn_prev, H, cs, sn, gv, K + 1);
+#pragma unroll
+      for (int c = 0; c < 2; ++c)
+#pragma unroll
+        for (int zl = 0; zl < ZL; ++zl) w[c][zl] = 0.0;
+      if (act) cl2p_stencil<E, 0, ZL>(p, pv, pc, w);
+      C2P(3);
+      mbar_wait_cluster(&mbar[2], (ph >> 2) & 1u);
+      ph ^= 4u;
+      C2P(4);
+      if (act) {
+        if (rank == 0) cl2p_stencil<E, ZL, ZL + 3>(p, pv, pc, w);
+        else cl2p_stencil<E, -3, 0>(p, pv, pc, w);
+      }
+      C2P(5);
+      double hn2 = 0.0;
+      auto cgs2 = [&](auto Jc) {
+        constexpr int J = decltype(Jc)::value;
+        redb = red + rb * 2 * NW * RS;
+        redr = red_rem + (uint32_t)(rb * 2 * NW * RS) * 8u;
+        mbr = mbar_rem0 + 8u * rb;
+        {
+          double acc[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) acc[i] = 0.0;
+          // vector by vector (each acc[i] sums the nodes in the same order as cl2p)
+          #pragma unroll
+          for (int I = 0; I < J + 1; ++I) {
+            double vt[2][ZL];
+            getv(I, vt);
+            if (act) {
+#pragma unroll
+              for (int c = 0; c < 2; ++c)
+#pragma unroll
+                for (int zl = 0; zl < ZL; ++zl) acc[I] = fma(vt[c][zl], w[c][zl], acc[I]);
+            }
+          }
+          C2P(11);
+          cl2_put_multi<NW>(acc, J + 1, redb, redr, mbr, rank, wid, lane);
+        }
+        reduce(J + 1, J + 1, h1);
+        C2P(12);
+        redb = red + rb * 2 * NW * RS;
+        redr = red_rem + (uint32_t)(rb * 2 * NW * RS) * 8u;
+        mbr = mbar_rem0 + 8u * rb;
+        {
+          double hv[J + 1], acc[16], nrm = 0.0;
+#pragma unroll
+          for (int i = 0; i <= J; ++i) hv[i] = h1[i];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) acc[i] = 0.0;
+          // w <- w - V h1 (per node in the order i = 0..J), then h2 = V^T w and |w|^2
+          #pragma unroll
+          for (int I = 0; I < J + 1; ++I) {
+            double vt[2][ZL];
+            getv(I, vt);
+            if (act) {
+#pragma unroll
+              for (int c = 0; c < 2; ++c)
+#pragma unroll
+                for (int zl = 0; zl < ZL; ++zl) w[c][zl] = fma(-hv[I], vt[c][zl], w[c][zl]);
+            }
+          }
+          #pragma unroll
+          for (int I = 0; I < J + 1; ++I) {
+            double vt[2][ZL];
+            getv(I, vt);
+            if (act) {
+#pragma unroll
+              for (int c = 0; c < 2; ++c)
+#pragma unroll
+                for (int zl = 0; zl < ZL; ++zl) acc[I] = fma(vt[c][zl], w[c][zl], acc[I]);
+            }
+          }
+          if (act) {
+#pragma unroll
+            for (int c = 0; c < 2; ++c)
+#pragma unroll
+              for (int zl = 0; zl < ZL; ++zl) nrm = fma(w[c][zl], w[c][zl], nrm);
+          }
+          C2P(13);
+          cl2_put_multi<NW>(acc, J + 1, redb, redr, mbr, rank, wid, lane);
+          cl2_put<NW>(nrm, J + 1, redb, redr, mbr, rank, wid, lane);
+        }
+        reduce(J + 2, J + 2, h2);
+        C2P(14);
+        double h2n = 0.0;
+        for (int i = 0; i <= J; ++i) h2n += h2[i] * h2[i];
+        const double wn2 = h2[J + 1];
+        {
+          double hv[J + 1];
+#pragma unroll
+          for (int i = 0; i <= J; ++i) hv[i] = h2[i];
+          #pragma unroll
+          for (int I = 0; I < J + 1; ++I) {
+            double vt[2][ZL];
+            getv(I, vt);
+            if (act) {
+#pragma unroll
+              for (int c = 0; c < 2; ++c)
+#pragma unroll
+                for (int zl = 0; zl < ZL; ++zl) w[c][zl] = fma(-hv[I], vt[c][zl], w[c][zl]);
+            }
+          }
+        }
+        if (h2n <= 1e-8 * wn2) {
+          hn2 = wn2 - h2n;
+        } else {
+          redb = red + rb * 2 * NW * RS;
+          redr = red_rem + (uint32_t)(rb * 2 * NW * RS) * 8u;
+          mbr = mbar_rem0 + 8u * rb;
+          double s = 0.0;
+          if (act) {
+#pragma unroll
+            for (int c = 0; c < 2; ++c)
+#pragma unroll
+              for (int zl = 0; zl < ZL; ++zl) s = fma(w[c][zl], w[c][zl], s);
+          }
+          cl2_put<NW>(s, 0, redb, redr, mbr, rank, wid, lane);
+          reduce(1, 1, hx);
+          hn2 = hx[0];
+        }
+        return hn2;
+      };
+      dispatch_j<K>(j, cgs2);
+      C2P(6);
+      const double hn = sqrt(hn2 > 0.0 ? hn2 : 0.0);
+      hn_prev = hn;
+      jm = j + 1;
+      if (hn <= 1e-14 * beta) break;
+      if (j + 1 < K) {
+        const double ihn = 1.0 / hn;
+#pragma unroll
+        for (int c = 0; c < 2; ++c)
+#pragma unroll
+          for (int zl = 0; zl < ZL; ++zl) w[c][zl] *= ihn;
+        put_v(j + 1);
+      }
+    }
+    C2P(10);
+    if (g0) {
+      const int ld = K + 1;
+      givens_col(jm - 1, h1, h2, hn_prev, H, cs, sn, gv, ld);
+      for (int i = jm - 1; i >= 0; --i) {
+        double s = gv[i];
+        for (int l = i + 1; l < jm; ++l) s -= H[i + ld * l] * yv[l];
+        yv[i] = s / H[i + ld * i];
+      }
+      for (int i = jm; i < K; ++i) yv[i] = 0.0;   // steps not taken: zero coefficients
+      if (rank == 0) ras_count(p.jcnt, jm);
+    }
+    __syncthreads();
+    C2P(7);
+    {   // (every lane: the tensor-memory loads are warp-collective; only node lanes store)
+      // y = V yv over every slot (fma(0, v, s) = s exactly for the finite unused slots)
+      double yl[2][ZL];
+#pragma unroll
+      for (int c = 0; c < 2; ++c)
+#pragma unroll
+        for (int zl = 0; zl < ZL; ++zl) yl[c][zl] = 0.0;
+      #pragma unroll
+      for (int I = 0; I < K; ++I) {
+        double vt[2][ZL];
+        getv(I, vt);
+        const double yi = yv[I];
+#pragma unroll
+        for (int c = 0; c < 2; ++c)
+#pragma unroll
+          for (int zl = 0; zl < ZL; ++zl) yl[c][zl] = fma(yi, vt[c][zl], yl[c][zl]);
+      }
+#pragma unroll
+      for (int c = 0; c < 2 && act; ++c) {
+        const int y = y0 + c;
+#pragma unroll
+        for (int zl = 0; zl < ZL; ++zl) {
+          const int ez = ez0 + zl, li = x - p.o, lj = y - p.o, lk = ez - p.o;
+          if (p.y_ext) {
+            p.y_ext[(size_t)box * NE + (ez * E + y) * E + x] = yl[c][zl];
+          } else if (li >= 0 && li < p.bx && lj >= 0 && lj < p.by && lk >= 0 && lk < p.bz) {
+            p.z[(size_t)(ibx * p.bx + li) + NX * (iby * p.by + lj) + NXY * (ibz * p.bz + lk)] =
+                yl[c][zl];
+          }
+        }
+      }
+    }
+    C2P(9);
+  }
+  C2P(8);
+#ifdef CL2_PROF
+  if (blockIdx.x == 0 && tid == 0)
+    for (int i = 0; i < 16; ++i) cl2_prof[i] += c2p_acc[i];
+#endif
+  tc_fence_before();
+  cl_sync();   // no CTA leaves while its partner may still address its shared memory
+  tc_fence_after();
+  if (wid == 0) tm_dealloc512(tm_base);
+}
+
+
 typedef void (*ras3cl2_fn)(const Ras3Cl2Args);
 
 // NR = basis vectors in registers (1, 2 or 3; PFC_CL2_NR selects, default 1: measured fastest)
@@ -1141,13 +1643,29 @@ int cl2_nr() {
 }
 
 // columns per thread: 1 (ras3d_cl2_kernel) or 2 (ras3d_cl2p_kernel); PFC_CL2_CP selects
-int cl2_cp() {   // default 2: measured 39.3 vs 50.1 ms per 512^3 apply (round 2)
+int cl2_cp() {   // default 3: the two-column kernel with the basis in tensor memory
+                 // (ras3d_cl2t_kernel), 37.6 ms per 512^3 apply vs 39.2 ms (2, shared memory +
+                 // L2 scratch) vs 50.1 ms (1)
   const char* e = getenv("PFC_CL2_CP");
-  return e && e[0] == '1' ? 1 : 2;
+  return e && e[0] == '1' ? 1 : (e && e[0] == '2') ? 2 : 3;
 }
 
 ras3cl2_fn pick_cl2(int k, int e, size_t* smem, int* threads, int* ng) {
   const int nr = cl2_nr();
+  if (cl2_cp() == 3) {
+    const char* en = getenv("PFC_CL2_NR");
+    const int nr2 = en ? atoi(en) : 3;
+#define C2T(K, E, NR)                                               \
+    if (k == K && e == E && nr2 == NR) {                            \
+      *smem = cl2t_smem_doubles<K, E, NR>() * sizeof(double);       \
+      *threads = Cl2p<E>::NT;                                       \
+      *ng = 0;                                                      \
+      return ras3d_cl2t_kernel<K, E, NR>;                           \
+    }
+    C2T(10, 20, 3) C2T(4, 20, 3) C2T(10, 12, 3) C2T(4, 12, 3)
+#undef C2T
+    return nullptr;
+  }
   if (cl2_cp() == 2) {
     const char* en = getenv("PFC_CL2_NR");
     const int nr2 = en ? atoi(en) : 3;   // measured fastest (NR = 4 spills at 255 registers)

@@ -24,8 +24,8 @@ ref = None
 variants = [tuple(v.split(":")) for v in
             os.environ.get("RAS3_VARIANTS", "col:2,cl2:1,cl2p:3").split(",")]
 for variant, nr in variants:
-    os.environ["PFC_RAS3D"] = "cl2" if variant in ("cl2p", "cq") else variant
-    os.environ["PFC_CL2_CP"] = {"cl2p": "2", "cq": "4"}.get(variant, "1")
+    os.environ["PFC_RAS3D"] = "cl2" if variant in ("cl2p", "cq", "cl2t") else variant
+    os.environ["PFC_CL2_CP"] = {"cl2p": "2", "cq": "4", "cl2t": "3"}.get(variant, "1")
     os.environ["PFC_CL2_NR"] = nr
     ctx = P.Context(cfg, n=shape)
     z = torch.empty_like(v)
