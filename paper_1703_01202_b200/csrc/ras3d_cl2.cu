@@ -1203,21 +1203,45 @@ __device__ __forceinline__ void tm_st_vec(uint32_t ta, const double (&w)[2][ZL])
   if constexpr (NC % 16 == 8) tm_st8(ta + (NC - 8), r + (NC - 8));
   asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
 }
+// 40 columns (ZL = 10) in one statement: three loads, one wait (one TMEM round trip)
+__device__ __forceinline__ void tm_ld40(uint32_t ta, uint32_t* v) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
+      "%15}, [%40];\n\t"
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,"
+      "%28,%29,%30,%31}, [%41];\n\t"
+      "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%32,%33,%34,%35,%36,%37,%38,%39}, [%42];\n\t"
+      "tcgen05.wait::ld.sync.aligned;"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+        "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]),
+        "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]),
+        "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31]),
+        "=r"(v[32]), "=r"(v[33]), "=r"(v[34]), "=r"(v[35]), "=r"(v[36]), "=r"(v[37]),
+        "=r"(v[38]), "=r"(v[39])
+      : "r"(ta), "r"(ta + 16), "r"(ta + 32)
+      : "memory");
+}
 template <int ZL>
 __device__ __forceinline__ void tm_ld_vec(uint32_t ta, double (&v)[2][ZL]) {
   constexpr int NC = 4 * ZL;
   uint32_t r[NC];
+  if constexpr (NC == 40) {
+    tm_ld40(ta, r);
+  } else {
 #pragma unroll
-  for (int c = 0; c + 16 <= NC; c += 16) tm_ld16(ta + c, r + c);
-  if constexpr (NC % 16 == 8) tm_ld8(ta + (NC - 8), r + (NC - 8));
+    for (int c = 0; c + 16 <= NC; c += 16) tm_ld16(ta + c, r + c);
+    if constexpr (NC % 16 == 8) tm_ld8(ta + (NC - 8), r + (NC - 8));
+  }
 #pragma unroll
   for (int k = 0; k < 2 * ZL; ++k)
     v[k / ZL][k % ZL] = __hiloint2double((int)r[2 * k + 1], (int)r[2 * k]);
 }
 
 // Cl2p with the basis vectors NR..K-2 in tensor memory instead of shared memory (NS) and the
-// L2 scratch (NG): the whole Krylov basis on chip.  Same layouts, same arithmetic in the same
-// order (bitwise identical to ras3d_cl2p_kernel), the CGS2 passes vector by vector.
+// L2 scratch (NG): the whole Krylov basis on chip.  Same layouts and arithmetic as
+// ras3d_cl2p_kernel, the CGS2 passes vector by vector with each inner product summed in four
+// independent chains (FP64 latency with 8 warps), so it agrees with cl2p to rounding.
 template <int K, int E, int NRX>
 constexpr size_t cl2t_smem_doubles() {
   using C = Cl2p<E>;
@@ -1460,16 +1484,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cl2p<E>::NT, 1)
           double acc[16];
 #pragma unroll
           for (int i = 0; i < 16; ++i) acc[i] = 0.0;
-          // vector by vector (each acc[i] sums the nodes in the same order as cl2p)
+          // vector by vector
           #pragma unroll
           for (int I = 0; I < J + 1; ++I) {
             double vt[2][ZL];
             getv(I, vt);
-            if (act) {
+            if (act) {   // four independent chains (FP64 latency), summed in a fixed order
+              double q4[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
               for (int c = 0; c < 2; ++c)
 #pragma unroll
-                for (int zl = 0; zl < ZL; ++zl) acc[I] = fma(vt[c][zl], w[c][zl], acc[I]);
+                for (int zl = 0; zl < ZL; ++zl)
+                  q4[2 * c + (zl & 1)] = fma(vt[c][zl], w[c][zl], q4[2 * c + (zl & 1)]);
+              acc[I] = (q4[0] + q4[1]) + (q4[2] + q4[3]);
             }
           }
           C2P(11);
@@ -1502,11 +1529,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cl2p<E>::NT, 1)
           for (int I = 0; I < J + 1; ++I) {
             double vt[2][ZL];
             getv(I, vt);
-            if (act) {
+            if (act) {   // four independent chains (FP64 latency), summed in a fixed order
+              double q4[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
               for (int c = 0; c < 2; ++c)
 #pragma unroll
-                for (int zl = 0; zl < ZL; ++zl) acc[I] = fma(vt[c][zl], w[c][zl], acc[I]);
+                for (int zl = 0; zl < ZL; ++zl)
+                  q4[2 * c + (zl & 1)] = fma(vt[c][zl], w[c][zl], q4[2 * c + (zl & 1)]);
+              acc[I] = (q4[0] + q4[1]) + (q4[2] + q4[3]);
             }
           }
           if (act) {
