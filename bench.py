@@ -249,7 +249,7 @@ def roofline_for(name, v, cfg, hbm_peak, peak_kind, clocks):
             clk_mhz = clocks.get("sm_mhz") or 1965.0
             peak, kind = 148 * 64 * 2 * clk_mhz * 1e6 / 1e12, "derived: 148 SM x 64 DFMA/clk x 2 x clock"
         ach = v["flops"] / (v["ms"] * 1e-3) / 1e12
-        kern = "ras2d_col_kernel" if cfg.ndim == 2 else "ras3d_cl2p_kernel"
+        kern = "ras2d_col_kernel" if cfg.ndim == 2 else "ras3d_cl2t_kernel"
         return {"kernel": "ras_apply", "bound": "alu", "achieved": round(ach, 3),
                 "peak": round(peak, 2), "unit": "TFLOP/s", "frac": round(ach / peak, 4),
                 "peak_kind": kind, "traffic": ncu_traffic(kern, cfg.name),
