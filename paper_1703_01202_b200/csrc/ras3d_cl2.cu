@@ -1201,6 +1201,9 @@ __device__ __forceinline__ void tm_st_vec(uint32_t ta, const double (&w)[2][ZL])
 #pragma unroll
   for (int c = 0; c + 16 <= NC; c += 16) tm_st16(ta + c, r + c);
   if constexpr (NC % 16 == 8) tm_st8(ta + (NC - 8), r + (NC - 8));
+  // (no wait here: the sources are consumed at issue; tm_wait_st() before the data is read back)
+}
+__device__ __forceinline__ void tm_wait_st() {
   asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
 }
 // 40 columns (ZL = 10) in one statement: three loads, one wait (one TMEM round trip)
@@ -1317,6 +1320,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cl2p<E>::NT, 1)
       for (int zl = 0; zl < ZL; ++zl) zr[c][zl] = 0.0;
 #pragma unroll
     for (int s = 0; s < NTM; ++s) tm_st_vec<ZL>(tma + (uint32_t)(s * TMC), zr);
+    tm_wait_st();
   }
 #ifdef CL2_PROF
   long long c2p_acc[16] = {0}, c2p_last = clock64();
@@ -1477,6 +1481,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cl2p<E>::NT, 1)
       double hn2 = 0.0;
       auto cgs2 = [&](auto Jc) {
         constexpr int J = decltype(Jc)::value;
+        tm_wait_st();   // this thread's TMEM stores of v_j (put_v, a stencil ago) have landed
         redb = red + rb * 2 * NW * RS;
         redr = red_rem + (uint32_t)(rb * 2 * NW * RS) * 8u;
         mbr = mbar_rem0 + 8u * rb;
@@ -1618,6 +1623,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cl2p<E>::NT, 1)
     }
     __syncthreads();
     C2P(7);
+    tm_wait_st();
     {   // (every lane: the tensor-memory loads are warp-collective; only node lanes store)
       // y = V yv over every slot (fma(0, v, s) = s exactly for the finite unused slots)
       double yl[2][ZL];
