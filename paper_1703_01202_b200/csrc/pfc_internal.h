@@ -112,6 +112,7 @@ struct pfc_ctx {
   int ras_threads = 0;
   int ras_cluster = 1;
   int ras_rows = 0;
+  int ras_tmem = 0;        // 2D: the two-boxes-per-SM kernel with the basis in tensor memory
   int tail = 0;            // 2D small grids: fused J v + CGS2 + next vector (tail2d.cu)
   int tail_rs = 0;         //   its tiled form: rows per thread (0: the gather form)
   int tail_blocks = 0;     //   and co-resident tiles

@@ -28,6 +28,7 @@
 #include "pfc_device.cuh"
 #include "pfc_internal.h"
 #include "ras_common.cuh"
+#include "tmem.cuh"
 
 #include <stdlib.h>
 
@@ -437,7 +438,7 @@ constexpr int PP = 48;          // padded plane pitch (doubles) at most: Ex + 6 
 // and then strip s+1 (R rows further), so its 8-byte loads are conflict-free when
 // R * pitch = Ex (mod 16): 45 for R = 4 (Ex = 36, 20: cfg2/3), 50 for R = 2 (Ex = 20: cfg1);
 // other shapes are correct at any pitch, just not conflict-free.
-constexpr int col_pp(int R) { return R == 4 ? 45 : R == 2 ? 50 : PP; }
+constexpr int col_pp(int R) { return R == 4 ? 45 : R == 2 ? 50 : R == 6 ? 46 : PP; }
 constexpr int PPY = 56;         // padded plane rows: Ey + R + 5 <= 56
 constexpr int NTC = 384;        // threads per CTA at most (1 CTA per SM, <= 168 registers)
 constexpr int NWC = NTC / 32;
@@ -948,6 +949,336 @@ __global__ void __launch_bounds__(NTC, 1) ras2d_col_kernel(const __grid_constant
   }
 }
 
+// ============================================================================================
+// Two boxes per SM (ras2d_colt_kernel, periodic, M = 1): the column kernel with the Krylov basis
+// in TENSOR MEMORY instead of registers, so a CTA of R = 6 rows per thread (36 x 6 strips = 216
+// node threads + the Givens warp) fits in 128 registers and two CTAs -- two boxes -- share each
+// SM: one box's reductions, barriers and Givens hide under the other's stencil (the column
+// kernel runs one box of 12 warps per SM, latency-bound on its block reductions).  Each CTA
+// allocates 256 TMEM columns; thread t of warp w keeps vector i of its R nodes at columns
+// 128 (w div 4) + 2 R i of lane 32 (w mod 4) + t mod 32 (K R <= 64).  Same arithmetic as
+// ras2d_col_kernel (the CGS2 sums per node and per vector in the same order).
+constexpr int NTT = 256;   // threads per CTA at most (two CTAs per SM at <= 128 registers)
+
+template <int K, int R, int J>
+__device__ __forceinline__ bool colt_step(uint32_t tma, double (&w)[R], double (&cvv)[R],
+                                          const double (&cr)[R], const bool (&own)[R],
+                                          double* red, int& rb, double* h1, double* h2,
+                                          double* hx, double* H, double* cs, double* sn,
+                                          double* gv, double* rd, double* pvb, double* pcvb,
+                                          double beta, int nwt, bool g0, double& hn_prev) {
+  constexpr int PP = col_pp(R);
+  if constexpr (J > 0) {
+    if (g0) col_givens<K, J - 1>(h1, h2, hn_prev, cs, sn, gv, H, rd);
+  }
+  tmem::wait_st();   // v_J (stored at the end of the previous step) has landed
+  // pass 1: h1 = V^T w
+  {
+    double acc[J + 1];
+#pragma unroll
+    for (int i = 0; i <= J; ++i) {
+      double vi[R];
+      tmem::ld<R>(tma + (uint32_t)(2 * R * i), vi);
+      double t = 0.0;
+#pragma unroll
+      for (int r = 0; r < R; ++r) t = fma(vi[r], w[r], t);
+      acc[i] = t;
+    }
+    col_allreduce<J + 1>(acc, red + rb * NWC * 16, h1, nwt);
+    rb ^= 1;
+  }
+  // w' = w - V h1 ; pass 2: h2 = V^T w', |w'|^2 in slot J+1
+  {
+    double hv[J + 1];
+#pragma unroll
+    for (int i = 0; i <= J; ++i) hv[i] = h1[i];
+#pragma unroll
+    for (int i = 0; i <= J; ++i) {   // per node in the order i = 0..J, as the column kernel
+      double vi[R];
+      tmem::ld<R>(tma + (uint32_t)(2 * R * i), vi);
+#pragma unroll
+      for (int r = 0; r < R; ++r) w[r] = fma(-hv[i], vi[r], w[r]);
+    }
+    double acc[J + 2];
+#pragma unroll
+    for (int i = 0; i <= J; ++i) {
+      double vi[R];
+      tmem::ld<R>(tma + (uint32_t)(2 * R * i), vi);
+      double t = 0.0;
+#pragma unroll
+      for (int r = 0; r < R; ++r) t = fma(vi[r], w[r], t);
+      acc[i] = t;
+    }
+    double t = 0.0;
+#pragma unroll
+    for (int r = 0; r < R; ++r) t = fma(w[r], w[r], t);
+    acc[J + 1] = t;
+    col_allreduce<J + 2>(acc, red + rb * NWC * 16, h2, nwt);
+    rb ^= 1;
+  }
+  double hv[J + 1];
+  double h2n = 0.0;
+#pragma unroll
+  for (int i = 0; i <= J; ++i) {
+    hv[i] = h2[i];
+    h2n += hv[i] * hv[i];
+  }
+  const double wn2 = h2[J + 1];
+#pragma unroll
+  for (int i = 0; i <= J; ++i) {
+    double vi[R];
+    tmem::ld<R>(tma + (uint32_t)(2 * R * i), vi);
+#pragma unroll
+    for (int r = 0; r < R; ++r) w[r] = fma(-hv[i], vi[r], w[r]);
+  }
+  double hn2;
+  if (h2n <= 1e-8 * wn2) {
+    hn2 = wn2 - h2n;                                  // |w''|^2 = |w'|^2 - |h2|^2
+  } else {                                            // rare: explicit |w''|^2
+    double acc[1] = {0.0};
+#pragma unroll
+    for (int r = 0; r < R; ++r) acc[0] = fma(w[r], w[r], acc[0]);
+    col_allreduce<1>(acc, red + rb * NWC * 16, hx, nwt);
+    rb ^= 1;
+    hn2 = hx[0];
+  }
+  const double hn = sqrt(hn2 > 0.0 ? hn2 : 0.0);
+  hn_prev = hn;                     // the Givens warp reduces column J during step J+1
+  if (hn <= 1e-14 * beta) return true;               // exact breakdown (uniform)
+  if constexpr (J + 1 < K) {
+    const double ihn = 1.0 / hn;
+    double vn[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      vn[r] = w[r] * ihn;
+      cvv[r] = cr[r] * vn[r];
+      if (own[r]) {
+        pvb[r * PP] = vn[r];
+        pcvb[r * PP] = cvv[r];
+      }
+    }
+    tmem::st<R>(tma + (uint32_t)(2 * R * (J + 1)), vn);
+  }
+  return false;
+}
+
+template <int K, int R, int J>
+__device__ __forceinline__ bool colt_dispatch(int j, uint32_t tma, double (&w)[R],
+                                              double (&cvv)[R], const double (&cr)[R],
+                                              const bool (&own)[R], double* red, int& rb,
+                                              double* h1, double* h2, double* hx, double* H,
+                                              double* cs, double* sn, double* gv, double* rd,
+                                              double* pvb, double* pcvb, double beta, int nwt,
+                                              bool g0, double& hn_prev) {
+  if constexpr (J < K) {
+    if (j == J)
+      return colt_step<K, R, J>(tma, w, cvv, cr, own, red, rb, h1, h2, hx, H, cs, sn, gv, rd,
+                                pvb, pcvb, beta, nwt, g0, hn_prev);
+    return colt_dispatch<K, R, J + 1>(j, tma, w, cvv, cr, own, red, rb, h1, h2, hx, H, cs, sn,
+                                      gv, rd, pvb, pcvb, beta, nwt, g0, hn_prev);
+  } else {
+    return true;
+  }
+}
+
+template <int K, int R>
+__global__ void __launch_bounds__(NTT, 2) ras2d_colt_kernel(const __grid_constant__ RasColArgs p) {
+  static_assert(K * R <= 64, "K R doubles = 2 K R <= 128 TMEM columns per thread");
+  constexpr int PP = col_pp(R);
+  extern __shared__ __align__(128) double smem_dyn[];
+  double* pv = smem_dyn;                     // PP x PPY padded v (zero ring)
+  double* pcv = pv + PP * PPY;               // PP x PPY padded c v
+  double* red = pcv + PP * PPY;              // 2 x NWC x 16
+  double* hwall = red + 2 * NWC * 16;        // NWC x 3 x 16
+  double* stg = hwall + NWC * 48;            // next box's v, c of each thread's nodes (2 x NTT x R)
+  __shared__ double H[(K + 1) * K];
+  __shared__ double gv[K + 1], cs[K], sn[K], yv[K], rd[K];
+  __shared__ uint32_t tm_base;
+
+  if (p.gate && *p.gate) return;
+  const double W0 = dt_w0<2>(p.dtp, p.W[0]);
+  const int tid = threadIdx.x, nwt = blockDim.x >> 5, wid = tid >> 5;
+  const bool gwarp = wid == nwt - 1;            // the Givens warp: no nodes, reduces H
+  const bool g0 = gwarp && (tid & 31) == 0;
+  double hn_prev = 0.0;
+  double* h1 = hwall + wid * 48;
+  double* h2 = h1 + 16;
+  double* hx = h2 + 16;
+  const int Ex = p.Ex;
+  const int nbx = p.nx / p.bx;
+  const int nboxes = nbx * (p.ny / p.by);
+
+  const int xs = tid % Ex, ss = tid / Ex;
+  const bool active = ss < p.ns;
+  const int x = active ? xs : 0, y0 = active ? ss * R : 0;   // inactive threads read in-bounds
+  bool own[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) own[r] = active && (y0 + r < p.Ey);
+  double* pvb = pv + (y0 + 3) * PP + x + 3;
+  double* pcvb = pcv + (y0 + 3) * PP + x + 3;
+
+  for (int q = tid; q < 2 * PP * PPY; q += blockDim.x) pv[q] = 0.0;   // the ring stays zero
+  if (wid == 0) tmem::alloc<256>(&tm_base);   // half of the SM's columns (two CTAs per SM)
+  tmem::fence_before();
+  __syncthreads();
+  tmem::fence_after();
+  const uint32_t tma = tm_base + ((uint32_t)(32 * (wid & 3)) << 16) + (uint32_t)(128 * (wid >> 2));
+  double* sv = stg + tid;              // [r][thread]: a warp's 8-byte accesses are contiguous
+  double* sc = stg + NTT * R + tid;
+  auto prefetch = [&](int box) {
+    if (box >= nboxes) return;
+    const int gx0 = (box % nbx) * p.bx - p.o, gy0 = (box / nbx) * p.by - p.o;
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+      if (own[r]) {
+        const size_t g = (size_t)wrapi(gx0 + x, p.nx) + (size_t)p.nx * wrapi(gy0 + y0 + r, p.ny);
+        cp_async8(sv + r * NTT, p.v + g);
+        cp_async8(sc + r * NTT, p.c + g);
+      }
+    cp_async_commit();
+  };
+  prefetch(blockIdx.x);
+  for (int box = blockIdx.x; box < nboxes; box += gridDim.x) {
+  const int ibx = box % nbx, iby = box / nbx;
+  cp_async_wait_all();
+  double w[R], cr[R], cvv[R];
+  double acc0[1] = {0.0};
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    w[r] = 0.0;
+    cr[r] = 0.0;
+    if (own[r]) {
+      const int li = x - p.o, lj = y0 + r - p.o;
+      const bool owned = li >= 0 && li < p.bx && lj >= 0 && lj < p.by;
+      w[r] = (p.restrict_owned && !owned) ? 0.0 : sv[r * NTT];
+      cr[r] = sc[r * NTT];
+      acc0[0] = fma(w[r], w[r], acc0[0]);
+    }
+  }
+  prefetch(box + gridDim.x);   // this thread's slots are free again
+  hn_prev = 0.0;
+  int rb = 0;
+  col_allreduce<1>(acc0, red + rb * NWC * 16, hx, nwt);   // also orders the zero fill
+  rb ^= 1;
+  const double beta = sqrt(hx[0]);
+  if (beta == 0.0) {
+    if (tid == 0) ras_count(p.jcnt, 0);
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int li = x - p.o, lj = y0 + r - p.o;
+      if (p.y_ext) {
+        if (own[r]) p.y_ext[(size_t)box * (Ex * p.Ey) + (y0 + r) * Ex + x] = 0.0;
+      } else if (own[r] && li >= 0 && li < p.bx && lj >= 0 && lj < p.by) {
+        p.z[(size_t)(ibx * p.bx + li) + (size_t)p.nx * (iby * p.by + lj)] = 0.0;
+      }
+    }
+    __syncthreads();   // every warp has read beta before the next box's first reduction
+    continue;
+  }
+  {
+    const double ib = 1.0 / beta;
+    double v0[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      v0[r] = w[r] * ib;
+      cvv[r] = cr[r] * v0[r];
+      if (own[r]) {
+        pvb[r * PP] = v0[r];
+        pcvb[r * PP] = cvv[r];
+      }
+    }
+    tmem::st<R>(tma, v0);
+  }
+  if (tid == 0) gv[0] = beta;
+  int jm = 0;
+#pragma unroll 1
+  for (int j = 0; j < K; ++j) {
+    __syncthreads();                                  // planes hold v_j and c v_j
+    if (!gwarp) {   // ---- w = A_k v_j: direct 25-point linear part, column by column
+      double out[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r) out[r] = 0.0;
+#pragma unroll
+      for (int dx = -3; dx <= 3; ++dx) {
+        const int a = 3 - iabs(dx);
+        double col[R + 6];
+#pragma unroll
+        for (int rr = -a; rr < R + a; ++rr) col[rr + a] = pvb[rr * PP + dx];
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+#pragma unroll
+          for (int dy = -a; dy <= a; ++dy)
+            out[r] = fma(wclass(iabs(dx), iabs(dy)) == 0 ? W0 : p.W[wclass(iabs(dx), iabs(dy))],
+                         col[r + dy + a], out[r]);
+      }
+      // ---- minus Delta(c v): x-neighbours from the plane, y-neighbours from registers
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const double up = r == 0 ? pcvb[(r - 1) * PP] : cvv[r - 1];
+        const double dn = r == R - 1 ? pcvb[(r + 1) * PP] : cvv[r + 1];
+        const double lap = (pcvb[r * PP - 1] + pcvb[r * PP + 1]) + (up + dn) - 4.0 * cvv[r];
+        w[r] = own[r] ? fma(-p.ih2, lap, out[r]) : 0.0;
+      }
+    } else {
+#pragma unroll
+      for (int r = 0; r < R; ++r) w[r] = 0.0;
+    }
+    const bool stop = colt_dispatch<K, R, 0>(j, tma, w, cvv, cr, own, red, rb, h1, h2, hx, H,
+                                             cs, sn, gv, rd, pvb, pcvb, beta, nwt, g0, hn_prev);
+    jm = j + 1;
+    if (stop) break;
+  }
+  if (g0) {   // last Hessenberg column, then back substitution R yv = g
+    col_givens_dispatch<K, 0>(jm - 1, h1, h2, hn_prev, cs, sn, gv, H, rd);
+    const int ld = K + 1;
+    double y[K];
+#pragma unroll
+    for (int i = K - 1; i >= 0; --i) {
+      if (i >= jm) continue;
+      double sacc = gv[i];
+#pragma unroll
+      for (int l = i + 1; l < K; ++l)
+        if (l < jm) sacc -= H[i + ld * l] * y[l];
+      y[i] = sacc * rd[i];
+      yv[i] = y[i];
+    }
+    ras_count(p.jcnt, jm);
+  }
+  __syncthreads();
+  // (R_k^0)^T: y = V yv at the owned nodes (every lane loads: TMEM loads are warp-collective)
+  {
+    double s[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) s[r] = 0.0;
+    tmem::wait_st();
+    for (int i = 0; i < jm; ++i) {
+      double vi[R];
+      tmem::ld<R>(tma + (uint32_t)(2 * R * i), vi);
+      const double yi = yv[i];
+#pragma unroll
+      for (int r = 0; r < R; ++r) s[r] = fma(yi, vi[r], s[r]);
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int li = x - p.o, lj = y0 + r - p.o;
+      const bool wr = p.y_ext ? own[r] : (own[r] && li >= 0 && li < p.bx && lj >= 0 && lj < p.by);
+      if (!wr) continue;
+      if (p.y_ext) p.y_ext[(size_t)box * (Ex * p.Ey) + (y0 + r) * Ex + x] = s[r];
+      else p.z[(size_t)(ibx * p.bx + li) + (size_t)p.nx * (iby * p.by + lj)] = s[r];
+    }
+  }
+  __syncthreads();   // yv, H and the planes are reused by the next box
+  }
+  tmem::fence_before();
+  __syncthreads();
+  tmem::fence_after();
+  if (wid == 0) tmem::dealloc<256>(tm_base);
+}
+
+size_t ras2d_colt_smem_bytes(int R) {
+  return (size_t)(2 * col_pp(R) * PPY + 2 * NWC * 16 + NWC * 48 + 2 * NTT * R) * sizeof(double);
+}
+
 #ifdef PFC_RAS_PROFILE
 }  // namespace
 extern "C" void pfc_ras_prof_read(long long* out) {
@@ -1018,6 +1349,34 @@ ras2d_col_fn pick_col(int k, int r, bool mirror = false, bool mob = false) {
 }
 
 // rows per thread for the column kernel: the fewest that fit the extended box in NTC threads
+// TMEM two-boxes-per-SM kernel (periodic, M = 1): rows per thread, 0 if not applicable
+typedef void (*ras2d_colt_fn)(const RasColArgs);
+ras2d_colt_fn pick_colt(int k, int r) {
+  if (k != 10) return nullptr;
+  switch (r) {
+    case 2: return ras2d_colt_kernel<10, 2>;
+    case 4: return ras2d_colt_kernel<10, 4>;
+    case 6: return ras2d_colt_kernel<10, 6>;
+  }
+  return nullptr;
+}
+// Opt-in (PFC_RAS2_TMEM=1): measured slower than the one-box column kernel (cfg2 apply 252 vs
+// 238 us, Test C 971 vs 921 us; two CTAs of 8 warps per SM, R = 6 rows per thread)
+int colt_rows(int k, int Ex, int Ey) {
+  const char* e = getenv("PFC_RAS2_TMEM");
+  if (!(e && e[0] == '1') || Ex + 6 > PP || Ey + 11 > PPY) return 0;
+  const char* force = getenv("PFC_RAS2_ROWS");   // A/B probes only: rows per thread
+  const int rmin = force ? atoi(force) : 1;
+  const int cand[3] = {2, 4, 6};
+  for (int i = 0; i < 3; ++i) {
+    const int r = cand[i];
+    if (r < rmin) continue;
+    const int ns = (Ey + r - 1) / r;
+    if (Ex + 6 <= col_pp(r) && (Ex * ns + 31) / 32 * 32 + 32 <= NTT && pick_colt(k, r)) return r;
+  }
+  return 0;
+}
+
 int col_rows(int k, int Ex, int Ey, bool mirror = false, bool mob = false) {
   if (Ex + 6 > PP || Ey > 42) return 0;
   const int cand[4] = {1, 2, 4, 5};
@@ -1040,6 +1399,18 @@ int ras2d_plan(pfc_ctx* ctx) {
   const int Ex = c.ras_box[0] + 2 * c.ras_overlap, Ey = c.ras_box[1] + 2 * c.ras_overlap;
   if (Ex * Ey > MAXN) return 0;
   const bool mir = c.bc == PFC_BC_MIRROR, mob = c.mobility != PFC_MOBILITY_ONE;
+  ctx->ras_tmem = 0;
+  if (getenv("PFC_RAS_SMEM_BASIS") == nullptr && !mir && !mob) {
+    const int r = colt_rows(c.ras_local_k, Ex, Ey);
+    if (r) {
+      const int ns = (Ey + r - 1) / r;
+      ctx->ras_smem = (int)ras2d_colt_smem_bytes(r);
+      ctx->ras_threads = (Ex * ns + 31) / 32 * 32 + 32;
+      ctx->ras_rows = r;
+      ctx->ras_tmem = 1;
+      return 1;
+    }
+  }
   if (getenv("PFC_RAS_SMEM_BASIS") == nullptr) {
     const int r = col_rows(c.ras_local_k, Ex, Ey, mir, mob);
     if (r) {
@@ -1064,7 +1435,38 @@ cudaError_t launch_ras_2d(pfc_ctx* ctx, const double* v, const double* c, double
   const int Ex = cf.ras_box[0] + 2 * cf.ras_overlap, Ey = cf.ras_box[1] + 2 * cf.ras_overlap;
   const int nb = (cf.n[0] / cf.ras_box[0]) * (cf.n[1] / cf.ras_box[1]);
   cudaError_t e;
-  if (ctx->ras_rows > 0) {
+  if (ctx->ras_tmem) {   // two boxes per SM, basis in tensor memory
+    const int R = ctx->ras_rows;
+    ras2d_colt_fn fn = pick_colt(cf.ras_local_k, R);
+    if (!fn) return cudaErrorInvalidValue;
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, ctx->ras_smem);
+    if (e != cudaSuccess) return e;
+    RasColArgs p{};
+    p.v = v; p.c = c; p.z = z;
+    p.nx = cf.n[0]; p.ny = cf.n[1]; p.bx = cf.ras_box[0]; p.by = cf.ras_box[1];
+    p.o = cf.ras_overlap; p.Ex = Ex; p.Ey = Ey; p.ns = (Ey + R - 1) / R;
+    p.restrict_owned = cf.ras_variant == PFC_RAS_RIGHT;
+    p.y_ext = cf.ras_variant == PFC_RAS_LEFT ? nullptr : ctx->ras_y;
+    p.gate = ctx->gate;
+    p.jcnt = ctx->prof ? ctx->d_jcnt : nullptr;
+    const double ih2 = ctx->ih2, ih4 = ih2 * ih2, ih6 = ih4 * ih2;
+    const double al = 0.5 * (1.0 - cf.gamma);
+    p.W[0] = 1.0 / dt + 4.0 * al * ih2 - 20.0 * ih4 + 56.0 * ih6;
+    p.dtp = ctx->dtdev;
+    p.W[1] = -al * ih2 + 8.0 * ih4 - 28.5 * ih6;
+    p.W[2] = -ih4 + 6.0 * ih6;
+    p.W[3] = -2.0 * ih4 + 12.0 * ih6;
+    p.W[4] = -0.5 * ih6;
+    p.W[5] = -1.5 * ih6;
+    p.ih2 = ih2;
+    int nsm = 148, per_sm = 1;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, ctx->device);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, ctx->ras_threads,
+                                                      ctx->ras_smem) != cudaSuccess || per_sm < 1)
+      per_sm = 1;
+    if (per_sm > 2) per_sm = 2;   // 256 TMEM columns per CTA: at most two CTAs per SM
+    fn<<<std::min(nb, nsm * per_sm), ctx->ras_threads, ctx->ras_smem, ctx->stream>>>(p);
+  } else if (ctx->ras_rows > 0) {
     const int R = ctx->ras_rows;
     const bool mob = cf.mobility != PFC_MOBILITY_ONE;
     ras2d_col_fn fn = pick_col(cf.ras_local_k, R, cf.bc == PFC_BC_MIRROR, mob);
