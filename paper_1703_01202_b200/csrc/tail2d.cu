@@ -390,8 +390,13 @@ int tail_tile_plan(pfc_ctx* ctx, int* blocks, int* rs_out, int* smem_out) {
   if ((e && e[0] == '0') || nx % TXT != 0) return 0;
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
+  // PFC_TAIL_RS=r forces r rows per thread (A/B probes); small grids prefer ONE tile (the grid
+  // syncs become block barriers of a single co-resident block)
+  const char* fr = getenv("PFC_TAIL_RS");
+  const int rforce = fr ? atoi(fr) : 0;
   for (int rs = 1; rs <= 16; rs *= 2) {
     if (ny % (4 * rs) != 0) continue;
+    if (rforce && rs != rforce) continue;
     int smem = 0;
     tail_tile_fn fn = pick_tail_tile(rs, &smem);
     if (!fn) continue;
