@@ -355,8 +355,30 @@ __global__ void __launch_bounds__(NT, 1) stencil3d_kernel(const __grid_constant_
       // ---- every compute warp has finished iteration t-1 (its reads and its plane stores)
       if (t > 0) mbar_wait(&itbar, (uint32_t)((t - 1) & 1));
       // outside neighbours of the planes produced in iteration t-1 (all loads before any store)
-      const q4 x1 = (OP == OP_RESID) ? out_split(Ssp + ((t - 1) & 1) * SPLANE, e0)
-                                     : out_ring(ringA + prv * WS, bo);
+      q4 x1;
+      if constexpr (OP == OP_RESID) {
+        x1 = out_split(Ssp + ((t - 1) & 1) * SPLANE, e0);
+      } else {
+        // left / right neighbours of the block are the adjacent lanes' own plane-(t-1) values
+        // (shuffles; the stride-2 ring loads were 2-way bank conflicts), from the ring only at
+        // the region edge and across warps; top / bottom pairs from the ring
+        const double* f = ringA + prv * WS;
+        const double lb = __shfl_up_sync(0xffffffffu, A1.b, 1);
+        const double ld = __shfl_up_sync(0xffffffffu, A1.d, 1);
+        const double ra = __shfl_down_sync(0xffffffffu, A1.a, 1);
+        const double rc = __shfl_down_sync(0xffffffffu, A1.c, 1);
+        double L0 = lb, L1 = ld, R0 = ra, R1 = rc;
+        if (!(pc > 1 && lane > 0)) {   // (predicated: only these lanes touch shared memory)
+          L0 = f[bo.l];
+          L1 = f[bo.l + bo.pitch];
+        }
+        if (!(pc < NPB && lane < 31)) {
+          R0 = f[bo.r];
+          R1 = f[bo.r + bo.pitch];
+        }
+        const double2 T = lds2(f + bo.t), D = lds2(f + bo.d);
+        x1 = {L0 + T.x, R0 + T.y, L1 + D.x, R1 + D.y};
+      }
       const q4 x2 = out_split(Lr, e0);
       const q4 x3 = out_split(Mr, e0);
       // ---- stage 1: Lt s | Lt v at plane t-1
