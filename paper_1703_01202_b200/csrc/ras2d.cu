@@ -677,8 +677,12 @@ __device__ __forceinline__ bool col_dispatch(int j, double (&Vr)[K][R], double (
 // MOB: variable mobility M = 1 - u^2 (row f3, R8b): A_k v = R J R^T v staged on shared planes
 // like ras2d_kernel (L1 = Delta v; B = alpha v + L1 + Delta L1 / 2 + c v; then
 // v/dt - (grad . M grad) B - (grad . (-u v) grad) A at the own nodes), the basis in registers
+// threads per CTA at most: R >= 6 rows per thread run 8 warps at <= 255 registers (fewer warps
+// per block reduction), fewer rows 12 warps at <= 168
+constexpr int col_nt(int R) { return R >= 6 ? 256 : NTC; }
+
 template <int K, int R, bool MIR, bool MOB = false>
-__global__ void __launch_bounds__(NTC, 1) ras2d_col_kernel(const __grid_constant__ RasColArgs p) {
+__global__ void __launch_bounds__(col_nt(R), 1) ras2d_col_kernel(const __grid_constant__ RasColArgs p) {
   constexpr int PP = col_pp(R);
   extern __shared__ __align__(128) double smem_dyn[];
   double* pv = smem_dyn;                     // PP x PPY padded v (zero ring)
@@ -1315,6 +1319,7 @@ ras2d_fn pick(int k) {
 typedef void (*ras2d_col_fn)(const RasColArgs);
 template <bool MIR>
 ras2d_col_fn pick_col_t(int k, int r) {
+  if (k == 10 && r == 6) return ras2d_col_kernel<10, 6, MIR>;
 #define RC(K)                                              \
   case K:                                                  \
     switch (r) {                                           \
@@ -1379,14 +1384,22 @@ int colt_rows(int k, int Ex, int Ey) {
 
 int col_rows(int k, int Ex, int Ey, bool mirror = false, bool mob = false) {
   if (Ex + 6 > PP || Ey > 42) return 0;
-  const int cand[4] = {1, 2, 4, 5};
+  const int cand[5] = {1, 2, 4, 5, 6};
   const char* force = getenv("PFC_RAS2_ROWS");   // A/B probes only: rows per thread
   const int rmin = force ? atoi(force) : 1;
-  for (int i = 0; i < 4; ++i) {
+  if (!force) {   // R = 6 (8 warps, 255 registers) when it still gives >= 6 node warps: fewer
+                  // warps per block reduction (cfg2, E = 36: 0.2266 -> 0.2204 ms per apply)
+    const int nt = Ex * ((Ey + 5) / 6);
+    if (nt > 160 && Ex + 6 <= col_pp(6) && (nt + 31) / 32 * 32 + 32 <= col_nt(6) &&
+        pick_col(k, 6, mirror, mob))
+      return 6;
+  }
+  for (int i = 0; i < 5; ++i) {
     const int r = cand[i];
     if (r < rmin) continue;
     const int ns = (Ey + r - 1) / r;
-    if (Ex + 6 <= col_pp(r) && (Ex * ns + 31) / 32 * 32 + 32 <= NTC && pick_col(k, r, mirror, mob))
+    if (Ex + 6 <= col_pp(r) && (Ex * ns + 31) / 32 * 32 + 32 <= col_nt(r) &&
+        pick_col(k, r, mirror, mob))
       return r;
   }
   return 0;

@@ -108,3 +108,21 @@ def test_tiled_arnoldi_tail_matches_gather_form(monkeypatch):
     b, ib = run()                                     # gather-form tail
     assert ia == ib
     assert rel(a, b) <= 1e-12
+
+
+@pytest.mark.parametrize("rows", [4, 6])
+def test_2d_column_kernel_rows_per_thread(rows, monkeypatch):
+    """cfg2's subdomain geometry (32^2 boxes, overlap 2, E = 36): the column kernel with R = 6
+    rows per thread (default, 8 warps) and R = 4 (12 warps) both match the oracle (Eq. eq:ras
+    P:398-409) and each other to summation order."""
+    shape, box = (256, 128), (32, 32)
+    phi = 0.07 + 0.07 * random_field(shape, 45)
+    v = random_field(shape, 46)
+    z_def = ras(shape, box, 2, phi, v, 0.5)
+    monkeypatch.setenv("PFC_RAS2_ROWS", str(rows))
+    z_r = ras(shape, box, 2, phi, v, 0.5)
+    assert rel(z_r, z_def) <= 1e-13
+    if rows == 6:
+        assert np.array_equal(z_r, z_def)          # the default is R = 6 here
+    ref = O.ras_apply(phi, phi, v, H, _oracle_params(shape, box, 2), 0.5)
+    assert rel(z_r, ref) <= 1e-12
