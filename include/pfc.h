@@ -83,7 +83,7 @@ typedef struct pfc_config {
  *   PFC_LOCAL_ILU    the paper's ILU(k) of A_k in natural order (Table 1
  *                    P:872-909), U^{-1} L^{-1} per apply; with ras_ilu_reuse the factors of the
  *                    step's first Newton iteration (Phi_0 = phi^n) serve all its iterations
- *                    (P:910-915).  M = 1 only; usable at small dt for the configurations' h
+ *                    (P:910-915).  M = 1 only, either bc; usable at small dt for the configurations' h
  *                    (ILU(0) loses positive pivots near dt >= 0.5);
  *   PFC_LOCAL_LU     the paper's LU (Table 1): the same factor path with unlimited fill, i.e.
  *                    the exact factorisation of A_k in natural order (no pivoting: A_k of the
@@ -100,8 +100,10 @@ enum { PFC_LOCAL_GMRES = 0, PFC_LOCAL_ILU = 1, PFC_LOCAL_LU = 2 };
  *                    (so D+ / D- vanish across the walls, mass is conserved and the energy
  *                    law of P:280-308 holds).  Subdomains are clipped at the walls: ext-box nodes
  *                    outside the domain are no unknowns of A_k = R_k J R_k^T.  Built for
- *                    ndim = 2 and 3 (3D since round 2), PFC_LOCAL_GMRES, ras_box >= 3; either
- *                    mobility.  Runs the global-memory operator chain (mobility.cu); the
+ *                    ndim = 2 and 3 (3D since round 2), ras_box >= 3; PFC_LOCAL_GMRES with
+ *                    either mobility, PFC_LOCAL_ILU / PFC_LOCAL_LU with M = 1 (identity rows
+ *                    for the ext-box nodes outside the domain, one symbolic factorisation per
+ *                    class of boxes by their position relative to the walls, ilu.cu).  Runs the global-memory operator chain (mobility.cu); the
  *                    subdomain solves run, in 2D for ras_local_k = 10 (any k with M = 1), the
  *                    column kernel with the basis in registers (ras2d.cu, MIR instantiation),
  *                    else the shared-memory-basis kernel, and in 3D the global-scratch kernel

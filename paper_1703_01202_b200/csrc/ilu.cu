@@ -21,6 +21,17 @@
 // value array is laid out as [L block | U block].
 // Same operations as the oracle (or_ilu_dense / ilu_solve) per entry; the parallel order only
 // regroups independent updates and the triangular-solve dot products.
+//
+// Mirror walls (PFC_BC_MIRROR, reading R23; round 2): A_k = R J R^T with the mirror J, the
+// ext box clipped at the walls.  The stencil point x_i + d of an in-domain row lands on the
+// mirror image of that node, so near a wall several offsets d hit one column: the entry is the
+// SUM of their class weights (and of the -h^-2 c_j of the unit offsets, which may hit the row's
+// own node); ext-box nodes outside the domain are no unknowns and get identity rows, as in the
+// oracle (local_ilu).  The pattern, its ILU(k) fill and the schedules then depend on where the
+// box sits relative to the walls: one symbolic factorisation per CLASS of boxes (per axis: the
+// clipped layers and the distance of the ext box to either wall, capped at the stencil radius;
+// <= 3^d classes on the configs' grids), one launch per class over that class's box list.  The
+// periodic grid is the single-class case with the original per-entry class table.
 #include "pfc_device.cuh"
 #include "pfc_internal.h"
 
@@ -55,7 +66,12 @@ struct IluArgs {
   const int* ucol;
   int nL, nU;           // value position of U entry t of row i: nL + uptr[i] + t
   const int* ecls;      // per entry: linear-weight class, -1 for fill
-  const int* ectype;    // per entry: 0 none, 1 -h^-2 c_j, 2 +2d h^-2 c_i
+  const int* ectype;    // per entry: 0 none, 1 -h^-2 c_j, 2 +2d h^-2 c_i, 3 identity row
+  const double* elin;   // mirror classes: per entry, the summed dt-free class weights (else null)
+  const int* eccnt;     // mirror classes: per entry, the number of unit offsets that hit the column
+  const int* boxes;     // this launch's boxes (global box ids), or null = every box in order
+  int mirror;           // PFC_BC_MIRROR: ext-box nodes outside the domain are identity rows
+  double idt;           // 1/dt (mirror classes: added to the in-domain diagonal)
   const int* ukptr;     // updates of L entry q: [ukptr[q], ukptr[q+1]) of ...
   const int* usrc;      // ... the value position of a_kj (final row k)
   const int* udst;      // ... and the slot of a_ij within row i
@@ -84,21 +100,37 @@ __device__ __forceinline__ size_t gnode(const IluArgs& p, int l, int gx0, int gy
   return (size_t)wrapi(gx0 + li, p.nx) + (size_t)p.nx * wrapi(gy0 + lj, p.ny) +
          (size_t)p.nx * p.ny * (p.nd == 3 ? wrapi(gz0 + lk, p.nz) : 0);
 }
+// mirror walls: is ext-box node l an unknown (inside the domain)?
+__device__ __forceinline__ bool in_dom(const IluArgs& p, int l, int gx0, int gy0, int gz0) {
+  if (!p.mirror) return true;
+  const int Ex = p.bx + 2 * p.o, Ey = p.by + 2 * p.o;
+  const int x = gx0 + l % Ex, y = gy0 + (l / Ex) % Ey, z = p.nd == 3 ? gz0 + l / (Ex * Ey) : 0;
+  return x >= 0 && x < p.nx && y >= 0 && y < p.ny && z >= 0 && z < p.nz;
+}
 
 // numeric ILU(k) of every box: A values from the class weights and c, then IKJ by levels
 __global__ void __launch_bounds__(NT) k_ilu_factor(const IluArgs p) {
-  const int box = blockIdx.x;
+  const int box = p.boxes ? p.boxes[blockIdx.x] : blockIdx.x;
   int gx0, gy0, gz0, ibx, iby, ibz;
   box_origin(p, box, gx0, gy0, gz0, ibx, iby, ibz);
-  double* a = p.vals + (size_t)box * p.nnz;
+  double* a = p.vals + (size_t)blockIdx.x * p.nnz;
   const int d2 = 2 * p.nd;
   for (int i = threadIdx.x; i < p.n; i += blockDim.x) {
-    const double ci = p.c[gnode(p, i, gx0, gy0, gz0)];
+    const double ci = in_dom(p, i, gx0, gy0, gz0) ? p.c[gnode(p, i, gx0, gy0, gz0)] : 0.0;
     auto set = [&](int q, int col) {
-      const int cl = p.ecls[q], ct = p.ectype[q];
-      double val = cl >= 0 ? p.W[cl] : 0.0;
-      if (ct == 2) val += d2 * p.ih2 * ci;
-      else if (ct == 1) val -= p.ih2 * p.c[gnode(p, col, gx0, gy0, gz0)];
+      const int ct = p.ectype[q];
+      double val;
+      if (p.elin) {   // mirror class: summed weights; columns of in-domain rows are in-domain
+        val = p.elin[q];
+        if (ct == 2) val += p.idt + d2 * p.ih2 * ci;
+        const int cc = p.eccnt[q];
+        if (cc) val -= cc * (p.ih2 * p.c[gnode(p, col, gx0, gy0, gz0)]);
+      } else {
+        const int cl = p.ecls[q];
+        val = cl >= 0 ? p.W[cl] : 0.0;
+        if (ct == 2) val += d2 * p.ih2 * ci;
+        else if (ct == 1) val -= p.ih2 * p.c[gnode(p, col, gx0, gy0, gz0)];
+      }
       a[q] = val;
     };
     for (int q = p.lptr[i]; q < p.lptr[i + 1]; ++q) set(q, p.lcol[q]);
@@ -160,18 +192,20 @@ __global__ void __launch_bounds__(AWMAX * 32) k_ilu_apply(const IluArgs p, int n
   extern __shared__ double ysh[];
   if (p.gate && *p.gate) return;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int box = blockIdx.x * (blockDim.x >> 5) + wid;
-  if (box >= nbox) return;                     // whole warps only
+  const int bl = blockIdx.x * (blockDim.x >> 5) + wid;   // position in this launch's box list
+  if (bl >= nbox) return;                      // whole warps only
+  const int box = p.boxes ? p.boxes[bl] : bl;
   double* y = ysh + (size_t)wid * p.n;
   int gx0, gy0, gz0, ibx, iby, ibz;
   box_origin(p, box, gx0, gy0, gz0, ibx, iby, ibz);
-  const double* a = p.vals + (size_t)box * p.nnz;
+  const double* a = p.vals + (size_t)bl * p.nnz;
   const int Ex = p.bx + 2 * p.o, Ey = p.by + 2 * p.o;
   for (int l = lane; l < p.n; l += 32) {
     const int li = l % Ex, lj = (l / Ex) % Ey, lk = l / (Ex * Ey);
     const bool owned = li >= p.o && li < p.o + p.bx && lj >= p.o && lj < p.o + p.by &&
                        (p.nd == 2 || (lk >= p.o && lk < p.o + p.bz));
-    y[l] = (p.restrict_owned && !owned) ? 0.0 : p.v[gnode(p, l, gx0, gy0, gz0)];
+    y[l] = ((p.restrict_owned && !owned) || !in_dom(p, l, gx0, gy0, gz0))
+               ? 0.0 : p.v[gnode(p, l, gx0, gy0, gz0)];
   }
   __syncwarp();
   // Both sweeps: rows of a level on the lanes.  The factor values and column indices of a row
@@ -313,17 +347,27 @@ __global__ void __launch_bounds__(AWMAX * 32) k_ilu_apply(const IluArgs p, int n
 
 // ---------------------------------------------------------------- host: symbolic setup
 
-struct pfc_ilu {
-  int n = 0, nnz = 0, nflev = 0, nblev = 0;
+// one class of boxes: pattern, IKJ lists, schedules and the factor values of its boxes
+struct IluClass {
+  int nnz = 0, nflev = 0, nblev = 0;
   int nL = 0, nU = 0, maxrow = 0, maxupd = 0;
   int maxlev = 1;                 // rows of the widest factorisation level
   int* d_ukptr = nullptr; int* d_usrc = nullptr; int* d_udst = nullptr;
   int* d_lptr = nullptr; int* d_lcol = nullptr; int* d_uptr = nullptr; int* d_ucol = nullptr;
-  int* d_ecls = nullptr; int* d_ectype = nullptr;
+  int* d_ecls = nullptr; int* d_ectype = nullptr; int* d_eccnt = nullptr;
+  double* d_elin = nullptr;
   int* d_flev_ptr = nullptr; int* d_flev_row = nullptr;
   int* d_blev_ptr = nullptr; int* d_blev_row = nullptr;
+  int* d_boxes = nullptr;         // global ids of the class's boxes (null: every box in order)
   double* d_vals = nullptr;
   size_t nbox = 0;
+};
+
+struct pfc_ilu {
+  int n = 0;
+  size_t nbox = 0;        // all boxes
+  size_t nnz_total = 0;   // factor entries over all boxes
+  std::vector<IluClass> cls;
 };
 
 static bool up(pfc_ctx* ctx, int** d, const std::vector<int>& h) {
@@ -331,49 +375,90 @@ static bool up(pfc_ctx* ctx, int** d, const std::vector<int>& h) {
   return cudaMemcpy(*d, h.data(), h.size() * sizeof(int), cudaMemcpyHostToDevice) == cudaSuccess;
 }
 
-pfc_status ilu_setup(pfc_ctx* ctx) {
+constexpr size_t kSmemPlan = 200 * 1024;
+
+// dt-free class weights of the linear part (as in ras2d.cu / ras3d_col.cu);
+// class 0 gets 1/dt at factor time
+static void class_weights(const pfc_ctx* ctx, double* W) {
+  const pfc_config& cf = ctx->cfg;
+  const double ih2 = ctx->ih2, ih4 = ih2 * ih2, ih6 = ih4 * ih2, al = 0.5 * (1.0 - cf.gamma);
+  if (cf.ndim == 2) {
+    W[0] = 4.0 * al * ih2 - 20.0 * ih4 + 56.0 * ih6;
+    W[1] = -al * ih2 + 8.0 * ih4 - 28.5 * ih6;
+    W[2] = -ih4 + 6.0 * ih6;
+    W[3] = -2.0 * ih4 + 12.0 * ih6;
+    W[4] = -0.5 * ih6;
+    W[5] = -1.5 * ih6;
+    W[6] = 0.0;
+  } else {
+    W[0] = 6.0 * al * ih2 - 42.0 * ih4 + 162.0 * ih6;
+    W[1] = -al * ih2 + 12.0 * ih4 - 61.5 * ih6;
+    W[2] = -ih4 + 9.0 * ih6;
+    W[3] = -2.0 * ih4 + 18.0 * ih6;
+    W[4] = -0.5 * ih6;
+    W[5] = -1.5 * ih6;
+    W[6] = -3.0 * ih6;
+  }
+}
+
+// Symbolic factorisation of one class.  g0 = global coordinates of ext-box node (0,0,0) of a
+// box of the class (mirror walls only; the class fixes g0 up to shifts that change nothing).
+static pfc_status build_class(pfc_ctx* ctx, const int* E, const int* g0, bool mirror,
+                              IluClass* I) {
   const pfc_config& c = ctx->cfg;
   const int nd = c.ndim;
-  int E[3] = {1, 1, 1};
-  for (int d = 0; d < nd; ++d) E[d] = c.ras_box[d] + 2 * c.ras_overlap;
   const int n = E[0] * E[1] * E[2];
-  // cheap early rejection (before the symbolic factorisation, whose lists grow like band^2):
-  // the ext box must fit the factor kernel's shared-memory plan, and so must the complete fill
-  // of the natural-order LU, whose rows span the band b = 3 E0 (2D) / 3 E0 E1 (3D) on both
-  // sides of the diagonal (row length <= 2b+1) with up to b^2 IKJ updates per row
-  constexpr size_t kSmemPlan = 200 * 1024;
-  if ((size_t)n * sizeof(double) > kSmemPlan)
-    return pfc_fail(ctx, PFC_EINVAL, "ILU: ext box too large for the shared-memory plan");
-  if (c.ras_local_solver == PFC_LOCAL_LU) {
-    const size_t b = (size_t)3 * E[0] * (nd == 3 ? E[1] : 1);
-    const size_t mr = 2 * b + 1, mu = b * b;
-    if ((2 * mr + mu) * 8 + (mr + 1 + mu) * 4 > kSmemPlan)
-      return pfc_fail(ctx, PFC_EINVAL,
-                      "LU: complete fill of this ext box exceeds the shared-memory plan "
-                      "(every 3D box of the configs; use PFC_LOCAL_ILU or PFC_LOCAL_GMRES)");
-  }
   auto pos = [&](int i, int j, int k) { return i + E[0] * (j + E[1] * k); };
+  // ext-box coordinate of stencil point l + d on one axis, or -1: outside the ext box (the
+  // zero ring of R8); mirror walls: the even extension's image of a point beyond a wall (R23)
+  auto target = [&](int ax, int l, int d) {
+    int t = l + d;
+    if (mirror) {
+      int g = g0[ax] + t;
+      if (g < 0) g = -1 - g;
+      else if (g >= c.n[ax]) g = 2 * c.n[ax] - 1 - g;
+      t = g - g0[ax];
+    }
+    return (t < 0 || t >= E[ax]) ? -1 : t;
+  };
+  auto inside = [&](int i, int j, int k) {
+    if (!mirror) return true;
+    const int l[3] = {i, j, k};
+    for (int d = 0; d < nd; ++d)
+      if (g0[d] + l[d] < 0 || g0[d] + l[d] >= c.n[d]) return false;
+    return true;
+  };
   // pattern of A: the radius-3 L1 stencil truncated at the box, per row a map col -> level
+  struct Meta { int cnt[7] = {0, 0, 0, 0, 0, 0, 0}; int ccnt = 0; int ct = 0; };
   std::vector<std::map<int, int>> rows(n);
-  std::vector<std::map<int, std::pair<int, int>>> meta(n);   // col -> (class, ctype)
+  std::vector<std::map<int, Meta>> meta(n);
   const int R = 3;
   for (int k = 0; k < E[2]; ++k)
     for (int j = 0; j < E[1]; ++j)
       for (int i = 0; i < E[0]; ++i) {
         const int r = pos(i, j, k);
+        if (!inside(i, j, k)) {      // no unknown: identity row
+          rows[r][r] = 0;
+          meta[r][r].ct = 3;
+          continue;
+        }
         for (int dz = (nd == 3 ? -R : 0); dz <= (nd == 3 ? R : 0); ++dz)
           for (int dy = -R; dy <= R; ++dy)
             for (int dx = -R; dx <= R; ++dx) {
               const int ax = std::abs(dx), ay = std::abs(dy), az = std::abs(dz);
               if (ax + ay + az > R) continue;
-              const int ii = i + dx, jj = j + dy, kk = k + dz;
-              if (ii < 0 || ii >= E[0] || jj < 0 || jj >= E[1] || kk < 0 || kk >= E[2]) continue;
+              const int ii = target(0, i, dx), jj = target(1, j, dy);
+              const int kk = nd == 3 ? target(2, k, dz) : 0;
+              if (ii < 0 || jj < 0 || kk < 0) continue;
               int s[3] = {ax, ay, az};
               std::sort(s, s + 3);
-              const int cl = wclass(s[0], s[1], s[2]);
-              const int ct = (ax + ay + az == 0) ? 2 : (ax + ay + az == 1) ? 1 : 0;
-              rows[r][pos(ii, jj, kk)] = 0;
-              meta[r][pos(ii, jj, kk)] = {cl, ct};
+              const int col = pos(ii, jj, kk);
+              rows[r][col] = 0;
+              Meta& m = meta[r][col];
+              m.cnt[wclass(s[0], s[1], s[2])]++;
+              if (ax + ay + az == 1) m.ccnt++;
+              if (col == r) m.ct = 2;
+              else if (m.ct == 0 && ax + ay + az == 1) m.ct = 1;
             }
       }
   // ILU(k) fill levels, row by row (rows k < i are final when row i is processed); the paper's
@@ -394,7 +479,8 @@ pfc_status ilu_setup(pfc_ctx* ctx) {
   }
   // value positions: the L block (strictly lower entries of every row, in row order), then the
   // U block (diagonal first, then the upper entries, in row order)
-  std::vector<int> lptr(n + 1, 0), uptr(n + 1, 0), lcol, ucol, ecls, ectype;
+  std::vector<int> lptr(n + 1, 0), uptr(n + 1, 0), lcol, ucol, ecls, ectype, eccnt;
+  std::vector<double> elin;
   std::vector<std::map<int, int>> where(n);
   for (int i = 0; i < n; ++i) {
     for (auto& e : rows[i])
@@ -408,12 +494,31 @@ pfc_status ilu_setup(pfc_ctx* ctx) {
   const int nL = (int)lcol.size(), nU = (int)ucol.size(), nnz = nL + nU;
   ecls.assign(nnz, -1);
   ectype.assign(nnz, 0);
+  if (mirror) {
+    eccnt.assign(nnz, 0);
+    elin.assign(nnz, 0.0);
+  }
+  double Wn[7];
+  class_weights(ctx, Wn);
   for (int i = 0; i < n; ++i) {
     for (int q = lptr[i]; q < lptr[i + 1]; ++q) where[i][lcol[q]] = q;
     for (int t = uptr[i]; t < uptr[i + 1]; ++t) where[i][ucol[t]] = nL + t;
     for (auto& w : where[i]) {
       auto m = meta[i].find(w.first);
-      if (m != meta[i].end()) { ecls[w.second] = m->second.first; ectype[w.second] = m->second.second; }
+      if (m == meta[i].end()) continue;
+      const Meta& mm = m->second;
+      ectype[w.second] = mm.ct;
+      if (!mirror) {   // exactly one offset per column: its class, as before
+        for (int cl = 0; cl < 7; ++cl)
+          if (mm.cnt[cl]) ecls[w.second] = cl;
+      } else if (mm.ct == 3) {
+        elin[w.second] = 1.0;
+      } else {
+        double v = 0.0;
+        for (int cl = 0; cl < 7; ++cl) v += mm.cnt[cl] * Wn[cl];
+        elin[w.second] = v;
+        eccnt[w.second] = mm.ccnt;
+      }
     }
   }
   // IKJ updates per row: for the L entry q of row i (column k, ascending), the updates
@@ -455,16 +560,12 @@ pfc_status ilu_setup(pfc_ctx* ctx) {
     return nl;
   };
   std::vector<int> fptr, frow, bptr, brow;
-  pfc_ilu* I = new pfc_ilu();
-  ctx->ilu = I;
-  I->n = n; I->nnz = nnz; I->nL = nL; I->nU = nU; I->maxupd = maxupd;
+  I->nnz = nnz; I->nL = nL; I->nU = nU; I->maxupd = maxupd;
   for (int i = 0; i < n; ++i)
     I->maxrow = std::max(I->maxrow, (lptr[i + 1] - lptr[i]) + (uptr[i + 1] - uptr[i]));
   I->nflev = group(flev, fptr, frow);
   for (int l = 0; l < I->nflev; ++l) I->maxlev = std::max(I->maxlev, fptr[l + 1] - fptr[l]);
   I->nblev = group(blev, bptr, brow);
-  I->nbox = 1;
-  for (int d = 0; d < nd; ++d) I->nbox *= (size_t)(c.n[d] / c.ras_box[d]);
   if (!up(ctx, &I->d_lptr, lptr) || !up(ctx, &I->d_lcol, lcol) || !up(ctx, &I->d_uptr, uptr) ||
       !up(ctx, &I->d_ucol, ucol) ||
       !up(ctx, &I->d_ecls, ecls) || !up(ctx, &I->d_ectype, ectype) ||
@@ -472,36 +573,116 @@ pfc_status ilu_setup(pfc_ctx* ctx) {
       !up(ctx, &I->d_flev_ptr, fptr) || !up(ctx, &I->d_flev_row, frow) ||
       !up(ctx, &I->d_blev_ptr, bptr) || !up(ctx, &I->d_blev_row, brow))
     return pfc_fail(ctx, PFC_ENOMEM, "ILU structures");
+  if (mirror) {
+    if (!up(ctx, &I->d_eccnt, eccnt) ||
+        cudaMalloc(&I->d_elin, std::max<size_t>(nnz, 1) * sizeof(double)) != cudaSuccess ||
+        cudaMemcpy(I->d_elin, elin.data(), (size_t)nnz * sizeof(double),
+                   cudaMemcpyHostToDevice) != cudaSuccess)
+      return pfc_fail(ctx, PFC_ENOMEM, "ILU structures");
+  }
   if ((size_t)(2 * I->maxrow + I->maxupd) * 8 + (I->maxrow + 1 + I->maxupd) * 4 > kSmemPlan)
     return pfc_fail(ctx, PFC_EINVAL, "ILU: rows too large for the shared-memory plan");
-  if (cudaMalloc(&I->d_vals, I->nbox * nnz * sizeof(double)) != cudaSuccess)   // after the checks
-    return pfc_fail(ctx, PFC_ENOMEM, "ILU factor values");
+  return PFC_OK;
+}
+
+pfc_status ilu_setup(pfc_ctx* ctx) {
+  const pfc_config& c = ctx->cfg;
+  const int nd = c.ndim;
+  const bool mirror = c.bc == PFC_BC_MIRROR;
+  int E[3] = {1, 1, 1};
+  for (int d = 0; d < nd; ++d) E[d] = c.ras_box[d] + 2 * c.ras_overlap;
+  const int n = E[0] * E[1] * E[2];
+  // cheap early rejection (before the symbolic factorisation, whose lists grow like band^2):
+  // the ext box must fit the factor kernel's shared-memory plan, and so must the complete fill
+  // of the natural-order LU, whose rows span the band b = 3 E0 (2D) / 3 E0 E1 (3D) on both
+  // sides of the diagonal (row length <= 2b+1) with up to b^2 IKJ updates per row
+  if ((size_t)n * sizeof(double) > kSmemPlan)
+    return pfc_fail(ctx, PFC_EINVAL, "ILU: ext box too large for the shared-memory plan");
+  if (c.ras_local_solver == PFC_LOCAL_LU) {
+    const size_t b = (size_t)3 * E[0] * (nd == 3 ? E[1] : 1);
+    const size_t mr = 2 * b + 1, mu = b * b;
+    if ((2 * mr + mu) * 8 + (mr + 1 + mu) * 4 > kSmemPlan)
+      return pfc_fail(ctx, PFC_EINVAL,
+                      "LU: complete fill of this ext box exceeds the shared-memory plan "
+                      "(every 3D box of the configs; use PFC_LOCAL_ILU or PFC_LOCAL_GMRES)");
+  }
+  pfc_ilu* I = new pfc_ilu();
+  ctx->ilu = I;
+  I->n = n;
+  int nb[3] = {1, 1, 1};
+  for (int d = 0; d < nd; ++d) nb[d] = c.n[d] / c.ras_box[d];
+  I->nbox = (size_t)nb[0] * nb[1] * nb[2];
+  // classes of boxes.  Periodic: one.  Mirror walls: per axis the position of the ext box
+  // relative to either wall, capped at the stencil radius (beyond it no stencil point of the
+  // box reaches the wall); negative = clipped layers
+  std::map<std::vector<int>, int> index;
+  std::vector<std::vector<int>> members;      // global box ids per class
+  std::vector<std::vector<int>> origin;       // g0 of the class's first box
+  for (int bz = 0; bz < nb[2]; ++bz)
+    for (int by = 0; by < nb[1]; ++by)
+      for (int bx = 0; bx < nb[0]; ++bx) {
+        const int ib[3] = {bx, by, bz};
+        std::vector<int> key, g0(3, 0);
+        for (int d = 0; d < nd; ++d) {
+          g0[d] = ib[d] * c.ras_box[d] - c.ras_overlap;
+          if (mirror) {
+            key.push_back(std::min(g0[d], 3));
+            key.push_back(std::min(c.n[d] - g0[d] - E[d], 3));
+          }
+        }
+        auto it = index.find(key);
+        if (it == index.end()) {
+          it = index.emplace(key, (int)members.size()).first;
+          members.emplace_back();
+          origin.push_back(g0);
+        }
+        members[it->second].push_back(bx + nb[0] * (by + nb[1] * bz));
+      }
+  I->cls.resize(members.size());
+  for (size_t k = 0; k < members.size(); ++k) {
+    IluClass* C = &I->cls[k];
+    C->nbox = members[k].size();
+    pfc_status st = build_class(ctx, E, origin[k].data(), mirror, C);
+    if (st) return st;
+    if (mirror && !up(ctx, &C->d_boxes, members[k]))
+      return pfc_fail(ctx, PFC_ENOMEM, "ILU box lists");
+    I->nnz_total += C->nbox * (size_t)C->nnz;
+  }
+  for (auto& C : I->cls)   // after every check
+    if (cudaMalloc(&C.d_vals, C.nbox * (size_t)C.nnz * sizeof(double)) != cudaSuccess)
+      return pfc_fail(ctx, PFC_ENOMEM, "ILU factor values");
   return PFC_OK;
 }
 
 void ilu_free(pfc_ctx* ctx) {
   pfc_ilu* I = ctx->ilu;
   if (!I) return;
-  int* a[] = {I->d_lptr, I->d_lcol, I->d_uptr, I->d_ucol, I->d_ecls, I->d_ectype, I->d_ukptr,
-              I->d_usrc, I->d_udst, I->d_flev_ptr, I->d_flev_row, I->d_blev_ptr, I->d_blev_row};
-  for (int* p : a)
-    if (p) cudaFree(p);
-  if (I->d_vals) cudaFree(I->d_vals);
+  for (auto& C : I->cls) {
+    int* a[] = {C.d_lptr, C.d_lcol, C.d_uptr, C.d_ucol, C.d_ecls, C.d_ectype, C.d_eccnt,
+                C.d_ukptr, C.d_usrc, C.d_udst, C.d_flev_ptr, C.d_flev_row, C.d_blev_ptr,
+                C.d_blev_row, C.d_boxes};
+    for (int* p : a)
+      if (p) cudaFree(p);
+    if (C.d_elin) cudaFree(C.d_elin);
+    if (C.d_vals) cudaFree(C.d_vals);
+  }
   delete I;
   ctx->ilu = nullptr;
 }
 
-static IluArgs ilu_args(pfc_ctx* ctx, double dt) {
+static IluArgs ilu_args(pfc_ctx* ctx, const IluClass& C, double dt) {
   const pfc_config& cf = ctx->cfg;
-  pfc_ilu* I = ctx->ilu;
   IluArgs p{};
-  p.vals = I->d_vals; p.lptr = I->d_lptr; p.lcol = I->d_lcol; p.uptr = I->d_uptr;
-  p.ucol = I->d_ucol; p.nL = I->nL; p.nU = I->nU;
-  p.ecls = I->d_ecls; p.ectype = I->d_ectype; p.ukptr = I->d_ukptr; p.usrc = I->d_usrc;
-  p.udst = I->d_udst; p.maxrow = I->maxrow; p.maxupd = I->maxupd;
-  p.flev_ptr = I->d_flev_ptr; p.flev_row = I->d_flev_row;
-  p.blev_ptr = I->d_blev_ptr; p.blev_row = I->d_blev_row;
-  p.nflev = I->nflev; p.nblev = I->nblev; p.n = I->n; p.nnz = I->nnz;
+  p.vals = C.d_vals; p.lptr = C.d_lptr; p.lcol = C.d_lcol; p.uptr = C.d_uptr;
+  p.ucol = C.d_ucol; p.nL = C.nL; p.nU = C.nU;
+  p.ecls = C.d_ecls; p.ectype = C.d_ectype; p.ukptr = C.d_ukptr; p.usrc = C.d_usrc;
+  p.elin = C.d_elin; p.eccnt = C.d_eccnt; p.boxes = C.d_boxes;
+  p.mirror = cf.bc == PFC_BC_MIRROR;
+  p.idt = 1.0 / dt;
+  p.udst = C.d_udst; p.maxrow = C.maxrow; p.maxupd = C.maxupd;
+  p.flev_ptr = C.d_flev_ptr; p.flev_row = C.d_flev_row;
+  p.blev_ptr = C.d_blev_ptr; p.blev_row = C.d_blev_row;
+  p.nflev = C.nflev; p.nblev = C.nblev; p.n = ctx->ilu->n; p.nnz = C.nnz;
   p.nx = cf.n[0]; p.ny = cf.n[1]; p.nz = cf.ndim == 3 ? cf.n[2] : 1;
   p.bx = cf.ras_box[0]; p.by = cf.ras_box[1]; p.bz = cf.ndim == 3 ? cf.ras_box[2] : 1;
   p.o = cf.ras_overlap; p.nd = cf.ndim;
@@ -529,53 +710,58 @@ static IluArgs ilu_args(pfc_ctx* ctx, double dt) {
 }
 
 cudaError_t launch_ilu_factor(pfc_ctx* ctx, const double* c, double dt) {
-  IluArgs p = ilu_args(ctx, dt);
-  p.c = c;
-  const size_t per_warp = (2 * p.maxrow + p.maxupd) * sizeof(double) +
-                          (p.maxrow + 1 + p.maxupd) * sizeof(int);
-  // one warp per row of the widest level (12 for 36^2 boxes): more warps only wait at the level
-  // barriers and cost resident CTAs (measured: 16 warps 3.10 ms, 12 warps 2.35 ms at cfg2)
-  int nw = (int)std::max<size_t>(1, std::min<size_t>(NT / 32, (200 * 1024) / per_warp));
-  nw = std::max(1, std::min(nw, ctx->ilu->maxlev));
-  const size_t sm = (size_t)nw * per_warp;
   static size_t attr = 0;
-  if (sm > 48 * 1024 && sm > attr) {
-    cudaError_t e = cudaFuncSetAttribute(k_ilu_factor, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)sm);
-    if (e != cudaSuccess) return e;
-    attr = sm;
+  for (const IluClass& C : ctx->ilu->cls) {
+    IluArgs p = ilu_args(ctx, C, dt);
+    p.c = c;
+    const size_t per_warp = (2 * p.maxrow + p.maxupd) * sizeof(double) +
+                            (p.maxrow + 1 + p.maxupd) * sizeof(int);
+    // one warp per row of the widest level (12 for 36^2 boxes): more warps only wait at the
+    // level barriers and cost resident CTAs (measured: 16 warps 3.10 ms, 12 warps 2.35 ms at
+    // cfg2)
+    int nw = (int)std::max<size_t>(1, std::min<size_t>(NT / 32, kSmemPlan / per_warp));
+    nw = std::max(1, std::min(nw, C.maxlev));
+    const size_t sm = (size_t)nw * per_warp;
+    if (sm > 48 * 1024 && sm > attr) {
+      cudaError_t e = cudaFuncSetAttribute(
+          k_ilu_factor, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      if (e != cudaSuccess) return e;
+      attr = sm;
+    }
+    k_ilu_factor<<<(int)C.nbox, nw * 32, sm, ctx->stream>>>(p);
+    ctx->launches++;
   }
-  k_ilu_factor<<<(int)ctx->ilu->nbox, nw * 32, sm, ctx->stream>>>(p);
-  ctx->launches++;
   ctx->ilu_dt = dt;
-  pfc_account(ctx, PFC_K_RAS, 8.0 * ctx->N + 8.0 * ctx->ilu->nbox * ctx->ilu->nnz,
-              2.0 * ctx->ilu->nbox * ctx->ilu->nnz);
+  pfc_account(ctx, PFC_K_RAS, 8.0 * ctx->N + 8.0 * ctx->ilu->nnz_total,
+              2.0 * ctx->ilu->nnz_total);
   return cudaGetLastError();
 }
 
 cudaError_t launch_ras_ilu(pfc_ctx* ctx, const double* v, double* z) {
   const pfc_config& cf = ctx->cfg;
-  IluArgs p = ilu_args(ctx, ctx->ilu_dt);
-  p.v = v;
-  p.z = z;
-  p.y_ext = cf.ras_variant == PFC_RAS_LEFT ? nullptr : ctx->ras_y;
-  p.gate = ctx->gate;
-  const int aw = std::max(1, std::min<int>(AWMAX, (int)((200 * 1024) / ((size_t)p.n * 8))));
-  const size_t sm = (size_t)aw * p.n * sizeof(double);
   static size_t attr = 0;
-  if (sm > 48 * 1024 && sm > attr) {
-    cudaError_t e = cudaFuncSetAttribute(k_ilu_apply, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)sm);
-    if (e != cudaSuccess) return e;
-    attr = sm;
+  for (const IluClass& C : ctx->ilu->cls) {
+    IluArgs p = ilu_args(ctx, C, ctx->ilu_dt);
+    p.v = v;
+    p.z = z;
+    p.y_ext = cf.ras_variant == PFC_RAS_LEFT ? nullptr : ctx->ras_y;
+    p.gate = ctx->gate;
+    const int aw = std::max(1, std::min<int>(AWMAX, (int)(kSmemPlan / ((size_t)p.n * 8))));
+    const size_t sm = (size_t)aw * p.n * sizeof(double);
+    if (sm > 48 * 1024 && sm > attr) {
+      cudaError_t e = cudaFuncSetAttribute(
+          k_ilu_apply, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      if (e != cudaSuccess) return e;
+      attr = sm;
+    }
+    const int nbox = (int)C.nbox;
+    k_ilu_apply<<<(nbox + aw - 1) / aw, aw * 32, sm, ctx->stream>>>(p, nbox);
+    ctx->launches++;
   }
-  const int nbox = (int)ctx->ilu->nbox;
-  k_ilu_apply<<<(nbox + aw - 1) / aw, aw * 32, sm, ctx->stream>>>(p, nbox);
-  ctx->launches++;
   {
     const double next = (double)ctx->ilu->nbox * ctx->ilu->n;
-    pfc_account(ctx, PFC_K_RAS, 8.0 * (next + ctx->N) + 8.0 * ctx->ilu->nbox * ctx->ilu->nnz,
-                4.0 * ctx->ilu->nbox * ctx->ilu->nnz);
+    pfc_account(ctx, PFC_K_RAS, 8.0 * (next + ctx->N) + 8.0 * ctx->ilu->nnz_total,
+                4.0 * ctx->ilu->nnz_total);
   }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess || cf.ras_variant == PFC_RAS_LEFT) return e;

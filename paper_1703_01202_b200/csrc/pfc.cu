@@ -489,8 +489,6 @@ static pfc_status validate(const pfc_config& c, std::string* why) {
     return bad("PFC_LOCAL_ILU / PFC_LOCAL_LU are built for PFC_MOBILITY_ONE");
   if (c.bc != PFC_BC_PERIODIC && c.bc != PFC_BC_MIRROR)
     return bad("bc must be PFC_BC_PERIODIC or PFC_BC_MIRROR");
-  if (c.bc == PFC_BC_MIRROR && c.ras_local_solver != PFC_LOCAL_GMRES)
-    return bad("PFC_BC_MIRROR is built for PFC_LOCAL_GMRES subdomain solves");
   if (c.bc == PFC_BC_MIRROR &&
       (c.ras_box[0] < 3 || c.ras_box[1] < 3 || (c.ndim == 3 && c.ras_box[2] < 3)))
     return bad("PFC_BC_MIRROR needs ras_box >= 3 (mirror partners inside the boundary box)");

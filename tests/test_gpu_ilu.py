@@ -180,3 +180,68 @@ def test_factor_one_step_parity_cfg2_geometry(solver, level, dt):
     assert ok and info["converged"]
     assert info["newton_its"] == oinfo.newton_its and info["gmres_its"] == oinfo.gmres_its
     assert rel(host(phi), ref) <= 1e-10
+
+
+# ---- mirror walls with the factor-based solves (round 2; rows f2 + f3, reading R23): the ext
+# boxes are clipped at the walls, near a wall several stencil offsets land on one column, and
+# the pattern / fill / schedules are built per class of boxes (ilu.cu)
+MIRROR_ILU_CASES = [
+    ((64, 64), (16, 16), 2, 0),
+    ((64, 64), (16, 16), 2, 1),
+    ((48, 36), (12, 12), 1, 2),
+    ((18, 15), (3, 3), 2, 1),        # unclipped boxes whose stencils still reach a wall
+    ((24, 24, 24), (8, 8, 8), 1, 0),
+]
+
+
+@pytest.mark.parametrize("variant", [P.PFC_RAS_LEFT, P.PFC_RAS_AS, P.PFC_RAS_RIGHT])
+@pytest.mark.parametrize("shape,box,o,level", MIRROR_ILU_CASES)
+def test_mirror_ilu_schwarz_parity(shape, box, o, level, variant):
+    phi = random_field(shape, 621, 0.07, 0.07)
+    psi = random_field(shape, 622, 0.07, 0.07)
+    v = random_field(shape, 623, 0.0, 1.0)
+    dt = 0.05
+    ctx = ctx_ilu(shape, box, o, level, ras_variant=variant, bc=P.PFC_BC_MIRROR)
+    z = host(ctx.ras_apply(dev(phi), dev(psi), dt, dev(v)))
+    zo = O.ras_apply(phi, psi, v, H, prm_ilu(box, o, level, ras_variant=variant,
+                                             bc=O.BC_MIRROR), dt)
+    assert rel(z, zo) <= 1e-12
+
+
+@pytest.mark.parametrize("variant", [P.PFC_RAS_LEFT, P.PFC_RAS_AS, P.PFC_RAS_RIGHT])
+@pytest.mark.parametrize("shape,box,o", [((64, 64), (16, 16), 2), ((18, 15), (3, 3), 2)])
+def test_mirror_lu_schwarz_parity(shape, box, o, variant):
+    phi = random_field(shape, 631, 0.07, 0.07)
+    psi = random_field(shape, 632, 0.07, 0.07)
+    v = random_field(shape, 633, 0.0, 1.0)
+    dt = 0.5
+    ctx = P.Context(None, ndim=2, n=shape, h=H, gamma=G, ras_box=list(box) + [1], ras_overlap=o,
+                    ras_local_solver=P.PFC_LOCAL_LU, ras_variant=variant, bc=P.PFC_BC_MIRROR)
+    z = host(ctx.ras_apply(dev(phi), dev(psi), dt, dev(v)))
+    zo = O.ras_apply(phi, psi, v, H, O.params(gamma=G, ras_box=box, ras_overlap=o,
+                                              ras_local_solver=O.LOCAL_LU, ras_variant=variant,
+                                              bc=O.BC_MIRROR), dt)
+    assert rel(z, zo) <= 1e-12
+
+
+@pytest.mark.parametrize("solver,dt", [("ilu", 0.02), ("lu", 0.5)])
+def test_mirror_factor_one_step_parity(solver, dt):
+    shape = (64, 64)
+    phi0 = random_field(shape, 1, 0.07, 0.07)
+    kw = dict(ras_ilu_reuse=1)
+    if solver == "ilu":
+        ctx = ctx_ilu(shape, (16, 16), 2, 0, bc=P.PFC_BC_MIRROR, **kw)
+        prm = prm_ilu((16, 16), 2, 0, bc=O.BC_MIRROR, **kw)
+    else:
+        ctx = P.Context(None, ndim=2, n=shape, h=H, gamma=G, ras_box=[16, 16, 1], ras_overlap=2,
+                        ras_local_solver=P.PFC_LOCAL_LU, bc=P.PFC_BC_MIRROR, **kw)
+        prm = O.params(gamma=G, ras_box=(16, 16), ras_overlap=2, ras_local_solver=O.LOCAL_LU,
+                       bc=O.BC_MIRROR, **kw)
+    phi = dev(phi0)
+    _, info = ctx.step(phi, dt)
+    ref, ok, oinfo = O.newton(phi0, H, prm, dt)
+    assert ok and info["converged"]
+    assert info["newton_its"] == oinfo.newton_its and info["gmres_its"] == oinfo.gmres_its
+    assert rel(host(phi), ref) <= 1e-10
+    m0 = O.mass(phi0, H, O.BC_MIRROR)
+    assert abs(info["mass"] - m0) <= 1e-9 * abs(m0)

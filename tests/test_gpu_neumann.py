@@ -138,8 +138,8 @@ def test_mirror_argument_errors():
     with pytest.raises(P.PfcError):   # 3D: a wall box needs its mirror partners (ras_box >= 3)
         P.Context(None, ndim=3, n=(24, 24, 24), h=H, gamma=G, ras_box=[8, 8, 2], ras_overlap=1,
                   bc=P.PFC_BC_MIRROR)
-    with pytest.raises(P.PfcError):   # factor path is periodic
-        ctx_n((64, 64), (16, 16), ras_local_solver=P.PFC_LOCAL_ILU)
+    with pytest.raises(P.PfcError):   # the factor path is built for M = 1
+        ctx_n((64, 64), (16, 16), mob=P.PFC_MOBILITY_QUADRATIC, ras_local_solver=P.PFC_LOCAL_ILU)
     with pytest.raises(P.PfcError):
         P.Context(None, ndim=2, n=(64, 64), h=H, gamma=G, ras_box=[16, 16, 1], bc=7)
 

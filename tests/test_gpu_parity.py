@@ -66,6 +66,10 @@ OPERATOR_CASES = [
     ((96, 72, 20), (16, 8, 10)),      # TMA path: edge tiles on every side, ragged y tail
     ((66, 50, 20), (11, 10, 10)),     # TMA path: ragged x and y tails
     ((128, 128, 128), (16, 16, 16)),
+    # seam-aligned TMA tiles (n_x, n_y multiples of 32: the producer-free 3D kernels, the
+    # residual with s written in place), several tiles per axis, z not a multiple of the unroll
+    ((64, 96, 24), (16, 16, 8)),
+    ((96, 32, 50), (16, 16, 10)),
 ]
 
 
