@@ -34,6 +34,15 @@
 #include "pfc_device.cuh"
 #include "pfc_internal.h"
 
+#include <algorithm>
+#include <functional>
+#include <queue>
+#include <vector>
+
+#ifndef ST3_TWO_PHASE
+#define ST3_TWO_PHASE 1   // 0: chunks only (the round-1 plan), diagnostic
+#endif
+
 namespace {
 
 constexpr int TX = 32, TY = 32;
@@ -82,11 +91,13 @@ struct S3Args {
   double* out;
   double* partials;
   int nx, ny, nz;
-  int zc;            // planes per chunk
+  int zc;            // planes per chunk (items beyond the first n1)
   double idt, k0, k1, k2, kout;   // (1-gamma)/2, ih2, ih2^2/2, -ih2
   int mode;          // 0: plain loads; 1: TMA + wrapped re-reads; 2: seam-aligned TMA tiles
   const int* gate;   // device-resident FGMRES: skip the launch when *gate != 0 (f1)
   const double* dtp; // graph path (f1): dt on the device
+  int n1;            // the first n1 items are whole z-columns of tiles 0..n1-1 (two-phase plan)
+  int ntiles;
 };
 
 struct q4 { double a, b, c, d; };   // (row0,col0) (row0,col1) (row1,col0) (row1,col1)
@@ -171,11 +182,23 @@ __global__ void __launch_bounds__(NT, 1) stencil3d_kernel(const __grid_constant_
   const bool tma = p.mode != 0, seam = p.mode == 2;
   // seam-aligned tiles (mode 2): the periodic seam lies on the boxes' shared edge; only the
   // tile column that straddles x = 0 needs the split (four-box) layout
-  const bool split = seam && blockIdx.x % ntx == 0;
-  const int x0 = (blockIdx.x % ntx) * TX - (seam ? 18 : 0);
-  const int y0 = (blockIdx.x / ntx) * TY - (seam ? 16 : 0);
-  const int z0 = blockIdx.y * p.zc;
-  const int zc = min(p.zc, nz - z0);
+  // work item -> (tile, z-chunk).  J v (1D grid): whole columns first, then the other tiles
+  // chunk by chunk.  The residual keeps the chunk-only plan on a (tiles, chunks) grid: the
+  // item decode costs it registers it does not have (24 B of spills in the z-march loop,
+  // 0.735 -> 0.80 ms at 512^3).
+  int tile = blockIdx.x, z0 = 0, zc = nz;
+  if (OP == OP_RESID) {
+    z0 = blockIdx.y * p.zc;
+    zc = min(p.zc, nz - z0);
+  } else if ((int)blockIdx.x >= p.n1) {
+    const int r = blockIdx.x - p.n1, nt2 = p.ntiles - p.n1;
+    tile = p.n1 + r % nt2;
+    z0 = (r / nt2) * p.zc;
+    zc = min(p.zc, nz - z0);
+  }
+  const bool split = seam && tile % ntx == 0;
+  const int x0 = (tile % ntx) * TX - (seam ? 18 : 0);
+  const int y0 = (tile / ntx) * TY - (seam ? 16 : 0);
   const int gx0 = x0 - 4, gy0 = y0 - 4;     // global coordinates of window cell (0,0)
   const size_t plane = (size_t)nx * ny;
   const int T = zc + 6;
@@ -436,16 +459,43 @@ __global__ void __launch_bounds__(NT, 1) stencil3d_kernel(const __grid_constant_
   }
 }
 
-// z chunking: minimise (waves of resident CTAs) x (planes streamed per CTA)
-int choose_chunks(int ntiles, int nz, int nsm) {
-  int best = 1;
-  double best_cost = 1e300;
-  for (int nzc = 1; nzc <= nz && nzc <= 256; ++nzc) {
-    const int zc = (nz + nzc - 1) / nzc;
-    if ((nz + zc - 1) / zc != nzc) continue;
-    const double waves = (double)((ntiles * nzc + nsm - 1) / nsm);
-    const double cost = waves * (zc + 6);
-    if (cost < best_cost - 1e-9) { best_cost = cost; best = nzc; }
+// Work plan: the first n1 tiles are streamed as whole z-columns (one item each, 6 halo planes
+// per 512 instead of per chunk), the other tiles in nzc chunks, launched chunk by chunk with the
+// tile index fastest, so the CTAs resident at any time march neighbouring tiles through the same
+// planes (their halos hit in L2).  n1 is 0 or a multiple of the SM count (a full wave of
+// columns); the plan minimising the makespan of in-order list scheduling on nsm SMs wins
+// (cost of an item = its streamed planes, padded to the unroll factor).
+struct Plan3 { int n1, nzc, zc, nitems; };
+Plan3 choose_plan(int ntiles, int nz, int nsm, bool two_phase) {
+  auto makespan = [&](int n1, int nzc, int zc) {
+    std::priority_queue<long, std::vector<long>, std::greater<long>> fin;   // SM finish times
+    for (int i = 0; i < nsm; ++i) fin.push(0);
+    long m = 0;
+    auto put = [&](int planes) {
+      const long f = fin.top() + (planes + 6 + 2) / 3 * 3;
+      fin.pop();
+      fin.push(f);
+      m = std::max(m, f);
+    };
+    for (int i = 0; i < n1; ++i) put(nz);
+    for (int c = 0; c < nzc; ++c)
+      for (int i = n1; i < ntiles; ++i) put(std::min(zc, nz - c * zc));
+    return m;
+  };
+  Plan3 best{0, 1, nz, ntiles};
+  long best_cost = -1;
+  for (int n1 = 0; n1 <= ntiles; n1 += nsm) {
+    for (int nzc = 1; nzc <= nz && nzc <= 64; ++nzc) {
+      const int zc = (nz + nzc - 1) / nzc;
+      if ((nz + zc - 1) / zc != nzc) continue;
+      if (n1 == ntiles && nzc > 1) break;
+      const long cost = makespan(n1, nzc, zc);
+      if (best_cost < 0 || cost < best_cost) {
+        best_cost = cost;
+        best = {n1, nzc, zc, n1 + (ntiles - n1) * nzc};
+      }
+    }
+    if (!two_phase) break;
   }
   return best;
 }
@@ -468,11 +518,18 @@ cudaError_t launch3d(pfc_ctx* ctx, const double* a, const double* b, double dt, 
   }
   const int nx = ctx->cfg.n[0], ny = ctx->cfg.n[1], nz = ctx->cfg.n[2];
   const int ntiles = ((nx + TX - 1) / TX) * ((ny + TY - 1) / TY);
-  const int nzc = choose_chunks(ntiles, nz, nsm);
-  const int zc = (nz + nzc - 1) / nzc;
+  static Plan3 plan{-1, 0, 0, 0};
+  static int plan_key[3] = {0, 0, 0};
+  if (plan.n1 < 0 || plan_key[0] != ntiles || plan_key[1] != nz || plan_key[2] != nsm) {
+    plan = choose_plan(ntiles, nz, nsm, OP == OP_JV && ST3_TWO_PHASE);
+    plan_key[0] = ntiles; plan_key[1] = nz; plan_key[2] = nsm;
+  }
+  const int zc = plan.zc;
   const double ih2 = ctx->ih2;
   S3Args p{a, b, out, partials, nx, ny, nz, zc, 1.0 / dt, 0.5 * (1.0 - ctx->cfg.gamma), ih2,
            0.5 * ih2 * ih2, -ih2, 0, OP == OP_JV ? ctx->gate : nullptr};
+  p.n1 = plan.n1;
+  p.ntiles = ntiles;
   p.dtp = ctx->dtdev;
   S3Maps m;
   memset(&m, 0, sizeof(m));
@@ -482,8 +539,8 @@ cudaError_t launch3d(pfc_ctx* ctx, const double* a, const double* b, double dt, 
       tma_encode(&m.a, a, 3, ctx->cfg.n, box) && tma_encode(&m.b, b, 3, ctx->cfg.n, box) &&
       tma_encode(&m.a22, a, 3, ctx->cfg.n, box22) && tma_encode(&m.b22, b, 3, ctx->cfg.n, box22))
     p.mode = (nx % TX == 0 && ny % TY == 0) ? 2 : 1;
-  dim3 grid(ntiles, nzc);
-  if (nparts) *nparts = grid.x * grid.y;
+  const dim3 grid = OP == OP_JV ? dim3(plan.nitems) : dim3(ntiles, plan.nzc);
+  if (nparts) *nparts = plan.nitems;
   stencil3d_kernel<OP><<<grid, NT, smem_bytes<OP>(), ctx->stream>>>(m, p);
   ctx->launches++;
   pfc_account(ctx, OP == OP_RESID ? PFC_K_RESIDUAL : PFC_K_JV, 24.0 * ctx->N,
