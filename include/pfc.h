@@ -233,6 +233,15 @@ pfc_status pfc_profile_enable(pfc_ctx* ctx, int on);
 pfc_status pfc_profile_query(pfc_ctx* ctx, int cls, long long* count, double* total_ms,
                              double* bytes, double* flops);
 
+/* Host-only diagnostic (no GPU needed): the work plan of the 3D stencil kernels
+ * for a grid of `ntiles` 32 x 32 xy-tiles and nz planes on nsm SMs.  plan[0] = n1, the number
+ * of tiles streamed as whole z-columns (0 or a multiple of nsm); plan[1] = nzc, the number of
+ * z-chunks of every other tile; plan[2] = zc, planes per chunk; plan[3] = the number of work
+ * items n1 + (ntiles - n1) nzc; plan[4] = the plan's makespan in streamed planes under in-order
+ * list scheduling (what the choice minimises).  two_phase = 0 restricts the choice to n1 = 0
+ * (the residual kernel's plan).  Returns PFC_EINVAL for non-positive sizes or a NULL plan. */
+pfc_status pfc_plan_stencil3d(int ntiles, int nz, int nsm, int two_phase, long long plan[5]);
+
 #ifdef __cplusplus
 }
 #endif

@@ -465,7 +465,7 @@ __global__ void __launch_bounds__(NT, 1) stencil3d_kernel(const __grid_constant_
 // planes (their halos hit in L2).  n1 is 0 or a multiple of the SM count (a full wave of
 // columns); the plan minimising the makespan of in-order list scheduling on nsm SMs wins
 // (cost of an item = its streamed planes, padded to the unroll factor).
-struct Plan3 { int n1, nzc, zc, nitems; };
+struct Plan3 { int n1, nzc, zc, nitems; long makespan; };
 Plan3 choose_plan(int ntiles, int nz, int nsm, bool two_phase) {
   auto makespan = [&](int n1, int nzc, int zc) {
     std::priority_queue<long, std::vector<long>, std::greater<long>> fin;   // SM finish times
@@ -482,7 +482,7 @@ Plan3 choose_plan(int ntiles, int nz, int nsm, bool two_phase) {
       for (int i = n1; i < ntiles; ++i) put(std::min(zc, nz - c * zc));
     return m;
   };
-  Plan3 best{0, 1, nz, ntiles};
+  Plan3 best{0, 1, nz, ntiles, 0};
   long best_cost = -1;
   for (int n1 = 0; n1 <= ntiles; n1 += nsm) {
     for (int nzc = 1; nzc <= nz && nzc <= 64; ++nzc) {
@@ -492,7 +492,7 @@ Plan3 choose_plan(int ntiles, int nz, int nsm, bool two_phase) {
       const long cost = makespan(n1, nzc, zc);
       if (best_cost < 0 || cost < best_cost) {
         best_cost = cost;
-        best = {n1, nzc, zc, n1 + (ntiles - n1) * nzc};
+        best = {n1, nzc, zc, n1 + (ntiles - n1) * nzc, cost};
       }
     }
     if (!two_phase) break;
@@ -518,7 +518,7 @@ cudaError_t launch3d(pfc_ctx* ctx, const double* a, const double* b, double dt, 
   }
   const int nx = ctx->cfg.n[0], ny = ctx->cfg.n[1], nz = ctx->cfg.n[2];
   const int ntiles = ((nx + TX - 1) / TX) * ((ny + TY - 1) / TY);
-  static Plan3 plan{-1, 0, 0, 0};
+  static Plan3 plan{-1, 0, 0, 0, 0};
   static int plan_key[3] = {0, 0, 0};
   if (plan.n1 < 0 || plan_key[0] != ntiles || plan_key[1] != nz || plan_key[2] != nsm) {
     plan = choose_plan(ntiles, nz, nsm, OP == OP_JV && ST3_TWO_PHASE);
@@ -549,6 +549,13 @@ cudaError_t launch3d(pfc_ctx* ctx, const double* a, const double* b, double dt, 
 }
 
 }  // namespace
+
+pfc_status pfc_plan_stencil3d(int ntiles, int nz, int nsm, int two_phase, long long plan[5]) {
+  if (ntiles < 1 || nz < 1 || nsm < 1 || !plan) return PFC_EINVAL;
+  const Plan3 pl = choose_plan(ntiles, nz, nsm, two_phase != 0);
+  plan[0] = pl.n1; plan[1] = pl.nzc; plan[2] = pl.zc; plan[3] = pl.nitems; plan[4] = pl.makespan;
+  return PFC_OK;
+}
 
 cudaError_t launch_residual_3d(pfc_ctx* ctx, const double* phi_new, const double* phi_old,
                                double dt, double* F, double* partials, int* nparts) {

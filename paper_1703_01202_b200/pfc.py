@@ -16,7 +16,8 @@ STATUS = {0: "PFC_OK", 1: "PFC_EINVAL", 2: "PFC_ENOMEM", 3: "PFC_ECUDA", 4: "PFC
 
 EXPORTS = ["pfc_config_default", "pfc_create", "pfc_destroy", "pfc_residual",
            "pfc_jacobian_apply", "pfc_ras_apply", "pfc_step", "pfc_energy", "pfc_mass",
-           "pfc_last_error", "pfc_kernel_launches", "pfc_profile_enable", "pfc_profile_query"]
+           "pfc_last_error", "pfc_kernel_launches", "pfc_profile_enable", "pfc_profile_query",
+           "pfc_plan_stencil3d"]
 
 KERNEL_CLASSES = ["residual", "jv", "ras", "coef", "orth", "finalize", "vector", "energy"]
 
@@ -86,11 +87,23 @@ def load():
     L.pfc_profile_query.argtypes = [vp, C.c_int, C.POINTER(C.c_longlong), C.POINTER(C.c_double),
                                     C.POINTER(C.c_double), C.POINTER(C.c_double)]
     L.pfc_profile_query.restype = C.c_int
+    L.pfc_plan_stencil3d.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int,
+                                     C.POINTER(C.c_longlong)]
+    L.pfc_plan_stencil3d.restype = C.c_int
     for name in ("pfc_create", "pfc_residual", "pfc_jacobian_apply", "pfc_ras_apply", "pfc_step",
                  "pfc_energy", "pfc_mass"):
         getattr(L, name).restype = C.c_int
     _lib = L
     return L
+
+
+def plan_stencil3d(ntiles: int, nz: int, nsm: int = 148, two_phase: bool = True) -> dict:
+    """Work plan of the 3D stencil kernels (host-only diagnostic, include/pfc.h)."""
+    out = (C.c_longlong * 5)()
+    st = load().pfc_plan_stencil3d(int(ntiles), int(nz), int(nsm), int(bool(two_phase)), out)
+    if st != PFC_OK:
+        raise PfcError(st, "pfc_plan_stencil3d: sizes must be positive")
+    return dict(n1=out[0], nzc=out[1], zc=out[2], nitems=out[3], makespan=out[4])
 
 
 def make_config(cfg=None, **over) -> PfcConfig:
