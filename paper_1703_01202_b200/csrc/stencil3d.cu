@@ -43,6 +43,12 @@
 #define ST3_TWO_PHASE 1   // 0: chunks only (the round-1 plan), diagnostic
 #endif
 
+#ifndef ST3_RES_SHFL
+#define ST3_RES_SHFL 0    // 1: residual takes the left / right stage-1 neighbours of s by warp
+                          // shuffles (diagnostic: bitwise equal, but 68 B of spills in the z-march
+                          // loop at the 168-register cap: 0.736 -> 1.172 ms at 512^3, not kept)
+#endif
+
 namespace {
 
 constexpr int TX = 32, TY = 32;
@@ -380,7 +386,35 @@ __global__ void __launch_bounds__(NT, 1) stencil3d_kernel(const __grid_constant_
       // outside neighbours of the planes produced in iteration t-1 (all loads before any store)
       q4 x1;
       if constexpr (OP == OP_RESID) {
+#if ST3_RES_SHFL
+        // left / right neighbours of s = Phi + psi at plane t-1 from the adjacent lanes'
+        // registers (the same sums the s plane holds), top / bottom from the s plane
+        const double* S = Ssp + ((t - 1) & 1) * SPLANE;
+        // (recomputed here by opaque adds: sharing them with c1's sums would keep four more
+        // doubles live across the iteration barrier, which spills at the 168-register cap)
+        double sa, sb, sc, sd;
+        asm volatile("add.f64 %0, %1, %2;" : "=d"(sa) : "d"(A1.a), "d"(B1.a));
+        asm volatile("add.f64 %0, %1, %2;" : "=d"(sb) : "d"(A1.b), "d"(B1.b));
+        asm volatile("add.f64 %0, %1, %2;" : "=d"(sc) : "d"(A1.c), "d"(B1.c));
+        asm volatile("add.f64 %0, %1, %2;" : "=d"(sd) : "d"(A1.d), "d"(B1.d));
+        double L0 = __shfl_up_sync(0xffffffffu, sb, 1);
+        double L1 = __shfl_up_sync(0xffffffffu, sd, 1);
+        double R0 = __shfl_down_sync(0xffffffffu, sa, 1);
+        double R1 = __shfl_down_sync(0xffffffffu, sc, 1);
+        if (!(pc > 1 && lane > 0)) {
+          L0 = S[SO + e0 - 1];
+          L1 = S[SO + e0 + SP - 1];
+        }
+        if (!(pc < NPB && lane < 31)) {
+          R0 = S[e0 + 1];
+          R1 = S[e0 + SP + 1];
+        }
+        const double Ta = S[e0 - SP], Tb = S[SO + e0 - SP];
+        const double Da = S[e0 + 2 * SP], Db = S[SO + e0 + 2 * SP];
+        x1 = {L0 + Ta, R0 + Tb, L1 + Da, R1 + Db};
+#else
         x1 = out_split(Ssp + ((t - 1) & 1) * SPLANE, e0);
+#endif
       } else {
         // left / right neighbours of the block are the adjacent lanes' own plane-(t-1) values
         // (shuffles; the stride-2 ring loads were 2-way bank conflicts), from the ring only at
