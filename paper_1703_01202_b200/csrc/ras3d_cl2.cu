@@ -72,6 +72,9 @@ struct Ras3Cl2Args {
   const int* gate;       // device-resident FGMRES: skip when *gate != 0
   double W[7];           // classes (0,0,0) (0,0,1) (0,0,2) (0,1,1) (0,0,3) (0,1,2) (1,1,1)
   double ih2;
+  double idt;            // 1 / dt (host value; the graph path reads dtp[1])
+  double HW[9];          // Horner-in-T form (CL2T_HORNER): z-weights of q0 (|dz| = 0..3, [0] without
+                         // the 1/dt term), q1 (|dz| = 0..2), q2 (|dz| = 0..1)
   unsigned long long* jcnt;
   const double* dtp;     // graph path (f1): dt-dependent scalars on the device
 };
@@ -1245,10 +1248,139 @@ __device__ __forceinline__ void tm_ld_vec(uint32_t ta, double (&v)[2][ZL]) {
 // L2 scratch (NG): the whole Krylov basis on chip.  Same layouts and arithmetic as
 // ras3d_cl2p_kernel, the CGS2 passes vector by vector with each inner product summed in four
 // independent chains (FP64 latency with 8 warps), so it agrees with cl2p to rounding.
+// ---- Horner-in-T form of the subdomain operator (CL2T_HORNER = 1) ---------------------------
+// With the unscaled Laplacian split as L = T + Z (T: 5-point xy part, Z: 3-point z part; they
+// commute) and A_k v = p(L) v + L (c' v), p(L) = a0 + a1 L + a2 L^2 + a3 L^3 (a0 = 1/dt,
+// a1 = -(1-gamma)/2 h^-2, a2 = -h^-4, a3 = -h^-6 / 2, c' = -c / h^2):
+//   U2 = q2(Z) v + a3 T v,   U1 = q1(Z) v + c' v + T U2,   A_k v = q0(Z) v + Z (c' v) + T U1,
+//   q0 = a0 + a1 Z + a2 Z^2 + a3 Z^3,  q1 = a1 + 2 a2 Z + 3 a3 Z^2,  q2 = a2 + 3 a3 Z.
+// Every q_m(Z) acts along the thread's own z-columns (their z-halo comes from the partner's
+// planes), each T stage reads the 6 outside xy neighbour columns of the thread's column pair
+// over the OWN z-range from a plane set the previous stage wrote (U2, then U1; c'-plane layout),
+// with a CTA barrier between stages.  v = 0 outside the box leaves U2 and U1 non-zero only on
+// the 4 E ring columns next to a box face (corners stay zero): the Givens warp computes those.
+#ifndef CL2T_HORNER
+#define CL2T_HORNER 0
+#endif
+
+// PART 0: the contributions of the CTA's own planes (before the partner's halo planes have
+// landed); PART 1: those of the halo planes.  U2 goes to its plane set as soon as an entry is
+// complete; U1 (without T U2) and w stay in registers.
+template <int E, int PART>
+__device__ __forceinline__ void hz_stage1(const Ras3Cl2Args& p, double q00, const double* pv,
+                                          const double* pc, double* pu, int rank,
+                                          double (&w)[2][E / 2], double (&u1)[2][E / 2],
+                                          double (&u2)[2][E / 2]) {
+  using C = Cl2p<E>;
+  constexpr int ZL = C::ZL, PX = C::PX, PP = C::PP, CX = C::CX, CP = C::CP;
+#pragma unroll
+  for (int zz = -3; zz < ZL + 3; ++zz) {
+    const bool own = zz >= 0 && zz < ZL;
+    if ((PART == 0) != own) continue;
+    // planes this CTA holds: rank 0 [0, ZL+3), rank 1 [-3, ZL); beyond the box face v = 0
+    const bool live = (zz >= 0 || rank != 0) && (zz < ZL || rank != 1);
+    if (live) {
+      const double val[2] = {pv[zz * PP], pv[zz * PP + PX]};
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+#pragma unroll
+        for (int z = (zz - 3 > 0 ? zz - 3 : 0); z <= (zz + 3 < ZL - 1 ? zz + 3 : ZL - 1); ++z) {
+          const int dz = zz > z ? zz - z : z - zz;
+          w[c][z] = fma(dz == 0 ? q00 : dz == 1 ? p.HW[1] : dz == 2 ? p.HW[2] : p.HW[3], val[c],
+                        w[c][z]);
+          if (dz <= 2)
+            u1[c][z] = fma(dz == 0 ? p.HW[4] : dz == 1 ? p.HW[5] : p.HW[6], val[c], u1[c][z]);
+          if (dz <= 1) u2[c][z] = fma(dz == 0 ? p.HW[7] : p.HW[8], val[c], u2[c][z]);
+        }
+      }
+      if (own) {   // a3 T v over the own z-range
+        const double n0 = pv[zz * PP - 1], n1 = pv[zz * PP + 1], n2 = pv[zz * PP - PX];
+        const double n3 = pv[zz * PP + 2 * PX], n4 = pv[zz * PP + PX - 1],
+                     n5 = pv[zz * PP + PX + 1];
+        const double t0 = fma(-4.0, val[0], (n0 + n1) + (n2 + val[1]));
+        const double t1 = fma(-4.0, val[1], (n4 + n5) + (n3 + val[0]));
+        u2[0][zz] = fma(p.HW[3], t0, u2[0][zz]);
+        u2[1][zz] = fma(p.HW[3], t1, u2[1][zz]);
+      }
+      if (zz >= -1 && zz <= ZL) {   // c' v: into U1 at its plane, Z (c' v) into w
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          const double cv = pc[zz * CP + c * CX] * val[c];
+          if (zz - 1 >= 0 && zz - 1 < ZL) w[c][zz - 1] += cv;
+          if (zz + 1 >= 0 && zz + 1 < ZL) w[c][zz + 1] += cv;
+          if (own) {
+            w[c][zz] = fma(-2.0, cv, w[c][zz]);
+            u1[c][zz] += cv;
+          }
+        }
+      }
+    }
+    // U2 entries that only own planes contribute to, as soon as they are complete
+    if (PART == 0 && zz - 1 >= 1 && zz - 1 <= ZL - 2) {
+      pu[(zz - 1) * CP] = u2[0][zz - 1];
+      pu[(zz - 1) * CP + CX] = u2[1][zz - 1];
+    }
+  }
+  if (PART == 1) {
+    pu[0] = u2[0][0];
+    pu[CX] = u2[1][0];
+    pu[(ZL - 1) * CP] = u2[0][ZL - 1];
+    pu[(ZL - 1) * CP + CX] = u2[1][ZL - 1];
+  }
+}
+
+// U1 += T U2 at the thread's nodes (registers), written to its plane set for the neighbours
+template <int E>
+__device__ __forceinline__ void hz_stage2(const double* pu, double* pq, double (&u1)[2][E / 2]) {
+  using C = Cl2p<E>;
+  constexpr int ZL = C::ZL, CX = C::CX, CP = C::CP;
+#pragma unroll
+  for (int zl = 0; zl < ZL; ++zl) {
+    const double* u = pu + zl * CP;
+    const double o0 = u[0], o1 = u[CX];
+    u1[0][zl] += fma(-4.0, o0, (u[-1] + u[1]) + (u[-CX] + o1));
+    u1[1][zl] += fma(-4.0, o1, (u[CX - 1] + u[CX + 1]) + (u[2 * CX] + o0));
+    pq[zl * CP] = u1[0][zl];
+    pq[zl * CP + CX] = u1[1][zl];
+  }
+}
+
+// w += T U1 at the thread's nodes
+template <int E>
+__device__ __forceinline__ void hz_stage3(const double* pq, const double (&u1)[2][E / 2],
+                                          double (&w)[2][E / 2]) {
+  using C = Cl2p<E>;
+  constexpr int ZL = C::ZL, CX = C::CX, CP = C::CP;
+#pragma unroll
+  for (int zl = 0; zl < ZL; ++zl) {
+    const double* u = pq + zl * CP;
+    const double o0 = u1[0][zl], o1 = u1[1][zl];
+    w[0][zl] += fma(-4.0, o0, (u[-1] + u[1]) + (u[-CX] + o1));
+    w[1][zl] += fma(-4.0, o1, (u[CX - 1] + u[CX + 1]) + (u[2 * CX] + o0));
+  }
+}
+
+// ring column q in [0, 4E) next to a box face: offsets (c'-plane layout) of the ring column,
+// its box neighbour and the step along the face; v-plane offset of the box neighbour
+template <int E>
+__device__ __forceinline__ void hz_ring(int q, int& ro, int& bo, int& eo, int& vo) {
+  using C = Cl2p<E>;
+  const int s = q / E, i = q - s * E;
+  int bx, by, rx, ry;
+  if (s == 0) { bx = 0; by = i; rx = -1; ry = i; eo = C::CX; }
+  else if (s == 1) { bx = E - 1; by = i; rx = E; ry = i; eo = C::CX; }
+  else if (s == 2) { bx = i; by = 0; rx = i; ry = -1; eo = 1; }
+  else { bx = i; by = E - 1; rx = i; ry = E; eo = 1; }
+  ro = (ry + 1) * C::CX + rx + 1;
+  bo = (by + 1) * C::CX + bx + 1;
+  vo = (by + 3) * C::PX + bx + 3;
+}
+
 template <int K, int E, int NRX>
 constexpr size_t cl2t_smem_doubles() {
   using C = Cl2p<E>;
-  return (size_t)C::NVB * C::PP + (size_t)C::NCB * C::CP + 2 * 2 * C::NW * RS + C::NW * 3 * RS;
+  return (size_t)C::NVB * C::PP + (size_t)C::NCB * C::CP + 2 * 2 * C::NW * RS + C::NW * 3 * RS +
+         (CL2T_HORNER ? 2 * (size_t)C::ZL * C::CP : 0);
 }
 
 template <int K, int E, int NRX>
@@ -1269,7 +1401,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cl2p<E>::NT, 1)
   double* cb = vb + NVB * PP;            // NCB padded planes of c' (rank 0: [0, ZL], rank 1:
                                          // [-1, ZL))
   double* vs = cb + NCB * CP;            // NS x [col][zl][thread]: basis vectors NR..NR+NS-1
-  double* red = vs + NS * 2 * ZL * NTN;  // 2 buffers x [rank][warp][RS]
+  constexpr int HZP = CL2T_HORNER ? ZL * CP : 0;
+  double* ub = vs + NS * 2 * ZL * NTN;   // Horner form: ZL planes of U2 (c'-plane layout) ...
+  double* qb = ub + HZP;                 // ... and of U1
+  double* red = qb + HZP;                // 2 buffers x [rank][warp][RS]
   double* hw = red + 2 * 2 * NW * RS;    // per warp: h1, h2, scratch
   __shared__ double H[(K + 1) * K];
   __shared__ double gv[K + 1], cs[K], sn[K], yv[K];
@@ -1287,6 +1422,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cl2p<E>::NT, 1)
   const int pv0 = rank == 0 ? 0 : 3, pc0 = rank == 0 ? 0 : 1;   // plane of zl = 0
   const double* pv = vb + pv0 * PP + colp;
   const double* pc = cb + pc0 * CP + colc;
+  double* pu = ub + colc;
+  double* pq = qb + colc;
   double* gs = p.gscr + (size_t)blockIdx.x * (NG > 0 ? NG : 1) * 2 * ZL * NTN + tid;
   double* h1 = hw + wid * 3 * RS;
   double* h2 = h1 + RS;
@@ -1300,7 +1437,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cl2p<E>::NT, 1)
   int rb = 0;
   const uint32_t mbar_rem0 = mapa_rank(smem_u32(&mbar[0]), (uint32_t)partner);
   // zero v planes (ring stays zero) and finite c'
-  for (int q = tid; q < NVB * PP + NCB * CP; q += blockDim.x) vb[q] = 0.0;
+  for (int q = tid; q < NVB * PP + NCB * CP + 2 * HZP; q += blockDim.x) vb[q] = 0.0;
   if (tid == 0) {
     for (int q = 0; q < 3; ++q) mbar_init(&mbar[q], 1);
     fence_mbar_init();
@@ -1468,6 +1605,51 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cl2p<E>::NT, 1)
       for (int c = 0; c < 2; ++c)
 #pragma unroll
         for (int zl = 0; zl < ZL; ++zl) w[c][zl] = 0.0;
+#if CL2T_HORNER
+      double u1[2][ZL], u2[2][ZL];
+#pragma unroll
+      for (int c = 0; c < 2; ++c)
+#pragma unroll
+        for (int zl = 0; zl < ZL; ++zl) {
+          u1[c][zl] = 0.0;
+          u2[c][zl] = 0.0;
+        }
+      const double q00 = dt_inv(p.dtp, p.idt) + p.HW[0];
+      if (act) {
+        hz_stage1<E, 0>(p, q00, pv, pc, pu, rank, w, u1, u2);
+      } else if (wid == NW - 1) {   // ring columns: U2 = a3 v(box neighbour)
+        for (int q = lane; q < 4 * E; q += 32) {
+          int ro, bo, eo, vo;
+          hz_ring<E>(q, ro, bo, eo, vo);
+#pragma unroll
+          for (int zl = 0; zl < ZL; ++zl)
+            ub[zl * CP + ro] = p.HW[3] * vb[(zl + pv0) * PP + vo];
+        }
+      }
+      C2P(3);
+      mbar_wait_cluster(&mbar[2], (ph >> 2) & 1u);
+      ph ^= 4u;
+      if (act) hz_stage1<E, 1>(p, q00, pv, pc, pu, rank, w, u1, u2);
+      __syncthreads();
+      C2P(4);
+      if (act) {
+        hz_stage2<E>(pu, pq, u1);
+      } else if (wid == NW - 1) {   // ring columns: U1 = T U2 (the outer neighbour is zero)
+        for (int q = lane; q < 4 * E; q += 32) {
+          int ro, bo, eo, vo;
+          hz_ring<E>(q, ro, bo, eo, vo);
+#pragma unroll
+          for (int zl = 0; zl < ZL; ++zl) {
+            const double* u = ub + zl * CP;
+            qb[zl * CP + ro] = fma(-4.0, u[ro], (u[bo] + u[ro + eo]) + u[ro - eo]);
+          }
+        }
+      }
+      __syncthreads();
+      C2P(15);
+      if (act) hz_stage3<E>(pq, u1, w);
+      C2P(5);
+#else
       if (act) cl2p_stencil<E, 0, ZL>(p, pv, pc, w);
       C2P(3);
       mbar_wait_cluster(&mbar[2], (ph >> 2) & 1u);
@@ -1478,6 +1660,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cl2p<E>::NT, 1)
         else cl2p_stencil<E, -3, 0>(p, pv, pc, w);
       }
       C2P(5);
+#endif
       double hn2 = 0.0;
       auto cgs2 = [&](auto Jc) {
         constexpr int J = decltype(Jc)::value;
@@ -1785,6 +1968,20 @@ cudaError_t launch_ras_3d_cl2(pfc_ctx* ctx, const double* v, const double* c, do
   p.W[5] = -1.5 * ih6;
   p.W[6] = -3.0 * ih6;
   p.ih2 = ih2;
+  p.idt = 1.0 / dt;
+  {   // Horner-in-T form: z-weights of q0, q1, q2 (Z = [1 -2 1], Z^2 = [1 -4 6 -4 1],
+      // Z^3 = [1 -6 15 -20 15 -6 1])
+    const double a1 = -al * ih2, a2 = -ih4, a3 = -0.5 * ih6;
+    p.HW[0] = -2.0 * a1 + 6.0 * a2 - 20.0 * a3;   // + 1/dt in the kernel
+    p.HW[1] = a1 - 4.0 * a2 + 15.0 * a3;
+    p.HW[2] = a2 - 6.0 * a3;
+    p.HW[3] = a3;
+    p.HW[4] = a1 - 4.0 * a2 + 18.0 * a3;
+    p.HW[5] = 2.0 * a2 - 12.0 * a3;
+    p.HW[6] = 3.0 * a3;
+    p.HW[7] = a2 - 6.0 * a3;
+    p.HW[8] = 3.0 * a3;
+  }
   fn<<<2 * clusters, threads, smem, ctx->stream>>>(p);
   ctx->launches++;
   {
