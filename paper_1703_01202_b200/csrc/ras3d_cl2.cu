@@ -75,6 +75,8 @@ struct Ras3Cl2Args {
   double idt;            // 1 / dt (host value; the graph path reads dtp[1])
   double HW[9];          // Horner-in-T form (CL2T_HORNER): z-weights of q0 (|dz| = 0..3, [0] without
                          // the 1/dt term), q1 (|dz| = 0..2), q2 (|dz| = 0..1)
+  double GW[7];          // two-stage form (CL2T_HORNER = 2), U1 = [q1(Z) + T q2(Z) + a3 T^2] v: own
+                         // column |dz| = 0..2, R1 columns |dz| = 0..1, R2 axis, R2 diagonal
   unsigned long long* jcnt;
   const double* dtp;     // graph path (f1): dt-dependent scalars on the device
 };
@@ -1360,6 +1362,101 @@ __device__ __forceinline__ void hz_stage3(const double* pq, const double (&u1)[2
   }
 }
 
+// ---- two-stage form (CL2T_HORNER = 2): U1 = [q1(Z) + T q2(Z) + a3 T^2] v + c' v evaluated directly
+// (radius-2 xy diamond, union of the two columns' diamonds, z-reach 2 / 1 / 0 for the own / R1 /
+// R2 columns) together with the own-column part q0(Z) v + Z (c' v) of w; then w += T U1.
+template <int E, int ZZ>
+__device__ __forceinline__ void hy_plane(const Ras3Cl2Args& p, double q00, const double* pv,
+                                         const double* pc, int rank, double (&w)[2][E / 2],
+                                         double (&u1)[2][E / 2]) {
+  using C = Cl2p<E>;
+  constexpr int ZL = C::ZL, PX = C::PX, PP = C::PP, CX = C::CX, CP = C::CP;
+  constexpr int zz = ZZ;
+  {
+    constexpr bool own = zz >= 0 && zz < ZL;
+    // planes this CTA holds: rank 0 [0, ZL+3), rank 1 [-3, ZL); beyond the box face v = 0
+    const bool live = (zz >= 0 || rank != 0) && (zz < ZL || rank != 1);
+    if (live) {
+    double g[2][4];
+#pragma unroll
+    for (int o = 0; o < 2; ++o)
+#pragma unroll
+      for (int k = 0; k < 4; ++k) g[o][k] = 0.0;
+#pragma unroll
+    for (int dx = -2; dx <= 2; ++dx) {
+#pragma unroll
+      for (int du = -2; du <= 3; ++du) {
+        bool need = false;
+#pragma unroll
+        for (int o = 0; o < 2; ++o) {
+          const int k = cl2p_group(o, dx, du);
+          const int reach = k == 0 ? 3 : k == 1 ? 1 : 0;
+          if (k >= 0 && k <= 3 && zz >= -reach && zz < ZL + reach) need = true;
+        }
+        if (!need) continue;
+        const double val = pv[zz * PP + dx + PX * du];
+#pragma unroll
+        for (int o = 0; o < 2; ++o) {
+          const int k = cl2p_group(o, dx, du);
+          const int reach = k == 0 ? 3 : k == 1 ? 1 : 0;
+          if (k < 0 || k > 3 || zz < -reach || zz >= ZL + reach) continue;
+          g[o][k] += val;
+        }
+      }
+    }
+#pragma unroll
+    for (int o = 0; o < 2; ++o) {
+#pragma unroll
+      for (int z = (zz - 3 > 0 ? zz - 3 : 0); z <= (zz + 3 < ZL - 1 ? zz + 3 : ZL - 1); ++z) {
+        const int dz = zz > z ? zz - z : z - zz;
+        w[o][z] = fma(dz == 0 ? q00 : dz == 1 ? p.HW[1] : dz == 2 ? p.HW[2] : p.HW[3], g[o][0],
+                      w[o][z]);
+        if (dz <= 2)
+          u1[o][z] = fma(dz == 0 ? p.GW[0] : dz == 1 ? p.GW[1] : p.GW[2], g[o][0], u1[o][z]);
+        if (dz <= 1) u1[o][z] = fma(dz == 0 ? p.GW[3] : p.GW[4], g[o][1], u1[o][z]);
+        if (dz == 0) {
+          u1[o][z] = fma(p.GW[5], g[o][2], u1[o][z]);
+          u1[o][z] = fma(p.GW[6], g[o][3], u1[o][z]);
+        }
+      }
+      if (zz >= -1 && zz <= ZL) {   // c' v: into U1 at its plane, Z (c' v) into w
+        const double cv = pc[zz * CP + o * CX] * g[o][0];
+        if (zz - 1 >= 0 && zz - 1 < ZL) w[o][zz - 1] += cv;
+        if (zz + 1 >= 0 && zz + 1 < ZL) w[o][zz + 1] += cv;
+        if (own) {
+          w[o][zz] = fma(-2.0, cv, w[o][zz]);
+          u1[o][zz] += cv;
+        }
+      }
+    }
+    }
+  }
+}
+
+// planes [ZZ, ZEND), unrolled by recursion (a 16-plane loop of this body is not fully unrolled
+// by the compiler at E = 20, which would put w and U1 in local memory)
+template <int E, int ZZ, int ZEND>
+__device__ __forceinline__ void hy_planes(const Ras3Cl2Args& p, double q00, const double* pv,
+                                          const double* pc, int rank, double (&w)[2][E / 2],
+                                          double (&u1)[2][E / 2]) {
+  if constexpr (ZZ < ZEND) {
+    hy_plane<E, ZZ>(p, q00, pv, pc, rank, w, u1);
+    hy_planes<E, ZZ + 1, ZEND>(p, q00, pv, pc, rank, w, u1);
+  }
+}
+template <int E, int PART>
+__device__ __forceinline__ void hy_stageA(const Ras3Cl2Args& p, double q00, const double* pv,
+                                          const double* pc, int rank, double (&w)[2][E / 2],
+                                          double (&u1)[2][E / 2]) {
+  constexpr int ZL = E / 2;
+  if constexpr (PART == 0) {
+    hy_planes<E, 0, ZL>(p, q00, pv, pc, rank, w, u1);
+  } else {
+    hy_planes<E, -3, 0>(p, q00, pv, pc, rank, w, u1);
+    hy_planes<E, ZL, ZL + 3>(p, q00, pv, pc, rank, w, u1);
+  }
+}
+
 // ring column q in [0, 4E) next to a box face: offsets (c'-plane layout) of the ring column,
 // its box neighbour and the step along the face; v-plane offset of the box neighbour
 template <int E>
@@ -1605,7 +1702,51 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cl2p<E>::NT, 1)
       for (int c = 0; c < 2; ++c)
 #pragma unroll
         for (int zl = 0; zl < ZL; ++zl) w[c][zl] = 0.0;
-#if CL2T_HORNER
+#if CL2T_HORNER == 2
+      double u1[2][ZL];
+#pragma unroll
+      for (int c = 0; c < 2; ++c)
+#pragma unroll
+        for (int zl = 0; zl < ZL; ++zl) u1[c][zl] = 0.0;
+      const double q00 = dt_inv(p.dtp, p.idt) + p.HW[0];
+      if (act) hy_stageA<E, 0>(p, q00, pv, pc, rank, w, u1);
+      C2P(3);
+      mbar_wait_cluster(&mbar[2], (ph >> 2) & 1u);
+      ph ^= 4u;
+      if (act) {
+        hy_stageA<E, 1>(p, q00, pv, pc, rank, w, u1);
+#pragma unroll
+        for (int zl = 0; zl < ZL; ++zl) {
+          pq[zl * CP] = u1[0][zl];
+          pq[zl * CP + CX] = u1[1][zl];
+        }
+      } else if (wid == NW - 1) {
+        // ring columns next to a box face: U1 from the box columns within radius 2 (the box
+        // neighbour b with its z-neighbours, b +- the step along the face, b one step inwards)
+        for (int q = lane; q < 4 * E; q += 32) {
+          int ro, bo, eo, vo;
+          hz_ring<E>(q, ro, bo, eo, vo);
+          const int s = q / E;
+          const int ev = s < 2 ? PX : 1;                               // along the face (v planes)
+          const int nv = s == 0 ? 1 : s == 1 ? -1 : s == 2 ? PX : -PX;   // inwards
+#pragma unroll
+          for (int zl = 0; zl < ZL; ++zl) {
+            const double* vp = vb + (zl + pv0) * PP + vo;
+            const double dn = (zl > 0 || rank != 0) ? vp[-PP] : 0.0;
+            const double up = (zl < ZL - 1 || rank != 1) ? vp[PP] : 0.0;
+            double r = p.GW[3] * vp[0];
+            r = fma(p.GW[4], dn + up, r);
+            r = fma(p.GW[6], vp[ev] + vp[-ev], r);
+            r = fma(p.GW[5], vp[nv], r);
+            qb[zl * CP + ro] = r;
+          }
+        }
+      }
+      __syncthreads();
+      C2P(4);
+      if (act) hz_stage3<E>(pq, u1, w);
+      C2P(5);
+#elif CL2T_HORNER
       double u1[2][ZL], u2[2][ZL];
 #pragma unroll
       for (int c = 0; c < 2; ++c)
@@ -1981,6 +2122,13 @@ cudaError_t launch_ras_3d_cl2(pfc_ctx* ctx, const double* v, const double* c, do
     p.HW[6] = 3.0 * a3;
     p.HW[7] = a2 - 6.0 * a3;
     p.HW[8] = 3.0 * a3;
+    p.GW[0] = p.HW[4] - 4.0 * p.HW[7] + 20.0 * a3;   // T = [1 1 -4 1 1], T^2: 20, -8, 1, 2
+    p.GW[1] = p.HW[5] - 4.0 * p.HW[8];
+    p.GW[2] = p.HW[6];
+    p.GW[3] = p.HW[7] - 8.0 * a3;
+    p.GW[4] = p.HW[8];
+    p.GW[5] = a3;
+    p.GW[6] = 2.0 * a3;
   }
   fn<<<2 * clusters, threads, smem, ctx->stream>>>(p);
   ctx->launches++;
